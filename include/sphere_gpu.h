@@ -1,0 +1,153 @@
+/* sphere_gpu.h -- C ABI of the B200-native spherical-operator hot path (libsphgpu.so).
+ *
+ * Drop-in for the operator API of the reference library spheretk
+ * (/root/reference/proj/include/sphere/, namespace sphere).  Each entry point names the
+ * reference function it replaces (file:line).  Conventions:
+ *   - every call returns an int status (SPH_OK or an error code); the message of the
+ *     last failure on the calling thread is available from sph_last_error();
+ *   - plans are immutable after creation and may be shared between threads; execute
+ *     calls are stream-ordered (cudaStream_t passed as void*, NULL = legacy stream);
+ *   - the caller owns every data buffer.  Unless stated otherwise data pointers are
+ *     DEVICE pointers of the current device, fp32, in the reference layouts:
+ *         fields  [F][nlat][nlon]                 (field.hpp:15-35, F = batch*channels)
+ *         coeffs  [F][lmax][mmax] complex64       (harmonics.hpp:24-42, zeros above
+ *                                                  the diagonal) for SPH_LAYOUT_DENSE_LM
+ *         mix     [c_out][c_in][K]                (convolution.hpp:126-139)
+ *   - `lmax` / `mmax` are COUNTS as in the reference (degrees 0..lmax-1,
+ *     harmonics.hpp:25-26).
+ * No torch types, no C++ types: plain pointers and sizes.
+ */
+#ifndef SPHERE_GPU_H
+#define SPHERE_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mirror the reference's exception classes) ---------------- */
+#define SPH_OK 0
+#define SPH_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument */
+#define SPH_ERR_RUNTIME 2          /* std::runtime_error (e.g. grid.hpp:117-119) */
+#define SPH_ERR_CUDA 3
+#define SPH_ERR_NCCL 4
+#define SPH_ERR_OOM 5
+
+/* ---- enums ------------------------------------------------------------------- */
+#define SPH_EQUIANGULAR 0 /* grid.hpp:69  build_equiangular */
+#define SPH_GAUSSIAN 1    /* grid.hpp:91  build_gaussian    */
+
+/* precision of the tensor-core contractions (Legendre, channel mixes) */
+#define SPH_PREC_3XTF32 0   /* default: hi*hi + hi*lo + lo*hi on tcgen05, fp32 accum */
+#define SPH_PREC_TF32 1     /* reduced-precision mode: one tcgen05 tf32 MMA (~1e-3)  */
+#define SPH_PREC_FP32_SIMT 2 /* fp32 FMA SIMT kernels (parity anchor)                */
+
+/* plan flags */
+#define SPH_FLAG_PREC_MASK 0x3
+/* sharp edge of the reference: sht_forward throws on equiangular grids
+ * (harmonics.hpp:129-130); the reference's equiangular forward is dist_sht_forward
+ * (distsim.hpp:404).  Plans created without this flag reject equiangular forwards. */
+#define SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD 0x10
+
+/* coefficient layouts */
+#define SPH_LAYOUT_DENSE_LM 0 /* reference [F][lmax][mmax] complex64 */
+#define SPH_LAYOUT_INTERNAL 1 /* GEMM-native parity-folded layout (sph_sht_coeffs_elems) */
+
+/* DISCO filter bases */
+#define SPH_BASIS_MORLET 0    /* convolution.hpp:73-76, K = 9 */
+#define SPH_BASIS_ISOTROPIC 1 /* convolution.hpp:78-81, K = 1 */
+
+typedef struct sph_sht_plan_s* sph_sht_plan;
+typedef struct sph_disco_plan_s* sph_disco_plan;
+
+/* ---- diagnostics --------------------------------------------------------------- */
+const char* sph_last_error(void);
+const char* sph_version(void);
+/* number of kernels this process launched through the library (all plans) */
+uint64_t sph_launch_count(void);
+/* stream-ordered per-kernel timing: when enabled every library kernel launch is
+ * bracketed by a CUDA event pair on its own stream; sph_profile_read returns CSV
+ * "name,launches,total_ms,work" aggregated since the previous read. */
+int sph_profile_enable(int on);
+int sph_profile_read(char* csv, size_t cap);
+
+/* ---- grids (grid.hpp:69-128), host fp64 ---------------------------------------- */
+int sph_grid(int kind, int64_t nlat, int64_t nlon, double* colatitudes, double* quad_weights);
+
+/* ---- SHT (harmonics.hpp) --------------------------------------------------------- */
+/* Replaces the per-call table builds of sht_forward/sht_inverse
+ * (harmonics.hpp:159-162, :202-205): grid, Phat tables (harmonics.hpp:59-117) are
+ * built once on the host in fp64, parity-folded, split hi/lo and uploaded. */
+int sph_sht_plan_create(int kind, int64_t nlat, int64_t nlon, int64_t lmax, int64_t mmax,
+                        int flags, sph_sht_plan* plan);
+int sph_sht_plan_destroy(sph_sht_plan plan);
+/* element counts (floats) of a coefficient buffer for F fields in `layout` */
+int64_t sph_sht_coeffs_elems(sph_sht_plan plan, int64_t F, int layout);
+/* bytes of caller workspace needed by forward/inverse for F fields */
+int64_t sph_sht_workspace_bytes(sph_sht_plan plan, int64_t F);
+
+/* sphere::sht_forward (harmonics.hpp:126 / :159 / :164; equiangular arithmetic of
+ * distsim.hpp:413-459).  x: fields [F][nlat][nlon]; coeffs: F fields in `layout`.
+ * workspace: >= sph_sht_workspace_bytes(plan, F) bytes of device memory, or NULL to use
+ * a plan-owned buffer (then calls on the same plan must be serialised). */
+int sph_sht_forward(sph_sht_plan plan, const float* x, int64_t F, float* coeffs, int layout,
+                    void* workspace, void* stream);
+/* sphere::sht_inverse (harmonics.hpp:173 / :202) */
+int sph_sht_inverse(sph_sht_plan plan, const float* coeffs, int64_t F, int layout, float* y,
+                    void* workspace, void* stream);
+/* sht_inverse(sht_forward(x)) for HOST buffers (pageable or pinned): the F fields are
+ * streamed through the device in chunks with H2D / compute / D2H overlapped on
+ * internal streams.  Blocks until y_host is written. */
+int sph_sht_roundtrip_host(sph_sht_plan plan, const float* x_host, int64_t F, float* y_host,
+                           int64_t chunk_fields);
+
+/* Stage entry points used by the distributed (pencil) SHT, distsim.hpp:404-463.
+ * fft stage: rings [F][h_count][nlon] -> bins [F][h_count][mmax] complex64, scaled
+ *   by 2*pi/nlon (distsim.hpp:413-430).
+ * legendre stage: bins [F][nlat][m_count] complex64 for global orders
+ *   m0..m0+m_count-1 -> coeffs [F][lmax][m_count] complex64 (distsim.hpp:437-459). */
+int sph_sht_fft_stage(sph_sht_plan plan, const float* rings, int64_t F, int64_t h_count,
+                      float* bins, void* stream);
+int sph_sht_legendre_stage(sph_sht_plan plan, const float* bins, int64_t F, int64_t m0,
+                           int64_t m_count, float* coeffs, void* workspace, void* stream);
+int64_t sph_sht_stage_workspace_bytes(sph_sht_plan plan, int64_t F, int64_t m_count);
+
+/* ---- DISCO (convolution.hpp) --------------------------------------------------- */
+/* assemble_disco (convolution.hpp:141-177) on the host in fp64, then the device
+ * tables.  Errors as the reference: longitudes not a uniform subset (:143-145) and empty
+ * support rows (:172-174) -> SPH_ERR_INVALID_ARGUMENT. */
+int sph_disco_plan_create(int in_kind, int64_t in_nlat, int64_t in_nlon, int out_kind,
+                          int64_t out_nlat, int64_t out_nlon, int basis, double theta_cutoff,
+                          int flags, sph_disco_plan* plan);
+int sph_disco_plan_destroy(sph_disco_plan plan);
+/* K (real basis functions), stride, total entries per basis function */
+int sph_disco_plan_info(sph_disco_plan plan, int64_t* n_basis, int64_t* stride,
+                        int64_t* nnz_per_basis);
+int64_t sph_disco_workspace_bytes(sph_disco_plan plan, int64_t B, int64_t c_in, int64_t c_out);
+/* disco_apply (convolution.hpp:181-220): x [B][c_in][in_nlat][in_nlon],
+ * mix [c_out][c_in][K], y [B][c_out][out_nlat][out_nlon]. */
+int sph_disco_apply(sph_disco_plan plan, const float* x, const float* mix, int64_t B,
+                    int64_t c_in, int64_t c_out, float* y, void* workspace, void* stream);
+
+/* ---- spectral convolution + block epilogue ------------------------------------ */
+/* spectral_conv (convolution.hpp:286-304): Gaussian grids only (:287-288);
+ * kernel [c_out][c_in][klmax]; x [B][c_in][nlat][nlon] -> y [B][c_out][nlat][nlon].
+ * The plan must have lmax = min(klmax, nlat), mmax = min(lmax, nlon/2) (:291-292). */
+int sph_spectral_conv(sph_sht_plan plan, const float* x, const float* kernel, int64_t B,
+                      int64_t c_in, int64_t c_out, int64_t klmax, float* y, void* workspace,
+                      void* stream);
+int64_t sph_spectral_conv_workspace_bytes(sph_sht_plan plan, int64_t B, int64_t c_in,
+                                          int64_t c_out);
+/* block_apply epilogue (model.hpp:355-368): per point
+ *   y = x + scales .* (W2 gelu(W1 gelu(conv) + b1) + b2),  gelu exact-erfc (model.hpp:42)
+ * conv, x, y: [B][C][npts]; w1 [H][C], b1 [H], w2 [C][H], b2 [C], scales [C]. */
+int sph_block_epilogue(const float* conv, const float* x, const float* w1, const float* b1,
+                       const float* w2, const float* b2, const float* scales, int64_t B,
+                       int64_t C, int64_t H, int64_t npts, float* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHERE_GPU_H */

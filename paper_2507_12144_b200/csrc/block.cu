@@ -1,0 +1,321 @@
+// Spectral convolution (convolution.hpp:286-304) and the neural-operator block
+// epilogue (model.hpp:355-368), both on the shared tcgen05 grouped-GEMM engine.
+#include <algorithm>
+
+#include "disco.cuh"
+
+namespace sph {
+
+namespace {
+
+__device__ __forceinline__ float gelu_erfc(float x) {  // model.hpp:42-44
+    return x * 0.5f * erfcf(-x * 0.70710678118654752440f);
+}
+
+// kernel [cout][cin][klmax] -> Kt hi/lo [(l*cout + o)][ldk], l < lmax (tiled transpose)
+__global__ void kernel_transpose_split(const float* __restrict__ k, int64_t cout, int64_t cin,
+                                       int64_t klmax, int64_t lmax, int64_t ldk,
+                                       float* __restrict__ hi, float* __restrict__ lo) {
+    __shared__ float tile[32][33];
+    const int64_t o = blockIdx.z;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, l0 = static_cast<int64_t>(blockIdx.y) * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, l = l0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < cin && l < lmax) ? k[(o * cin + i) * klmax + l] : 0.f;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t l = l0 + r, i = i0 + threadIdx.x;
+        if (l < lmax && i < ldk) {
+            const float x = i < cin ? tile[threadIdx.x][r] : 0.f;
+            uint32_t u;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+            const float h = __uint_as_float(u);
+            const int64_t idx = (l * cout + o) * ldk + i;
+            hi[idx] = h;
+            lo[idx] = x - h;
+        }
+    }
+}
+
+// C_int (F = B*cin fields) -> Xg[row_off[l] + (m*2 + reim)*B + b][i]
+__global__ void spec_gather_kernel(const float* __restrict__ cint, const int64_t* __restrict__ row_off,
+                                   int64_t lmax, int64_t mmax, int64_t B, int64_t cin, int Lp,
+                                   int64_t ldx, int64_t nrows, float* __restrict__ Xg,
+                                   const int32_t* __restrict__ row_l) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= nrows * ldx) return;
+    const int64_t i = idx % ldx, row = idx / ldx;
+    float v = 0.f;
+    if (i < cin) {
+        const int64_t l = row_l[row];
+        const int64_t r = row - row_off[l];
+        const int64_t b = r % B;
+        const int64_t reim = (r / B) & 1;
+        const int64_t m = r / (2 * B);
+        const int64_t p = (l - m) & 1, lp = (l - m) >> 1;
+        const int64_t twoF = 2 * B * cin;
+        v = cint[((m * 2 + p) * twoF + 2 * (b * cin + i) + reim) * Lp + lp];
+    }
+    Xg[idx] = v;
+    (void)lmax;
+    (void)mmax;
+}
+
+// Yg[row_off[l] + (m*2+reim)*B + b][o] -> C_int (F = B*cout) incl. zero padding
+__global__ void spec_scatter_kernel(const float* __restrict__ Yg, const int64_t* __restrict__ row_off,
+                                    int64_t lmax, int64_t mmax, int64_t B, int64_t cout, int Lp,
+                                    int64_t ldy, float* __restrict__ cint) {
+    const int64_t twoF = 2 * B * cout;
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= mmax * 2 * twoF * Lp) return;
+    const int64_t lp = idx % Lp;
+    const int64_t n = (idx / Lp) % twoF;
+    const int64_t g = idx / (Lp * twoF);
+    const int64_t m = g >> 1, p = g & 1;
+    const int64_t l = m + p + 2 * lp;
+    float v = 0.f;
+    if (l < lmax) {
+        const int64_t f = n >> 1, reim = n & 1;
+        const int64_t b = f / cout, o = f % cout;
+        const int64_t row = row_off[l] + (m * 2 + reim) * B + b;
+        v = Yg[row * ldy + o];
+    }
+    cint[idx] = v;
+}
+
+// G[(b*P + p)][c] = gelu(conv[b][c][p])  (tiled transpose)
+__global__ void gelu_transpose_kernel(const float* __restrict__ conv, int64_t C, int64_t P,
+                                      int64_t ldc, float* __restrict__ G) {
+    __shared__ float tile[32][33];
+    const int64_t b = blockIdx.z;
+    const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t c = c0 + r, p = p0 + threadIdx.x;
+        tile[r][threadIdx.x] = (c < C && p < P) ? gelu_erfc(conv[(b * C + c) * P + p]) : 0.f;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t p = p0 + r, c = c0 + threadIdx.x;
+        if (p < P && c < ldc) G[(b * P + p) * ldc + c] = c < C ? tile[threadIdx.x][r] : 0.f;
+    }
+}
+
+__global__ void bias_gelu_kernel(float* __restrict__ Hm, int64_t rows, int64_t H, int64_t ldh,
+                                 const float* __restrict__ b1) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows * ldh) return;
+    const int64_t h = i % ldh;
+    Hm[i] = h < H ? gelu_erfc(Hm[i] + b1[h]) : 0.f;
+}
+
+__global__ void residual_kernel(float* __restrict__ y, const float* __restrict__ x, int64_t B,
+                                int64_t C, int64_t P, const float* __restrict__ b2,
+                                const float* __restrict__ scales) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= B * C * P) return;
+    const int64_t c = (i / P) % C;
+    y[i] = x[i] + scales[c] * (y[i] + b2[c]);
+}
+
+inline unsigned nblk(int64_t n) { return static_cast<unsigned>((n + 255) / 256); }
+
+struct SpecProblem {
+    std::vector<int64_t> row_off;
+    std::vector<int32_t> row_l;
+    DevBuf<int64_t> d_row_off;
+    DevBuf<int32_t> d_row_l;
+    int64_t nrows = 0;
+    GroupedGemm gemm;
+};
+
+std::mutex g_mu;
+std::map<std::tuple<const void*, int64_t, int64_t, int64_t>, std::unique_ptr<SpecProblem>> g_spec;
+std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int>, std::unique_ptr<GroupedGemm>> g_mlp;
+
+struct SpecWs {
+    int64_t ldx, ldy, cin_off, cout_off, x_off, y_off, khi_off, klo_off, sht_off, total;
+};
+SpecWs spec_ws(const ShtPlan& p, int64_t B, int64_t cin, int64_t cout) {
+    SpecWs w;
+    w.ldx = static_cast<int64_t>(round_up(cin, 4));
+    w.ldy = static_cast<int64_t>(round_up(cout, 4));
+    int64_t nrows = 0;
+    for (int64_t l = 0; l < p.lmax; ++l) nrows += 2 * B * (std::min(l, p.mmax - 1) + 1);
+    int64_t o = 0;
+    w.cin_off = o;  o += round_up(p.cint_elems(B * cin) * 4, 256);
+    w.cout_off = o; o += round_up(p.cint_elems(B * cout) * 4, 256);
+    w.x_off = o;    o += round_up(nrows * w.ldx * 4, 256);
+    w.y_off = o;    o += round_up(nrows * w.ldy * 4, 256);
+    w.khi_off = o;  o += round_up(p.lmax * cout * w.ldx * 4, 256);
+    w.klo_off = o;  o += round_up(p.lmax * cout * w.ldx * 4, 256);
+    w.sht_off = o;  o += round_up(std::max(p.workspace_bytes(B * cin), p.workspace_bytes(B * cout)), 256);
+    w.total = o;
+    return w;
+}
+
+}  // namespace
+
+int64_t spectral_conv_ws_bytes(const ShtPlan& p, int64_t B, int64_t cin, int64_t cout) {
+    return spec_ws(p, B, cin, cout).total;
+}
+
+void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, int64_t cin,
+                   int64_t cout, int64_t klmax, float* y, void* ws, cudaStream_t st) {
+    require(p.kind == SPH_GAUSSIAN, "spectral_conv: requires a gaussian grid");  // :287-288
+    require(cin >= 1 && cout >= 1 && klmax >= 1, "spectral_conv: kernel channel mismatch");
+    const int64_t lmax = std::min<int64_t>(klmax, p.nlat);
+    const int64_t mmax = std::min<int64_t>(lmax, p.nlon / 2);
+    require(p.lmax == lmax && p.mmax == mmax,
+            "spectral_conv: plan truncation must be lmax=min(klmax,nlat), mmax=min(lmax,nlon/2)");
+    if (B == 0) return;
+    SPH_CUDA(cudaSetDevice(p.device));
+    const SpecWs w = spec_ws(p, B, cin, cout);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    DevBuf<uint8_t> tmp;
+    if (!base) {
+        tmp.alloc(w.total, false);
+        base = tmp.p;
+    }
+    float* cin_i = reinterpret_cast<float*>(base + w.cin_off);
+    float* cout_i = reinterpret_cast<float*>(base + w.cout_off);
+    float* Xg = reinterpret_cast<float*>(base + w.x_off);
+    float* Yg = reinterpret_cast<float*>(base + w.y_off);
+    float* khi = reinterpret_cast<float*>(base + w.khi_off);
+    float* klo = reinterpret_cast<float*>(base + w.klo_off);
+    void* sws = base + w.sht_off;
+
+    SpecProblem* sp;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto& slot = g_spec[std::make_tuple(static_cast<const void*>(&p), B, cin, cout)];
+        if (!slot) {
+            auto s = std::make_unique<SpecProblem>();
+            s->row_off.assign(lmax + 1, 0);
+            for (int64_t l = 0; l < lmax; ++l)
+                s->row_off[l + 1] = s->row_off[l] + 2 * B * (std::min(l, mmax - 1) + 1);
+            s->nrows = s->row_off[lmax];
+            s->row_l.resize(s->nrows);
+            for (int64_t l = 0; l < lmax; ++l)
+                for (int64_t r = s->row_off[l]; r < s->row_off[l + 1]; ++r) s->row_l[r] = static_cast<int32_t>(l);
+            s->d_row_off.alloc(s->row_off.size(), false);
+            SPH_CUDA(cudaMemcpy(s->d_row_off.p, s->row_off.data(), s->row_off.size() * 8, cudaMemcpyHostToDevice));
+            s->d_row_l.alloc(std::max<size_t>(s->row_l.size(), 1), false);
+            SPH_CUDA(cudaMemcpy(s->d_row_l.p, s->row_l.data(), s->row_l.size() * 4, cudaMemcpyHostToDevice));
+            GroupedGemm& g = s->gemm;
+            g.A = {nullptr, s->nrows, cin, w.ldx};
+            g.Bhi = {nullptr, lmax * cout, cin, w.ldx};
+            g.Blo = {nullptr, lmax * cout, cin, w.ldx};
+            g.store = STORE_ROW;
+            g.bn = cout >= 256 ? 256 : 128;
+            for (int64_t l = 0; l < lmax; ++l) {
+                GemmGroup gr;
+                gr.a_row0 = static_cast<int32_t>(s->row_off[l]);
+                gr.b_row0 = static_cast<int32_t>(l * cout);
+                gr.M = static_cast<int32_t>(s->row_off[l + 1] - s->row_off[l]);
+                gr.N = static_cast<int32_t>(cout);
+                gr.K = static_cast<int32_t>(cin);
+                gr.ldd = static_cast<int32_t>(w.ldy);
+                gr.zero_to = 0;
+                gr.d_off = s->row_off[l] * w.ldy;
+                g.groups.push_back(gr);
+            }
+            g.finalize();
+            slot = std::move(s);
+        }
+        sp = slot.get();
+    }
+    // 1. forward SHT of the B*cin input fields (convolution.hpp:294)
+    p.forward(x, B * cin, cin_i, SPH_LAYOUT_INTERNAL, sws, st);
+    // 2. y(o,l,m) = sum_i c(i,l,m) k(o,i,l)  (convolution.hpp:295-302) as per-l GEMMs
+    {
+        dim3 grid(static_cast<unsigned>((w.ldx + 31) / 32), static_cast<unsigned>((lmax + 31) / 32),
+                  static_cast<unsigned>(cout));
+        kernel_transpose_split<<<grid, dim3(32, 8), 0, st>>>(kernel, cout, cin, klmax, lmax, w.ldx, khi, klo);
+        SPH_LAUNCH_CHECK();
+        spec_gather_kernel<<<nblk(sp->nrows * w.ldx), 256, 0, st>>>(
+            cin_i, sp->d_row_off.p, lmax, mmax, B, cin, p.Lp, w.ldx, sp->nrows, Xg, sp->d_row_l.p);
+        SPH_LAUNCH_CHECK();
+        count_launch(2);
+        gemm_run(sp->gemm, Xg, Yg, p.prec, st, khi, klo);
+        spec_scatter_kernel<<<nblk(mmax * 2 * 2 * B * cout * p.Lp), 256, 0, st>>>(
+            Yg, sp->d_row_off.p, lmax, mmax, B, cout, p.Lp, w.ldy, cout_i);
+        SPH_LAUNCH_CHECK();
+        count_launch();
+    }
+    // 3. inverse SHT (convolution.hpp:303)
+    p.inverse(cout_i, B * cout, SPH_LAYOUT_INTERNAL, y, sws, st);
+    if (tmp.p) SPH_CUDA(cudaStreamSynchronize(st));
+}
+
+void block_epilogue(const float* conv, const float* x, const float* w1, const float* b1,
+                    const float* w2, const float* b2, const float* scales, int64_t B, int64_t C,
+                    int64_t H, int64_t P, float* y, cudaStream_t st) {
+    require(B >= 0 && C >= 1 && H >= 1 && P >= 0, "block_apply: bad shapes");
+    if (B == 0 || P == 0) return;
+    const int prec = SPH_PREC_3XTF32;
+    const int64_t ldc = static_cast<int64_t>(round_up(C, 4)), ldh = static_cast<int64_t>(round_up(H, 4));
+    // workspace: G [B*P][ldc], Hm [B*P][ldh], W1 hi/lo [H][ldc], W2 hi/lo [C][ldh]
+    const int64_t nG = B * P * ldc, nH = B * P * ldh, nW1 = H * ldc, nW2 = C * ldh;
+    float* wsp = nullptr;
+    SPH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wsp), 4 * (nG + nH + 2 * nW1 + 2 * nW2) + 1024, st));
+    float* G = wsp;
+    float* Hm = G + round_up(nG, 64);
+    float* w1h = Hm + round_up(nH, 64);
+    float* w1l = w1h + round_up(nW1, 64);
+    float* w2h = w1l + round_up(nW1, 64);
+    float* w2l = w2h + round_up(nW2, 64);
+    GroupedGemm *g1, *g2;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto& s1 = g_mlp[std::make_tuple(B, C, H, P, 1)];
+        if (!s1) {
+            auto g = std::make_unique<GroupedGemm>();
+            g->A = {nullptr, B * P, C, ldc};
+            g->Bhi = {nullptr, H, C, ldc};
+            g->Blo = {nullptr, H, C, ldc};
+            g->store = STORE_ROW;
+            g->bn = H >= 256 ? 256 : 128;
+            require(B * P < (1LL << 31), "block: too many points");
+            g->groups.push_back({0, 0, static_cast<int32_t>(B * P), static_cast<int32_t>(H),
+                                 static_cast<int32_t>(C), static_cast<int32_t>(ldh), 0, 0});
+            g->finalize();
+            s1 = std::move(g);
+        }
+        auto& s2 = g_mlp[std::make_tuple(B, C, H, P, 2)];
+        if (!s2) {
+            auto g = std::make_unique<GroupedGemm>();
+            g->A = {nullptr, B * P, H, ldh};
+            g->Bhi = {nullptr, C, H, ldh};
+            g->Blo = {nullptr, C, H, ldh};
+            g->store = STORE_TRANS;
+            g->bn = C >= 256 ? 256 : 128;
+            for (int64_t b = 0; b < B; ++b)
+                g->groups.push_back({static_cast<int32_t>(b * P), 0, static_cast<int32_t>(P),
+                                     static_cast<int32_t>(C), static_cast<int32_t>(H),
+                                     static_cast<int32_t>(P), 0, b * C * P});
+            g->finalize();
+            s2 = std::move(g);
+        }
+        g1 = s1.get();
+        g2 = s2.get();
+    }
+    split_rows(w1, H, C, ldc, w1h, w1l, st);
+    split_rows(w2, C, H, ldh, w2h, w2l, st);
+    dim3 grid(static_cast<unsigned>((P + 31) / 32), static_cast<unsigned>((ldc + 31) / 32),
+              static_cast<unsigned>(B));
+    gelu_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(conv, C, P, ldc, G);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+    gemm_run(*g1, G, Hm, prec, st, w1h, w1l);
+    bias_gelu_kernel<<<nblk(B * P * ldh), 256, 0, st>>>(Hm, B * P, H, ldh, b1);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+    gemm_run(*g2, Hm, y, prec, st, w2h, w2l);
+    residual_kernel<<<nblk(B * C * P), 256, 0, st>>>(y, x, B, C, P, b2, scales);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+    SPH_CUDA(cudaFreeAsync(wsp, st));
+}
+
+}  // namespace sph

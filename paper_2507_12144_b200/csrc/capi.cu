@@ -1,0 +1,300 @@
+// extern "C" boundary of libsphgpu.so (include/sphere_gpu.h).  Converts the
+// library's C++ exceptions into status codes + a thread-local message, the
+// C-ABI analogue of the reference's std::invalid_argument / std::runtime_error.
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "disco.cuh"
+#include "sht.cuh"
+
+struct sph_sht_plan_s {
+    sph::ShtPlan p;
+};
+struct sph_disco_plan_s {
+    sph::DiscoPlan p;
+};
+
+namespace sph {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+
+namespace {
+struct ProfRec {
+    std::string name;
+    cudaEvent_t e0, e1;
+    double work;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof_on{false};
+std::vector<ProfRec> g_prof;
+}  // namespace
+
+ProfScope::ProfScope(const char* name, cudaStream_t s, double work) : st(s) {
+    if (!g_prof_on.load(std::memory_order_relaxed)) return;
+    ProfRec r{name, nullptr, nullptr, work};
+    cudaEventCreate(&r.e0);
+    cudaEventCreate(&r.e1);
+    cudaEventRecord(r.e0, st);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    slot = static_cast<int>(g_prof.size());
+    g_prof.push_back(r);
+}
+ProfScope::~ProfScope() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEventRecord(g_prof[slot].e1, st);
+}
+}  // namespace sph
+
+namespace {
+thread_local std::string g_err;
+
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return SPH_OK;
+    } catch (const sph::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("host allocation failed: ") + e.what();
+        return SPH_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SPH_ERR_RUNTIME;
+    }
+}
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+const char* sph_last_error(void) { return g_err.c_str(); }
+const char* sph_version(void) { return "sphgpu 0.1 sm_100a"; }
+uint64_t sph_launch_count(void) { return sph::g_launches.load(); }
+
+int sph_profile_enable(int on) {
+    sph::g_prof_on.store(on != 0);
+    return SPH_OK;
+}
+
+// CSV "name,launches,total_ms,work" per kernel name since the last read; resets.
+int sph_profile_read(char* csv, size_t cap) {
+    return guarded([&] {
+        std::vector<sph::ProfRec> recs;
+        {
+            std::lock_guard<std::mutex> lk(sph::g_prof_mu);
+            recs.swap(sph::g_prof);
+        }
+        std::map<std::string, std::tuple<int, double, double>> agg;
+        for (auto& r : recs) {
+            SPH_CUDA(cudaEventSynchronize(r.e1));
+            float ms = 0.f;
+            SPH_CUDA(cudaEventElapsedTime(&ms, r.e0, r.e1));
+            auto& a = agg[r.name];
+            std::get<0>(a) += 1;
+            std::get<1>(a) += ms;
+            std::get<2>(a) += r.work;
+            cudaEventDestroy(r.e0);
+            cudaEventDestroy(r.e1);
+        }
+        std::string out = "name,launches,total_ms,work\n";
+        for (auto& [k, v] : agg)
+            out += k + "," + std::to_string(std::get<0>(v)) + "," + std::to_string(std::get<1>(v)) +
+                   "," + std::to_string(std::get<2>(v)) + "\n";
+        if (csv && cap) std::snprintf(csv, cap, "%s", out.c_str());
+    });
+}
+
+int sph_grid(int kind, int64_t nlat, int64_t nlon, double* colat, double* w) {
+    return guarded([&] {
+        std::vector<double> c, ww;
+        sph::build_grid(kind, nlat, nlon, c, ww);
+        std::memcpy(colat, c.data(), sizeof(double) * nlat);
+        std::memcpy(w, ww.data(), sizeof(double) * nlat);
+    });
+}
+
+// ------------------------------------------------------------------------ SHT
+int sph_sht_plan_create(int kind, int64_t nlat, int64_t nlon, int64_t lmax, int64_t mmax,
+                        int flags, sph_sht_plan* plan) {
+    return guarded([&] {
+        sph::require(plan != nullptr, "sph_sht_plan_create: null plan pointer");
+        auto* h = new sph_sht_plan_s();
+        try {
+            h->p.create(kind, nlat, nlon, lmax, mmax, flags);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *plan = h;
+    });
+}
+
+int sph_sht_plan_destroy(sph_sht_plan plan) {
+    return guarded([&] { delete plan; });
+}
+
+int64_t sph_sht_coeffs_elems(sph_sht_plan plan, int64_t F, int layout) {
+    if (!plan) return -1;
+    return layout == SPH_LAYOUT_INTERNAL ? plan->p.cint_elems(F) : plan->p.dense_elems(F);
+}
+
+int64_t sph_sht_workspace_bytes(sph_sht_plan plan, int64_t F) {
+    return plan ? plan->p.workspace_bytes(F) : -1;
+}
+
+int sph_sht_forward(sph_sht_plan plan, const float* x, int64_t F, float* coeffs, int layout,
+                    void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "sht_forward: null plan");
+        plan->p.forward(x, F, coeffs, layout, workspace, S(stream));
+    });
+}
+
+int sph_sht_inverse(sph_sht_plan plan, const float* coeffs, int64_t F, int layout, float* y,
+                    void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "sht_inverse: null plan");
+        plan->p.inverse(coeffs, F, layout, y, workspace, S(stream));
+    });
+}
+
+int sph_sht_roundtrip_host(sph_sht_plan plan, const float* xh, int64_t F, float* yh,
+                           int64_t chunk) {
+    return guarded([&] {
+        sph::require(plan, "sht roundtrip: null plan");
+        sph::ShtPlan& p = plan->p;
+        SPH_CUDA(cudaSetDevice(p.device));
+        if (F <= 0) return;
+        if (chunk <= 0) chunk = 32;
+        chunk = std::min(chunk, F);
+        const int64_t np = p.nlat * p.nlon;
+        cudaStream_t st[2];
+        cudaEvent_t done[2];
+        for (int i = 0; i < 2; ++i) {
+            SPH_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+            SPH_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+        }
+        struct Bufs {
+            sph::DevBuf<float> x, y, c;
+            sph::DevBuf<uint8_t> ws;
+        } b[2];
+        for (int i = 0; i < 2; ++i) {
+            b[i].x.alloc(chunk * np, false);
+            b[i].y.alloc(chunk * np, false);
+            b[i].c.alloc(p.cint_elems(chunk), true);
+            b[i].ws.alloc(p.workspace_bytes(chunk), true);
+        }
+        int it = 0;
+        for (int64_t f0 = 0; f0 < F; f0 += chunk, ++it) {
+            const int s = it & 1;
+            const int64_t n = std::min(chunk, F - f0);
+            SPH_CUDA(cudaMemcpyAsync(b[s].x.p, xh + f0 * np, sizeof(float) * n * np,
+                                     cudaMemcpyHostToDevice, st[s]));
+            p.forward(b[s].x.p, n, b[s].c.p, SPH_LAYOUT_INTERNAL, b[s].ws.p, st[s]);
+            p.inverse(b[s].c.p, n, SPH_LAYOUT_INTERNAL, b[s].y.p, b[s].ws.p, st[s]);
+            SPH_CUDA(cudaMemcpyAsync(yh + f0 * np, b[s].y.p, sizeof(float) * n * np,
+                                     cudaMemcpyDeviceToHost, st[s]));
+        }
+        for (int i = 0; i < 2; ++i) {
+            SPH_CUDA(cudaStreamSynchronize(st[i]));
+            cudaEventDestroy(done[i]);
+            cudaStreamDestroy(st[i]);
+        }
+    });
+}
+
+int sph_sht_fft_stage(sph_sht_plan plan, const float* rings, int64_t F, int64_t h_count,
+                      float* bins, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "fft stage: null plan");
+        plan->p.fft_stage(rings, F, h_count, bins, S(stream));
+    });
+}
+
+int sph_sht_legendre_stage(sph_sht_plan plan, const float* bins, int64_t F, int64_t m0,
+                           int64_t m_count, float* coeffs, void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "legendre stage: null plan");
+        plan->p.legendre_stage(bins, F, m0, m_count, coeffs, workspace, S(stream));
+    });
+}
+
+int64_t sph_sht_stage_workspace_bytes(sph_sht_plan plan, int64_t F, int64_t m_count) {
+    return plan ? plan->p.stage_ws_bytes(F, m_count) : -1;
+}
+
+// ---------------------------------------------------------------------- DISCO
+int sph_disco_plan_create(int in_kind, int64_t in_nlat, int64_t in_nlon, int out_kind,
+                          int64_t out_nlat, int64_t out_nlon, int basis, double theta_cutoff,
+                          int flags, sph_disco_plan* plan) {
+    return guarded([&] {
+        sph::require(plan != nullptr, "sph_disco_plan_create: null plan pointer");
+        auto* h = new sph_disco_plan_s();
+        try {
+            h->p.create(in_kind, in_nlat, in_nlon, out_kind, out_nlat, out_nlon, basis,
+                        theta_cutoff, flags);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *plan = h;
+    });
+}
+
+int sph_disco_plan_destroy(sph_disco_plan plan) {
+    return guarded([&] { delete plan; });
+}
+
+int sph_disco_plan_info(sph_disco_plan plan, int64_t* n_basis, int64_t* stride,
+                        int64_t* nnz_per_basis) {
+    return guarded([&] {
+        sph::require(plan, "disco info: null plan");
+        if (n_basis) *n_basis = plan->p.K;
+        if (stride) *stride = plan->p.stride;
+        if (nnz_per_basis) *nnz_per_basis = plan->p.nnz;
+    });
+}
+
+int64_t sph_disco_workspace_bytes(sph_disco_plan plan, int64_t B, int64_t c_in, int64_t c_out) {
+    return plan ? plan->p.workspace_bytes(B, c_in, c_out) : -1;
+}
+
+int sph_disco_apply(sph_disco_plan plan, const float* x, const float* mix, int64_t B,
+                    int64_t c_in, int64_t c_out, float* y, void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "disco_apply: null plan");
+        plan->p.apply(x, mix, B, c_in, c_out, y, workspace, S(stream));
+    });
+}
+
+// ------------------------------------------------------ spectral conv + block
+int sph_spectral_conv(sph_sht_plan plan, const float* x, const float* kernel, int64_t B,
+                      int64_t c_in, int64_t c_out, int64_t klmax, float* y, void* workspace,
+                      void* stream) {
+    return guarded([&] {
+        sph::require(plan, "spectral_conv: null plan");
+        sph::spectral_conv(plan->p, x, kernel, B, c_in, c_out, klmax, y, workspace, S(stream));
+    });
+}
+
+int64_t sph_spectral_conv_workspace_bytes(sph_sht_plan plan, int64_t B, int64_t c_in,
+                                          int64_t c_out) {
+    return plan ? sph::spectral_conv_ws_bytes(plan->p, B, c_in, c_out) : -1;
+}
+
+int sph_block_epilogue(const float* conv, const float* x, const float* w1, const float* b1,
+                       const float* w2, const float* b2, const float* scales, int64_t B, int64_t C,
+                       int64_t H, int64_t npts, float* y, void* stream) {
+    return guarded([&] {
+        sph::block_epilogue(conv, x, w1, b1, w2, b2, scales, B, C, H, npts, y, S(stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,444 @@
+// DISCO convolution on sm_100a (convolution.hpp:141-220).
+//
+// The operator is assembled on the host in fp64 exactly as the reference does
+// (every k shares one (h_in, w_rel) index list per output row; the input quadrature
+// weight is folded in).  Two device paths:
+//
+//  * default (SPH_PREC_3XTF32 / TF32): longitude-Fourier restructure.  psi_k for a fixed
+//    (h_out, h_in) pair is a circular correlation filter over the longitude index, so
+//        t_hat[k,c,h](m) = sum_{h_in in band(h)} conj(psi_hat_k[h,h_in](m)) u_hat[c,h_in](m)
+//    and the stride-s output sampling folds the spectrum:  S(m') = sum_q R(m' + W_out q).
+//    Kernels: channel-minor R2C of the input rings -> band contraction (<= ~12 rows per
+//    output row, independent of the polar row nnz) -> tcgen05 3xTF32 channel-mix GEMM
+//    (mix [c_out][c_in*K] is the table operand) in the Fourier domain -> C2R of the
+//    output rings.  Parity is by tolerance (summation order differs).
+//  * SPH_PREC_FP32_SIMT anchor: the reference's own operation order (gather t, then
+//    the channel mix) in fp32 FMA.
+#include <algorithm>
+#include <cmath>
+#include <thread>
+
+#include "disco.cuh"
+
+namespace sph {
+
+namespace {
+constexpr double kPi = 3.14159265358979323846;
+}
+
+int Basis::n_real() const {
+    int n = 0;
+    for (auto& p : pairs) n += (p.first == 0 && p.second == 0) ? 1 : 2;
+    return n;
+}
+
+// convolution.hpp:38-68 (Hann-windowed Morlet modes, real then imaginary parts)
+double Basis::eval_real(int k, double theta, double phi) const {
+    size_t b = 0;
+    for (; b < pairs.size(); ++b) {
+        const int parts = (pairs[b].first == 0 && pairs[b].second == 0) ? 1 : 2;
+        if (k < parts) break;
+        k -= parts;
+    }
+    const double tp = theta / cutoff;
+    if (tp > 1.0) return 0.0;
+    const double c = std::cos(0.5 * kPi * tp);
+    const double h = c * c;
+    const double arg = kPi * tp * (pairs[b].first * std::sin(phi) + pairs[b].second * std::cos(phi));
+    return k == 0 ? h * std::cos(arg) : h * std::sin(arg);
+}
+
+Basis make_basis(int kind, double cutoff) {
+    require(cutoff > 0.0, kind == SPH_BASIS_ISOTROPIC ? "isotropic_basis: cutoff must be > 0"
+                                                      : "morlet_basis: cutoff must be > 0");
+    Basis b;
+    b.cutoff = cutoff;
+    if (kind == SPH_BASIS_MORLET)
+        b.pairs = {{0, 0}, {0, 1}, {0, 2}, {2, 1}, {2, 2}};  // convolution.hpp:73-76
+    else if (kind == SPH_BASIS_ISOTROPIC)
+        b.pairs = {{0, 0}};
+    else
+        fail(SPH_ERR_INVALID_ARGUMENT, "disco: unknown basis");
+    return b;
+}
+
+namespace {
+
+// convolution.hpp:93-101: great-circle distance and azimuth from the southward meridian
+inline void chart(double theta_out, double theta_in, double dphi, double& dist, double& az) {
+    const double st_o = std::sin(theta_out), ct_o = std::cos(theta_out);
+    const double st_i = std::sin(theta_in), ct_i = std::cos(theta_in);
+    const double cd = std::cos(dphi);
+    const double x = ct_o * st_i * cd - st_o * ct_i;
+    const double y = st_i * std::sin(dphi);
+    const double z = st_o * st_i * cd + ct_o * ct_i;
+    dist = std::atan2(std::hypot(x, y), z);
+    az = std::atan2(y, x);
+}
+
+template <class Fn>
+void parallel_for(int64_t n, Fn fn) {
+    int nt = static_cast<int>(std::min<int64_t>(n, std::max(1u, std::thread::hardware_concurrency())));
+    nt = std::min(nt, 32);
+    if (nt <= 1) {
+        for (int64_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (int64_t i = t; i < n; i += nt) fn(i);
+        });
+    for (auto& t : th) t.join();
+}
+
+template <class T>
+void upload(DevBuf<T>& d, const std::vector<T>& h) {
+    d.alloc(std::max<size_t>(h.size(), 1), false);
+    if (!h.empty()) SPH_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void split_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
+                                  int64_t ld, float* __restrict__ hi, float* __restrict__ lo) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows * ld) return;
+    const int64_t r = i / ld, c = i % ld;
+    const float x = c < cols ? src[r * cols + c] : 0.f;
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+    const float h = __uint_as_float(u);
+    hi[i] = h;
+    lo[i] = x - h;
+}
+
+// Fourier band contraction + stride fold.  Block (m'-tile of 4, h_out, b); thread
+// (m' in tile, channel lane).  Output S[((b*Hout + h)*nbo + m')*2 + reim][c*K + k].
+__global__ void __launch_bounds__(256) disco_band_kernel(
+    const float2* __restrict__ U, const float2* __restrict__ psi_hat, const int32_t* __restrict__ band0,
+    const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, int64_t Hin, int64_t nbi,
+    int64_t Hout, int64_t nbo, int win, int wout, int s, int K, int64_t C, int64_t ldS,
+    float* __restrict__ S) {
+    const int mi = threadIdx.x / 64, cl = threadIdx.x % 64;
+    const int64_t mp = static_cast<int64_t>(blockIdx.x) * 4 + mi;
+    const int64_t h = blockIdx.y, b = blockIdx.z;
+    if (mp >= nbo) return;
+    const int h0 = band0[h], nb = bandc[h];
+    const int64_t po = psi_off[h];
+    const int half = win / 2;
+    for (int64_t c0 = 0; c0 < C; c0 += 64) {
+        const int64_t c = c0 + cl;
+        const bool valid = c < C;
+        float2 acc[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[k] = make_float2(0.f, 0.f);
+        for (int bi = 0; bi < nb; ++bi) {
+            const int64_t hi = h0 + bi;
+            for (int q = 0; q < s; ++q) {
+                const int kq = static_cast<int>(mp) + wout * q;
+                const bool cj = kq > half;
+                const int idx = cj ? win - kq : kq;
+                const float2 u = valid ? U[((b * Hin + hi) * nbi + idx) * C + c] : make_float2(0.f, 0.f);
+                const float2* ps = psi_hat + ((po + bi) * nbi + idx) * K;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    if (k < K) {
+                        const float2 p = __ldg(ps + k);
+                        if (!cj) {  // conj(psi) * u
+                            acc[k].x += p.x * u.x + p.y * u.y;
+                            acc[k].y += p.x * u.y - p.y * u.x;
+                        } else {    // psi * conj(u)
+                            acc[k].x += p.x * u.x + p.y * u.y;
+                            acc[k].y += p.y * u.x - p.x * u.y;
+                        }
+                    }
+                }
+            }
+        }
+        if (valid) {
+            const int64_t row = ((b * Hout + h) * nbo + mp) * 2;
+            float* sr = S + row * ldS + c * K;
+            float* si = S + (row + 1) * ldS + c * K;
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                if (k < K) {
+                    sr[k] = acc[k].x;
+                    si[k] = acc[k].y;
+                }
+        }
+    }
+}
+
+// Direct gather in the reference order (convolution.hpp:192-205), fp32:
+// T[(b*Hout + h)*Wout + w][c*K + k] = sum_e vals[e][k] u[b][c][h_in][(w_rel + s w) % Win]
+__global__ void __launch_bounds__(256) disco_gather_kernel(
+    const float* __restrict__ x, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ h_in,
+    const int32_t* __restrict__ w_rel, const float* __restrict__ vals, int64_t Hin, int64_t Win,
+    int64_t Hout, int64_t Wout, int64_t stride, int K, int64_t C, int64_t ldS, float* __restrict__ T) {
+    const int64_t h = blockIdx.x, c = blockIdx.y, b = blockIdx.z;
+    const float* u = x + (b * C + c) * Hin * Win;
+    const int64_t e0 = row_ptr[h], e1 = row_ptr[h + 1];
+    for (int64_t w = threadIdx.x; w < Wout; w += blockDim.x) {
+        float acc[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[k] = 0.f;
+        for (int64_t e = e0; e < e1; ++e) {
+            int64_t col = w_rel[e] + stride * w;
+            col %= Win;
+            const float v = __ldg(u + static_cast<int64_t>(h_in[e]) * Win + col);
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                if (k < K) acc[k] = fmaf(__ldg(vals + e * K + k), v, acc[k]);
+        }
+        float* dst = T + ((b * Hout + h) * Wout + w) * ldS + c * K;
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+            if (k < K) dst[k] = acc[k];
+    }
+}
+
+}  // namespace
+
+void split_rows(const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
+                cudaStream_t st) {
+    const int64_t n = rows * ld;
+    if (n == 0) return;
+    split_rows_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(src, rows, cols, ld,
+                                                                              hi, lo);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+}
+
+void DiscoPlan::create(int in_kind_, int64_t in_nlat, int64_t in_nlon, int out_kind_,
+                       int64_t out_nlat, int64_t out_nlon, int basis_kind, double cutoff,
+                       int flags) {
+    SPH_CUDA(cudaGetDevice(&device));
+    in_kind = in_kind_;
+    out_kind = out_kind_;
+    hin = in_nlat;
+    win = in_nlon;
+    hout = out_nlat;
+    wout = out_nlon;
+    prec = flags & SPH_FLAG_PREC_MASK;
+    require(prec <= SPH_PREC_FP32_SIMT, "disco plan: unknown precision mode");
+    build_grid(in_kind, hin, win, in_colat, in_w);
+    build_grid(out_kind, hout, wout, out_colat, out_w);
+    const Basis basis = make_basis(basis_kind, cutoff);
+    if (wout == 0 || win % wout != 0)  // convolution.hpp:143-145
+        fail(SPH_ERR_INVALID_ARGUMENT,
+             "assemble_disco: output longitudes must be a uniform subset of the input");
+    require(hin < (1LL << 31) && win < (1LL << 31), "disco: grid too large");
+    K = basis.n_real();
+    require(K <= 9, "disco: at most 9 real basis functions supported");
+    stride = win / wout;
+
+    // ---- assemble (convolution.hpp:150-176), per output row in parallel
+    std::vector<std::vector<int32_t>> rh(hout), rw(hout);
+    std::vector<std::vector<double>> rv(hout);
+    std::vector<double> lon(win);
+    for (int64_t j = 0; j < win; ++j) lon[j] = 2.0 * kPi * static_cast<double>(j) / static_cast<double>(win);
+    parallel_for(hout, [&](int64_t h) {
+        const double theta_out = out_colat[h];
+        for (int64_t hi = 0; hi < hin; ++hi) {
+            const double theta_in = in_colat[hi];
+            if (std::abs(theta_in - theta_out) >= basis.cutoff) continue;
+            const double w_in = in_w[hi];
+            for (int64_t wj = 0; wj < win; ++wj) {
+                double dist, az;
+                chart(theta_out, theta_in, lon[wj], dist, az);
+                if (dist >= basis.cutoff) continue;
+                rh[h].push_back(static_cast<int32_t>(hi));
+                rw[h].push_back(static_cast<int32_t>(wj));
+                for (int k = 0; k < K; ++k) rv[h].push_back(basis.eval_real(k, dist, az) * w_in);
+            }
+        }
+    });
+    row_ptr.assign(hout + 1, 0);
+    for (int64_t h = 0; h < hout; ++h) {
+        if (rh[h].empty())  // convolution.hpp:172-174
+            fail(SPH_ERR_INVALID_ARGUMENT,
+                 "assemble_disco: empty filter support (cutoff below grid spacing)");
+        row_ptr[h + 1] = row_ptr[h] + static_cast<int64_t>(rh[h].size());
+    }
+    nnz = row_ptr[hout];
+    h_in.resize(nnz);
+    w_rel.resize(nnz);
+    vals.resize(nnz * K);
+    for (int64_t h = 0; h < hout; ++h) {
+        std::copy(rh[h].begin(), rh[h].end(), h_in.begin() + row_ptr[h]);
+        std::copy(rw[h].begin(), rw[h].end(), w_rel.begin() + row_ptr[h]);
+        std::copy(rv[h].begin(), rv[h].end(), vals.begin() + row_ptr[h] * K);
+    }
+    upload(d_row_ptr, row_ptr);
+    upload(d_h_in, h_in);
+    upload(d_w_rel, w_rel);
+    {
+        std::vector<float> vf(vals.begin(), vals.end());
+        upload(d_vals, vf);
+    }
+
+    // ---- longitude-Fourier tables
+    nbi = win / 2 + 1;
+    nbo = wout / 2 + 1;
+    band0.assign(hout, 0);
+    bandc.assign(hout, 0);
+    psi_off.assign(hout + 1, 0);
+    for (int64_t h = 0; h < hout; ++h) {
+        int32_t lo = INT32_MAX, hi = -1;
+        for (int64_t e = row_ptr[h]; e < row_ptr[h + 1]; ++e) {
+            lo = std::min(lo, h_in[e]);
+            hi = std::max(hi, h_in[e]);
+        }
+        band0[h] = lo;
+        bandc[h] = hi - lo + 1;
+        psi_off[h + 1] = psi_off[h] + bandc[h];
+    }
+    std::vector<double> cw(win), sw(win);
+    for (int64_t j = 0; j < win; ++j) {
+        const double a = -2.0 * kPi * static_cast<double>(j) / static_cast<double>(win);
+        cw[j] = std::cos(a);
+        sw[j] = std::sin(a);
+    }
+    const int64_t nrow = psi_off[hout];
+    std::vector<float2> ph(static_cast<size_t>(nrow) * nbi * K);
+    parallel_for(hout, [&](int64_t h) {
+        std::vector<double> acc(static_cast<size_t>(bandc[h]) * nbi * K * 2, 0.0);
+        for (int64_t e = row_ptr[h]; e < row_ptr[h + 1]; ++e) {
+            const int64_t bi = h_in[e] - band0[h];
+            const int64_t wr = w_rel[e];
+            double* a = acc.data() + bi * nbi * K * 2;
+            int64_t ph_idx = 0;  // (wr * m) mod win
+            for (int64_t m = 0; m < nbi; ++m) {
+                const double c = cw[ph_idx], s = sw[ph_idx];
+                for (int k = 0; k < K; ++k) {
+                    const double v = vals[e * K + k];
+                    a[(m * K + k) * 2] += v * c;
+                    a[(m * K + k) * 2 + 1] += v * s;
+                }
+                ph_idx += wr;
+                if (ph_idx >= win) ph_idx -= win;
+            }
+        }
+        float2* out = ph.data() + psi_off[h] * nbi * K;
+        for (size_t i = 0; i < static_cast<size_t>(bandc[h]) * nbi * K; ++i)
+            out[i] = make_float2(static_cast<float>(acc[2 * i]), static_cast<float>(acc[2 * i + 1]));
+    });
+    upload(d_psi_hat, ph);
+    upload(d_band0, band0);
+    upload(d_bandc, bandc);
+    upload(d_psi_off, psi_off);
+    fft_in.build(static_cast<int>(win));
+    fft_out.build(static_cast<int>(wout));
+}
+
+namespace {
+struct DiscoWs {
+    int64_t ldS, u_off, s_off, y_off, whi_off, wlo_off, total;
+};
+DiscoWs disco_ws(const DiscoPlan& p, int64_t B, int64_t cin, int64_t cout) {
+    DiscoWs w;
+    w.ldS = static_cast<int64_t>(round_up(cin * p.K, 4));
+    const int64_t whi = cout * w.ldS * 4;
+    int64_t o = 0;
+    w.whi_off = o;
+    o += round_up(whi, 256);
+    w.wlo_off = o;
+    o += round_up(whi, 256);
+    if (p.prec == SPH_PREC_FP32_SIMT) {
+        w.s_off = o;  // T (direct gather)
+        o += round_up(B * p.hout * p.wout * w.ldS * 4, 256);
+        w.u_off = w.y_off = 0;
+    } else {
+        w.u_off = o;
+        o += round_up(B * p.hin * p.nbi * cin * 8, 256);
+        w.s_off = o;
+        o += round_up(B * p.hout * p.nbo * 2 * w.ldS * 4, 256);
+        w.y_off = o;
+        o += round_up(B * cout * p.hout * p.nbo * 2 * 4, 256);
+    }
+    w.total = o + 256;
+    return w;
+}
+}  // namespace
+
+int64_t DiscoPlan::workspace_bytes(int64_t B, int64_t cin, int64_t cout) const {
+    return disco_ws(*this, B, cin, cout).total;
+}
+
+void DiscoPlan::apply(const float* x, const float* mix, int64_t B, int64_t cin, int64_t cout,
+                      float* y, void* ws, cudaStream_t st) {
+    require(B >= 0 && cin >= 1 && cout >= 1, "disco_apply: mix tensor shape mismatch");
+    if (B == 0) return;
+    SPH_CUDA(cudaSetDevice(device));
+    const DiscoWs w = disco_ws(*this, B, cin, cout);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    if (!base) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (own_ws.n < static_cast<size_t>(w.total)) own_ws.alloc(w.total, true);
+        base = own_ws.p;
+    }
+    float* whi = reinterpret_cast<float*>(base + w.whi_off);
+    float* wlo = reinterpret_cast<float*>(base + w.wlo_off);
+    split_rows(mix, cout, cin * K, w.ldS, whi, wlo, st);
+    const bool direct = prec == SPH_PREC_FP32_SIMT;
+    const int64_t rows_per_b = direct ? hout * wout : hout * nbo * 2;
+    const GroupedGemm* gp;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto& slot = gemm_cache[std::make_tuple(B, cin, cout, direct ? 1 : 0)];
+        if (!slot) {
+            auto g = std::make_unique<GroupedGemm>();
+            g->A = {nullptr, B * rows_per_b, cin * K, w.ldS};
+            g->Bhi = {nullptr, cout, cin * K, w.ldS};
+            g->Blo = {nullptr, cout, cin * K, w.ldS};
+            g->store = STORE_TRANS;
+            g->bn = cout >= 256 ? 256 : 128;
+            require(B * rows_per_b < (1LL << 31), "disco: batch too large for one call");
+            for (int64_t b = 0; b < B; ++b) {
+                GemmGroup gr;
+                gr.a_row0 = static_cast<int32_t>(b * rows_per_b);
+                gr.b_row0 = 0;
+                gr.M = static_cast<int32_t>(rows_per_b);
+                gr.N = static_cast<int32_t>(cout);
+                gr.K = static_cast<int32_t>(cin * K);
+                gr.ldd = static_cast<int32_t>(rows_per_b);
+                gr.zero_to = 0;
+                gr.d_off = b * cout * rows_per_b;
+                g->groups.push_back(gr);
+            }
+            g->finalize();
+            slot = std::move(g);
+        }
+        gp = slot.get();
+    }
+    float* S = reinterpret_cast<float*>(base + w.s_off);
+    if (direct) {
+        dim3 grid(static_cast<unsigned>(hout), static_cast<unsigned>(cin), static_cast<unsigned>(B));
+        require(cin <= 65535 && B <= 65535, "disco: too many channels for the gather grid");
+        ProfScope prof("disco_gather", st);
+        disco_gather_kernel<<<grid, 256, 0, st>>>(x, d_row_ptr.p, d_h_in.p, d_w_rel.p, d_vals.p, hin,
+                                                  win, hout, wout, stride, K, cin, w.ldS, S);
+        SPH_LAUNCH_CHECK();
+        count_launch();
+        gemm_run(*gp, S, y, prec, st, whi, wlo);
+        return;
+    }
+    float2* U = reinterpret_cast<float2*>(base + w.u_off);
+    float* Yh = reinterpret_cast<float*>(base + w.y_off);
+    fft_forward_cminor(fft_in, x, B, cin, hin, static_cast<int>(nbi), U, st);
+    dim3 grid(static_cast<unsigned>((nbo + 3) / 4), static_cast<unsigned>(hout), static_cast<unsigned>(B));
+    require(hout <= 65535 && B <= 65535, "disco: grid too large");
+    ProfScope prof("disco_band", st);
+    disco_band_kernel<<<grid, 256, 0, st>>>(U, d_psi_hat.p, d_band0.p, d_bandc.p, d_psi_off.p, hin,
+                                            nbi, hout, nbo, static_cast<int>(win),
+                                            static_cast<int>(wout), static_cast<int>(stride), K,
+                                            cin, w.ldS, S);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+    gemm_run(*gp, S, Yh, prec, st, whi, wlo);
+    fft_inverse_plain(fft_out, reinterpret_cast<const float2*>(Yh), B * cout * hout,
+                      static_cast<int>(nbo), static_cast<float>(1.0 / static_cast<double>(win)), y,
+                      st);
+}
+
+}  // namespace sph

@@ -1,0 +1,72 @@
+// DISCO convolution plan (convolution.hpp:141-220) + spectral convolution
+// (convolution.hpp:286-304) + block epilogue (model.hpp:355-368).
+#pragma once
+
+#include <vector>
+
+#include "fft.cuh"
+#include "gemm.cuh"
+#include "sht.cuh"
+
+namespace sph {
+
+// Morlet / isotropic filter basis (convolution.hpp:30-81)
+struct Basis {
+    double cutoff = 0;
+    std::vector<std::pair<int, int>> pairs;
+    int n_real() const;
+    double eval_real(int k, double theta, double phi) const;
+};
+Basis make_basis(int kind, double cutoff);
+
+struct DiscoPlan {
+    int device = 0;
+    int in_kind = 0, out_kind = 0;
+    int64_t hin = 0, win = 0, hout = 0, wout = 0;
+    int K = 0;
+    int64_t stride = 1, nnz = 0;
+    std::vector<double> in_colat, in_w, out_colat, out_w;
+    // assembled operator, reference entry order: row h holds entries
+    // [row_ptr[h], row_ptr[h+1]); vals[e*K + k] = b_k * w_in (fp64 on host)
+    std::vector<int64_t> row_ptr;
+    std::vector<int32_t> h_in, w_rel;
+    std::vector<double> vals;
+    // device: direct-gather anchor tables
+    DevBuf<int64_t> d_row_ptr;
+    DevBuf<int32_t> d_h_in, d_w_rel;
+    DevBuf<float> d_vals;
+    // device: longitude-Fourier tables.  band of input rows per output row,
+    // psi_hat[(psi_off[h] + bi) * nbi + m][k] complex = sum_e psi_k[e] e^{-2 pi i w_rel m / win}
+    std::vector<int32_t> band0, bandc;
+    std::vector<int64_t> psi_off;
+    DevBuf<int32_t> d_band0, d_bandc;
+    DevBuf<int64_t> d_psi_off;
+    DevBuf<float2> d_psi_hat;
+    int64_t nbi = 0, nbo = 0;  // win/2+1, wout/2+1
+    FftPlan fft_in, fft_out;
+    int prec = SPH_PREC_3XTF32;
+
+    std::mutex mu;
+    std::map<std::tuple<int64_t, int64_t, int64_t, int>, std::unique_ptr<GroupedGemm>> gemm_cache;
+    DevBuf<uint8_t> own_ws;
+
+    void create(int in_kind, int64_t in_nlat, int64_t in_nlon, int out_kind, int64_t out_nlat,
+                int64_t out_nlon, int basis, double cutoff, int flags);
+    int64_t workspace_bytes(int64_t B, int64_t cin, int64_t cout) const;
+    void apply(const float* x, const float* mix, int64_t B, int64_t cin, int64_t cout, float* y,
+               void* ws, cudaStream_t st);
+};
+
+void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, int64_t cin,
+                   int64_t cout, int64_t klmax, float* y, void* ws, cudaStream_t st);
+int64_t spectral_conv_ws_bytes(const ShtPlan& p, int64_t B, int64_t cin, int64_t cout);
+
+void block_epilogue(const float* conv, const float* x, const float* w1, const float* b1,
+                    const float* w2, const float* b2, const float* scales, int64_t B, int64_t C,
+                    int64_t H, int64_t npts, float* y, cudaStream_t st);
+
+// fp32 -> tf32 hi/lo split of a device matrix [rows][cols] into [rows][ld] (zero padded)
+void split_rows(const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
+                cudaStream_t st);
+
+}  // namespace sph

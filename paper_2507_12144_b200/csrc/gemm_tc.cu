@@ -1,0 +1,483 @@
+// tcgen05 / TMEM / TMA grouped GEMM for sm_100a with a 3xTF32 precision split.
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0        TMA producer: A_hi tile (data), B_hi and B_lo tiles (table) per stage
+//   warp 1        MMA issuer (one elected thread): per K=8 step
+//                   D += A_hi*B_hi ; D += A_hi*B_lo ; D += A_lo*B_hi   (kind::tf32)
+//   warp 2        TMEM allocator
+//   warps 4..7    converter: A (fp32 as landed by TMA) -> A_hi = rna_tf32(A) in place,
+//                 A_lo = A - A_hi into its own SMEM buffer (elementwise, so the 128B
+//                 swizzle is irrelevant), fence.proxy.async, arrive
+//   warps 8..11   epilogue: TMEM -> registers (tcgen05.ld 32x32b) -> global
+// Pipelines: SMEM ring (full -> converted -> empty) and a double-buffered TMEM
+// accumulator (full/empty) so the epilogue of tile i overlaps the MMAs of tile i+1.
+// Operand tiles are K-major, SWIZZLE_128B (32 fp32 of K per 128-byte row, 8-row /
+// 1024-byte atoms, SBO = 1024).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "gemm.cuh"
+
+namespace sph {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 32;               // fp32 elements per 128-byte swizzle row
+constexpr int NUM_THREADS = 384;     // 12 warps
+constexpr int A_TILE_BYTES = BM * BK * 4;  // 16 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns per lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B, version 1.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);          // start address
+    d |= static_cast<uint64_t>(1) << 16;                          // LBO (unused for SW128 K-major)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;                  // SBO: 8-row group stride
+    d |= static_cast<uint64_t>(1) << 46;                          // descriptor version (sm100)
+    d |= static_cast<uint64_t>(2) << 61;                          // SWIZZLE_128B
+    return d;
+}
+// Instruction descriptor: kind::tf32, D f32, A/B tf32, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t make_idesc(int n) {
+    uint32_t d = 0;
+    d |= 1u << 4;                             // D format f32
+    d |= 2u << 7;                             // A format tf32
+    d |= 2u << 10;                            // B format tf32
+    d |= static_cast<uint32_t>(n >> 3) << 17; // N >> 3
+    d |= static_cast<uint32_t>(BM >> 4) << 24;// M >> 4
+    return d;
+}
+
+template <int BN, int STAGES>
+struct Smem {
+    static constexpr int B_TILE_BYTES = BN * BK * 4;
+    static constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    // full[S], conv[S], empty[S], tfull[2], tempty[2], tmem slot
+    static constexpr int TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_bhi,
+                   const __grid_constant__ CUtensorMap map_blo, const GemmGroup* __restrict__ groups,
+                   const GemmTile* __restrict__ tiles, int ntiles, float* __restrict__ D,
+                   int store_mode, int three_pass) {
+    using L = Smem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const uint32_t sbase = smem_u32(smem);
+    auto a_hi = [&](int s) { return sbase + s * L::STAGE_BYTES; };
+    auto a_lo = [&](int s) { return sbase + s * L::STAGE_BYTES + A_TILE_BYTES; };
+    auto b_hi = [&](int s) { return sbase + s * L::STAGE_BYTES + 2 * A_TILE_BYTES; };
+    auto b_lo = [&](int s) {
+        return sbase + s * L::STAGE_BYTES + 2 * A_TILE_BYTES + L::B_TILE_BYTES;
+    };
+    const uint32_t bars = sbase + L::BAR_OFF;
+    auto full_bar = [&](int s) { return bars + 8 * s; };
+    auto conv_bar = [&](int s) { return bars + 8 * (STAGES + s); };
+    auto empty_bar = [&](int s) { return bars + 8 * (2 * STAGES + s); };
+    auto tfull_bar = [&](int a) { return bars + 8 * (3 * STAGES + a); };
+    auto tempty_bar = [&](int a) { return bars + 8 * (3 * STAGES + 2 + a); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::BAR_OFF + (3 * STAGES + 4) * 8);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(conv_bar(s), 128);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar(a), 1);
+            mbar_init(tempty_bar(a), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(2 * BN)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------- producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const GemmTile tl = tiles[t];
+                const GemmGroup g = groups[tl.group];
+                const int nkb = (g.K + BK - 1) / BK;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(empty_bar(s), ph ^ 1);
+                    mbar_expect_tx(full_bar(s), A_TILE_BYTES + (three_pass ? 2 : 1) * L::B_TILE_BYTES);
+                    tma_load_2d(a_hi(s), &map_a, kb * BK, g.a_row0 + tl.m0, full_bar(s));
+                    tma_load_2d(b_hi(s), &map_bhi, kb * BK, g.b_row0 + tl.n0, full_bar(s));
+                    if (three_pass)
+                        tma_load_2d(b_lo(s), &map_blo, kb * BK, g.b_row0 + tl.n0, full_bar(s));
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            int lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+                const GemmTile tl = tiles[t];
+                const GemmGroup g = groups[tl.group];
+                const int nkb = (g.K + BK - 1) / BK;
+                const int acc = lt & 1;
+                const uint32_t aph = (lt >> 1) & 1;
+                int nrem = g.N - tl.n0;
+                if (nrem > BN) nrem = BN;
+                const int ninst = (nrem + 15) / 16 * 16;
+                const uint32_t idesc = make_idesc(ninst);
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                mbar_wait(tempty_bar(acc), aph ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(conv_bar(s), ph);
+                    tc_fence_after();
+                    const int ksteps = min(BK / 8, (g.K - kb * BK + 7) / 8);
+                    for (int kk = 0; kk < ksteps; ++kk) {
+                        const uint64_t ahi = make_sdesc(a_hi(s) + kk * 32);
+                        const uint64_t bhi = make_sdesc(b_hi(s) + kk * 32);
+                        tc_mma_tf32(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
+                        if (three_pass) {
+                            const uint64_t alo = make_sdesc(a_lo(s) + kk * 32);
+                            const uint64_t blo = make_sdesc(b_lo(s) + kk * 32);
+                            tc_mma_tf32(tmem_d, ahi, blo, idesc, 1u);
+                            tc_mma_tf32(tmem_d, alo, bhi, idesc, 1u);
+                        }
+                    }
+                    tc_commit(empty_bar(s));
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                }
+                tc_commit(tfull_bar(acc));
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ----------------------------------------------------------- converter
+        const int ct = threadIdx.x - 128;
+        int s = 0;
+        uint32_t ph = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const GemmTile tl = tiles[t];
+            const GemmGroup g = groups[tl.group];
+            const int nkb = (g.K + BK - 1) / BK;
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(full_bar(s), ph);
+                if (three_pass) {
+                    float4* hi = reinterpret_cast<float4*>(smem + (a_hi(s) - sbase));
+                    float4* lo = reinterpret_cast<float4*>(smem + (a_lo(s) - sbase));
+#pragma unroll
+                    for (int i = 0; i < A_TILE_BYTES / 16 / 128; ++i) {
+                        const int idx = ct + i * 128;
+                        float4 v = hi[idx];
+                        float4 h, l;
+                        uint32_t u;
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v.x)); h.x = __uint_as_float(u);
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v.y)); h.y = __uint_as_float(u);
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v.z)); h.z = __uint_as_float(u);
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v.w)); h.w = __uint_as_float(u);
+                        l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+                        hi[idx] = h;
+                        lo[idx] = l;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
+                mbar_arrive(conv_bar(s));
+                if (++s == STAGES) { s = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp >= 8) {
+        // ------------------------------------------------------------- epilogue
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        int lt = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+            const GemmTile tl = tiles[t];
+            const GemmGroup g = groups[tl.group];
+            const int acc = lt & 1;
+            const uint32_t aph = (lt >> 1) & 1;
+            int nrem = g.N - tl.n0;
+            if (nrem > BN) nrem = BN;
+            mbar_wait(tfull_bar(acc), aph);
+            tc_fence_after();
+            const int m = tl.m0 + q * 32 + lane;
+            const bool mok = m < g.M;
+            const uint32_t trow = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+            float* dbase = D + g.d_off;
+            for (int c = 0; c < nrem; c += 16) {
+                float v[16];
+                tmem_ld16(trow + c, v);
+                const int n = tl.n0 + c;
+                if (store_mode == STORE_ROW) {
+                    if (mok) {
+                        float* dp = dbase + static_cast<int64_t>(m) * g.ldd + n;
+                        if (c + 16 <= nrem && (reinterpret_cast<uintptr_t>(dp) & 15) == 0) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                *reinterpret_cast<float4*>(dp + j) =
+                                    make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (c + j < nrem) dp[j] = v[j];
+                        }
+                        if (c + 16 >= nrem && tl.n0 + nrem == g.N)
+                            for (int z = g.N; z < g.zero_to; ++z)
+                                dbase[static_cast<int64_t>(m) * g.ldd + z] = 0.f;
+                    }
+                } else {
+                    if (mok) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (c + j < nrem)
+                                dbase[static_cast<int64_t>(n + j) * g.ldd + m] = v[j];
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty_bar(acc));
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(2 * BN)
+                     : "memory");
+    }
+}
+
+// ------------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) fail(SPH_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+static CUtensorMap make_map(const Mat2D& m, int box_rows) {
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    require(m.ld * 4 % 16 == 0, "gemm: operand row stride must be a multiple of 16 bytes");
+    require((reinterpret_cast<uintptr_t>(m.p) & 15) == 0, "gemm: operand must be 16B aligned");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(m.cols), static_cast<cuuint64_t>(m.rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(m.ld * 4)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(m.p), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SPH_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return map;
+}
+
+template <int BN, int STAGES>
+static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
+                   float* D, bool three, cudaStream_t st) {
+    using L = Smem<BN, STAGES>;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(gemm_tf32x3_kernel<BN, STAGES>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    });
+    Mat2D am = g.A;
+    am.p = A;
+    const CUtensorMap ma = make_map(am, BM);
+    Mat2D bh = g.Bhi, bl = g.Blo;
+    bh.p = Bhi;
+    bl.p = Blo;
+    const CUtensorMap mbh = make_map(bh, BN);
+    const CUtensorMap mbl = make_map(three ? bl : bh, BN);
+    const int grid = static_cast<int>(std::min<int64_t>(g.ntiles, num_sms()));
+    ProfScope prof(g.name, st, g.flops);
+    gemm_tf32x3_kernel<BN, STAGES><<<grid, NUM_THREADS, L::TOTAL, st>>>(
+        ma, mbh, mbl, g.d_groups.p, g.d_tiles.p, static_cast<int>(g.ntiles), D, g.store,
+        three ? 1 : 0);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace tc
+
+void gemm_run_simt(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
+                   float* D, cudaStream_t st);
+void build_simt_tiles(GroupedGemm& g);                                  // gemm_simt.cu
+
+void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStream_t st,
+              const float* Bhi, const float* Blo) {
+    if (g.ntiles == 0) return;
+    if (!Bhi) Bhi = g.Bhi.p;
+    if (!Blo) Blo = g.Blo.p;
+    if (prec == SPH_PREC_FP32_SIMT) {
+        gemm_run_simt(g, A, Bhi, Blo, D, st);
+        return;
+    }
+    const bool three = prec == SPH_PREC_3XTF32;
+    require(!three || Blo, "gemm: 3xTF32 needs the lo table");
+    if (g.bn == 256)
+        tc::launch<256, 2>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 128)
+        tc::launch<128, 3>(g, A, Bhi, Blo, D, three, st);
+    else
+        fail(SPH_ERR_INVALID_ARGUMENT, "gemm: unsupported N tile");
+}
+
+void GroupedGemm::finalize() {
+    std::vector<GemmTile> t;
+    std::vector<double> cost;
+    flops = 0;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const GemmGroup& gr = groups[gi];
+        if (gr.M <= 0 || gr.N <= 0 || gr.K <= 0) continue;
+        flops += 2.0 * gr.M * static_cast<double>(gr.N) * gr.K;
+        for (int n0 = 0; n0 < gr.N; n0 += bn)
+            for (int m0 = 0; m0 < gr.M; m0 += tc::BM) {
+                t.push_back({static_cast<int32_t>(gi), m0, n0, 0});
+                cost.push_back(static_cast<double>(std::min(bn, gr.N - n0) + 16) *
+                               ((gr.K + 31) / 32));
+            }
+    }
+    // LPT order: most expensive tiles first, ties keep group-major order so
+    // concurrently running CTAs share the same table tile in L2.
+    std::vector<size_t> idx(t.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
+    std::vector<GemmTile> ts(t.size());
+    for (size_t i = 0; i < idx.size(); ++i) ts[i] = t[idx[i]];
+    ntiles = static_cast<int64_t>(ts.size());
+    d_groups.alloc(groups.size(), false);
+    d_tiles.alloc(std::max<size_t>(ts.size(), 1), false);
+    if (!groups.empty())
+        SPH_CUDA(cudaMemcpy(d_groups.p, groups.data(), groups.size() * sizeof(GemmGroup),
+                            cudaMemcpyHostToDevice));
+    if (!ts.empty())
+        SPH_CUDA(cudaMemcpy(d_tiles.p, ts.data(), ts.size() * sizeof(GemmTile),
+                            cudaMemcpyHostToDevice));
+    build_simt_tiles(*this);
+}
+
+static inline float rna_tf32(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return x;  // inf/nan untouched
+    u += 0x1000u;                                    // round to nearest (ties away)
+    u &= 0xffffe000u;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
+    for (size_t i = 0; i < n; ++i) {
+        const float h = rna_tf32(x[i]);
+        hi[i] = h;
+        lo[i] = x[i] - h;
+    }
+}
+
+}  // namespace sph

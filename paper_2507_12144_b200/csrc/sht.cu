@@ -1,0 +1,452 @@
+// Spherical harmonic transforms on sm_100a (see sht.cuh).
+//
+// Parity folding.  The reference grids are symmetric about the equator: Gaussian
+// nodes pair i <-> nlat-1-i, the reference equiangular grid pairs i <-> nlat-i (its
+// pole row theta = 0 has no mirror, grid.hpp:80-83).  With x_b = -x_a and
+// Phat_l^m(-x) = (-1)^(l+m) Phat_l^m(x), the contraction over latitude
+// (harmonics.hpp:147-154) splits per order m into two half-size contractions:
+//   uhat_lm = sum_r Pw_lm(x_r) E_r   (l-m even),   sum_r Pw_lm(x_r) O_r  (l-m odd)
+// with E_r = G_a + G_b, O_r = G_a - G_b, and the synthesis (harmonics.hpp:184-187)
+// returns Ev+Od on ring a and Ev-Od on ring b.  Unpaired rows enter both classes
+// with G_b = 0.  Each (m, parity) block is one group of the grouped GEMM.
+#include <algorithm>
+#include <cmath>
+#include <thread>
+
+#include "sht.cuh"
+
+namespace sph {
+
+void build_grid(int kind, int64_t nlat, int64_t nlon, std::vector<double>& colat,
+                std::vector<double>& w) {
+    const double pi = 3.14159265358979323846;
+    if (kind == SPH_EQUIANGULAR) {
+        require(nlat >= 2 && nlon >= 2, "build_equiangular: nlat and nlon must be >= 2");
+        colat.resize(nlat);
+        w.resize(nlat);
+        const double wfac = 2.0 * pi * pi / (static_cast<double>(nlat) * static_cast<double>(nlon));
+        for (int64_t i = 0; i < nlat; ++i) {
+            colat[i] = pi * static_cast<double>(i) / static_cast<double>(nlat);
+            w[i] = wfac * std::sin(colat[i]);
+        }
+        return;
+    }
+    require(kind == SPH_GAUSSIAN, "grid: unknown grid kind");
+    require(nlat >= 1 && nlon >= 2, "build_gaussian: need nlat >= 1 and nlon >= 2");
+    colat.resize(nlat);
+    w.resize(nlat);
+    const double dphi = 2.0 * pi / static_cast<double>(nlon);
+    auto pn_dpn = [](int64_t n, double x, double& pn, double& dpn) {
+        double p0 = 1.0, p1 = x;
+        if (n == 0) { pn = 1.0; dpn = 0.0; return; }
+        for (int64_t k = 2; k <= n; ++k) {
+            const double kk = static_cast<double>(k);
+            const double p2 = ((2.0 * kk - 1.0) * x * p1 - (kk - 1.0) * p0) / kk;
+            p0 = p1;
+            p1 = p2;
+        }
+        pn = p1;
+        dpn = static_cast<double>(n) * (x * p1 - p0) / (x * x - 1.0);
+    };
+    for (int64_t i = 0; i < nlat; ++i) {
+        double x = std::cos(pi * (static_cast<double>(i) + 0.75) / (static_cast<double>(nlat) + 0.5));
+        double pn = 0, dpn = 0;
+        bool ok = false;
+        for (int it = 0; it < 100; ++it) {
+            pn_dpn(nlat, x, pn, dpn);
+            const double dx = pn / dpn;
+            x -= dx;
+            if (std::abs(dx) <= 1e-15) { ok = true; break; }
+        }
+        if (!ok) fail(SPH_ERR_RUNTIME, "build_gaussian: Newton iteration failed at node " + std::to_string(i));
+        pn_dpn(nlat, x, pn, dpn);
+        colat[i] = std::acos(x);
+        w[i] = 2.0 / ((1.0 - x * x) * dpn * dpn) * dphi;
+    }
+}
+
+namespace {
+
+// Phat_l^m(x) for l in [m, lmax) by the reference recurrence (harmonics.hpp:68-100),
+// fp64.  fl[l] = sqrt((4l^2-1)/(l^2-m^2)) precomputed per m.
+void legendre_column(double x, int64_t m, int64_t lmax, const double* fl, double* out) {
+    const double four_pi = 4.0 * 3.14159265358979323846;
+    const double omx2 = (1.0 - x) * (1.0 + x);
+    double pmm = 1.0, fact = 1.0;
+    for (int64_t k = 1; k <= m; ++k) {
+        pmm *= omx2 * fact / (fact + 1.0);
+        fact += 2.0;
+    }
+    pmm = std::sqrt((2.0 * static_cast<double>(m) + 1.0) * pmm / four_pi);
+    if (m & 1) pmm = -pmm;
+    if (m < lmax) out[m] = pmm;
+    if (m + 1 < lmax) {
+        const double s3 = std::sqrt(2.0 * static_cast<double>(m) + 3.0);
+        const double pmmp1 = x * s3 * pmm;
+        out[m + 1] = pmmp1;
+        double oldfact = s3, pa = pmm, pb = pmmp1;
+        for (int64_t l = m + 2; l < lmax; ++l) {
+            const double f = fl[l];
+            const double pl = (x * pb - pa / oldfact) * f;
+            out[l] = pl;
+            oldfact = f;
+            pa = pb;
+            pb = pl;
+        }
+    }
+}
+
+template <class Fn>
+void parallel_for(int64_t n, Fn fn) {
+    int nt = static_cast<int>(std::min<int64_t>(n, std::max(1u, std::thread::hardware_concurrency())));
+    nt = std::min(nt, 32);
+    if (nt <= 1) {
+        for (int64_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (int64_t i = t; i < n; i += nt) fn(i);
+        });
+    for (auto& t : th) t.join();
+}
+
+template <class T>
+void upload(DevBuf<T>& d, const std::vector<T>& h) {
+    d.alloc(h.size(), false);
+    if (!h.empty()) SPH_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int64_t lmax,
+                                     int64_t m0, int64_t mcount, int64_t out_mcount, int Lp,
+                                     float2* __restrict__ dense) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= F * lmax * out_mcount) return;
+    const int64_t ml = i % out_mcount;
+    const int64_t l = (i / out_mcount) % lmax;
+    const int64_t f = i / (out_mcount * lmax);
+    float2 v = make_float2(0.f, 0.f);
+    const int64_t m = m0 + ml;
+    if (ml < mcount && l >= m) {
+        const int64_t p = (l - m) & 1, lp = (l - m) >> 1;
+        const int64_t row = (ml * 2 + p) * 2 * F + 2 * f;
+        v = make_float2(cint[row * Lp + lp], cint[(row + 1) * Lp + lp]);
+    }
+    dense[i] = v;
+}
+
+__global__ void dense_to_cint_kernel(const float2* __restrict__ dense, int64_t F, int64_t lmax,
+                                     int64_t mmax, int Lp, float* __restrict__ cint) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t twoF = 2 * F;
+    if (i >= mmax * 2 * twoF * Lp) return;
+    const int64_t lp = i % Lp;
+    const int64_t n = (i / Lp) % twoF;
+    const int64_t g = i / (Lp * twoF);
+    const int64_t m = g >> 1, p = g & 1;
+    const int64_t l = m + p + 2 * lp;
+    float v = 0.f;
+    if (l < lmax) {
+        const int64_t f = n >> 1;
+        const float2 c = dense[(f * lmax + l) * mmax + m];
+        v = (n & 1) ? c.y : c.x;
+    }
+    cint[i] = v;
+}
+
+// bins [F][nlat][mcount] complex (scaled by 2pi/nlon) -> EO_loc [mcount][2][2F][Rp]
+__global__ void fold_bins_kernel(const float2* __restrict__ bins, const int2* __restrict__ rows,
+                                 int R, int Rp, int64_t F, int64_t nlat, int64_t mcount,
+                                 float unscale, float* __restrict__ eo) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t twoF = 2 * F;
+    if (i >= mcount * 2 * twoF * R) return;
+    const int r = static_cast<int>(i % R);
+    const int64_t n = (i / R) % twoF;
+    const int64_t g = i / (static_cast<int64_t>(R) * twoF);
+    const int64_t ml = g >> 1;
+    const int p = static_cast<int>(g & 1);
+    const int64_t f = n >> 1;
+    const int2 rw = rows[r];
+    const float2 a = bins[(f * nlat + rw.x) * mcount + ml];
+    const float2 b = rw.y >= 0 ? bins[(f * nlat + rw.y) * mcount + ml] : make_float2(0.f, 0.f);
+    const float va = (n & 1) ? a.y : a.x, vb = (n & 1) ? b.y : b.x;
+    eo[(g * twoF + n) * Rp + r] = (p == 0 ? va + vb : va - vb) * unscale;
+}
+
+}  // namespace
+
+void cint_to_dense(const ShtPlan& p, const float* cint, int64_t F, int64_t m0, int64_t mcount,
+                   int64_t out_mcount, float* dense, cudaStream_t st) {
+    const int64_t n = F * p.lmax * out_mcount;
+    if (n == 0) return;
+    cint_to_dense_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+        cint, F, p.lmax, m0, mcount, out_mcount, p.Lp, reinterpret_cast<float2*>(dense));
+    SPH_LAUNCH_CHECK();
+    count_launch();
+}
+
+void dense_to_cint(const ShtPlan& p, const float* dense, int64_t F, float* cint, cudaStream_t st) {
+    const int64_t n = p.mmax * 2 * 2 * F * p.Lp;
+    if (n == 0) return;
+    dense_to_cint_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const float2*>(dense), F, p.lmax, p.mmax, p.Lp, cint);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+}
+
+void ShtPlan::create(int kind_, int64_t nlat_, int64_t nlon_, int64_t lmax_, int64_t mmax_,
+                     int flags_) {
+    SPH_CUDA(cudaGetDevice(&device));
+    kind = kind_;
+    nlat = nlat_;
+    nlon = nlon_;
+    lmax = lmax_;
+    mmax = mmax_;
+    flags = flags_;
+    prec = flags & SPH_FLAG_PREC_MASK;
+    require(prec <= SPH_PREC_FP32_SIMT, "sht plan: unknown precision mode");
+    require(lmax >= 1 && mmax >= 1, "sht plan: lmax and mmax must be >= 1");
+    require(mmax <= lmax, "SpectralCoeffs: mmax must be <= lmax");
+    require(nlat <= 65535 && nlon <= 65535 && lmax <= 16384, "sht plan: size out of range");
+    build_grid(kind, nlat, nlon, colat, w);
+    msynth = std::min<int64_t>(mmax, (nlon - 1) / 2 + 1);  // harmonics.hpp:179
+
+    // ---- fold rows
+    const double pi = 3.14159265358979323846;
+    std::vector<bool> used(nlat, false);
+    fold.rows.clear();
+    for (int64_t i = 0; i < nlat; ++i) {
+        if (used[i]) continue;
+        used[i] = true;
+        const double target = pi - colat[i];
+        auto it = std::lower_bound(colat.begin(), colat.end(), target - 1e-9);
+        int64_t j = -1;
+        for (; it != colat.end() && *it <= target + 1e-9; ++it) {
+            const int64_t c = it - colat.begin();
+            if (c != i && !used[c]) { j = c; break; }
+        }
+        if (j >= 0) used[j] = true;
+        fold.rows.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
+    }
+    R = fold.R = static_cast<int>(fold.rows.size());
+    Rp = static_cast<int>(round_up(R, 4));
+    upload(fold.d_rows, fold.rows);
+    Lmax_p = static_cast<int>(L(0, 0));
+    Lp = static_cast<int>(round_up(Lmax_p, 4));
+    fft.build(static_cast<int>(nlon));
+
+    // ---- Legendre tables (host fp64 -> fp32 hi/lo)
+    pf_off.assign(2 * mmax + 1, 0);
+    for (int64_t m = 0; m < mmax; ++m)
+        for (int p = 0; p < 2; ++p) pf_off[m * 2 + p + 1] = pf_off[m * 2 + p] + L(m, p);
+    pf_rows = pf_off[2 * mmax];
+    std::vector<float> pf(static_cast<size_t>(pf_rows) * Rp, 0.f);
+    std::vector<float> pit(static_cast<size_t>(mmax) * 2 * R * Lp, 0.f);
+    parallel_for(mmax, [&](int64_t m) {
+        std::vector<double> fl(lmax, 0.0), col(lmax, 0.0);
+        for (int64_t l = m + 2; l < lmax; ++l) {
+            const double ld = static_cast<double>(l), md = static_cast<double>(m);
+            fl[l] = std::sqrt((4.0 * ld * ld - 1.0) / (ld * ld - md * md));
+        }
+        for (int r = 0; r < R; ++r) {
+            const int ia = fold.rows[r].x;
+            const double x = std::cos(colat[ia]);
+            legendre_column(x, m, lmax, fl.data(), col.data());
+            for (int p = 0; p < 2; ++p) {
+                const int64_t Lmp = L(m, p);
+                for (int64_t lp = 0; lp < Lmp; ++lp) {
+                    const double v = col[m + p + 2 * lp];
+                    pf[(pf_off[m * 2 + p] + lp) * Rp + r] = static_cast<float>(v * w[ia]);
+                    pit[((m * 2 + p) * R + r) * static_cast<int64_t>(Lp) + lp] = static_cast<float>(v);
+                }
+            }
+        }
+    });
+    {
+        std::vector<float> hi(pf.size()), lo(pf.size());
+        tf32_split_host(pf.data(), pf.size(), hi.data(), lo.data());
+        upload(pf_hi, hi);
+        upload(pf_lo, lo);
+    }
+    {
+        std::vector<float> hi(pit.size()), lo(pit.size());
+        tf32_split_host(pit.data(), pit.size(), hi.data(), lo.data());
+        upload(pi_hi, hi);
+        upload(pi_lo, lo);
+    }
+}
+
+const GroupedGemm& ShtPlan::fwd_gemm(int64_t F) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = fwd_cache[F];
+    if (!slot) {
+        auto g = std::make_unique<GroupedGemm>();
+        g->A = {nullptr, mmax * 2 * 2 * F, R, Rp};
+        g->Bhi = {pf_hi.p, pf_rows, R, Rp};
+        g->Blo = {pf_lo.p, pf_rows, R, Rp};
+        g->store = STORE_ROW;
+        g->bn = 256;
+        g->name = "gemm_legendre_fwd";
+        for (int64_t m = 0; m < mmax; ++m)
+            for (int p = 0; p < 2; ++p) {
+                const int64_t Lmp = L(m, p);
+                if (Lmp == 0) continue;
+                GemmGroup gr;
+                gr.a_row0 = static_cast<int32_t>((m * 2 + p) * 2 * F);
+                gr.b_row0 = static_cast<int32_t>(pf_off[m * 2 + p]);
+                gr.M = static_cast<int32_t>(2 * F);
+                gr.N = static_cast<int32_t>(Lmp);
+                gr.K = R;
+                gr.ldd = Lp;
+                gr.zero_to = static_cast<int32_t>(std::min<int64_t>(Lp, round_up(Lmp, 8)));
+                gr.d_off = (m * 2 + p) * 2 * F * Lp;
+                g->groups.push_back(gr);
+            }
+        require(mmax * 2 * 2 * F < (1LL << 31), "sht: too many fields for one call");
+        g->finalize();
+        slot = std::move(g);
+    }
+    return *slot;
+}
+
+const GroupedGemm& ShtPlan::inv_gemm(int64_t F) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = inv_cache[F];
+    if (!slot) {
+        auto g = std::make_unique<GroupedGemm>();
+        g->A = {nullptr, mmax * 2 * 2 * F, Lmax_p, Lp};
+        g->Bhi = {pi_hi.p, mmax * 2 * R, Lmax_p, Lp};
+        g->Blo = {pi_lo.p, mmax * 2 * R, Lmax_p, Lp};
+        g->store = STORE_ROW;
+        g->bn = 256;
+        g->name = "gemm_legendre_inv";
+        for (int64_t m = 0; m < msynth; ++m)
+            for (int p = 0; p < 2; ++p) {
+                const int64_t Lmp = L(m, p);
+                if (Lmp == 0) continue;
+                GemmGroup gr;
+                gr.a_row0 = static_cast<int32_t>((m * 2 + p) * 2 * F);
+                gr.b_row0 = static_cast<int32_t>((m * 2 + p) * R);
+                gr.M = static_cast<int32_t>(2 * F);
+                gr.N = R;
+                gr.K = static_cast<int32_t>(Lmp);
+                gr.ldd = Rp;
+                gr.zero_to = 0;
+                gr.d_off = (m * 2 + p) * 2 * F * Rp;
+                g->groups.push_back(gr);
+            }
+        require(mmax * 2 * 2 * F < (1LL << 31), "sht: too many fields for one call");
+        g->finalize();
+        slot = std::move(g);
+    }
+    return *slot;
+}
+
+const GroupedGemm& ShtPlan::stage_gemm(int64_t F, int64_t m0, int64_t mcount) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = stage_cache[std::make_tuple(F, m0, mcount)];
+    if (!slot) {
+        auto g = std::make_unique<GroupedGemm>();
+        g->A = {nullptr, mcount * 2 * 2 * F, R, Rp};
+        g->Bhi = {pf_hi.p, pf_rows, R, Rp};
+        g->Blo = {pf_lo.p, pf_rows, R, Rp};
+        g->store = STORE_ROW;
+        g->bn = 256;
+        for (int64_t ml = 0; ml < mcount; ++ml)
+            for (int p = 0; p < 2; ++p) {
+                const int64_t m = m0 + ml;
+                const int64_t Lmp = L(m, p);
+                if (Lmp == 0) continue;
+                GemmGroup gr;
+                gr.a_row0 = static_cast<int32_t>((ml * 2 + p) * 2 * F);
+                gr.b_row0 = static_cast<int32_t>(pf_off[m * 2 + p]);
+                gr.M = static_cast<int32_t>(2 * F);
+                gr.N = static_cast<int32_t>(Lmp);
+                gr.K = R;
+                gr.ldd = Lp;
+                gr.zero_to = static_cast<int32_t>(std::min<int64_t>(Lp, round_up(Lmp, 8)));
+                gr.d_off = (ml * 2 + p) * 2 * F * Lp;
+                g->groups.push_back(gr);
+            }
+        g->finalize();
+        slot = std::move(g);
+    }
+    return *slot;
+}
+
+void* ShtPlan::workspace(void* ws, int64_t bytes) {
+    if (ws) return ws;
+    std::lock_guard<std::mutex> lk(mu);
+    if (own_ws.n < static_cast<size_t>(bytes)) own_ws.alloc(bytes, true);
+    return own_ws.p;
+}
+
+void ShtPlan::forward(const float* x, int64_t F, float* out, int layout, void* ws, cudaStream_t st) {
+    require(kind == SPH_GAUSSIAN || (flags & SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD),
+            "sht_forward: requires a gaussian grid");
+    require(nlat >= lmax && nlon >= 2 * mmax, "sht_forward: resolution insufficient for lmax/mmax");
+    require(layout == SPH_LAYOUT_DENSE_LM || layout == SPH_LAYOUT_INTERNAL, "sht_forward: bad layout");
+    require(F >= 0, "sht_forward: negative field count");
+    if (F == 0) return;
+    SPH_CUDA(cudaSetDevice(device));
+    uint8_t* w8 = static_cast<uint8_t*>(workspace(ws, workspace_bytes(F)));
+    float* eo = reinterpret_cast<float*>(w8);
+    float* ctmp = reinterpret_cast<float*>(w8 + round_up(4 * eo_elems(F), 256));
+    fft_forward_fold(fft, fold, x, F, static_cast<int>(nlat), static_cast<int>(mmax), eo, Rp, st);
+    float* target = layout == SPH_LAYOUT_INTERNAL ? out : ctmp;
+    gemm_run(fwd_gemm(F), eo, target, prec, st);
+    if (layout == SPH_LAYOUT_DENSE_LM) cint_to_dense(*this, target, F, 0, mmax, mmax, out, st);
+}
+
+void ShtPlan::inverse(const float* coeffs, int64_t F, int layout, float* y, void* ws,
+                      cudaStream_t st) {
+    require(layout == SPH_LAYOUT_DENSE_LM || layout == SPH_LAYOUT_INTERNAL, "sht_inverse: bad layout");
+    require(F >= 0, "sht_inverse: negative field count");
+    if (F == 0) return;
+    SPH_CUDA(cudaSetDevice(device));
+    uint8_t* w8 = static_cast<uint8_t*>(workspace(ws, workspace_bytes(F)));
+    float* eoi = reinterpret_cast<float*>(w8);
+    float* ctmp = reinterpret_cast<float*>(w8 + round_up(4 * eo_elems(F), 256));
+    const float* src = coeffs;
+    if (layout == SPH_LAYOUT_DENSE_LM) {
+        dense_to_cint(*this, coeffs, F, ctmp, st);
+        src = ctmp;
+    }
+    gemm_run(inv_gemm(F), src, eoi, prec, st);
+    fft_inverse_unfold(fft, fold, eoi, F, static_cast<int>(nlat), static_cast<int>(mmax),
+                       static_cast<int>(msynth), static_cast<int>(lmax), Rp, y, st);
+}
+
+void ShtPlan::fft_stage(const float* rings, int64_t F, int64_t h, float* bins, cudaStream_t st) {
+    require(nlon >= 2 * mmax, "dist_sht_forward: resolution insufficient for mmax");
+    SPH_CUDA(cudaSetDevice(device));
+    const double pi = 3.14159265358979323846;
+    fft_forward_plain(fft, rings, F * h, static_cast<int>(mmax),
+                      static_cast<float>(2.0 * pi / static_cast<double>(nlon)),
+                      reinterpret_cast<float2*>(bins), st);
+}
+
+void ShtPlan::legendre_stage(const float* bins, int64_t F, int64_t m0, int64_t mcount,
+                             float* coeffs, void* ws, cudaStream_t st) {
+    require(m0 >= 0 && mcount >= 0 && m0 + mcount <= mmax, "legendre stage: order range");
+    require(nlat >= lmax, "dist_sht_forward: resolution insufficient for lmax");
+    if (F == 0 || mcount == 0) return;
+    SPH_CUDA(cudaSetDevice(device));
+    uint8_t* w8 = static_cast<uint8_t*>(workspace(ws, stage_ws_bytes(F, mcount)));
+    float* eo = reinterpret_cast<float*>(w8);
+    float* cl = reinterpret_cast<float*>(w8 + round_up(4 * mcount * 2 * 2 * F * Rp, 256));
+    const int64_t n = mcount * 2 * 2 * F * R;
+    const double pi = 3.14159265358979323846;
+    fold_bins_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const float2*>(bins), fold.d_rows.p, R, Rp, F, nlat, mcount,
+        static_cast<float>(static_cast<double>(nlon) / (2.0 * pi)), eo);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+    gemm_run(stage_gemm(F, m0, mcount), eo, cl, prec, st);
+    cint_to_dense(*this, cl, F, m0, mcount, mcount, coeffs, st);
+}
+
+}  // namespace sph

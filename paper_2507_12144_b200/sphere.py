@@ -1,0 +1,452 @@
+"""Python mirror of the reference operator API (namespace ``sphere`` of spheretk).
+
+Same names, argument meaning and error behaviour as the reference
+(/root/reference/proj/include/sphere/*.hpp), computed by libsphgpu.so on the GPU:
+
+=====================================  ==============================================
+reference                              here
+=====================================  ==============================================
+build_equiangular / build_gaussian     same (grid.hpp:69 / :91), fp64 host arrays
+SphericalField [C][nlat][nlon]         ``SphericalField`` (data: fp32 CUDA tensor,
+                                       leading batch dims allowed: [..., C, nlat, nlon])
+SpectralCoeffs [C][lmax][mmax]         ``SpectralCoeffs`` (complex64 CUDA tensor)
+sht_forward (harmonics.hpp:126-169)    ``sht_forward`` -- Gaussian only, like the ref
+sht_inverse (harmonics.hpp:173-205)    ``sht_inverse``
+morlet_basis / isotropic_basis         same (convolution.hpp:73-81)
+assemble_disco (convolution.hpp:141)   ``assemble_disco`` -> DiscoOperator (device plan)
+disco_apply (convolution.hpp:181)      ``disco_apply``
+spectral_conv (convolution.hpp:286)    ``spectral_conv``
+block_apply (model.hpp:337)            ``block_apply``
+=====================================  ==============================================
+
+``std::invalid_argument`` surfaces as ``ValueError`` (``SphInvalidArgument``), other
+failures as ``RuntimeError``.  Tensors are torch CUDA tensors: torch is used for
+device memory and streams only; every operator runs in the library's own kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+from dataclasses import dataclass, field as dc_field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check
+
+PI = math.pi
+EQUIANGULAR = L.SPH_EQUIANGULAR
+GAUSSIAN = L.SPH_GAUSSIAN
+PRECISIONS = {"3xtf32": L.SPH_PREC_3XTF32, "tf32": L.SPH_PREC_TF32, "fp32": L.SPH_PREC_FP32_SIMT}
+
+
+# ------------------------------------------------------------------- grids
+@dataclass(frozen=True)
+class GridSpec:
+    """grid.hpp:25-43."""
+    kind: int
+    nlat: int
+    nlon: int
+    colatitudes: np.ndarray = dc_field(repr=False, compare=False)
+    longitudes: np.ndarray = dc_field(repr=False, compare=False)
+    quad_weights: np.ndarray = dc_field(repr=False, compare=False)
+
+    def same_sampling(self, o: "GridSpec") -> bool:
+        return self.kind == o.kind and self.nlat == o.nlat and self.nlon == o.nlon
+
+    def total_weight(self) -> float:
+        return float(self.quad_weights.sum() * self.nlon)
+
+
+def _grid(kind: int, nlat: int, nlon: int) -> GridSpec:
+    c = np.zeros(max(nlat, 1))
+    w = np.zeros(max(nlat, 1))
+    check(L.lib.sph_grid(kind, nlat, nlon, c.ctypes.data_as(C.POINTER(C.c_double)),
+                         w.ctypes.data_as(C.POINTER(C.c_double))))
+    lon = 2.0 * PI * np.arange(nlon, dtype=np.float64) / nlon
+    return GridSpec(kind, nlat, nlon, c[:nlat], lon, w[:nlat])
+
+
+def build_equiangular(nlat: int, nlon: int) -> GridSpec:
+    """grid.hpp:69-87: theta_i = pi i / nlat (north-pole row included)."""
+    return _grid(EQUIANGULAR, nlat, nlon)
+
+
+def build_gaussian(nlat: int, nlon: int) -> GridSpec:
+    """grid.hpp:91-128: Gauss-Legendre nodes in cos(theta)."""
+    return _grid(GAUSSIAN, nlat, nlon)
+
+
+def default_mmax(lmax: int, nlon: int) -> int:
+    """harmonics.hpp:120-122."""
+    return min(lmax, nlon // 2 + 1)
+
+
+# ------------------------------------------------------------------ fields
+@dataclass
+class SphericalField:
+    """field.hpp:15-35; data [..., channels, nlat, nlon] fp32 on a CUDA device."""
+    grid: GridSpec
+    data: torch.Tensor
+
+    @property
+    def channels(self) -> int:
+        return int(self.data.shape[-3])
+
+    def npoints(self) -> int:
+        return self.grid.nlat * self.grid.nlon
+
+
+@dataclass
+class SpectralCoeffs:
+    """harmonics.hpp:24-42; coeffs [..., channels, lmax, mmax] complex64."""
+    lmax: int
+    mmax: int
+    coeffs: torch.Tensor
+
+    @property
+    def channels(self) -> int:
+        return int(self.coeffs.shape[-3])
+
+
+def require_same_sampling(f: SphericalField, g: GridSpec, where: str) -> None:
+    """field.hpp:37-43."""
+    if not f.grid.same_sampling(g):
+        raise L.SphInvalidArgument(1, f"{where}: grid/field shape mismatch")
+    if tuple(f.data.shape[-2:]) != (g.nlat, g.nlon):
+        raise L.SphInvalidArgument(1, f"{where}: field storage inconsistent")
+
+
+def _stream(dev: torch.device) -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _dev_f32(t: torch.Tensor, what: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise L.SphInvalidArgument(1, f"{what}: tensor must live on a CUDA device")
+    return t.to(torch.float32).contiguous()
+
+
+# -------------------------------------------------------------------- plans
+_plan_lock = threading.Lock()
+_sht_plans: dict = {}
+_disco_plans: dict = {}
+
+
+class ShtPlan:
+    """One-time host precompute + device tables for (grid, lmax, mmax): replaces the
+    per-call table builds of harmonics.hpp:159-162 / :202-205."""
+
+    def __init__(self, grid: GridSpec, lmax: int, mmax: int, precision: str = "3xtf32",
+                 allow_equiangular_forward: bool = False, device=None):
+        self.grid, self.lmax, self.mmax = grid, int(lmax), int(mmax)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        flags = PRECISIONS[precision] | (L.SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD
+                                         if allow_equiangular_forward else 0)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            check(L.lib.sph_sht_plan_create(grid.kind, grid.nlat, grid.nlon, self.lmax,
+                                            self.mmax, flags, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and L is not None and L.lib is not None:
+            L.lib.sph_sht_plan_destroy(h)
+            self.h = None
+
+    # sizes
+    def coeffs_elems(self, F: int, layout: int) -> int:
+        return int(L.lib.sph_sht_coeffs_elems(self.h, F, layout))
+
+    def workspace(self, F: int) -> torch.Tensor:
+        n = int(L.lib.sph_sht_workspace_bytes(self.h, F))
+        return torch.empty(n, dtype=torch.uint8, device=self.device)
+
+    # raw tensor entry points: x [F, nlat, nlon] -> coeffs
+    def forward(self, x: torch.Tensor, layout: int = L.SPH_LAYOUT_DENSE_LM, out=None, ws=None):
+        g = self.grid
+        x = _dev_f32(x, "sht_forward")
+        F = x.numel() // (g.nlat * g.nlon)
+        if out is None:
+            if layout == L.SPH_LAYOUT_DENSE_LM:
+                out = torch.empty((F, self.lmax, self.mmax, 2), dtype=torch.float32, device=x.device)
+            else:
+                out = torch.empty(self.coeffs_elems(F, layout), dtype=torch.float32, device=x.device)
+        ws = self.workspace(F) if ws is None else ws
+        check(L.lib.sph_sht_forward(self.h, _ptr(x), F, _ptr(out), layout, _ptr(ws),
+                                    _stream(x.device)))
+        return out
+
+    def inverse(self, coeffs: torch.Tensor, F: int, layout: int = L.SPH_LAYOUT_DENSE_LM,
+                out=None, ws=None):
+        g = self.grid
+        if coeffs.dtype == torch.complex64:
+            coeffs = torch.view_as_real(coeffs.contiguous())
+        coeffs = _dev_f32(coeffs, "sht_inverse")
+        if out is None:
+            out = torch.empty((F, g.nlat, g.nlon), dtype=torch.float32, device=coeffs.device)
+        ws = self.workspace(F) if ws is None else ws
+        check(L.lib.sph_sht_inverse(self.h, _ptr(coeffs), F, layout, _ptr(out), _ptr(ws),
+                                    _stream(coeffs.device)))
+        return out
+
+    def roundtrip_host(self, x_host: torch.Tensor, y_host: torch.Tensor, chunk: int = 32):
+        """sht_inverse(sht_forward(x)) for host buffers, H2D/compute/D2H pipelined."""
+        F = x_host.numel() // (self.grid.nlat * self.grid.nlon)
+        with torch.cuda.device(self.device):
+            check(L.lib.sph_sht_roundtrip_host(self.h, _ptr(x_host), F, _ptr(y_host), chunk))
+
+    # distributed stages (distsim.hpp:413-430, :437-459)
+    def fft_stage(self, rings: torch.Tensor, F: int, h_count: int, out=None):
+        if out is None:
+            out = torch.empty((F, h_count, self.mmax, 2), dtype=torch.float32, device=rings.device)
+        check(L.lib.sph_sht_fft_stage(self.h, _ptr(rings), F, h_count, _ptr(out),
+                                      _stream(rings.device)))
+        return out
+
+    def legendre_stage(self, bins: torch.Tensor, F: int, m0: int, m_count: int, out=None):
+        if out is None:
+            out = torch.empty((F, self.lmax, m_count, 2), dtype=torch.float32, device=bins.device)
+        n = int(L.lib.sph_sht_stage_workspace_bytes(self.h, F, m_count))
+        ws = torch.empty(n, dtype=torch.uint8, device=bins.device)
+        check(L.lib.sph_sht_legendre_stage(self.h, _ptr(bins), F, m0, m_count, _ptr(out),
+                                           _ptr(ws), _stream(bins.device)))
+        return out
+
+
+def get_sht_plan(grid: GridSpec, lmax: int, mmax: int, precision: str = "3xtf32",
+                 allow_equiangular_forward: bool = False) -> ShtPlan:
+    dev = torch.cuda.current_device()
+    key = (grid.kind, grid.nlat, grid.nlon, lmax, mmax, precision, allow_equiangular_forward, dev)
+    with _plan_lock:
+        p = _sht_plans.get(key)
+        if p is None:
+            p = ShtPlan(grid, lmax, mmax, precision, allow_equiangular_forward)
+            _sht_plans[key] = p
+        return p
+
+
+# --------------------------------------------------------------------- SHT
+def sht_forward(field: SphericalField, lmax: Optional[int] = None, mmax: Optional[int] = None,
+                precision: str = "3xtf32") -> SpectralCoeffs:
+    """harmonics.hpp:126-169.  Gaussian grids only: the reference throws
+    std::invalid_argument on equiangular grids (harmonics.hpp:129-130); its equiangular
+    forward path is dist_sht_forward (see paper_2507_12144_b200.dist)."""
+    g = field.grid
+    if lmax is None:  # harmonics.hpp:164-169
+        lmax = g.nlat
+        mmax = max(min(default_mmax(lmax, g.nlon), g.nlon // 2), 1)
+    elif mmax is None:
+        raise L.SphInvalidArgument(1, "sht_forward: give both lmax and mmax")
+    if g.kind != GAUSSIAN:
+        raise L.SphInvalidArgument(1, "sht_forward: requires a gaussian grid")
+    if g.nlat < lmax or g.nlon < 2 * mmax:
+        raise L.SphInvalidArgument(1, "sht_forward: resolution insufficient for lmax/mmax")
+    if mmax > lmax:
+        raise L.SphInvalidArgument(1, "SpectralCoeffs: mmax must be <= lmax")
+    return _forward(field, lmax, mmax, precision, allow_eq=False)
+
+
+def _forward(field: SphericalField, lmax: int, mmax: int, precision: str,
+             allow_eq: bool) -> SpectralCoeffs:
+    g = field.grid
+    lead = tuple(field.data.shape[:-2])
+    plan = get_sht_plan(g, lmax, mmax, precision, allow_eq)
+    with torch.cuda.device(field.data.device):
+        out = plan.forward(field.data)
+    return SpectralCoeffs(lmax, mmax, torch.view_as_complex(out).reshape(*lead, lmax, mmax))
+
+
+def sht_inverse(coeffs: SpectralCoeffs, grid: GridSpec,
+                precision: str = "3xtf32") -> SphericalField:
+    """harmonics.hpp:173-205 (any grid kind)."""
+    if coeffs.mmax > coeffs.lmax:
+        raise L.SphInvalidArgument(1, "SpectralCoeffs: mmax must be <= lmax")
+    c = coeffs.coeffs
+    lead = tuple(c.shape[:-2])
+    F = int(np.prod(lead)) if lead else 1
+    plan = get_sht_plan(grid, coeffs.lmax, coeffs.mmax, precision)
+    with torch.cuda.device(c.device):
+        y = plan.inverse(c.to(torch.complex64), F)
+    return SphericalField(grid, y.reshape(*lead, grid.nlat, grid.nlon))
+
+
+# ------------------------------------------------------------------- DISCO
+@dataclass(frozen=True)
+class FilterBasis:
+    """convolution.hpp:30-69."""
+    theta_cutoff: float
+    indices: tuple
+    kind: int
+
+    def n_pairs(self) -> int:
+        return len(self.indices)
+
+    def n_real(self) -> int:
+        return sum(1 if p == (0, 0) else 2 for p in self.indices)
+
+
+def morlet_basis(theta_cutoff: float) -> FilterBasis:
+    """convolution.hpp:73-76 (K = 9)."""
+    if theta_cutoff <= 0.0:
+        raise L.SphInvalidArgument(1, "morlet_basis: cutoff must be > 0")
+    return FilterBasis(float(theta_cutoff), ((0, 0), (0, 1), (0, 2), (2, 1), (2, 2)),
+                       L.SPH_BASIS_MORLET)
+
+
+def isotropic_basis(theta_cutoff: float) -> FilterBasis:
+    """convolution.hpp:78-81 (K = 1)."""
+    if theta_cutoff <= 0.0:
+        raise L.SphInvalidArgument(1, "isotropic_basis: cutoff must be > 0")
+    return FilterBasis(float(theta_cutoff), ((0, 0),), L.SPH_BASIS_ISOTROPIC)
+
+
+class DiscoOperator:
+    """convolution.hpp:105-123: the assembled operator lives on the device."""
+
+    def __init__(self, in_grid: GridSpec, out_grid: GridSpec, basis: FilterBasis,
+                 precision: str = "3xtf32"):
+        self.in_grid, self.out_grid, self.basis = in_grid, out_grid, basis
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        h = C.c_void_p()
+        check(L.lib.sph_disco_plan_create(in_grid.kind, in_grid.nlat, in_grid.nlon,
+                                          out_grid.kind, out_grid.nlat, out_grid.nlon,
+                                          basis.kind, basis.theta_cutoff, PRECISIONS[precision],
+                                          C.byref(h)))
+        self.h = h
+        k, s, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        check(L.lib.sph_disco_plan_info(h, C.byref(k), C.byref(s), C.byref(nnz)))
+        self.n_basis, self.stride, self.nnz_per_basis = k.value, s.value, nnz.value
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and L is not None and L.lib is not None:
+            L.lib.sph_disco_plan_destroy(h)
+            self.h = None
+
+    def workspace(self, B: int, cin: int, cout: int) -> torch.Tensor:
+        n = int(L.lib.sph_disco_workspace_bytes(self.h, B, cin, cout))
+        return torch.empty(n, dtype=torch.uint8, device=self.device)
+
+    def apply(self, x: torch.Tensor, mix: torch.Tensor, out=None, ws=None) -> torch.Tensor:
+        """x [B, cin, hin, win] -> y [B, cout, hout, wout]."""
+        mix = _dev_f32(mix, "disco_apply")
+        x = _dev_f32(x, "disco_apply")
+        cout, cin, K = mix.shape
+        if K != self.n_basis or x.shape[-3] != cin:
+            raise L.SphInvalidArgument(1, "disco_apply: mix tensor shape mismatch")
+        B = x.numel() // (cin * self.in_grid.nlat * self.in_grid.nlon)
+        if out is None:
+            out = torch.empty((B, cout, self.out_grid.nlat, self.out_grid.nlon),
+                              dtype=torch.float32, device=x.device)
+        ws = self.workspace(B, cin, cout) if ws is None else ws
+        check(L.lib.sph_disco_apply(self.h, _ptr(x), _ptr(mix), B, cin, cout, _ptr(out),
+                                    _ptr(ws), _stream(x.device)))
+        return out
+
+
+def assemble_disco(in_grid: GridSpec, out_grid: GridSpec, basis: FilterBasis,
+                   precision: str = "3xtf32") -> DiscoOperator:
+    """convolution.hpp:141-177."""
+    key = (in_grid.kind, in_grid.nlat, in_grid.nlon, out_grid.kind, out_grid.nlat,
+           out_grid.nlon, basis, precision, torch.cuda.current_device())
+    with _plan_lock:
+        op = _disco_plans.get(key)
+    if op is None:
+        op = DiscoOperator(in_grid, out_grid, basis, precision)
+        with _plan_lock:
+            _disco_plans[key] = op
+    return op
+
+
+def disco_apply(op: DiscoOperator, field: SphericalField, mix: torch.Tensor) -> SphericalField:
+    """convolution.hpp:181-220: y[o] = sum_{c,k} mix[o,c,k] (psi_k * u_c)."""
+    require_same_sampling(field, op.in_grid, "disco_apply")
+    if mix.shape[1] != field.channels or mix.shape[2] != op.n_basis:
+        raise L.SphInvalidArgument(1, "disco_apply: mix tensor shape mismatch")
+    lead = tuple(field.data.shape[:-3])
+    with torch.cuda.device(field.data.device):
+        y = op.apply(field.data, mix)
+    return SphericalField(op.out_grid, y.reshape(*lead, mix.shape[0], op.out_grid.nlat,
+                                                  op.out_grid.nlon))
+
+
+# ----------------------------------------------------------- spectral conv
+def spectral_conv(field: SphericalField, kernel: torch.Tensor,
+                  precision: str = "3xtf32") -> SphericalField:
+    """convolution.hpp:286-304; kernel [c_out][c_in][klmax]."""
+    g = field.grid
+    if g.kind != GAUSSIAN:
+        raise L.SphInvalidArgument(1, "spectral_conv: requires a gaussian grid")
+    cout, cin, klmax = kernel.shape
+    if cin != field.channels:
+        raise L.SphInvalidArgument(1, "spectral_conv: kernel channel mismatch")
+    lmax = min(klmax, g.nlat)
+    mmax = min(lmax, g.nlon // 2)
+    plan = get_sht_plan(g, lmax, mmax, precision)
+    x = _dev_f32(field.data, "spectral_conv")
+    lead = tuple(x.shape[:-3])
+    B = x.numel() // (cin * g.nlat * g.nlon)
+    kernel = _dev_f32(kernel, "spectral_conv")
+    y = torch.empty((B, cout, g.nlat, g.nlon), dtype=torch.float32, device=x.device)
+    n = int(L.lib.sph_spectral_conv_workspace_bytes(plan.h, B, cin, cout))
+    ws = torch.empty(n, dtype=torch.uint8, device=x.device)
+    with torch.cuda.device(x.device):
+        check(L.lib.sph_spectral_conv(plan.h, _ptr(x), _ptr(kernel), B, cin, cout, klmax,
+                                      _ptr(y), _ptr(ws), _stream(x.device)))
+    return SphericalField(g, y.reshape(*lead, cout, g.nlat, g.nlon))
+
+
+# ------------------------------------------------------------------- block
+@dataclass
+class BlockWeights:
+    """model.hpp:108-115 (one processor block)."""
+    global_: bool
+    conv: torch.Tensor        # mix [C][C+Cc][K] (local) or kernel [C][C+Cc][klmax] (global)
+    w1: torch.Tensor          # [H][C]
+    b1: torch.Tensor          # [H]
+    w2: torch.Tensor          # [C][H]
+    b2: torch.Tensor          # [C]
+    scales: torch.Tensor      # [C]
+
+
+def block_epilogue(conv: torch.Tensor, x: torch.Tensor, bw: BlockWeights) -> torch.Tensor:
+    """model.hpp:355-368: y = x + scales * (W2 gelu(W1 gelu(conv) + b1) + b2)."""
+    x = _dev_f32(x, "block_apply")
+    conv = _dev_f32(conv, "block_apply")
+    C_, H = bw.w2.shape
+    P = x.shape[-1] * x.shape[-2]
+    B = x.numel() // (C_ * P)
+    y = torch.empty_like(x)
+    w = [_dev_f32(t, "block_apply") for t in (bw.w1, bw.b1, bw.w2, bw.b2, bw.scales)]
+    with torch.cuda.device(x.device):
+        check(L.lib.sph_block_epilogue(_ptr(conv), _ptr(x), *[_ptr(t) for t in w], B, C_, H, P,
+                                       _ptr(y), _stream(x.device)))
+    return y
+
+
+def block_apply(latent: SphericalField, conditioning: SphericalField, bw: BlockWeights,
+                block_op: Optional[DiscoOperator] = None,
+                precision: str = "3xtf32") -> SphericalField:
+    """model.hpp:337-370: conv(concat(x, cond)) -> GeLU -> MLP -> layer-scaled residual.
+    global blocks use spectral_conv, local blocks disco_apply with ``block_op``."""
+    g = latent.grid
+    require_same_sampling(latent, g, "block_apply")
+    require_same_sampling(conditioning, g, "block_apply")
+    cat = SphericalField(g, torch.cat([latent.data, conditioning.data], dim=-3))
+    if bw.global_:
+        conv = spectral_conv(cat, bw.conv, precision)
+    else:
+        if block_op is None:
+            raise L.SphInvalidArgument(1, "block_apply: local block needs the block DISCO operator")
+        conv = disco_apply(block_op, cat, bw.conv)
+    return SphericalField(g, block_epilogue(conv.data, latent.data, bw).reshape(latent.data.shape))

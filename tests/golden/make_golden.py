@@ -1,0 +1,137 @@
+"""Generate the golden vectors in tests/golden/golden.npz from the UNMODIFIED reference.
+
+Runs only where /root/reference exists (it drives oracle/_ref/libsphref.so, the
+reference headers compiled behind oracle/ref_driver.cpp).  Inputs are the reference
+test-suite RNG stream (proj/tests/oracles.hpp:105-112: mt19937_64 + U(-1,1)), so
+every fixture stores its seed; outputs are the reference's fp64 results.
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+
+EQ, GA = oracle.EQUIANGULAR, oracle.GAUSSIAN
+PI = np.pi
+
+
+def main():
+    r = oracle.ref()
+    G = {}
+
+    # RNG stream (oracles.hpp:105-112)
+    G["rng_seed1"] = r.random_uniform((64,), 1)
+
+    # grids (grid.hpp:69-128; test_grid.cpp pins)
+    for kind, nlat, nlon in [(EQ, 9, 16), (EQ, 91, 180), (EQ, 721, 1440), (GA, 16, 32),
+                             (GA, 6, 12), (GA, 360, 720), (GA, 1, 4)]:
+        c, w = r.grid(kind, nlat, nlon)
+        G[f"grid_{kind}_{nlat}_{nlon}_colat"] = c
+        G[f"grid_{kind}_{nlat}_{nlon}_w"] = w
+
+    # rfft_bins (fft.hpp:97) on the lengths the hot path uses + test_fft.cpp lengths
+    for n in [1, 2, 3, 5, 7, 12, 16, 20, 33, 90, 180, 720, 1440]:
+        x = r.random_uniform((n,), 1000 + n)
+        G[f"rfft_{n}"] = r.rfft_bins(x, n // 2 + 1)
+
+    # Legendre tables (harmonics.hpp:59 / :106)
+    G["leg_eq_9_16_w"] = r.legendre_table(9, 8, EQ, 9, 16, weighted=True)
+    G["leg_ga_16_32"] = r.legendre_table(16, 16, GA, 16, 32, weighted=False)
+
+    # SHT cfg1: 91x180 equiangular, lmax=91, mmax=90; 4-channel subset of the seed-1
+    # 32-channel field (the reference loops per channel, harmonics.hpp:139, so the
+    # subset is exact).  Forward = dist_sht_forward 1x1 (the reference's equiangular path).
+    x = r.random_uniform((32, 91, 180), 1)
+    c = r.sht_forward(EQ, 91, 180, 91, 90, x[:4])
+    G["cfg1_fwd"] = c
+    G["cfg1_rt"] = r.sht_inverse(EQ, 91, 180, c)
+
+    # Gaussian round trip 32x64 (test_harmonics.cpp:116-131 / acceptance c1 shape)
+    x = r.random_uniform((2, 32, 64), 7)
+    c = r.sht_forward(GA, 32, 64, 32, 32, x)
+    G["ga32_fwd"] = c
+    G["ga32_rt"] = r.sht_inverse(GA, 32, 64, c)
+    # Gaussian 16x32 mode truncation (test_distsim.cpp:188-202)
+    x = r.random_uniform((2, 16, 32), 31)
+    G["ga16_m8_fwd"] = r.sht_forward(GA, 16, 32, 16, 8, x)
+    # equiangular odd sizes (uneven pole handling), 9x16 (test_harmonics.cpp:102)
+    x = r.random_uniform((3, 9, 16), 5)
+    c = r.sht_forward(EQ, 9, 16, 9, 8, x)
+    G["eq9_fwd"] = c
+    G["eq9_rt"] = r.sht_inverse(EQ, 9, 16, c)
+    # inverse on a grid with fewer longitudes than 2*mmax (msynth clamp, harmonics.hpp:179)
+    cf = r.random_uniform((1, 8, 8, 2), 8)
+    cf = cf[..., 0] + 1j * cf[..., 1]
+    G["inv_msynth"] = r.sht_inverse(EQ, 9, 10, cf)
+
+    # DISCO (convolution.hpp:141-220, 226-266); mixes from random_mix semantics
+    # (test_convolution.cpp:76-82)
+    cases = {
+        "ga16_ga8": (GA, 16, 32, GA, 8, 16, 3 * PI / 8, 3, 2),
+        "eq16_eq16": (EQ, 16, 32, EQ, 16, 32, 4 * PI / 16, 3, 2),
+        "eq12_stride3": (EQ, 12, 24, EQ, 12, 8, 3 * PI / 12, 1, 1),
+        "eq91_ga45": (EQ, 91, 180, GA, 45, 90, 3 * PI / 45, 4, 8),
+        "eq9_eq9": (EQ, 9, 16, EQ, 9, 16, 3 * PI / 9, 2, 1),
+    }
+    for name, (ik, ih, iw, ok, oh, ow, cut, cin, cout) in cases.items():
+        rows, K, hh, ww, vv, bb = r.disco_entries(ik, ih, iw, ok, oh, ow, cut)
+        mix = r.random_uniform((cout, cin, K), 77)
+        x = r.random_uniform((cin, ih, iw), 78)
+        G[f"disco_{name}_rows"] = rows
+        G[f"disco_{name}_y"] = r.disco_apply(ik, ih, iw, ok, oh, ow, cut, x, mix)
+        v = r.random_uniform((cout, oh, ow), 79)
+        G[f"disco_{name}_yT"] = r.disco_transpose_apply(ik, ih, iw, ok, oh, ow, cut, v, mix)
+    # isotropic basis (K = 1) one-cell cutoff (test_convolution.cpp:153-163)
+    x = r.random_uniform((1, 12, 24), 5)
+    G["disco_iso_eq12_y"] = r.disco_apply(EQ, 12, 24, EQ, 12, 24, PI / 12, x,
+                                          np.ones((1, 1, 1)), basis=1)
+    # cfg3 row structure (721x1440 eq -> 360x720 Gaussian, cutoff 3pi/360)
+    rows, K = r.disco_rows(EQ, 721, 1440, GA, 360, 720, 3 * PI / 360)
+    G["disco_cfg3_rows"] = rows
+
+    # spectral conv (convolution.hpp:286)
+    x = r.random_uniform((3, 16, 32), 55)
+    k = r.random_uniform((2, 3, 12), 56)
+    G["sconv_ga16_y"] = r.spectral_conv(GA, 16, 32, k, x)
+
+    # block_apply (model.hpp:337-370): levels 1, embed 8 -> C = 16, cond 8, hidden 32
+    C_, Cc, H = 16, 8, 32
+    for glob in (0, 1):
+        x = r.random_uniform((C_, 16, 32), 90)
+        cond = r.random_uniform((Cc, 16, 32), 91)
+        convw = r.random_uniform((C_, C_ + Cc, 16 if glob else 9), 92) * 0.2
+        w1 = r.random_uniform((H, C_), 93) * 0.3
+        b1 = r.random_uniform((H,), 94) * 0.1
+        w2 = r.random_uniform((C_, H), 95) * 0.3
+        b2 = r.random_uniform((C_,), 96) * 0.1
+        sc = r.random_uniform((C_,), 97)
+        G[f"block_g{glob}_y"] = r.block_apply(16, 32, 1, 8, H, glob, 3 * PI / 16, 16, x, cond,
+                                              convw, w1, b1, w2, b2, sc)
+
+    # distributed (distsim.hpp:404, :468) -- outputs and traffic CSV
+    x = r.random_uniform((3, 16, 32), 30)
+    for nh, nw in [(2, 4), (1, 2), (2, 1), (4, 2)]:
+        out, csv = r.dist_sht_forward(GA, 16, 32, 16, 16, x, nh, nw)
+        G[f"dist_sht_{nh}x{nw}"] = out
+        G[f"dist_sht_{nh}x{nw}_csv"] = np.array(csv)
+    x = r.random_uniform((3, 16, 32), 33)
+    mix = r.random_uniform((2, 3, 9), 32)
+    for nh, nw in [(2, 2), (2, 1), (1, 2)]:
+        y, csv = r.dist_disco_apply(GA, 16, 32, GA, 8, 16, 3 * PI / 8, x, mix, nh, nw)
+        G[f"dist_disco_{nh}x{nw}"] = y
+        G[f"dist_disco_{nh}x{nw}_csv"] = np.array(csv)
+
+    out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+    np.savez_compressed(out, **G)
+    print("wrote", out, os.path.getsize(out), "bytes,", len(G), "arrays")
+
+
+if __name__ == "__main__":
+    main()
