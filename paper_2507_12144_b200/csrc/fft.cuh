@@ -1,8 +1,7 @@
 // Longitude ring transforms (fft.hpp:97-113 rfft_bins / real_synthesis) for sm_100a.
 //
-// Two real rings are packed into one complex ring z = a + i b and transformed by an
-// mixed-radix Stockham FFT in shared memory (radices 2,3,4,5,8; ping-pong
-// buffers, one pass per radix).  The forward epilogue splits
+// Two real rings are packed into one complex ring z = a + i b and transformed in
+// shared memory (register four-step for n = N1*45, mixed-radix Stockham otherwise).  The forward epilogue splits
 // A = (Z + conj Z_{N-k})/2, B = (Z - conj Z_{N-k})/2i and writes the parity-folded
 // E = A + B / O = A - B straight into the Legendre GEMM operand layout; the inverse
 // prologue builds Z from Ev +- Od (harmonics.hpp:188-193 Hermitian completion).
@@ -23,7 +22,9 @@ struct FftPlan {
     int radix[FFT_MAX_STAGES] = {};
     bool direct = false;     // n has a prime factor > 5: O(n^2) fallback kernel
     DevBuf<float2> tw;       // W_n^q = exp(-2 pi i q / n), q = 0..n-1 (fp64 -> fp32)
-    int rows_per_block = 1;  // rings (complex) per CTA
+    int rows_per_block = 1;  // rings (complex) per CTA of the Stockham engine
+    int fft4_n1 = 0;         // n = fft4_n1 * 45 -> register four-step engine (fft4.cuh)
+    DevBuf<float2> twT;      // four-step inter-twiddles W_n^{n2 k1} at [k1*45 + n2]
     void build(int n_);
 };
 

@@ -6,6 +6,9 @@
 // blocks of the Legendre contraction (harmonics.hpp:147-154 / :184-194).
 #pragma once
 
+#include <map>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -23,6 +26,11 @@ struct GemmGroup {
 
 struct GemmTile {
     int32_t group, m0, n0, pad;
+};
+
+struct GemmTileList {
+    DevBuf<GemmTile> d;
+    int64_t n = 0;
 };
 
 enum GemmStore : int {
@@ -43,9 +51,12 @@ struct GroupedGemm {
     std::vector<GemmGroup> groups; // host copy
     int store = STORE_ROW;
     int bn = 256;                  // N tile (<= 256, multiple of 16)
+    int cluster = 0;               // CTAs per cluster sharing the table tile (0 = auto)
     DevBuf<GemmGroup> d_groups;
-    DevBuf<GemmTile> d_tiles;
-    int64_t ntiles = 0;
+    int64_t ntiles = 0;            // tiles at cluster size 1 (0 -> nothing to do)
+    mutable std::map<int, std::unique_ptr<GemmTileList>> tile_lists;
+    std::unique_ptr<std::mutex> tiles_mu = std::make_unique<std::mutex>();
+    const GemmTileList& tiles_for(int cl) const;
     DevBuf<GemmTile> d_tiles_simt;  // 64x64 tiles for the SIMT anchor
     int64_t ntiles_simt = 0;
     double flops = 0;              // algorithmic 2*M*N*K summed over groups

@@ -14,6 +14,7 @@
 // Operand tiles are K-major, SWIZZLE_128B (32 fp32 of K per 128-byte row, 8-row /
 // 1024-byte atoms, SBO = 1024).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -59,6 +60,28 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                               uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -125,7 +148,11 @@ struct Smem {
     static constexpr int TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
 };
 
-template <int BN, int STAGES>
+// CL > 1: thread-block cluster of CL CTAs on CL consecutive M-tiles of one (group,
+// N-tile); each CTA TMA-loads 1/CL of the table tile and multicasts it to the whole
+// cluster, so the L2 -> SMEM table traffic per CTA drops by CL.  A stage is refilled
+// only after all CL consumers released it (multicast tcgen05.commit, count CL).
+template <int BN, int STAGES, int CL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_bhi,
@@ -158,7 +185,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar(s), 1);
             mbar_init(conv_bar(s), 128);
-            mbar_init(empty_bar(s), 1);
+            mbar_init(empty_bar(s), CL);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
@@ -182,23 +209,37 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const int crank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
+    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+    const uint16_t cmask = static_cast<uint16_t>((1u << CL) - 1);
+    constexpr int B_ROWS = BN / CL;  // table rows loaded (and multicast) by this CTA
+    if (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
 
     if (warp == 0) {
         // ------------------------------------------------------------- producer
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int t = cid; t < ntiles; t += ncl) {
                 const GemmTile tl = tiles[t];
                 const GemmGroup g = groups[tl.group];
                 const int nkb = (g.K + BK - 1) / BK;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(empty_bar(s), ph ^ 1);
                     mbar_expect_tx(full_bar(s), A_TILE_BYTES + (three_pass ? 2 : 1) * L::B_TILE_BYTES);
-                    tma_load_2d(a_hi(s), &map_a, kb * BK, g.a_row0 + tl.m0, full_bar(s));
-                    tma_load_2d(b_hi(s), &map_bhi, kb * BK, g.b_row0 + tl.n0, full_bar(s));
-                    if (three_pass)
-                        tma_load_2d(b_lo(s), &map_blo, kb * BK, g.b_row0 + tl.n0, full_bar(s));
+                    tma_load_2d(a_hi(s), &map_a, kb * BK, g.a_row0 + tl.m0 + crank * BM, full_bar(s));
+                    if (CL == 1) {
+                        tma_load_2d(b_hi(s), &map_bhi, kb * BK, g.b_row0 + tl.n0, full_bar(s));
+                        if (three_pass)
+                            tma_load_2d(b_lo(s), &map_blo, kb * BK, g.b_row0 + tl.n0, full_bar(s));
+                    } else {
+                        const uint32_t off = crank * B_ROWS * 128;
+                        tma_load_2d_mc(b_hi(s) + off, &map_bhi, kb * BK,
+                                       g.b_row0 + tl.n0 + crank * B_ROWS, full_bar(s), cmask);
+                        if (three_pass)
+                            tma_load_2d_mc(b_lo(s) + off, &map_blo, kb * BK,
+                                           g.b_row0 + tl.n0 + crank * B_ROWS, full_bar(s), cmask);
+                    }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
             }
@@ -209,7 +250,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             int s = 0;
             uint32_t ph = 0;
             int lt = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+            for (int t = cid; t < ntiles; t += ncl, ++lt) {
                 const GemmTile tl = tiles[t];
                 const GemmGroup g = groups[tl.group];
                 const int nkb = (g.K + BK - 1) / BK;
@@ -237,7 +278,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                             tc_mma_tf32(tmem_d, alo, bhi, idesc, 1u);
                         }
                     }
-                    tc_commit(empty_bar(s));
+                    if (CL == 1)
+                        tc_commit(empty_bar(s));
+                    else
+                        tc_commit_mc(empty_bar(s), cmask);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
                 tc_commit(tfull_bar(acc));
@@ -248,7 +292,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         const int ct = threadIdx.x - 128;
         int s = 0;
         uint32_t ph = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int t = cid; t < ntiles; t += ncl) {
             const GemmTile tl = tiles[t];
             const GemmGroup g = groups[tl.group];
             const int nkb = (g.K + BK - 1) / BK;
@@ -281,7 +325,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         // ------------------------------------------------------------- epilogue
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         int lt = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+        for (int t = cid; t < ntiles; t += ncl, ++lt) {
             const GemmTile tl = tiles[t];
             const GemmGroup g = groups[tl.group];
             const int acc = lt & 1;
@@ -290,7 +334,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             if (nrem > BN) nrem = BN;
             mbar_wait(tfull_bar(acc), aph);
             tc_fence_after();
-            const int m = tl.m0 + q * 32 + lane;
+            const int m = tl.m0 + crank * BM + q * 32 + lane;
             const bool mok = m < g.M;
             const uint32_t trow = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
             float* dbase = D + g.d_off;
@@ -330,6 +374,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     }
 
     __syncthreads();
+    if (CL > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast into it
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -376,14 +421,32 @@ static CUtensorMap make_map(const Mat2D& m, int box_rows) {
     return map;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CL>
 static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
                    float* D, bool three, cudaStream_t st) {
     using L = Smem<BN, STAGES>;
+    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL>;
+    static int grid = 0;
     static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(gemm_tf32x3_kernel<BN, STAGES>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    std::call_once(once, [&] {
+        SPH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+        grid = num_sms() / CL * CL;
+        if (CL > 1) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(NUM_THREADS);
+            cfg.dynamicSmemBytes = L::TOTAL;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = CL;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0)
+                grid = std::min(grid, ncl * CL);
+        }
     });
     Mat2D am = g.A;
     am.p = A;
@@ -391,14 +454,27 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     Mat2D bh = g.Bhi, bl = g.Blo;
     bh.p = Bhi;
     bl.p = Blo;
-    const CUtensorMap mbh = make_map(bh, BN);
-    const CUtensorMap mbl = make_map(three ? bl : bh, BN);
-    const int grid = static_cast<int>(std::min<int64_t>(g.ntiles, num_sms()));
+    const CUtensorMap mbh = make_map(bh, BN / CL);
+    const CUtensorMap mbl = make_map(three ? bl : bh, BN / CL);
+    const GemmTileList& tl = g.tiles_for(CL);
+    int gsz = static_cast<int>(std::min<int64_t>(tl.n * CL, grid));
+    gsz = std::max(CL, gsz / CL * CL);
     ProfScope prof(g.name, st, g.flops);
-    gemm_tf32x3_kernel<BN, STAGES><<<grid, NUM_THREADS, L::TOTAL, st>>>(
-        ma, mbh, mbl, g.d_groups.p, g.d_tiles.p, static_cast<int>(g.ntiles), D, g.store,
-        three ? 1 : 0);
-    SPH_LAUNCH_CHECK();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(gsz);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = L::TOTAL;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = CL > 1 ? 1 : 0;
+    SPH_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, static_cast<const GemmGroup*>(g.d_groups.p),
+                                static_cast<const GemmTile*>(tl.d.p), static_cast<int>(tl.n), D,
+                                g.store, three ? 1 : 0));
     count_launch();
 }
 
@@ -419,45 +495,77 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
     }
     const bool three = prec == SPH_PREC_3XTF32;
     require(!three || Blo, "gemm: 3xTF32 needs the lo table");
-    if (g.bn == 256)
-        tc::launch<256, 2>(g, A, Bhi, Blo, D, three, st);
-    else if (g.bn == 128)
-        tc::launch<128, 3>(g, A, Bhi, Blo, D, three, st);
+    const int cl = g.cluster;
+    if (g.bn == 256 && cl == 1)
+        tc::launch<256, 2, 1>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 256 && cl == 2)
+        tc::launch<256, 2, 2>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 256 && cl == 4)
+        tc::launch<256, 2, 4>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 128 && cl == 1)
+        tc::launch<128, 3, 1>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 128 && cl == 2)
+        tc::launch<128, 3, 2>(g, A, Bhi, Blo, D, three, st);
     else
         fail(SPH_ERR_INVALID_ARGUMENT, "gemm: unsupported N tile");
 }
 
-void GroupedGemm::finalize() {
+// LPT-ordered tile list for cluster size cl: one entry per (group, n-tile, run of
+// cl consecutive M-tiles); ties keep group-major order so concurrently running
+// clusters share table tiles in L2.
+static void build_tiles(const GroupedGemm& g, int cl, GemmTileList& out) {
     std::vector<GemmTile> t;
     std::vector<double> cost;
-    flops = 0;
-    for (size_t gi = 0; gi < groups.size(); ++gi) {
-        const GemmGroup& gr = groups[gi];
+    for (size_t gi = 0; gi < g.groups.size(); ++gi) {
+        const GemmGroup& gr = g.groups[gi];
         if (gr.M <= 0 || gr.N <= 0 || gr.K <= 0) continue;
-        flops += 2.0 * gr.M * static_cast<double>(gr.N) * gr.K;
-        for (int n0 = 0; n0 < gr.N; n0 += bn)
-            for (int m0 = 0; m0 < gr.M; m0 += tc::BM) {
+        for (int n0 = 0; n0 < gr.N; n0 += g.bn)
+            for (int m0 = 0; m0 < gr.M; m0 += tc::BM * cl) {
                 t.push_back({static_cast<int32_t>(gi), m0, n0, 0});
-                cost.push_back(static_cast<double>(std::min(bn, gr.N - n0) + 16) *
-                               ((gr.K + 31) / 32));
+                cost.push_back(static_cast<double>(std::min(g.bn, gr.N - n0) + 16) * ((gr.K + 31) / 32));
             }
     }
-    // LPT order: most expensive tiles first, ties keep group-major order so
-    // concurrently running CTAs share the same table tile in L2.
     std::vector<size_t> idx(t.size());
     for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
     std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
     std::vector<GemmTile> ts(t.size());
     for (size_t i = 0; i < idx.size(); ++i) ts[i] = t[idx[i]];
-    ntiles = static_cast<int64_t>(ts.size());
-    d_groups.alloc(groups.size(), false);
-    d_tiles.alloc(std::max<size_t>(ts.size(), 1), false);
+    out.n = static_cast<int64_t>(ts.size());
+    out.d.alloc(std::max<size_t>(ts.size(), 1), false);
+    if (!ts.empty())
+        SPH_CUDA(cudaMemcpy(out.d.p, ts.data(), ts.size() * sizeof(GemmTile), cudaMemcpyHostToDevice));
+}
+
+const GemmTileList& GroupedGemm::tiles_for(int cl) const {
+    std::lock_guard<std::mutex> lk(*tiles_mu);
+    auto& slot = tile_lists[cl];
+    if (!slot) {
+        slot = std::make_unique<GemmTileList>();
+        build_tiles(*this, cl, *slot);
+    }
+    return *slot;
+}
+
+void GroupedGemm::finalize() {
+    flops = 0;
+    int64_t mtiles = 0;
+    for (const GemmGroup& gr : groups) {
+        if (gr.M <= 0 || gr.N <= 0 || gr.K <= 0) continue;
+        flops += 2.0 * gr.M * static_cast<double>(gr.N) * gr.K;
+        mtiles = std::max<int64_t>(mtiles, (gr.M + tc::BM - 1) / tc::BM);
+    }
+    d_groups.alloc(std::max<size_t>(groups.size(), 1), false);
     if (!groups.empty())
         SPH_CUDA(cudaMemcpy(d_groups.p, groups.data(), groups.size() * sizeof(GemmGroup),
                             cudaMemcpyHostToDevice));
-    if (!ts.empty())
-        SPH_CUDA(cudaMemcpy(d_tiles.p, ts.data(), ts.size() * sizeof(GemmTile),
-                            cudaMemcpyHostToDevice));
+    // table multicast pays off when groups span several M-tiles
+    if (cluster == 0) cluster = mtiles >= 8 ? 2 : 1;
+    if (const char* e = std::getenv("SPH_GEMM_CLUSTER")) {  // test / tuning override
+        const int v = std::atoi(e);
+        if (v == 1 || v == 2 || v == 4) cluster = v;
+    }
+    if (bn == 128 && cluster > 2) cluster = 2;
+    ntiles = tiles_for(1).n;
     build_simt_tiles(*this);
 }
 

@@ -179,8 +179,8 @@ class ShtPlan:
         if out is None:
             if layout == L.SPH_LAYOUT_DENSE_LM:
                 out = torch.empty((F, self.lmax, self.mmax, 2), dtype=torch.float32, device=x.device)
-            else:
-                out = torch.empty(self.coeffs_elems(F, layout), dtype=torch.float32, device=x.device)
+            else:  # padding beyond each (m, parity) block stays zero
+                out = torch.zeros(self.coeffs_elems(F, layout), dtype=torch.float32, device=x.device)
         ws = self.workspace(F) if ws is None else ws
         check(L.lib.sph_sht_forward(self.h, _ptr(x), F, _ptr(out), layout, _ptr(ws),
                                     _stream(x.device)))

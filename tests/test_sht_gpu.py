@@ -203,3 +203,18 @@ def test_cfg2_721_subset_and_properties():
     b = p.forward(2.0 * xt, L.SPH_LAYOUT_INTERNAL)
     torch.cuda.synchronize()
     assert float((b - 2 * a).norm() / (2 * a).norm()) <= 1e-6
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "4"])
+def test_gemm_cluster_multicast_matches_simt(monkeypatch, cluster):
+    """The table-multicast cluster path of the tcgen05 GEMM (used at benchmark batch
+    sizes) against the fp32 SIMT anchor on the same inputs: 512 fields of cfg1."""
+    monkeypatch.setenv("SPH_GEMM_CLUSTER", cluster)
+    x = oracle.random_field((512, 91, 180), 9)
+    a = fwd(plan(0, 91, 180, 91, 90, "3xtf32"), x)
+    b = fwd(plan(0, 91, 180, 91, 90, "fp32"), x)
+    assert rel_l2(a, b) <= 2e-6
+    pa = plan(0, 91, 180, 91, 90, "3xtf32")
+    ya = inv(pa, a, 512)
+    yb = inv(plan(0, 91, 180, 91, 90, "fp32"), a, 512)
+    assert rel_l2(ya, yb) <= 2e-6
