@@ -162,61 +162,81 @@ __device__ __forceinline__ float2* stockham(float2* a, float2* b, int nrings, co
 // Each IO maps blockIdx to P complex rings and provides load (HBM -> buf, ring-major)
 // and store (buf, natural-order spectrum or signal -> HBM).
 
-// forward SHT: ring pairs (ia, ib) of field f, folded rows r0.. -> E/O operand
+// forward SHT: ring pairs (ia, ib) of field f, folded rows r0.. -> E/O operand.
+// P / n may be std::integral_constant (four-step path) so the index math folds.
 struct FoldIO {
     const float* x;
     const int2* rows;
     int R, nlat, mmax;
     float* eo;
     int64_t ld_eo, twoF;
-    __device__ void load(float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int r0 = blockIdx.x * P, f = blockIdx.y;
-        const int nr = min(P, R - r0);
+        const int nr = min(static_cast<int>(P), R - r0);
         const float* xf = x + static_cast<int64_t>(f) * nlat * n;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
         if ((n & 3) == 0) {
             const int n4 = n / 4;
-            for (int i = threadIdx.x; i < P * n4; i += blockDim.x) {
-                const int j = i / n4, k4 = i - j * n4;
-                float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
+            for (int j = warp; j < P; j += nw) {  // one ring pair per warp
+                float4* d = reinterpret_cast<float4*>(buf + j * ld);
                 if (j < nr) {
                     const int2 rw = rows[r0 + j];
-                    va = __ldg(reinterpret_cast<const float4*>(xf + static_cast<int64_t>(rw.x) * n) + k4);
-                    if (rw.y >= 0)
-                        vb = __ldg(reinterpret_cast<const float4*>(xf + static_cast<int64_t>(rw.y) * n) + k4);
+                    const float4* pa = reinterpret_cast<const float4*>(xf + static_cast<int64_t>(rw.x) * n);
+                    const float4* pb = reinterpret_cast<const float4*>(xf + static_cast<int64_t>(rw.y < 0 ? rw.x : rw.y) * n);
+                    const bool hb = rw.y >= 0;
+                    for (int k4 = lane; k4 < n4; k4 += 32) {
+                        const float4 va = __ldg(pa + k4);
+                        float4 vb = __ldg(pb + k4);
+                        if (!hb) vb = make_float4(0.f, 0.f, 0.f, 0.f);
+                        d[2 * k4] = make_float4(va.x, vb.x, va.y, vb.y);
+                        d[2 * k4 + 1] = make_float4(va.z, vb.z, va.w, vb.w);
+                    }
+                } else {
+                    for (int k4 = lane; k4 < n4; k4 += 32) {
+                        d[2 * k4] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        d[2 * k4 + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
                 }
-                float4* d = reinterpret_cast<float4*>(buf + j * ld + 4 * k4);  // ld % 2 == 0
-                d[0] = make_float4(va.x, vb.x, va.y, vb.y);
-                d[1] = make_float4(va.z, vb.z, va.w, vb.w);
             }
         } else {
-            for (int i = threadIdx.x; i < P * n; i += blockDim.x) {
-                const int j = i / n, k = i - j * n;
-                float2 v = make_float2(0.f, 0.f);
-                if (j < nr) {
-                    const int2 rw = rows[r0 + j];
-                    v.x = xf[static_cast<int64_t>(rw.x) * n + k];
-                    if (rw.y >= 0) v.y = xf[static_cast<int64_t>(rw.y) * n + k];
+            for (int j = warp; j < P; j += nw) {
+                const bool ok = j < nr;
+                const int2 rw = ok ? rows[r0 + j] : make_int2(0, -1);
+                for (int k = lane; k < n; k += 32) {
+                    float2 v = make_float2(0.f, 0.f);
+                    if (ok) {
+                        v.x = xf[static_cast<int64_t>(rw.x) * n + k];
+                        if (rw.y >= 0) v.y = xf[static_cast<int64_t>(rw.y) * n + k];
+                    }
+                    buf[j * ld + k] = v;
                 }
-                buf[j * ld + k] = v;
             }
         }
     }
-    __device__ void store(const float2* buf, int P, int n, int ld) const {
+    // one (m, ring) per thread, all four outputs (E re/im, O re/im); lanes with
+    // consecutive j write P-float runs of four E/O rows
+    template <class PT, class NT>
+    __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
         const int r0 = blockIdx.x * P, f = blockIdx.y;
-        const int nr = min(P, R - r0);
-        const int total = mmax * 4 * P;
-        for (int o = threadIdx.x; o < total; o += blockDim.x) {
-            const int j = o % P;
-            const int q = (o / P) & 3;
-            const int m = o / (4 * P);
-            if (j >= nr) continue;
-            const float2 z = buf[j * ld + m];
-            const float2 zc = buf[j * ld + (m == 0 ? 0 : n - m)];
+        const int nr = min(static_cast<int>(P), R - r0);
+        const int j = threadIdx.x % P;
+        const int mstep = blockDim.x / P;
+        if (j >= nr) return;
+        const float2* zr = buf + j * ld;
+        float* e = eo + (2 * static_cast<int64_t>(f)) * ld_eo + r0 + j;
+        const int64_t so = twoF * ld_eo;      // E -> O row offset
+        const int64_t sm = 2 * so;            // m -> m+1
+        for (int m = threadIdx.x / P; m < mmax; m += mstep) {
+            const float2 z = zr[m];
+            const float2 zc = zr[m == 0 ? 0 : n - m];
             const float ar = 0.5f * (z.x + zc.x), ai = 0.5f * (z.y - zc.y);
             const float br = 0.5f * (z.y + zc.y), bi = -0.5f * (z.x - zc.x);
-            const int p = q >> 1, reim = q & 1;
-            const float val = p == 0 ? (reim ? ai + bi : ar + br) : (reim ? ai - bi : ar - br);
-            eo[((static_cast<int64_t>(m) * 2 + p) * twoF + 2 * f + reim) * ld_eo + r0 + j] = val;
+            float* em = e + m * sm;
+            em[0] = ar + br;
+            em[ld_eo] = ai + bi;
+            em[so] = ar - br;
+            em[so + ld_eo] = ai - bi;
         }
     }
 };
@@ -228,55 +248,65 @@ struct UnfoldIO {
     int R, nlat, msynth, lmax;
     int64_t ld_eo, twoF;
     float* y;
-    __device__ void load(float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int r0 = blockIdx.x * P, f = blockIdx.y;
-        const int nr = min(P, R - r0);
-        for (int i = threadIdx.x; i < P * ld; i += blockDim.x) buf[i] = make_float2(0.f, 0.f);
-        __syncthreads();
-        for (int o = threadIdx.x; o < msynth * P; o += blockDim.x) {
-            const int j = o % P;
-            const int m = o / P;
-            if (j >= nr) continue;
-            const int2 rw = rows[r0 + j];
-            const int64_t c = r0 + j;
-            const int64_t g0 = (static_cast<int64_t>(m) * 2 + 0) * twoF + 2 * f;
-            const int64_t g1 = (static_cast<int64_t>(m) * 2 + 1) * twoF + 2 * f;
+        const int nr = min(static_cast<int>(P), R - r0);
+        const int j = threadIdx.x % P;
+        const int mstep = blockDim.x / P;
+        const int m0 = threadIdx.x / P;
+        float2* zr = buf + j * ld;
+        // bins [msynth, n - msynth] are zero
+        for (int k = msynth + m0; k <= n - msynth; k += mstep) zr[k] = make_float2(0.f, 0.f);
+        if (j >= nr) {
+            for (int m = m0; m < msynth; m += mstep) {
+                zr[m] = make_float2(0.f, 0.f);
+                if (m) zr[n - m] = make_float2(0.f, 0.f);
+            }
+            return;
+        }
+        const bool pair = rows[r0 + j].y >= 0;
+        const float* e = eoi + (2 * static_cast<int64_t>(f)) * ld_eo + r0 + j;
+        const int64_t so = twoF * ld_eo, sm = 2 * so;
+        for (int m = m0; m < msynth; m += mstep) {
+            const float* em = e + m * sm;
             const int l0 = (lmax - m + 1) / 2, l1 = (lmax - m) / 2;  // L_{m,0}, L_{m,1}
             float2 ev = make_float2(0.f, 0.f), od = make_float2(0.f, 0.f);
-            if (l0 > 0) ev = make_float2(eoi[g0 * ld_eo + c], eoi[(g0 + 1) * ld_eo + c]);
-            if (l1 > 0) od = make_float2(eoi[g1 * ld_eo + c], eoi[(g1 + 1) * ld_eo + c]);
+            if (l0 > 0) ev = make_float2(em[0], em[ld_eo]);
+            if (l1 > 0) od = make_float2(em[so], em[so + ld_eo]);
             const float2 ha = cadd(ev, od);
-            const float2 hb = rw.y >= 0 ? csub(ev, od) : make_float2(0.f, 0.f);
+            const float2 hb = pair ? csub(ev, od) : make_float2(0.f, 0.f);
             if (m == 0) {
-                buf[j * ld] = make_float2(ha.x, hb.x);  // Im of the DC bin is dropped
+                zr[0] = make_float2(ha.x, hb.x);  // Im of the DC bin is dropped
             } else {
-                buf[j * ld + m] = make_float2(ha.x - hb.y, ha.y + hb.x);      // ha + i hb
-                buf[j * ld + n - m] = make_float2(ha.x + hb.y, hb.x - ha.y);  // conj ha + i conj hb
+                zr[m] = make_float2(ha.x - hb.y, ha.y + hb.x);      // ha + i hb
+                zr[n - m] = make_float2(ha.x + hb.y, hb.x - ha.y);  // conj ha + i conj hb
             }
         }
     }
-    __device__ void store(const float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
         const int r0 = blockIdx.x * P, f = blockIdx.y;
-        const int nr = min(P, R - r0);
+        const int nr = min(static_cast<int>(P), R - r0);
         float* yf = y + static_cast<int64_t>(f) * nlat * n;
-        if ((n & 3) == 0) {
-            const int n4 = n / 4;
-            for (int i = threadIdx.x; i < nr * n4; i += blockDim.x) {
-                const int j = i / n4, k4 = i - j * n4;
-                const int2 rw = rows[r0 + j];
-                const float2* s = buf + j * ld + 4 * k4;
-                reinterpret_cast<float4*>(yf + static_cast<int64_t>(rw.x) * n)[k4] =
-                    make_float4(s[0].x, s[1].x, s[2].x, s[3].x);
-                if (rw.y >= 0)
-                    reinterpret_cast<float4*>(yf + static_cast<int64_t>(rw.y) * n)[k4] =
-                        make_float4(s[0].y, s[1].y, s[2].y, s[3].y);
-            }
-        } else {
-            for (int i = threadIdx.x; i < nr * n; i += blockDim.x) {
-                const int j = i / n, k = i - j * n;
-                const int2 rw = rows[r0 + j];
-                yf[static_cast<int64_t>(rw.x) * n + k] = buf[j * ld + k].x;
-                if (rw.y >= 0) yf[static_cast<int64_t>(rw.y) * n + k] = buf[j * ld + k].y;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int j = warp; j < nr; j += nw) {
+            const int2 rw = rows[r0 + j];
+            const float2* zr = buf + j * ld;
+            float* pa = yf + static_cast<int64_t>(rw.x) * n;
+            float* pb = yf + static_cast<int64_t>(rw.y) * n;
+            if ((n & 3) == 0) {
+                const float4* z4 = reinterpret_cast<const float4*>(zr);
+                for (int k4 = lane; k4 < n / 4; k4 += 32) {
+                    const float4 u = z4[2 * k4], v = z4[2 * k4 + 1];
+                    reinterpret_cast<float4*>(pa)[k4] = make_float4(u.x, u.z, v.x, v.z);
+                    if (rw.y >= 0) reinterpret_cast<float4*>(pb)[k4] = make_float4(u.y, u.w, v.y, v.w);
+                }
+            } else {
+                for (int k = lane; k < n; k += 32) {
+                    pa[k] = zr[k].x;
+                    if (rw.y >= 0) pb[k] = zr[k].y;
+                }
             }
         }
     }
@@ -289,7 +319,8 @@ struct PlainFwdIO {
     int nbins;
     float scale;
     float2* bins;
-    __device__ void load(float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P;
         for (int i = threadIdx.x; i < P * n; i += blockDim.x) {
             const int j = i / n, k = i - j * n;
@@ -298,7 +329,8 @@ struct PlainFwdIO {
                                           rb < nrings ? rings[rb * n + k] : 0.f);
         }
     }
-    __device__ void store(const float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P;
         for (int o = threadIdx.x; o < P * 2 * nbins; o += blockDim.x) {
             const int m = o % nbins;
@@ -322,7 +354,8 @@ struct PlainInvIO {
     int nbins;
     float scale;
     float* rings;
-    __device__ void load(float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P;
         const int half = n / 2;
         for (int i = threadIdx.x; i < P * n; i += blockDim.x) {
@@ -339,7 +372,8 @@ struct PlainInvIO {
             buf[j * ld + k] = make_float2(ha.x - hb.y, ha.y + hb.x);
         }
     }
-    __device__ void store(const float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P;
         for (int i = threadIdx.x; i < P * 2 * n; i += blockDim.x) {
             const int jj = i / n, k = i - jj * n;
@@ -358,7 +392,8 @@ struct CminorIO {
     int64_t C, H;
     int nbins;
     float2* U;
-    __device__ void load(float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
         const int64_t hi = blockIdx.y, b = blockIdx.z;
         for (int i = threadIdx.x; i < P * n; i += blockDim.x) {
@@ -368,7 +403,8 @@ struct CminorIO {
                                  cb < C ? x[((b * C + cb) * H + hi) * n + k] : 0.f);
         }
     }
-    __device__ void store(const float2* buf, int P, int n, int ld) const {
+    template <class PT, class NT>
+    __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
         const int64_t hi = blockIdx.y, b = blockIdx.z;
         float2* Ub = U + (b * H + hi) * static_cast<int64_t>(nbins) * C;
@@ -391,10 +427,12 @@ template <int N1, bool INV, class IO>
 __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_kernel(IO io, const float2* __restrict__ twT) {
     extern __shared__ float2 sm4[];
     constexpr int N = N1 * 45, P = fft4::THREADS / N1, LD = N + 2;  // padded ring stride
-    io.load(sm4, P, N, LD);
+    using PC = std::integral_constant<int, P>;
+    using NC = std::integral_constant<int, N>;
+    io.load(sm4, PC{}, NC{}, LD);
     __syncthreads();
     fft4::transform<N1, 45, LD, INV>(sm4, twT);
-    io.store(sm4, P, N, LD);
+    io.store(sm4, PC{}, NC{}, LD);
 }
 
 template <bool INV, class IO>

@@ -11,8 +11,8 @@
 //   warps 8..11   epilogue: TMEM -> registers (tcgen05.ld 32x32b) -> global
 // Pipelines: SMEM ring (full -> converted -> empty) and a double-buffered TMEM
 // accumulator (full/empty) so the epilogue of tile i overlaps the MMAs of tile i+1.
-// Operand tiles are K-major, SWIZZLE_128B (32 fp32 of K per 128-byte row, 8-row /
-// 1024-byte atoms, SBO = 1024).
+// Operand tiles are K-major, SWIZZLE_64B (16 fp32 of K per 64-byte row, 8-row /
+// 512-byte atoms, SBO = 512): small stages -> a 4-deep (BN=256) / 6-deep (BN=128) ring.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -24,7 +24,7 @@ namespace sph {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 32;               // fp32 elements per 128-byte swizzle row
+constexpr int BK = 16;               // fp32 elements per 64-byte swizzle row
 constexpr int NUM_THREADS = 384;     // 12 warps
 constexpr int A_TILE_BYTES = BM * BK * 4;  // 16 KB
 
@@ -118,14 +118,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B, version 1.
+// UMMA shared-memory descriptor: K-major, SWIZZLE_64B, SBO = 512 B, version 1.
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);          // start address
     d |= static_cast<uint64_t>(1) << 16;                          // LBO (unused for SW128 K-major)
-    d |= static_cast<uint64_t>(1024 >> 4) << 32;                  // SBO: 8-row group stride
+    d |= static_cast<uint64_t>((8 * BK * 4) >> 4) << 32;          // SBO: 8-row group stride
     d |= static_cast<uint64_t>(1) << 46;                          // descriptor version (sm100)
-    d |= static_cast<uint64_t>(2) << 61;                          // SWIZZLE_128B
+    d |= static_cast<uint64_t>(4) << 61;                          // SWIZZLE_64B
     return d;
 }
 // Instruction descriptor: kind::tf32, D f32, A/B tf32, both K-major, M = 128, N = n.
@@ -233,7 +233,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                         if (three_pass)
                             tma_load_2d(b_lo(s), &map_blo, kb * BK, g.b_row0 + tl.n0, full_bar(s));
                     } else {
-                        const uint32_t off = crank * B_ROWS * 128;
+                        const uint32_t off = crank * B_ROWS * BK * 4;
                         tma_load_2d_mc(b_hi(s) + off, &map_bhi, kb * BK,
                                        g.b_row0 + tl.n0 + crank * B_ROWS, full_bar(s), cmask);
                         if (three_pass)
@@ -415,7 +415,7 @@ static CUtensorMap make_map(const Mat2D& m, int box_rows) {
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(m.p), dims,
                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(SPH_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return map;
@@ -497,15 +497,15 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
     require(!three || Blo, "gemm: 3xTF32 needs the lo table");
     const int cl = g.cluster;
     if (g.bn == 256 && cl == 1)
-        tc::launch<256, 2, 1>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<256, 4, 1>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 256 && cl == 2)
-        tc::launch<256, 2, 2>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<256, 4, 2>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 256 && cl == 4)
-        tc::launch<256, 2, 4>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<256, 4, 4>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 128 && cl == 1)
-        tc::launch<128, 3, 1>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<128, 6, 1>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 128 && cl == 2)
-        tc::launch<128, 3, 2>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<128, 6, 2>(g, A, Bhi, Blo, D, three, st);
     else
         fail(SPH_ERR_INVALID_ARGUMENT, "gemm: unsupported N tile");
 }
@@ -514,22 +514,24 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
 // cl consecutive M-tiles); ties keep group-major order so concurrently running
 // clusters share table tiles in L2.
 static void build_tiles(const GroupedGemm& g, int cl, GemmTileList& out) {
-    std::vector<GemmTile> t;
-    std::vector<double> cost;
+    // Groups in decreasing cost (LPT over groups), and inside a group the N-tiles of
+    // one M-run adjacent: concurrently running CTAs then share the data (A) tile in
+    // L2 instead of re-reading it from HBM for the second N-tile.
+    std::vector<size_t> gorder;
+    std::vector<double> gcost(g.groups.size(), 0.0);
     for (size_t gi = 0; gi < g.groups.size(); ++gi) {
         const GemmGroup& gr = g.groups[gi];
         if (gr.M <= 0 || gr.N <= 0 || gr.K <= 0) continue;
-        for (int n0 = 0; n0 < gr.N; n0 += g.bn)
-            for (int m0 = 0; m0 < gr.M; m0 += tc::BM * cl) {
-                t.push_back({static_cast<int32_t>(gi), m0, n0, 0});
-                cost.push_back(static_cast<double>(std::min(g.bn, gr.N - n0) + 16) * ((gr.K + 31) / 32));
-            }
+        gcost[gi] = static_cast<double>(gr.N) * gr.K;
+        gorder.push_back(gi);
     }
-    std::vector<size_t> idx(t.size());
-    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
-    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
-    std::vector<GemmTile> ts(t.size());
-    for (size_t i = 0; i < idx.size(); ++i) ts[i] = t[idx[i]];
+    std::stable_sort(gorder.begin(), gorder.end(), [&](size_t a, size_t b) { return gcost[a] > gcost[b]; });
+    std::vector<GemmTile> ts;
+    for (size_t gi : gorder) {
+        const GemmGroup& gr = g.groups[gi];
+        for (int m0 = 0; m0 < gr.M; m0 += tc::BM * cl)
+            for (int n0 = 0; n0 < gr.N; n0 += g.bn) ts.push_back({static_cast<int32_t>(gi), m0, n0, 0});
+    }
     out.n = static_cast<int64_t>(ts.size());
     out.d.alloc(std::max<size_t>(ts.size(), 1), false);
     if (!ts.empty())
@@ -558,8 +560,9 @@ void GroupedGemm::finalize() {
     if (!groups.empty())
         SPH_CUDA(cudaMemcpy(d_groups.p, groups.data(), groups.size() * sizeof(GemmGroup),
                             cudaMemcpyHostToDevice));
-    // table multicast pays off when groups span several M-tiles
-    if (cluster == 0) cluster = mtiles >= 8 ? 2 : 1;
+    // table multicast: no measurable gain at cluster <= 4 (L2 does not dedup), keep 1
+    if (cluster == 0) cluster = 1;
+    (void)mtiles;
     if (const char* e = std::getenv("SPH_GEMM_CLUSTER")) {  // test / tuning override
         const int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) cluster = v;
