@@ -131,6 +131,19 @@ int64_t sph_disco_workspace_bytes(sph_disco_plan plan, int64_t B, int64_t c_in, 
 int sph_disco_apply(sph_disco_plan plan, const float* x, const float* mix, int64_t B,
                     int64_t c_in, int64_t c_out, float* y, void* workspace, void* stream);
 
+/* Latitude-shard form used by the distributed DISCO (distsim.hpp:468-547 with a
+ * latitude halo instead of the reduce-scatter of K-expanded partials): output rows
+ * [h_out0, h_out0+n_out) from the input rows [h_in0, h_in0+n_in) given in
+ * x [B][c_in][n_in][in_nlon]; y [B][c_out][n_out][out_nlon].  sph_disco_input_rows
+ * returns the input row range (filter support band) those output rows need. */
+int sph_disco_input_rows(sph_disco_plan plan, int64_t h_out0, int64_t n_out, int64_t* h_in0,
+                         int64_t* n_in);
+int64_t sph_disco_rows_workspace_bytes(sph_disco_plan plan, int64_t B, int64_t c_in, int64_t c_out,
+                                       int64_t n_in, int64_t n_out);
+int sph_disco_apply_rows(sph_disco_plan plan, const float* x, int64_t h_in0, int64_t n_in,
+                         int64_t h_out0, int64_t n_out, const float* mix, int64_t B, int64_t c_in,
+                         int64_t c_out, float* y, void* workspace, void* stream);
+
 /* ---- spectral convolution + block epilogue ------------------------------------ */
 /* spectral_conv (convolution.hpp:286-304): Gaussian grids only (:287-288);
  * kernel [c_out][c_in][klmax]; x [B][c_in][nlat][nlon] -> y [B][c_out][nlat][nlon].

@@ -274,6 +274,28 @@ int sph_disco_apply(sph_disco_plan plan, const float* x, const float* mix, int64
     });
 }
 
+int sph_disco_input_rows(sph_disco_plan plan, int64_t h_out0, int64_t n_out, int64_t* h_in0,
+                         int64_t* n_in) {
+    return guarded([&] {
+        sph::require(plan, "disco rows: null plan");
+        plan->p.input_rows(h_out0, n_out, h_in0, n_in);
+    });
+}
+
+int64_t sph_disco_rows_workspace_bytes(sph_disco_plan plan, int64_t B, int64_t c_in, int64_t c_out,
+                                       int64_t n_in, int64_t n_out) {
+    return plan ? plan->p.rows_workspace_bytes(B, c_in, c_out, n_in, n_out) : -1;
+}
+
+int sph_disco_apply_rows(sph_disco_plan plan, const float* x, int64_t h_in0, int64_t n_in,
+                         int64_t h_out0, int64_t n_out, const float* mix, int64_t B, int64_t c_in,
+                         int64_t c_out, float* y, void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "disco_apply: null plan");
+        plan->p.apply_rows(x, h_in0, n_in, h_out0, n_out, mix, B, c_in, c_out, y, workspace, S(stream));
+    });
+}
+
 // ------------------------------------------------------ spectral conv + block
 int sph_spectral_conv(sph_sht_plan plan, const float* x, const float* kernel, int64_t B,
                       int64_t c_in, int64_t c_out, int64_t klmax, float* y, void* workspace,

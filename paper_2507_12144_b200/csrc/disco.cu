@@ -118,13 +118,16 @@ __global__ void __launch_bounds__(256) disco_band_kernel(
     const float2* __restrict__ U, const float2* __restrict__ psi_hat, const int32_t* __restrict__ band0,
     const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, int64_t Hin, int64_t nbi,
     int64_t Hout, int64_t nbo, int win, int wout, int s, int K, int64_t C, int64_t ldS,
-    float* __restrict__ S) {
+    float* __restrict__ S, int64_t h_in0, int64_t ho0) {
+    // U holds input rows [h_in0, h_in0 + Hin); this launch computes output rows
+    // [ho0, ho0 + Hout) (local index h)
     const int mi = threadIdx.x / 64, cl = threadIdx.x % 64;
     const int64_t mp = static_cast<int64_t>(blockIdx.x) * 4 + mi;
     const int64_t h = blockIdx.y, b = blockIdx.z;
     if (mp >= nbo) return;
-    const int h0 = band0[h], nb = bandc[h];
-    const int64_t po = psi_off[h];
+    const int64_t hg = ho0 + h;
+    const int h0 = band0[hg] - static_cast<int>(h_in0), nb = bandc[hg];
+    const int64_t po = psi_off[hg];
     const int half = win / 2;
     for (int64_t c0 = 0; c0 < C; c0 += 64) {
         const int64_t c = c0 + cl;
@@ -174,10 +177,11 @@ __global__ void __launch_bounds__(256) disco_band_kernel(
 __global__ void __launch_bounds__(256) disco_gather_kernel(
     const float* __restrict__ x, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ h_in,
     const int32_t* __restrict__ w_rel, const float* __restrict__ vals, int64_t Hin, int64_t Win,
-    int64_t Hout, int64_t Wout, int64_t stride, int K, int64_t C, int64_t ldS, float* __restrict__ T) {
+    int64_t Hout, int64_t Wout, int64_t stride, int K, int64_t C, int64_t ldS, float* __restrict__ T,
+    int64_t h_in0, int64_t ho0) {
     const int64_t h = blockIdx.x, c = blockIdx.y, b = blockIdx.z;
-    const float* u = x + (b * C + c) * Hin * Win;
-    const int64_t e0 = row_ptr[h], e1 = row_ptr[h + 1];
+    const float* u = x + (b * C + c) * Hin * Win - h_in0 * Win;  // global row index h_in[e]
+    const int64_t e0 = row_ptr[ho0 + h], e1 = row_ptr[ho0 + h + 1];
     for (int64_t w = threadIdx.x; w < Wout; w += blockDim.x) {
         float acc[9];
 #pragma unroll
@@ -335,7 +339,8 @@ namespace {
 struct DiscoWs {
     int64_t ldS, u_off, s_off, y_off, whi_off, wlo_off, total;
 };
-DiscoWs disco_ws(const DiscoPlan& p, int64_t B, int64_t cin, int64_t cout) {
+// workspace for B samples, input rows nin, output rows nout
+DiscoWs disco_ws(const DiscoPlan& p, int64_t B, int64_t cin, int64_t cout, int64_t nin, int64_t nout) {
     DiscoWs w;
     w.ldS = static_cast<int64_t>(round_up(cin * p.K, 4));
     const int64_t whi = cout * w.ldS * 4;
@@ -346,15 +351,15 @@ DiscoWs disco_ws(const DiscoPlan& p, int64_t B, int64_t cin, int64_t cout) {
     o += round_up(whi, 256);
     if (p.prec == SPH_PREC_FP32_SIMT) {
         w.s_off = o;  // T (direct gather)
-        o += round_up(B * p.hout * p.wout * w.ldS * 4, 256);
+        o += round_up(B * nout * p.wout * w.ldS * 4, 256);
         w.u_off = w.y_off = 0;
     } else {
         w.u_off = o;
-        o += round_up(B * p.hin * p.nbi * cin * 8, 256);
+        o += round_up(B * nin * p.nbi * cin * 8, 256);
         w.s_off = o;
-        o += round_up(B * p.hout * p.nbo * 2 * w.ldS * 4, 256);
+        o += round_up(B * nout * p.nbo * 2 * w.ldS * 4, 256);
         w.y_off = o;
-        o += round_up(B * cout * p.hout * p.nbo * 2 * 4, 256);
+        o += round_up(B * cout * nout * p.nbo * 2 * 4, 256);
     }
     w.total = o + 256;
     return w;
@@ -362,15 +367,42 @@ DiscoWs disco_ws(const DiscoPlan& p, int64_t B, int64_t cin, int64_t cout) {
 }  // namespace
 
 int64_t DiscoPlan::workspace_bytes(int64_t B, int64_t cin, int64_t cout) const {
-    return disco_ws(*this, B, cin, cout).total;
+    return disco_ws(*this, B, cin, cout, hin, hout).total;
+}
+
+int64_t DiscoPlan::rows_workspace_bytes(int64_t B, int64_t cin, int64_t cout, int64_t nin,
+                                        int64_t nout) const {
+    return disco_ws(*this, B, cin, cout, nin, nout).total;
+}
+
+void DiscoPlan::input_rows(int64_t ho0, int64_t nout, int64_t* lo, int64_t* n) const {
+    require(ho0 >= 0 && nout >= 1 && ho0 + nout <= hout, "disco: output row range");
+    int64_t a = hin, b = -1;
+    for (int64_t h = ho0; h < ho0 + nout; ++h) {
+        a = std::min<int64_t>(a, band0[h]);
+        b = std::max<int64_t>(b, band0[h] + bandc[h]);
+    }
+    *lo = a;
+    *n = b - a;
 }
 
 void DiscoPlan::apply(const float* x, const float* mix, int64_t B, int64_t cin, int64_t cout,
                       float* y, void* ws, cudaStream_t st) {
+    apply_rows(x, 0, hin, 0, hout, mix, B, cin, cout, y, ws, st);
+}
+
+void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t ho0, int64_t nout,
+                           const float* mix, int64_t B, int64_t cin, int64_t cout, float* y,
+                           void* ws, cudaStream_t st) {
     require(B >= 0 && cin >= 1 && cout >= 1, "disco_apply: mix tensor shape mismatch");
+    require(ho0 >= 0 && nout >= 1 && ho0 + nout <= hout, "disco_apply: output row range");
+    require(h_in0 >= 0 && nin >= 1 && h_in0 + nin <= hin, "disco_apply: input row range");
+    for (int64_t h = ho0; h < ho0 + nout; ++h)
+        require(band0[h] >= h_in0 && band0[h] + bandc[h] <= h_in0 + nin,
+                "disco_apply: input rows do not cover the filter support of the output rows");
     if (B == 0) return;
     SPH_CUDA(cudaSetDevice(device));
-    const DiscoWs w = disco_ws(*this, B, cin, cout);
+    const DiscoWs w = disco_ws(*this, B, cin, cout, nin, nout);
     uint8_t* base = static_cast<uint8_t*>(ws);
     if (!base) {
         std::lock_guard<std::mutex> lk(mu);
@@ -381,11 +413,11 @@ void DiscoPlan::apply(const float* x, const float* mix, int64_t B, int64_t cin, 
     float* wlo = reinterpret_cast<float*>(base + w.wlo_off);
     split_rows(mix, cout, cin * K, w.ldS, whi, wlo, st);
     const bool direct = prec == SPH_PREC_FP32_SIMT;
-    const int64_t rows_per_b = direct ? hout * wout : hout * nbo * 2;
+    const int64_t rows_per_b = direct ? nout * wout : nout * nbo * 2;
     const GroupedGemm* gp;
     {
         std::lock_guard<std::mutex> lk(mu);
-        auto& slot = gemm_cache[std::make_tuple(B, cin, cout, direct ? 1 : 0)];
+        auto& slot = gemm_cache[std::make_tuple(B, cin, cout, nout)];
         if (!slot) {
             auto g = std::make_unique<GroupedGemm>();
             g->A = {nullptr, B * rows_per_b, cin * K, w.ldS};
@@ -393,6 +425,7 @@ void DiscoPlan::apply(const float* x, const float* mix, int64_t B, int64_t cin, 
             g->Blo = {nullptr, cout, cin * K, w.ldS};
             g->store = STORE_TRANS;
             g->bn = cout >= 256 ? 256 : 128;
+            g->name = "gemm_disco_mix";
             require(B * rows_per_b < (1LL << 31), "disco: batch too large for one call");
             for (int64_t b = 0; b < B; ++b) {
                 GemmGroup gr;
@@ -413,30 +446,35 @@ void DiscoPlan::apply(const float* x, const float* mix, int64_t B, int64_t cin, 
     }
     float* S = reinterpret_cast<float*>(base + w.s_off);
     if (direct) {
-        dim3 grid(static_cast<unsigned>(hout), static_cast<unsigned>(cin), static_cast<unsigned>(B));
+        dim3 grid(static_cast<unsigned>(nout), static_cast<unsigned>(cin), static_cast<unsigned>(B));
         require(cin <= 65535 && B <= 65535, "disco: too many channels for the gather grid");
-        ProfScope prof("disco_gather", st);
-        disco_gather_kernel<<<grid, 256, 0, st>>>(x, d_row_ptr.p, d_h_in.p, d_w_rel.p, d_vals.p, hin,
-                                                  win, hout, wout, stride, K, cin, w.ldS, S);
-        SPH_LAUNCH_CHECK();
+        {
+            ProfScope prof("disco_gather", st);
+            disco_gather_kernel<<<grid, 256, 0, st>>>(x, d_row_ptr.p, d_h_in.p, d_w_rel.p, d_vals.p,
+                                                      nin, win, nout, wout, stride, K, cin, w.ldS, S,
+                                                      h_in0, ho0);
+            SPH_LAUNCH_CHECK();
+        }
         count_launch();
         gemm_run(*gp, S, y, prec, st, whi, wlo);
         return;
     }
     float2* U = reinterpret_cast<float2*>(base + w.u_off);
     float* Yh = reinterpret_cast<float*>(base + w.y_off);
-    fft_forward_cminor(fft_in, x, B, cin, hin, static_cast<int>(nbi), U, st);
-    dim3 grid(static_cast<unsigned>((nbo + 3) / 4), static_cast<unsigned>(hout), static_cast<unsigned>(B));
-    require(hout <= 65535 && B <= 65535, "disco: grid too large");
-    ProfScope prof("disco_band", st);
-    disco_band_kernel<<<grid, 256, 0, st>>>(U, d_psi_hat.p, d_band0.p, d_bandc.p, d_psi_off.p, hin,
-                                            nbi, hout, nbo, static_cast<int>(win),
-                                            static_cast<int>(wout), static_cast<int>(stride), K,
-                                            cin, w.ldS, S);
-    SPH_LAUNCH_CHECK();
+    fft_forward_cminor(fft_in, x, B, cin, nin, static_cast<int>(nbi), U, st);
+    dim3 grid(static_cast<unsigned>((nbo + 3) / 4), static_cast<unsigned>(nout), static_cast<unsigned>(B));
+    require(nout <= 65535 && B <= 65535, "disco: grid too large");
+    {
+        ProfScope prof("disco_band", st);
+        disco_band_kernel<<<grid, 256, 0, st>>>(U, d_psi_hat.p, d_band0.p, d_bandc.p, d_psi_off.p, nin,
+                                                nbi, nout, nbo, static_cast<int>(win),
+                                                static_cast<int>(wout), static_cast<int>(stride), K,
+                                                cin, w.ldS, S, h_in0, ho0);
+        SPH_LAUNCH_CHECK();
+    }
     count_launch();
     gemm_run(*gp, S, Yh, prec, st, whi, wlo);
-    fft_inverse_plain(fft_out, reinterpret_cast<const float2*>(Yh), B * cout * hout,
+    fft_inverse_plain(fft_out, reinterpret_cast<const float2*>(Yh), B * cout * nout,
                       static_cast<int>(nbo), static_cast<float>(1.0 / static_cast<double>(win)), y,
                       st);
 }

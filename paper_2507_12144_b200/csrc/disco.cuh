@@ -47,7 +47,7 @@ struct DiscoPlan {
     int prec = SPH_PREC_3XTF32;
 
     std::mutex mu;
-    std::map<std::tuple<int64_t, int64_t, int64_t, int>, std::unique_ptr<GroupedGemm>> gemm_cache;
+    std::map<std::tuple<int64_t, int64_t, int64_t, int64_t>, std::unique_ptr<GroupedGemm>> gemm_cache;
     DevBuf<uint8_t> own_ws;
 
     void create(int in_kind, int64_t in_nlat, int64_t in_nlon, int out_kind, int64_t out_nlat,
@@ -55,6 +55,12 @@ struct DiscoPlan {
     int64_t workspace_bytes(int64_t B, int64_t cin, int64_t cout) const;
     void apply(const float* x, const float* mix, int64_t B, int64_t cin, int64_t cout, float* y,
                void* ws, cudaStream_t st);
+    // output rows [ho0, ho0+nout) from input rows [h_in0, h_in0+nin) (latitude shards)
+    void apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t ho0, int64_t nout,
+                    const float* mix, int64_t B, int64_t cin, int64_t cout, float* y, void* ws,
+                    cudaStream_t st);
+    void input_rows(int64_t ho0, int64_t nout, int64_t* lo, int64_t* n) const;
+    int64_t rows_workspace_bytes(int64_t B, int64_t cin, int64_t cout, int64_t nin, int64_t nout) const;
 };
 
 void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, int64_t cin,

@@ -1,0 +1,393 @@
+"""Domain-decomposed distributed SHT and DISCO (the paper's Algorithms 1-2,
+/root/reference/proj/include/sphere/distsim.hpp:404-547) across real processes.
+
+One process per GPU; ``torch.distributed`` (NCCL over NVLink/NVSwitch on the B200 box,
+gloo for the CPU tests of the host logic) carries the collectives; the per-rank compute
+runs in libsphgpu.so through a ``GpuBackend``.  The rank cube, canonical uneven splits,
+the transpose semantics and the traffic CSV mirror the reference simulator:
+
+* ``CommGrid`` / ``canonical_split`` / ``split_offset``      distsim.hpp:45-110
+* ``TrafficLog`` (operation,axis,collective,bytes,calls)      distsim.hpp:120-150
+* ``distributed_transpose``  all-to-all within an axis group  distsim.hpp:170-210
+* ``dist_sht_forward``       T1 -> FFT -> T2 -> T3 -> Legendre -> T4     :404-463
+* ``dist_disco_apply``       T1 -> latitude HALO -> local band contraction and partial
+                             channel mix -> reduce-scatter over azimuth (instead of the
+                             reference's reduce-scatter of K-expanded partial sums over
+                             polar + T2 + mix, :468-547)
+
+Byte counts in the traffic log are this implementation's (fp32 / complex64 payloads),
+summed over all ranks like the simulator's; the reference moves fp64.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+BATCH, ENSEMBLE, POLAR, AZIMUTH = 0, 1, 2, 3
+AXIS_NAMES = {BATCH: "batch", ENSEMBLE: "ensemble", POLAR: "polar", AZIMUTH: "azimuth"}
+
+
+def canonical_split(n: int, p: int) -> List[int]:
+    """ceil(n/p) for the first n mod p parts, floor(n/p) for the rest (distsim.hpp:100-104)."""
+    parts = [n // p] * p
+    for k in range(n % p):
+        parts[k] += 1
+    return parts
+
+
+def split_offset(parts: Sequence[int], k: int) -> int:
+    return int(sum(parts[:k]))
+
+
+@dataclass
+class CommGrid:
+    """Orthogonal (batch, ensemble, polar, azimuth) rank cube (distsim.hpp:45-98)."""
+    sizes: Tuple[int, int, int, int] = (1, 1, 1, 1)
+
+    def __post_init__(self):
+        if any(s < 1 for s in self.sizes):
+            raise ValueError("CommGrid: sizes must be >= 1")
+        self.sizes = tuple(int(s) for s in self.sizes)
+
+    def world(self) -> int:
+        n = 1
+        for s in self.sizes:
+            n *= s
+        return n
+
+    def axis_size(self, axis: int) -> int:
+        return self.sizes[axis]
+
+    def coords(self, rank: int) -> List[int]:
+        c = [0, 0, 0, 0]
+        c[3] = rank % self.sizes[3]
+        rank //= self.sizes[3]
+        c[2] = rank % self.sizes[2]
+        rank //= self.sizes[2]
+        c[1] = rank % self.sizes[1]
+        rank //= self.sizes[1]
+        c[0] = rank
+        return c
+
+    def rank_of(self, c: Sequence[int]) -> int:
+        return ((c[0] * self.sizes[1] + c[1]) * self.sizes[2] + c[2]) * self.sizes[3] + c[3]
+
+    def group_of(self, rank: int, axis: int) -> List[int]:
+        c = self.coords(rank)
+        out = []
+        for k in range(self.sizes[axis]):
+            c[axis] = k
+            out.append(self.rank_of(c))
+        return out
+
+    def groups(self, axis: int) -> List[List[int]]:
+        seen = [False] * self.world()
+        out = []
+        for r in range(self.world()):
+            if seen[r]:
+                continue
+            g = self.group_of(r, axis)
+            for m in g:
+                seen[m] = True
+            out.append(g)
+        return out
+
+
+@dataclass
+class TrafficRecord:
+    operation: str
+    axis: str
+    collective: str
+    bytes: int = 0
+    calls: int = 0
+
+
+class TrafficLog:
+    """Same CSV schema as the reference (distsim.hpp:120-150)."""
+
+    def __init__(self):
+        self.op = "unnamed"
+        self.records: List[TrafficRecord] = []
+
+    def set_operation(self, op: str) -> None:
+        self.op = op
+
+    def record(self, axis: str, collective: str, nbytes: int) -> None:
+        for r in self.records:
+            if r.operation == self.op and r.axis == axis and r.collective == collective:
+                r.bytes += nbytes
+                r.calls += 1
+                return
+        self.records.append(TrafficRecord(self.op, axis, collective, nbytes, 1))
+
+    def calls(self, op: str, collective: str) -> int:
+        return sum(r.calls for r in self.records if r.operation == op and r.collective == collective)
+
+    def csv(self) -> str:
+        out = "operation,axis,collective,bytes,calls\n"
+        for r in self.records:
+            out += f"{r.operation},{r.axis},{r.collective},{r.bytes},{r.calls}\n"
+        return out
+
+
+class DistContext:
+    """The rank's view of the communicator hierarchy (distsim.hpp:160-163), backed by
+    torch.distributed process groups, one per axis group (all ranks build every group
+    in the same order, as new_group requires)."""
+
+    def __init__(self, grid: CommGrid):
+        if not dist.is_initialized():
+            raise RuntimeError("DistContext: torch.distributed is not initialised")
+        if dist.get_world_size() != grid.world():
+            raise ValueError("DistContext: world size does not match the CommGrid")
+        self.grid = grid
+        self.rank = dist.get_rank()
+        self.coords = grid.coords(self.rank)
+        self.log = TrafficLog()
+        self.pg: Dict[int, Optional[dist.ProcessGroup]] = {}
+        self.members: Dict[int, List[int]] = {}
+        for axis in (BATCH, ENSEMBLE, POLAR, AZIMUTH):
+            mine = grid.group_of(self.rank, axis)
+            self.members[axis] = mine
+            self.pg[axis] = None
+            if grid.axis_size(axis) == 1:
+                continue
+            for g in grid.groups(axis):
+                pg = dist.new_group(g)
+                if self.rank in g:
+                    self.pg[axis] = pg
+
+    def index(self, axis: int) -> int:
+        return self.coords[axis]
+
+    def _sum_bytes(self, n: int, like: torch.Tensor) -> int:
+        t = torch.tensor([n], dtype=torch.int64, device=like.device)
+        dist.all_reduce(t)
+        return int(t.item())
+
+
+def distributed_transpose(ctx: DistContext, x: torch.Tensor, axis: int, dim_from: int, dim_to: int,
+                          parts_from: Sequence[int]) -> Tuple[torch.Tensor, List[int]]:
+    """All-to-all within this rank's ``axis`` group (distsim.hpp:170-210): ``dim_from``
+    (sharded as ``parts_from`` over the group) becomes local, ``dim_to`` (local) becomes
+    canonically sharded.  Returns the new local tensor and the split of ``dim_to``."""
+    p = ctx.grid.axis_size(axis)
+    extent_to = x.shape[dim_to]
+    parts_to = canonical_split(extent_to, p)
+    if p == 1:
+        ctx.log.record(AXIS_NAMES[axis], "all_to_all", 0)
+        return x, parts_to
+    me = ctx.index(axis)
+    # send: slice j of dim_to to member j
+    chunks = [x.narrow(dim_to, split_offset(parts_to, j), parts_to[j]).contiguous() for j in range(p)]
+    send = torch.cat([c.reshape(-1) for c in chunks])
+    in_splits = [c.numel() for c in chunks]
+    # receive: member i's block has dim_from = parts_from[i], dim_to = parts_to[me]
+    shapes = []
+    for i in range(p):
+        s = list(x.shape)
+        s[dim_from] = parts_from[i]
+        s[dim_to] = parts_to[me]
+        shapes.append(s)
+    out_splits = [int(torch.Size(s).numel()) for s in shapes]
+    recv = torch.empty(sum(out_splits), dtype=x.dtype, device=x.device)
+    dist.all_to_all_single(recv, send, out_splits, in_splits, group=ctx.pg[axis])
+    blocks = list(torch.split(recv, out_splits))
+    y = torch.cat([b.view(s) for b, s in zip(blocks, shapes)], dim=dim_from)
+    sent = (send.numel() - in_splits[me]) * x.element_size()
+    ctx.log.record(AXIS_NAMES[axis], "all_to_all", ctx._sum_bytes(sent, x))
+    return y, parts_to
+
+
+# ------------------------------------------------------------- compute backends
+class GpuBackend:
+    """Per-rank compute in libsphgpu.so (sm_100a): the FFT and Legendre stages of the
+    SHT (sph_sht_fft_stage / sph_sht_legendre_stage) and the latitude-shard DISCO
+    (sph_disco_apply_rows)."""
+
+    def __init__(self, precision: str = "3xtf32"):
+        from . import sphere as S
+        self.S = S
+        self.precision = precision
+
+    def _plan(self, grid, lmax, mmax):
+        return self.S.get_sht_plan(grid, lmax, mmax, self.precision, allow_equiangular_forward=True)
+
+    def fft_stage(self, grid, lmax, mmax, x: torch.Tensor) -> torch.Tensor:
+        """x [C, h, nlon] -> [C, h, mmax, 2] (complex bins * 2pi/nlon)."""
+        C, h, _ = x.shape
+        return self._plan(grid, lmax, mmax).fft_stage(x.contiguous(), C, h)
+
+    def legendre_stage(self, grid, lmax, mmax, bins: torch.Tensor, m0: int) -> torch.Tensor:
+        """bins [C, nlat, mloc, 2] -> [C, lmax, mloc, 2]."""
+        C, _, mloc, _ = bins.shape
+        return self._plan(grid, lmax, mmax).legendre_stage(bins.contiguous(), C, m0, mloc)
+
+    def disco_rows(self, op, x: torch.Tensor, h_in0: int, ho0: int, nout: int,
+                   mix: torch.Tensor) -> torch.Tensor:
+        """x [C, nin, win] -> partial y [Cout, nout, wout] over the channels of x."""
+        return op.apply_rows(x.unsqueeze(0), h_in0, ho0, nout, mix)[0]
+
+
+# ------------------------------------------------------------------- algorithms
+@dataclass
+class Sharded:
+    """A rank's local block plus the split bookkeeping of its sharded dims
+    (RankView, distsim.hpp:154-158)."""
+    local: torch.Tensor
+    split: Dict[int, List[int]] = field(default_factory=dict)
+
+
+def shard_field(ctx: DistContext, x: torch.Tensor) -> Sharded:
+    """[C, H, W] global -> this rank's [C, Hloc, Wloc] (dims 1/2 over polar/azimuth)."""
+    g = ctx.grid
+    hp = canonical_split(x.shape[1], g.axis_size(POLAR))
+    wp = canonical_split(x.shape[2], g.axis_size(AZIMUTH))
+    if hp[-1] == 0 or wp[-1] == 0:
+        raise ValueError("shard: extent smaller than rank count")
+    i, j = ctx.index(POLAR), ctx.index(AZIMUTH)
+    loc = x.narrow(1, split_offset(hp, i), hp[i]).narrow(2, split_offset(wp, j), wp[j]).contiguous()
+    return Sharded(loc, {1: hp, 2: wp})
+
+
+def unshard(ctx: DistContext, s: Sharded) -> torch.Tensor:
+    """Gather the global tensor of a (polar, azimuth)-sharded [C, A, B, ...] block on every
+    rank (test / inspection helper; all_gather_object-free, uses all_gather)."""
+    g = ctx.grid
+    hp, wp = s.split[1], s.split[2]
+    world = g.world()
+    locs = [None] * world
+    sizes = torch.tensor([s.local.numel()], device=s.local.device)
+    all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes)
+    maxn = int(max(a.item() for a in all_sizes))
+    buf = torch.zeros(maxn, dtype=s.local.dtype, device=s.local.device)
+    buf[: s.local.numel()] = s.local.reshape(-1)
+    bufs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf)
+    shape = list(s.local.shape)
+    shape[1] = sum(hp)
+    shape[2] = sum(wp)
+    out = torch.empty(shape, dtype=s.local.dtype, device=s.local.device)
+    for r in range(world):
+        c = g.coords(r)
+        if c[0] != ctx.coords[0] or c[1] != ctx.coords[1]:
+            continue
+        i, j = c[POLAR], c[AZIMUTH]
+        ls = list(s.local.shape)
+        ls[1], ls[2] = hp[i], wp[j]
+        n = int(torch.Size(ls).numel())
+        out.narrow(1, split_offset(hp, i), hp[i]).narrow(2, split_offset(wp, j), wp[j]).copy_(
+            bufs[r][:n].view(ls))
+    return out
+
+
+def dist_sht_forward(ctx: DistContext, x: Sharded, grid, lmax: int, mmax: int,
+                     backend=None) -> Sharded:
+    """Algorithm 1 (distsim.hpp:404-463).  x.local [C, Hloc, Wloc] -> [C, lmaxloc, mmaxloc, 2]
+    with dim 1 (l) over polar and dim 2 (m) over azimuth.  No grid-kind check, like the
+    reference (its only equiangular forward path)."""
+    backend = backend or GpuBackend()
+    ctx.log.set_operation("dist_sht")
+    if grid.nlon < 2 * mmax or grid.nlat < lmax:
+        raise ValueError("dist_sht_forward: resolution insufficient for lmax/mmax")
+    # T1: W -> C over azimuth
+    t, cparts_az = distributed_transpose(ctx, x.local, AZIMUTH, 2, 0, x.split[2])
+    if t.shape[2] != grid.nlon:
+        raise ValueError("dist_sht_forward: bookkeeping mismatch")
+    bins = backend.fft_stage(grid, lmax, mmax, t)                      # [Cloc, Hloc, mmax, 2]
+    # T2: C -> m over azimuth;  T3: H -> C over polar
+    bins, mparts = distributed_transpose(ctx, bins, AZIMUTH, 0, 2, cparts_az)
+    bins, cparts_pol = distributed_transpose(ctx, bins, POLAR, 1, 0, x.split[1])
+    if bins.shape[1] != grid.nlat:
+        raise ValueError("dist_sht_forward: latitude bookkeeping mismatch")
+    m0 = split_offset(mparts, ctx.index(AZIMUTH))
+    coeffs = backend.legendre_stage(grid, lmax, mmax, bins, m0)       # [Cloc, lmax, mloc, 2]
+    # T4: C -> l over polar
+    coeffs, lparts = distributed_transpose(ctx, coeffs, POLAR, 0, 1, cparts_pol)
+    return Sharded(coeffs, {1: lparts, 2: mparts})
+
+
+def _halo(ctx: DistContext, x: torch.Tensor, hparts: Sequence[int], need: Sequence[Tuple[int, int]]
+          ) -> torch.Tensor:
+    """Latitude halo over the polar group: every member q needs input rows
+    [need[q][0], need[q][0] + need[q][1]); this rank owns rows
+    [split_offset(hparts, me), +hparts[me]) of x [C, Hloc, W].  Returns this rank's
+    [C, need_n, W] block (own rows + halo rows from the neighbours)."""
+    p = ctx.grid.axis_size(POLAR)
+    me = ctx.index(POLAR)
+    own0, own_n = split_offset(hparts, me), hparts[me]
+    lo, n = need[me]
+    C, _, W = x.shape
+    if p == 1:
+        ctx.log.record("polar", "halo", 0)
+        return x.narrow(1, lo - own0, n)
+
+    def inter(a0, an, b0, bn):
+        s, e = max(a0, b0), min(a0 + an, b0 + bn)
+        return (s, max(0, e - s))
+
+    sends, in_splits = [], []
+    for q in range(p):
+        s, m = inter(own0, own_n, need[q][0], need[q][1])
+        blk = x.narrow(1, s - own0, m).contiguous() if m else x.new_zeros((C, 0, W))
+        sends.append(blk.reshape(-1))
+        in_splits.append(blk.numel())
+    recv_shapes, out_splits = [], []
+    for q in range(p):
+        s, m = inter(split_offset(hparts, q), hparts[q], lo, n)
+        recv_shapes.append((s, m))
+        out_splits.append(C * m * W)
+    recv = torch.empty(sum(out_splits), dtype=x.dtype, device=x.device)
+    send = torch.cat(sends)
+    dist.all_to_all_single(recv, send, out_splits, in_splits, group=ctx.pg[POLAR])
+    out = torch.empty((C, n, W), dtype=x.dtype, device=x.device)
+    for blk, (s, m) in zip(torch.split(recv, out_splits), recv_shapes):
+        if m:
+            out.narrow(1, s - lo, m).copy_(blk.view(C, m, W))
+    sent = (send.numel() - in_splits[me]) * x.element_size()
+    ctx.log.record("polar", "halo", ctx._sum_bytes(sent, x))
+    return out
+
+
+def dist_disco_apply(ctx: DistContext, x: Sharded, op, mix: torch.Tensor, backend=None) -> Sharded:
+    """Algorithm 2 with a latitude halo (distsim.hpp:468-547 reorganised).  x.local
+    [C_in, Hloc_in, Wloc_in] -> [C_out, Hloc_out, Wloc_out] (H_out over polar, W_out over
+    azimuth, canonical splits like the reference's reduce_scatter / T2)."""
+    backend = backend or GpuBackend()
+    ctx.log.set_operation("dist_disco")
+    g = ctx.grid
+    nh, nw = g.axis_size(POLAR), g.axis_size(AZIMUTH)
+    hin, win = op.in_grid.nlat, op.in_grid.nlon
+    hout, wout = op.out_grid.nlat, op.out_grid.nlon
+    cout, cin, K = mix.shape
+    # T1: W -> C over azimuth (full input rings per rank)
+    t, cparts = distributed_transpose(ctx, x.local, AZIMUTH, 2, 0, x.split[2])
+    if t.shape[2] != win or t.shape[1] != x.split[1][ctx.index(POLAR)]:
+        raise ValueError("dist_disco_apply: bookkeeping mismatch")
+    # output-row shard of this polar index, and the input rows each member needs
+    hoparts = canonical_split(hout, nh)
+    need = [op.input_rows(split_offset(hoparts, q), hoparts[q]) for q in range(nh)]
+    rows = _halo(ctx, t, x.split[1], need)
+    ho0, nout = split_offset(hoparts, ctx.index(POLAR)), hoparts[ctx.index(POLAR)]
+    c0 = split_offset(cparts, ctx.index(AZIMUTH))
+    part = backend.disco_rows(op, rows, need[ctx.index(POLAR)][0], ho0, nout,
+                              mix[:, c0:c0 + t.shape[0], :].contiguous())   # [Cout, nout, wout]
+    # sum the channel-slice partials over azimuth and scatter W_out canonically
+    wparts = canonical_split(wout, nw)
+    if nw == 1:
+        ctx.log.record("azimuth", "reduce_scatter", 0)
+        return Sharded(part, {1: hoparts, 2: wparts})
+    mx = max(wparts)
+    padded = part.new_zeros((nw, cout, nout, mx))
+    for j in range(nw):
+        padded[j, :, :, :wparts[j]] = part.narrow(2, split_offset(wparts, j), wparts[j])
+    out = part.new_empty((cout, nout, mx))
+    dist.reduce_scatter_tensor(out.view(-1), padded.view(-1), group=ctx.pg[AZIMUTH])
+    me = ctx.index(AZIMUTH)
+    ctx.log.record("azimuth", "reduce_scatter",
+                   ctx._sum_bytes((nw - 1) * out.numel() * out.element_size(), part))
+    return Sharded(out[:, :, :wparts[me]].contiguous(), {1: hoparts, 2: wparts})

@@ -354,6 +354,32 @@ class DiscoOperator:
         return out
 
 
+    def input_rows(self, ho0: int, nout: int):
+        """Input latitude rows (h_in0, n_in) covering the filter support of output rows
+        [ho0, ho0 + nout) -- the halo a latitude shard needs."""
+        lo, n = C.c_int64(), C.c_int64()
+        check(L.lib.sph_disco_input_rows(self.h, ho0, nout, C.byref(lo), C.byref(n)))
+        return lo.value, n.value
+
+    def apply_rows(self, x: torch.Tensor, h_in0: int, ho0: int, nout: int, mix: torch.Tensor,
+                   out=None) -> torch.Tensor:
+        """Latitude-shard apply: x [B, cin, nin, win] holds input rows [h_in0, h_in0+nin);
+        returns output rows [ho0, ho0+nout) as [B, cout, nout, wout]."""
+        mix = _dev_f32(mix, "disco_apply")
+        x = _dev_f32(x, "disco_apply")
+        cout, cin, K = mix.shape
+        if K != self.n_basis or x.shape[-3] != cin:
+            raise L.SphInvalidArgument(1, "disco_apply: mix tensor shape mismatch")
+        B, nin = x.shape[0], x.shape[-2]
+        if out is None:
+            out = torch.empty((B, cout, nout, self.out_grid.nlon), dtype=torch.float32, device=x.device)
+        n = int(L.lib.sph_disco_rows_workspace_bytes(self.h, B, cin, cout, nin, nout))
+        ws = torch.empty(n, dtype=torch.uint8, device=x.device)
+        check(L.lib.sph_disco_apply_rows(self.h, _ptr(x), h_in0, nin, ho0, nout, _ptr(mix), B, cin,
+                                         cout, _ptr(out), _ptr(ws), _stream(x.device)))
+        return out
+
+
 def assemble_disco(in_grid: GridSpec, out_grid: GridSpec, basis: FilterBasis,
                    precision: str = "3xtf32") -> DiscoOperator:
     """convolution.hpp:141-177."""
