@@ -295,6 +295,15 @@ def run_ours(args, ws, rank, local):
                     "unit": "GB/s", "frac": achieved / hbm, "peak_note": f"{peak_src} copy bandwidth",
                     "share_of_step": tot_ms / args.steps / ms}
         roof["traffic"] = None
+        try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic_sht.json")) as f:
+                tj = json.load(f)
+            if args.workload == "sht" and name in tj["dram_bytes_per_launch"]:
+                roof["traffic"] = tj["dram_bytes_per_launch"][name]
+                roof["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write)"
+                roof["algorithmic_per_launch"] = work / cnt
+        except Exception:
+            pass
         roof["per_kernel_ms"] = {k: v[1] / args.steps for k, v in sorted(prof.items())}
 
     # end-to-end through the public C ABI with pinned host buffers
