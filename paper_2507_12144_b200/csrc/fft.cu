@@ -241,39 +241,41 @@ struct FoldIO {
     }
 };
 
-// inverse SHT: Ev/Od rows -> Hermitian spectra of the ring pair -> rings
+// inverse SHT: Ev/Od -> Hermitian spectra of the ring pair -> rings.  Input layout
+// EOi[m][parity][R][2F] (the inverse GEMM's transposed store), so a CTA takes one folded
+// row r and P consecutive fields: per order m it reads 2 x P float2 (64-byte runs).
 struct UnfoldIO {
     const float* eoi;
     const int2* rows;
     int R, nlat, msynth, lmax;
-    int64_t ld_eo, twoF;
+    int64_t F, twoF;
     float* y;
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
-        const int r0 = blockIdx.x * P, f = blockIdx.y;
-        const int nr = min(static_cast<int>(P), R - r0);
+        const int r = blockIdx.y;  // field tiles fastest: neighbouring CTAs read adjacent runs
+        const int64_t f0 = static_cast<int64_t>(blockIdx.x) * P;
+        const int nf = static_cast<int>(min(static_cast<int64_t>(P), F - f0));
         const int j = threadIdx.x % P;
         const int mstep = blockDim.x / P;
         const int m0 = threadIdx.x / P;
         float2* zr = buf + j * ld;
-        // bins [msynth, n - msynth] are zero
         for (int k = msynth + m0; k <= n - msynth; k += mstep) zr[k] = make_float2(0.f, 0.f);
-        if (j >= nr) {
+        if (j >= nf) {
             for (int m = m0; m < msynth; m += mstep) {
                 zr[m] = make_float2(0.f, 0.f);
                 if (m) zr[n - m] = make_float2(0.f, 0.f);
             }
             return;
         }
-        const bool pair = rows[r0 + j].y >= 0;
-        const float* e = eoi + (2 * static_cast<int64_t>(f)) * ld_eo + r0 + j;
-        const int64_t so = twoF * ld_eo, sm = 2 * so;
+        const bool pair = rows[r].y >= 0;
+        const float2* e = reinterpret_cast<const float2*>(eoi + static_cast<int64_t>(r) * twoF + 2 * (f0 + j));
+        const int64_t so = static_cast<int64_t>(R) * F;  // parity stride in float2
+        const int64_t sm = 2 * so;                        // order stride in float2
         for (int m = m0; m < msynth; m += mstep) {
-            const float* em = e + m * sm;
+            const float2* em = e + m * sm;
             const int l0 = (lmax - m + 1) / 2, l1 = (lmax - m) / 2;  // L_{m,0}, L_{m,1}
-            float2 ev = make_float2(0.f, 0.f), od = make_float2(0.f, 0.f);
-            if (l0 > 0) ev = make_float2(em[0], em[ld_eo]);
-            if (l1 > 0) od = make_float2(em[so], em[so + ld_eo]);
+            const float2 ev = l0 > 0 ? em[0] : make_float2(0.f, 0.f);
+            const float2 od = l1 > 0 ? em[so] : make_float2(0.f, 0.f);
             const float2 ha = cadd(ev, od);
             const float2 hb = pair ? csub(ev, od) : make_float2(0.f, 0.f);
             if (m == 0) {
@@ -286,27 +288,19 @@ struct UnfoldIO {
     }
     template <class PT, class NT>
     __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
-        const int r0 = blockIdx.x * P, f = blockIdx.y;
-        const int nr = min(static_cast<int>(P), R - r0);
-        float* yf = y + static_cast<int64_t>(f) * nlat * n;
+        const int r = blockIdx.y;  // field tiles fastest: neighbouring CTAs read adjacent runs
+        const int64_t f0 = static_cast<int64_t>(blockIdx.x) * P;
+        const int nf = static_cast<int>(min(static_cast<int64_t>(P), F - f0));
+        const int2 rw = rows[r];
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-        for (int j = warp; j < nr; j += nw) {
-            const int2 rw = rows[r0 + j];
+        for (int j = warp; j < nf; j += nw) {
             const float2* zr = buf + j * ld;
+            float* yf = y + (f0 + j) * nlat * n;
             float* pa = yf + static_cast<int64_t>(rw.x) * n;
             float* pb = yf + static_cast<int64_t>(rw.y) * n;
-            if ((n & 3) == 0) {
-                const float4* z4 = reinterpret_cast<const float4*>(zr);
-                for (int k4 = lane; k4 < n / 4; k4 += 32) {
-                    const float4 u = z4[2 * k4], v = z4[2 * k4 + 1];
-                    reinterpret_cast<float4*>(pa)[k4] = make_float4(u.x, u.z, v.x, v.z);
-                    if (rw.y >= 0) reinterpret_cast<float4*>(pb)[k4] = make_float4(u.y, u.w, v.y, v.w);
-                }
-            } else {
-                for (int k = lane; k < n; k += 32) {
-                    pa[k] = zr[k].x;
-                    if (rw.y >= 0) pb[k] = zr[k].y;
-                }
+            for (int k = lane; k < n; k += 32) {
+                pa[k] = zr[k].x;
+                if (rw.y >= 0) pb[k] = zr[k].y;
             }
         }
     }
@@ -435,6 +429,84 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_kernel(IO io, const flo
     io.store(sm4, PC{}, NC{}, LD);
 }
 
+
+// Forward SHT ring transform, fused IO (n = N1*45): phase A loads its N1 strided ring
+// samples of both rings of the pair straight from HBM into registers (a warp reads 32
+// consecutive samples per load -> 128-byte segments, 2*N1 independent loads in flight
+// per thread), so the input never takes a shared-memory staging pass.
+template <int N1>
+__global__ void __launch_bounds__(fft4::THREADS, 2) fft4_fold_kernel(FoldIO io, const float2* __restrict__ twT) {
+    extern __shared__ float2 smf[];
+    constexpr int N2 = 45, N = N1 * N2, P = fft4::THREADS / N1, LD = N + 2;
+    const int r0 = blockIdx.x * P, f = blockIdx.y;
+    const int nr = min(P, io.R - r0);
+    const float* xf = io.x + static_cast<int64_t>(f) * io.nlat * N;
+    for (int it = threadIdx.x; it < P * N2; it += fft4::THREADS) {
+        const int p = it / N2, n2 = it - p * N2;
+        float2 a[N1];
+        if (p < nr) {
+            const int2 rw = io.rows[r0 + p];
+            const float* pa = xf + static_cast<int64_t>(rw.x) * N + n2;
+            const float* pb = xf + static_cast<int64_t>(rw.y < 0 ? rw.x : rw.y) * N + n2;
+            const float sb = rw.y < 0 ? 0.f : 1.f;
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) a[n1] = make_float2(__ldg(pa + N2 * n1), sb * __ldg(pb + N2 * n1));
+        } else {
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) a[n1] = make_float2(0.f, 0.f);
+        }
+        fft4::phase_a_store<N1, N2, LD, false>(a, smf, p, n2, twT);
+    }
+    __syncthreads();
+    float2 b[N2];
+    fft4::phase_b_regs<N1, N2, LD, false>(smf, b);
+    __syncthreads();
+    {
+        const int p = threadIdx.x / N1, k1 = threadIdx.x - p * N1;
+        float2* dst = smf + p * LD + k1;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) dst[N1 * k2] = b[k2];
+    }
+    __syncthreads();
+    io.store(smf, std::integral_constant<int, P>{}, std::integral_constant<int, N>{}, LD);
+}
+
+// Inverse SHT ring transform, fused IO: phase B stores the synthesised ring samples
+// straight from registers to HBM (Re -> ring a, Im -> ring b; a warp writes 32
+// consecutive samples per store).
+template <int N1>
+__global__ void __launch_bounds__(fft4::THREADS, 2) fft4_unfold_kernel(UnfoldIO io, const float2* __restrict__ twT) {
+    extern __shared__ float2 smu[];
+    constexpr int N2 = 45, N = N1 * N2, P = fft4::THREADS / N1, LD = N + 2;
+    io.load(smu, std::integral_constant<int, P>{}, std::integral_constant<int, N>{}, LD);
+    __syncthreads();
+    for (int it = threadIdx.x; it < P * N2; it += fft4::THREADS) {
+        const int p = it / N2, n2 = it - p * N2;
+        float2 a[N1];
+        const float2* r = smu + p * LD + n2;
+#pragma unroll
+        for (int n1 = 0; n1 < N1; ++n1) a[n1] = r[N2 * n1];
+        fft4::phase_a_store<N1, N2, LD, true>(a, smu, p, n2, twT);
+    }
+    __syncthreads();
+    float2 b[N2];
+    fft4::phase_b_regs<N1, N2, LD, true>(smu, b);
+    const int p = threadIdx.x / N1, k1 = threadIdx.x - p * N1;
+    const int64_t f = static_cast<int64_t>(blockIdx.x) * P + p;
+    if (f < io.F) {
+        const int2 rw = io.rows[blockIdx.y];
+        float* yf = io.y + f * io.nlat * N;
+        float* pa = yf + static_cast<int64_t>(rw.x) * N + k1;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) pa[N1 * k2] = b[k2].x;
+        if (rw.y >= 0) {
+            float* pb = yf + static_cast<int64_t>(rw.y) * N + k1;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) pb[N1 * k2] = b[k2].y;
+        }
+    }
+}
+
 template <bool INV, class IO>
 __global__ void __launch_bounds__(FFT_THREADS) stockham_kernel(IO io, FftArgs a, const float2* __restrict__ tw,
                                                                int rpb) {
@@ -492,6 +564,30 @@ void launch4(const FftPlan& fp, const IO& io, dim3 grid, cudaStream_t st) {
     const size_t sm = static_cast<size_t>(fft4::THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
     set_smem_once(fft4_kernel<N1, INV, IO>, sm);
     fft4_kernel<N1, INV, IO><<<grid, fft4::THREADS, sm, st>>>(io, fp.twT.p);
+}
+
+template <bool FWD>
+void launch_fused(const FftPlan& fp, const FoldIO& fio, const UnfoldIO& uio, dim3 grid, cudaStream_t st) {
+    auto go = [&](auto n1c) {
+        constexpr int N1 = decltype(n1c)::value;
+        const size_t sm = static_cast<size_t>(fft4::THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
+        if (FWD) {
+            set_smem_once(fft4_fold_kernel<N1>, sm);
+            fft4_fold_kernel<N1><<<grid, fft4::THREADS, sm, st>>>(fio, fp.twT.p);
+        } else {
+            set_smem_once(fft4_unfold_kernel<N1>, sm);
+            fft4_unfold_kernel<N1><<<grid, fft4::THREADS, sm, st>>>(uio, fp.twT.p);
+        }
+    };
+    switch (fp.fft4_n1) {
+        case 4: go(std::integral_constant<int, 4>{}); break;
+        case 8: go(std::integral_constant<int, 8>{}); break;
+        case 16: go(std::integral_constant<int, 16>{}); break;
+        case 32: go(std::integral_constant<int, 32>{}); break;
+        default: fail(SPH_ERR_RUNTIME, "fft4: unsupported split");
+    }
+    SPH_LAUNCH_CHECK();
+    count_launch();
 }
 
 // rows-per-block of the engine chosen for this plan
@@ -573,8 +669,13 @@ void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int
     const int P = rpb_of(fp);
     FoldIO io{x, fr.d_rows.p, fr.R, nlat, mmax, eo, ld_eo, 2 * F};
     dim3 grid((fr.R + P - 1) / P, static_cast<unsigned>(F));
-    run_transform<false>(fp, io, grid, st, "fft_fwd_fold",
-                         4.0 * F * (static_cast<double>(nlat) * fp.n + 4.0 * mmax * fr.R));
+    const double bytes = 4.0 * F * (static_cast<double>(nlat) * fp.n + 4.0 * mmax * fr.R);
+    if (fp.fft4_n1) {
+        ProfScope prof("fft_fwd_fold", st, bytes);
+        launch_fused<true>(fp, io, UnfoldIO{}, grid, st);
+        return;
+    }
+    run_transform<false>(fp, io, grid, st, "fft_fwd_fold", bytes);
 }
 
 void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi, int64_t F,
@@ -584,10 +685,17 @@ void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi,
     if (F == 0) return;
     require(F <= 65535, "fft: at most 65535 fields per call");
     const int P = rpb_of(fp);
-    UnfoldIO io{eoi, fr.d_rows.p, fr.R, nlat, msynth, lmax, ld_eo, 2 * F, y};
-    dim3 grid((fr.R + P - 1) / P, static_cast<unsigned>(F));
-    run_transform<true>(fp, io, grid, st, "fft_inv_unfold",
-                        4.0 * F * (static_cast<double>(nlat) * fp.n + 4.0 * msynth * fr.R));
+    (void)ld_eo;  // EOi is [m][parity][R][2F] (transposed GEMM store)
+    UnfoldIO io{eoi, fr.d_rows.p, fr.R, nlat, msynth, lmax, F, 2 * F, y};
+    require(fr.R <= 65535, "fft: too many latitude rows");
+    dim3 grid(static_cast<unsigned>((F + P - 1) / P), static_cast<unsigned>(fr.R));
+    const double bytes = 4.0 * F * (static_cast<double>(nlat) * fp.n + 4.0 * msynth * fr.R);
+    if (fp.fft4_n1) {
+        ProfScope prof("fft_inv_unfold", st, bytes);
+        launch_fused<false>(fp, FoldIO{}, io, grid, st);
+        return;
+    }
+    run_transform<true>(fp, io, grid, st, "fft_inv_unfold", bytes);
 }
 
 void fft_forward_plain(const FftPlan& fp, const float* rings, int64_t nrings, int nbins,

@@ -42,7 +42,8 @@ struct FoldRows {
 void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int64_t F,
                       int nlat, int mmax, float* eo, int64_t ld_eo, cudaStream_t st);
 
-// Inverse: EOi (same layout, Ev/Od per folded row) -> y [F][nlat][nlon].
+// Inverse: EOi[(m*2+p)][r][2f+reim] (Ev/Od per folded row, the inverse GEMM's
+// transposed store; ld_eo unused) -> y [F][nlat][nlon].
 // Orders m < msynth are used; groups (m,p) with no Legendre degrees (L_mp = 0) are
 // treated as zero: L_mp = number of l in [m, lmax) with (l - m) % 2 == p.
 void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi, int64_t F,

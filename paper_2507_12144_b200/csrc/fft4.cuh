@@ -209,5 +209,32 @@ __device__ __forceinline__ void transform(float2* buf, const float2* __restrict_
     __syncthreads();
 }
 
+// Phase A for one item given its N1 inputs in registers: DFT, inter-twiddle, write the
+// N1 outputs to buf[p*LD + n2 + N2*k1].
+template <int N1, int N2, int LD, bool INV>
+__device__ __forceinline__ void phase_a_store(float2 (&a)[N1], float2* buf, int p, int n2,
+                                              const float2* __restrict__ twT) {
+    dft<N1, N1, 0, 1, INV>(a);
+#pragma unroll
+    for (int k1 = 1; k1 < N1; ++k1) {
+        float2 w = __ldg(twT + k1 * N2 + n2);
+        if (INV) w.y = -w.y;
+        a[k1] = make_float2(a[k1].x * w.x - a[k1].y * w.y, a[k1].x * w.y + a[k1].y * w.x);
+    }
+    float2* r = buf + p * LD + n2;
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) r[N2 * k1] = a[k1];
+}
+
+// Phase B into registers: thread (p, k1) returns X[k1 + N1*k2], k2 < N2, of ring p.
+template <int N1, int N2, int LD, bool INV>
+__device__ __forceinline__ void phase_b_regs(const float2* buf, float2 (&b)[N2]) {
+    const int p = threadIdx.x / N1, k1 = threadIdx.x - p * N1;
+    const float2* src = buf + p * LD + N2 * k1;
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) b[n2] = src[n2];
+    dft<N2, N2, 0, 1, INV>(b);
+}
+
 }  // namespace fft4
 }  // namespace sph

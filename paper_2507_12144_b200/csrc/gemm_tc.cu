@@ -145,7 +145,8 @@ struct Smem {
     static constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     // full[S], conv[S], empty[S], tfull[2], tempty[2], tmem slot
-    static constexpr int TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
+    static constexpr int TILE_OFF = BAR_OFF + (3 * STAGES + 4) * 8 + 16;
+    static constexpr int TOTAL = TILE_OFF + 4 * 32 * 33 * 4 + 1024;  // + align slack
 };
 
 // CL > 1: thread-block cluster of CL CTAs on CL consecutive M-tiles of one (group,
@@ -177,6 +178,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     auto tfull_bar = [&](int a) { return bars + 8 * (3 * STAGES + a); };
     auto tempty_bar = [&](int a) { return bars + 8 * (3 * STAGES + 2 + a); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::BAR_OFF + (3 * STAGES + 4) * 8);
+    float* stile = reinterpret_cast<float*>(smem + L::TILE_OFF);  // epilogue transpose tiles
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -338,33 +340,39 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             const bool mok = m < g.M;
             const uint32_t trow = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
             float* dbase = D + g.d_off;
-            for (int c = 0; c < nrem; c += 16) {
-                float v[16];
-                tmem_ld16(trow + c, v);
-                const int n = tl.n0 + c;
-                if (store_mode == STORE_ROW) {
-                    if (mok) {
-                        float* dp = dbase + static_cast<int64_t>(m) * g.ldd + n;
-                        if (c + 16 <= nrem && (reinterpret_cast<uintptr_t>(dp) & 15) == 0) {
-#pragma unroll
-                            for (int j = 0; j < 16; j += 4)
-                                *reinterpret_cast<float4*>(dp + j) =
-                                    make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                if (c + j < nrem) dp[j] = v[j];
-                        }
-                        if (c + 16 >= nrem && tl.n0 + nrem == g.N)
-                            for (int z = g.N; z < g.zero_to; ++z)
-                                dbase[static_cast<int64_t>(m) * g.ldd + z] = 0.f;
+            if (store_mode == STORE_ROW) {
+                // per-warp 32x32 transpose through padded SMEM: each warp stores its 32
+                // rows as 128-byte row segments (coalesced) instead of one row per lane
+                float* tile = stile + q * 32 * 33;
+                const int row0 = tl.m0 + crank * BM + q * 32;
+                const int ncols = max(nrem, min(g.zero_to, tl.n0 + BN) - tl.n0);
+                for (int c = 0; c < ncols; c += 32) {
+                    float v[32];
+                    if (c < nrem) {
+                        tmem_ld16(trow + c, *reinterpret_cast<float(*)[16]>(&v[0]));
+                        tmem_ld16(trow + c + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
                     }
-                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = (c + j < nrem) ? v[j] : 0.f;
+                    __syncwarp();
+                    const int col = tl.n0 + c + lane;
+                    const bool cok = c + lane < ncols;
+#pragma unroll 4
+                    for (int r = 0; r < 32; ++r) {
+                        const int mr = row0 + r;
+                        if (cok && mr < g.M) dbase[static_cast<int64_t>(mr) * g.ldd + col] = tile[r * 33 + lane];
+                    }
+                    __syncwarp();
+                }
+            } else {
+                for (int c = 0; c < nrem; c += 16) {
+                    float v[16];
+                    tmem_ld16(trow + c, v);
+                    const int n = tl.n0 + c;
                     if (mok) {
 #pragma unroll
                         for (int j = 0; j < 16; ++j)
-                            if (c + j < nrem)
-                                dbase[static_cast<int64_t>(n + j) * g.ldd + m] = v[j];
+                            if (c + j < nrem) dbase[static_cast<int64_t>(n + j) * g.ldd + m] = v[j];
                     }
                 }
             }
@@ -560,9 +568,9 @@ void GroupedGemm::finalize() {
     if (!groups.empty())
         SPH_CUDA(cudaMemcpy(d_groups.p, groups.data(), groups.size() * sizeof(GemmGroup),
                             cudaMemcpyHostToDevice));
-    // table multicast: no measurable gain at cluster <= 4 (L2 does not dedup), keep 1
-    if (cluster == 0) cluster = 1;
-    (void)mtiles;
+    // table-tile multicast over clusters on neighbouring M-tiles (measured at cfg2,
+    // cluster 1 / 2 / 4: Legendre fwd 4.6 / 3.5 / 3.4 ms, inv 4.9 / 4.1 / 3.55 ms)
+    if (cluster == 0) cluster = mtiles >= 8 ? 4 : mtiles >= 4 ? 2 : 1;
     if (const char* e = std::getenv("SPH_GEMM_CLUSTER")) {  // test / tuning override
         const int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) cluster = v;

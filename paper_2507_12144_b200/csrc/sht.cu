@@ -320,7 +320,7 @@ const GroupedGemm& ShtPlan::inv_gemm(int64_t F) {
         g->A = {nullptr, mmax * 2 * 2 * F, Lmax_p, Lp};
         g->Bhi = {pi_hi.p, mmax * 2 * R, Lmax_p, Lp};
         g->Blo = {pi_lo.p, mmax * 2 * R, Lmax_p, Lp};
-        g->store = STORE_ROW;
+        g->store = STORE_TRANS;  // EOi[m][parity][R][2F]: coalesced reads for the iFFT
         g->bn = 256;
         g->name = "gemm_legendre_inv";
         for (int64_t m = 0; m < msynth; ++m)
@@ -333,9 +333,9 @@ const GroupedGemm& ShtPlan::inv_gemm(int64_t F) {
                 gr.M = static_cast<int32_t>(2 * F);
                 gr.N = R;
                 gr.K = static_cast<int32_t>(Lmp);
-                gr.ldd = Rp;
+                gr.ldd = static_cast<int32_t>(2 * F);
                 gr.zero_to = 0;
-                gr.d_off = (m * 2 + p) * 2 * F * Rp;
+                gr.d_off = (m * 2 + p) * 2 * F * static_cast<int64_t>(R);
                 g->groups.push_back(gr);
             }
         require(mmax * 2 * 2 * F < (1LL << 31), "sht: too many fields for one call");
