@@ -112,62 +112,109 @@ __global__ void split_rows_kernel(const float* __restrict__ src, int64_t rows, i
     lo[i] = x - h;
 }
 
-// Fourier band contraction + stride fold.  Block (m'-tile of 4, h_out, b); thread
-// (m' in tile, channel lane).  Output S[((b*Hout + h)*nbo + m')*2 + reim][c*K + k].
+// Fourier band contraction + stride fold.  Block = (m'-tile of 4, output row h);
+// threads = (m' in tile) x 64 channel lanes; the CTA loops over the batch.  The
+// psi_hat slice of the block (band rows x folds x 4 orders x K) is staged in shared
+// memory once and read as warp-broadcast float4s; the U loads of a band chunk are
+// issued together.  Output S[((b*Hout + h)*nbo + m')*2 + reim][c*K + k].
+constexpr int BAND_MAX_SLOTS = 64;  // band rows x folds staged per CTA
 __global__ void __launch_bounds__(256) disco_band_kernel(
     const float2* __restrict__ U, const float2* __restrict__ psi_hat, const int32_t* __restrict__ band0,
     const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, int64_t Hin, int64_t nbi,
     int64_t Hout, int64_t nbo, int win, int wout, int s, int K, int64_t C, int64_t ldS,
-    float* __restrict__ S, int64_t h_in0, int64_t ho0) {
+    float* __restrict__ S, int64_t h_in0, int64_t ho0, int64_t B) {
     // U holds input rows [h_in0, h_in0 + Hin); this launch computes output rows
     // [ho0, ho0 + Hout) (local index h)
+    __shared__ float4 ps[BAND_MAX_SLOTS][4][5];  // [band slot][m' in tile][k pairs] (K <= 9 -> 5 float4)
     const int mi = threadIdx.x / 64, cl = threadIdx.x % 64;
-    const int64_t mp = static_cast<int64_t>(blockIdx.x) * 4 + mi;
-    const int64_t h = blockIdx.y, b = blockIdx.z;
-    if (mp >= nbo) return;
+    const int64_t mp0 = static_cast<int64_t>(blockIdx.x) * 4;
+    const int64_t mp = mp0 + mi;
+    const int64_t h = blockIdx.y;
     const int64_t hg = ho0 + h;
     const int h0 = band0[hg] - static_cast<int>(h_in0), nb = bandc[hg];
     const int64_t po = psi_off[hg];
     const int half = win / 2;
-    for (int64_t c0 = 0; c0 < C; c0 += 64) {
-        const int64_t c = c0 + cl;
-        const bool valid = c < C;
-        float2 acc[9];
+    const int nslot = nb * s;
+    for (int slot0 = 0; slot0 < nslot; slot0 += BAND_MAX_SLOTS) {
+        const int ns = min(BAND_MAX_SLOTS, nslot - slot0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < ns * 4 * 10; i += blockDim.x) {
+            const int kk = i % 10, t = (i / 10) % 4, sl = i / 40;
+            const int slot = slot0 + sl;
+            const int bi = slot / s, q = slot - bi * s;
+            const int64_t m = mp0 + t;
+            float2 v = make_float2(0.f, 0.f);
+            if (m < nbo && kk < K) {
+                const int kq = static_cast<int>(m) + wout * q;
+                const int idx = kq > half ? win - kq : kq;
+                v = __ldg(psi_hat + ((po + bi) * nbi + idx) * K + kk);
+            }
+            reinterpret_cast<float2*>(&ps[sl][t][0])[kk] = v;
+        }
+        __syncthreads();
+        if (mp >= nbo) continue;
+        for (int64_t b = 0; b < B; ++b) {
+            for (int64_t c0 = 0; c0 < C; c0 += 64) {
+                const int64_t c = c0 + cl;
+                if (c >= C) break;
+                float2 acc[9];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) acc[k] = make_float2(0.f, 0.f);
-        for (int bi = 0; bi < nb; ++bi) {
-            const int64_t hi = h0 + bi;
-            for (int q = 0; q < s; ++q) {
-                const int kq = static_cast<int>(mp) + wout * q;
-                const bool cj = kq > half;
-                const int idx = cj ? win - kq : kq;
-                const float2 u = valid ? U[((b * Hin + hi) * nbi + idx) * C + c] : make_float2(0.f, 0.f);
-                const float2* ps = psi_hat + ((po + bi) * nbi + idx) * K;
+                for (int k = 0; k < 9; ++k) acc[k] = make_float2(0.f, 0.f);
+                const float2* Ub = U + (b * Hin + h0) * nbi * C + c;
+                constexpr int CH = 4;  // slots per load batch
+                for (int sl0 = 0; sl0 < ns; sl0 += CH) {
+                    float2 u[CH];
+                    bool cj[CH];
 #pragma unroll
-                for (int k = 0; k < 9; ++k) {
-                    if (k < K) {
-                        const float2 p = __ldg(ps + k);
-                        if (!cj) {  // conj(psi) * u
-                            acc[k].x += p.x * u.x + p.y * u.y;
-                            acc[k].y += p.x * u.y - p.y * u.x;
-                        } else {    // psi * conj(u)
-                            acc[k].x += p.x * u.x + p.y * u.y;
-                            acc[k].y += p.y * u.x - p.x * u.y;
+                    for (int j = 0; j < CH; ++j) {
+                        const int slot = slot0 + sl0 + j;
+                        const int bi = slot / s, q = slot - bi * s;
+                        const int kq = static_cast<int>(mp) + wout * q;
+                        cj[j] = kq > half;
+                        const int idx = cj[j] ? win - kq : kq;
+                        u[j] = sl0 + j < ns ? __ldg(Ub + (static_cast<int64_t>(bi) * nbi + idx) * C)
+                                            : make_float2(0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) {
+                        if (sl0 + j >= ns) break;
+                        const float4* pp = &ps[sl0 + j][mi][0];
+                        float2 p[10];
+#pragma unroll
+                        for (int k2 = 0; k2 < 5; ++k2) {
+                            const float4 t4 = pp[k2];
+                            p[2 * k2] = make_float2(t4.x, t4.y);
+                            p[2 * k2 + 1] = make_float2(t4.z, t4.w);
+                        }
+                        const float2 uu = u[j];
+                        // R = conj(psi) u for kq <= W/2, psi conj(u) above (Hermitian fold)
+                        const float sy = cj[j] ? -1.f : 1.f;
+#pragma unroll
+                        for (int k = 0; k < 9; ++k) {
+                            acc[k].x += p[k].x * uu.x + p[k].y * uu.y;
+                            acc[k].y += sy * (p[k].x * uu.y - p[k].y * uu.x);
                         }
                     }
                 }
-            }
-        }
-        if (valid) {
-            const int64_t row = ((b * Hout + h) * nbo + mp) * 2;
-            float* sr = S + row * ldS + c * K;
-            float* si = S + (row + 1) * ldS + c * K;
+                const int64_t row = ((b * Hout + h) * nbo + mp) * 2;
+                float* sr = S + row * ldS + c * K;
+                float* si = S + (row + 1) * ldS + c * K;
+                if (slot0 == 0) {
 #pragma unroll
-            for (int k = 0; k < 9; ++k)
-                if (k < K) {
-                    sr[k] = acc[k].x;
-                    si[k] = acc[k].y;
+                    for (int k = 0; k < 9; ++k)
+                        if (k < K) {
+                            sr[k] = acc[k].x;
+                            si[k] = acc[k].y;
+                        }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 9; ++k)
+                        if (k < K) {
+                            sr[k] += acc[k].x;
+                            si[k] += acc[k].y;
+                        }
                 }
+            }
         }
     }
 }
@@ -462,14 +509,14 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
     float2* U = reinterpret_cast<float2*>(base + w.u_off);
     float* Yh = reinterpret_cast<float*>(base + w.y_off);
     fft_forward_cminor(fft_in, x, B, cin, nin, static_cast<int>(nbi), U, st);
-    dim3 grid(static_cast<unsigned>((nbo + 3) / 4), static_cast<unsigned>(nout), static_cast<unsigned>(B));
-    require(nout <= 65535 && B <= 65535, "disco: grid too large");
+    dim3 grid(static_cast<unsigned>((nbo + 3) / 4), static_cast<unsigned>(nout));
+    require(nout <= 65535, "disco: grid too large");
     {
         ProfScope prof("disco_band", st);
         disco_band_kernel<<<grid, 256, 0, st>>>(U, d_psi_hat.p, d_band0.p, d_bandc.p, d_psi_off.p, nin,
                                                 nbi, nout, nbo, static_cast<int>(win),
                                                 static_cast<int>(wout), static_cast<int>(stride), K,
-                                                cin, w.ldS, S, h_in0, ho0);
+                                                cin, w.ldS, S, h_in0, ho0, B);
         SPH_LAUNCH_CHECK();
     }
     count_launch();

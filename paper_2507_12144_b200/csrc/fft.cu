@@ -271,18 +271,31 @@ struct UnfoldIO {
         const float2* e = reinterpret_cast<const float2*>(eoi + static_cast<int64_t>(r) * twoF + 2 * (f0 + j));
         const int64_t so = static_cast<int64_t>(R) * F;  // parity stride in float2
         const int64_t sm = 2 * so;                        // order stride in float2
-        for (int m = m0; m < msynth; m += mstep) {
-            const float2* em = e + m * sm;
-            const int l0 = (lmax - m + 1) / 2, l1 = (lmax - m) / 2;  // L_{m,0}, L_{m,1}
-            const float2 ev = l0 > 0 ? em[0] : make_float2(0.f, 0.f);
-            const float2 od = l1 > 0 ? em[so] : make_float2(0.f, 0.f);
-            const float2 ha = cadd(ev, od);
-            const float2 hb = pair ? csub(ev, od) : make_float2(0.f, 0.f);
-            if (m == 0) {
-                zr[0] = make_float2(ha.x, hb.x);  // Im of the DC bin is dropped
-            } else {
-                zr[m] = make_float2(ha.x - hb.y, ha.y + hb.x);      // ha + i hb
-                zr[n - m] = make_float2(ha.x + hb.y, hb.x - ha.y);  // conj ha + i conj hb
+        // batches of UB orders: all 2*UB loads issued before any use (memory-level
+        // parallelism for the latency-bound load phase)
+        constexpr int UB = 8;
+        for (int mb = m0; mb < msynth; mb += UB * mstep) {
+            float2 ev[UB], od[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int m = mb + u * mstep;
+                const bool ok = m < msynth;
+                const float2* em = e + (ok ? m : 0) * sm;
+                ev[u] = (ok && (lmax - m + 1) / 2 > 0) ? __ldg(em) : make_float2(0.f, 0.f);
+                od[u] = (ok && (lmax - m) / 2 > 0) ? __ldg(em + so) : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int m = mb + u * mstep;
+                if (m >= msynth) break;
+                const float2 ha = cadd(ev[u], od[u]);
+                const float2 hb = pair ? csub(ev[u], od[u]) : make_float2(0.f, 0.f);
+                if (m == 0) {
+                    zr[0] = make_float2(ha.x, hb.x);  // Im of the DC bin is dropped
+                } else {
+                    zr[m] = make_float2(ha.x - hb.y, ha.y + hb.x);      // ha + i hb
+                    zr[n - m] = make_float2(ha.x + hb.y, hb.x - ha.y);  // conj ha + i conj hb
+                }
             }
         }
     }
