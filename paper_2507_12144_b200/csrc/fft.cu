@@ -214,19 +214,61 @@ struct FoldIO {
             }
         }
     }
-    // one (m, ring) per thread, all four outputs (E re/im, O re/im); lanes with
-    // consecutive j write P-float runs of four E/O rows
+    // one (m, quad of 4 rings) per thread: all four outputs (E re/im, O re/im) of the
+    // four rings as float4 stores (P % 4 == 0, r0 % 4 == 0, ld_eo % 4 == 0); a partial
+    // tail quad falls back to scalar stores
     template <class PT, class NT>
     __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
         const int r0 = blockIdx.x * P, f = blockIdx.y;
         const int nr = min(static_cast<int>(P), R - r0);
+        const int64_t so = twoF * ld_eo;      // E -> O row offset
+        const int64_t sm = 2 * so;            // m -> m+1
+        float* e0 = eo + (2 * static_cast<int64_t>(f)) * ld_eo + r0;
+        if (P % 4 == 0 && (ld_eo & 3) == 0) {
+            const int nq = P / 4;
+            const int jq = threadIdx.x % nq;
+            const int mstep = blockDim.x / nq;
+            const int j0 = 4 * jq;
+            if (j0 >= nr) return;
+            float* e = e0 + j0;
+            for (int m = threadIdx.x / nq; m < mmax; m += mstep) {
+                float er[4], ei[4], orr[4], oi[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2* zr = buf + (j0 + t) * ld;
+                    const float2 z = zr[m];
+                    const float2 zc = zr[m == 0 ? 0 : n - m];
+                    const float ar = 0.5f * (z.x + zc.x), ai = 0.5f * (z.y - zc.y);
+                    const float br = 0.5f * (z.y + zc.y), bi = -0.5f * (z.x - zc.x);
+                    er[t] = ar + br;
+                    ei[t] = ai + bi;
+                    orr[t] = ar - br;
+                    oi[t] = ai - bi;
+                }
+                float* em = e + m * sm;
+                if (j0 + 4 <= nr) {
+                    *reinterpret_cast<float4*>(em) = make_float4(er[0], er[1], er[2], er[3]);
+                    *reinterpret_cast<float4*>(em + ld_eo) = make_float4(ei[0], ei[1], ei[2], ei[3]);
+                    *reinterpret_cast<float4*>(em + so) = make_float4(orr[0], orr[1], orr[2], orr[3]);
+                    *reinterpret_cast<float4*>(em + so + ld_eo) = make_float4(oi[0], oi[1], oi[2], oi[3]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (j0 + t < nr) {
+                            em[t] = er[t];
+                            em[ld_eo + t] = ei[t];
+                            em[so + t] = orr[t];
+                            em[so + ld_eo + t] = oi[t];
+                        }
+                }
+            }
+            return;
+        }
         const int j = threadIdx.x % P;
         const int mstep = blockDim.x / P;
         if (j >= nr) return;
         const float2* zr = buf + j * ld;
-        float* e = eo + (2 * static_cast<int64_t>(f)) * ld_eo + r0 + j;
-        const int64_t so = twoF * ld_eo;      // E -> O row offset
-        const int64_t sm = 2 * so;            // m -> m+1
+        float* e = e0 + j;
         for (int m = threadIdx.x / P; m < mmax; m += mstep) {
             const float2 z = zr[m];
             const float2 zc = zr[m == 0 ? 0 : n - m];
