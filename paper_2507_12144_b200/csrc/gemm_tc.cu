@@ -103,6 +103,28 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uin
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
         : "memory");
 }
+// A operand from TMEM ("TS"): D += A[tmem] * B[smem]
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15]))
+        : "memory");
+}
 // 32 lanes x 32 bit, 16 consecutive columns per lane
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];
@@ -139,10 +161,11 @@ __device__ __forceinline__ uint32_t make_idesc(int n) {
     return d;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool ATMEM = false>
 struct Smem {
     static constexpr int B_TILE_BYTES = BN * BK * 4;
-    static constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;
+    static constexpr int A_BYTES = ATMEM ? A_TILE_BYTES : 2 * A_TILE_BYTES;  // (A_hi, A_lo) or A
+    static constexpr int STAGE_BYTES = A_BYTES + 2 * B_TILE_BYTES;
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     // full[S], conv[S], empty[S], tfull[2], tempty[2], tmem slot
     static constexpr int TILE_OFF = BAR_OFF + (3 * STAGES + 4) * 8 + 16;
@@ -153,24 +176,28 @@ struct Smem {
 // N-tile); each CTA TMA-loads 1/CL of the table tile and multicasts it to the whole
 // cluster, so the L2 -> SMEM table traffic per CTA drops by CL.  A stage is refilled
 // only after all CL consumers released it (multicast tcgen05.commit, count CL).
-template <int BN, int STAGES, int CL>
+// ATMEM: the converter warps split the TMA-landed A tile into tf32 hi / lo in
+// registers and write both into TMEM (tcgen05.st); the MMAs take A from TMEM, so per
+// stage only the table tile is read from SMEM by the tensor core.  TMEM columns:
+// 2 x BN accumulators + STAGES x 2*BK A columns (BN = 192, STAGES = 4 -> 512).
+template <int BN, int STAGES, int CL, bool ATMEM>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_bhi,
                    const __grid_constant__ CUtensorMap map_blo, const GemmGroup* __restrict__ groups,
                    const GemmTile* __restrict__ tiles, int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass) {
-    using L = Smem<BN, STAGES>;
+    using L = Smem<BN, STAGES, ATMEM>;
+    static_assert(!ATMEM || 2 * BN + STAGES * 2 * BK <= 512, "TMEM budget");
+    constexpr uint32_t TMEM_COLS = ATMEM ? 512 : 2 * BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const uint32_t sbase = smem_u32(smem);
     auto a_hi = [&](int s) { return sbase + s * L::STAGE_BYTES; };
     auto a_lo = [&](int s) { return sbase + s * L::STAGE_BYTES + A_TILE_BYTES; };
-    auto b_hi = [&](int s) { return sbase + s * L::STAGE_BYTES + 2 * A_TILE_BYTES; };
-    auto b_lo = [&](int s) {
-        return sbase + s * L::STAGE_BYTES + 2 * A_TILE_BYTES + L::B_TILE_BYTES;
-    };
+    auto b_hi = [&](int s) { return sbase + s * L::STAGE_BYTES + L::A_BYTES; };
+    auto b_lo = [&](int s) { return sbase + s * L::STAGE_BYTES + L::A_BYTES + L::B_TILE_BYTES; };
     const uint32_t bars = sbase + L::BAR_OFF;
     auto full_bar = [&](int s) { return bars + 8 * s; };
     auto conv_bar = [&](int s) { return bars + 8 * (STAGES + s); };
@@ -203,7 +230,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(2 * BN)
+                     "r"(TMEM_COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -211,6 +238,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    auto tmem_a = [&](int s) { return tmem_base + 2 * BN + s * 2 * BK; };  // hi: +0, lo: +BK
     const int crank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
     const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
     const uint16_t cmask = static_cast<uint16_t>((1u << CL) - 1);
@@ -270,14 +298,24 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     tc_fence_after();
                     const int ksteps = min(BK / 8, (g.K - kb * BK + 7) / 8);
                     for (int kk = 0; kk < ksteps; ++kk) {
-                        const uint64_t ahi = make_sdesc(a_hi(s) + kk * 32);
                         const uint64_t bhi = make_sdesc(b_hi(s) + kk * 32);
-                        tc_mma_tf32(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
-                        if (three_pass) {
-                            const uint64_t alo = make_sdesc(a_lo(s) + kk * 32);
-                            const uint64_t blo = make_sdesc(b_lo(s) + kk * 32);
-                            tc_mma_tf32(tmem_d, ahi, blo, idesc, 1u);
-                            tc_mma_tf32(tmem_d, alo, bhi, idesc, 1u);
+                        if constexpr (ATMEM) {
+                            const uint32_t ahi = tmem_a(s) + kk * 8, alo = tmem_a(s) + BK + kk * 8;
+                            tc_mma_tf32_ts(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
+                            if (three_pass) {
+                                const uint64_t blo = make_sdesc(b_lo(s) + kk * 32);
+                                tc_mma_tf32_ts(tmem_d, ahi, blo, idesc, 1u);
+                                tc_mma_tf32_ts(tmem_d, alo, bhi, idesc, 1u);
+                            }
+                        } else {
+                            const uint64_t ahi = make_sdesc(a_hi(s) + kk * 32);
+                            tc_mma_tf32(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
+                            if (three_pass) {
+                                const uint64_t alo = make_sdesc(a_lo(s) + kk * 32);
+                                const uint64_t blo = make_sdesc(b_lo(s) + kk * 32);
+                                tc_mma_tf32(tmem_d, ahi, blo, idesc, 1u);
+                                tc_mma_tf32(tmem_d, alo, bhi, idesc, 1u);
+                            }
                         }
                     }
                     if (CL == 1)
@@ -300,7 +338,32 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             const int nkb = (g.K + BK - 1) / BK;
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(full_bar(s), ph);
-                if (three_pass) {
+                if constexpr (ATMEM) {
+                    // this warp owns TMEM lanes 32q..32q+31 = tile rows; read the row's BK
+                    // fp32 from the SWIZZLE_64B tile (16-byte chunk c of row r sits at
+                    // chunk c ^ ((r >> 1) & 3); conflict-free for 8 consecutive rows)
+                    const int q = warp & 3;
+                    const int row = 32 * q + lane;
+                    const float4* rowp = reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase) + row * BK * 4);
+                    float hi[16], lo[16];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float4 v = rowp[c ^ ((row >> 1) & 3)];
+                        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            uint32_t u;
+                            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(vv[e]));
+                            hi[4 * c + e] = three_pass ? __uint_as_float(u) : vv[e];
+                            lo[4 * c + e] = vv[e] - __uint_as_float(u);
+                        }
+                    }
+                    const uint32_t ta = tmem_a(s) + (static_cast<uint32_t>(32 * q) << 16);
+                    tmem_st16(ta, hi);
+                    if (three_pass) tmem_st16(ta + BK, lo);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_fence_before();
+                } else if (three_pass) {
                     float4* hi = reinterpret_cast<float4*>(smem + (a_hi(s) - sbase));
                     float4* lo = reinterpret_cast<float4*>(smem + (a_lo(s) - sbase));
 #pragma unroll
@@ -386,7 +449,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(2 * BN)
+                     "r"(TMEM_COLS)
                      : "memory");
     }
 }
@@ -429,11 +492,11 @@ static CUtensorMap make_map(const Mat2D& m, int box_rows) {
     return map;
 }
 
-template <int BN, int STAGES, int CL>
+template <int BN, int STAGES, int CL, bool ATMEM = false>
 static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
                    float* D, bool three, cudaStream_t st) {
-    using L = Smem<BN, STAGES>;
-    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL>;
+    using L = Smem<BN, STAGES, ATMEM>;
+    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL, ATMEM>;
     static int grid = 0;
     static std::once_flag once;
     std::call_once(once, [&] {
@@ -504,7 +567,13 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
     const bool three = prec == SPH_PREC_3XTF32;
     require(!three || Blo, "gemm: 3xTF32 needs the lo table");
     const int cl = g.cluster;
-    if (g.bn == 256 && cl == 1)
+    if (g.bn == 192 && cl == 1)
+        tc::launch<192, 4, 1, true>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 192 && cl == 2)
+        tc::launch<192, 4, 2, true>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 192 && cl == 4)
+        tc::launch<192, 4, 4, true>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 256 && cl == 1)
         tc::launch<256, 4, 1>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 256 && cl == 2)
         tc::launch<256, 4, 2>(g, A, Bhi, Blo, D, three, st);

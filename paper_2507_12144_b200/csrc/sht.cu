@@ -288,7 +288,7 @@ const GroupedGemm& ShtPlan::fwd_gemm(int64_t F) {
         g->Bhi = {pf_hi.p, pf_rows, R, Rp};
         g->Blo = {pf_lo.p, pf_rows, R, Rp};
         g->store = STORE_ROW;
-        g->bn = 256;
+        g->bn = 192;  // TMEM-resident A operand variant
         g->name = "gemm_legendre_fwd";
         for (int64_t m = 0; m < mmax; ++m)
             for (int p = 0; p < 2; ++p) {
@@ -321,7 +321,7 @@ const GroupedGemm& ShtPlan::inv_gemm(int64_t F) {
         g->Bhi = {pi_hi.p, mmax * 2 * R, Lmax_p, Lp};
         g->Blo = {pi_lo.p, mmax * 2 * R, Lmax_p, Lp};
         g->store = STORE_TRANS;  // EOi[m][parity][R][2F]: coalesced reads for the iFFT
-        g->bn = 256;
+        g->bn = 192;  // TMEM-resident A operand variant
         g->name = "gemm_legendre_inv";
         for (int64_t m = 0; m < msynth; ++m)
             for (int p = 0; p < 2; ++p) {
@@ -354,7 +354,7 @@ const GroupedGemm& ShtPlan::stage_gemm(int64_t F, int64_t m0, int64_t mcount) {
         g->Bhi = {pf_hi.p, pf_rows, R, Rp};
         g->Blo = {pf_lo.p, pf_rows, R, Rp};
         g->store = STORE_ROW;
-        g->bn = 256;
+        g->bn = 192;  // TMEM-resident A operand variant
         for (int64_t ml = 0; ml < mcount; ++ml)
             for (int p = 0; p < 2; ++p) {
                 const int64_t m = m0 + ml;
