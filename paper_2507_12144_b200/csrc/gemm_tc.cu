@@ -25,7 +25,9 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 16;               // fp32 elements per 64-byte swizzle row
-constexpr int NUM_THREADS = 384;     // 12 warps
+constexpr int NUM_THREADS = 384;     // 12 warps (smem-A variant)
+constexpr int NUM_THREADS_TM = 512;  // 16 warps (TMEM-A variant: two converter warpgroups)
+template <bool ATMEM> constexpr int nthreads() { return ATMEM ? NUM_THREADS_TM : NUM_THREADS; }
 constexpr int A_TILE_BYTES = BM * BK * 4;  // 16 KB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -181,7 +183,7 @@ struct Smem {
 // stage only the table tile is read from SMEM by the tensor core.  TMEM columns:
 // 2 x BN accumulators + STAGES x 2*BK A columns (BN = 192, STAGES = 4 -> 512).
 template <int BN, int STAGES, int CL, bool ATMEM>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(nthreads<ATMEM>(), 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_bhi,
                    const __grid_constant__ CUtensorMap map_blo, const GemmGroup* __restrict__ groups,
@@ -327,9 +329,12 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 tc_commit(tfull_bar(acc));
             }
         }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp >= 4 && warp < (ATMEM ? 12 : 8)) {
         // ----------------------------------------------------------- converter
+        // TMEM-A variant: two warpgroups take alternate stages (set = stage parity) so the
+        // per-stage convert latency does not gate small-N tiles
         const int ct = threadIdx.x - 128;
+        const int cset = ATMEM ? (warp - 4) / 4 : 0;
         int s = 0;
         uint32_t ph = 0;
         for (int t = cid; t < ntiles; t += ncl) {
@@ -337,6 +342,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             const GemmGroup g = groups[tl.group];
             const int nkb = (g.K + BK - 1) / BK;
             for (int kb = 0; kb < nkb; ++kb) {
+                if (ATMEM && (s & 1) != cset) {
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                    continue;
+                }
                 mbar_wait(full_bar(s), ph);
                 if constexpr (ATMEM) {
                     // this warp owns TMEM lanes 32q..32q+31 = tile rows; read the row's BK
@@ -386,7 +395,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
-    } else if (warp >= 8) {
+    } else if (warp >= (ATMEM ? 12 : 8)) {
         // ------------------------------------------------------------- epilogue
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         int lt = 0;
@@ -505,7 +514,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
         if (CL > 1) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(NUM_THREADS);
+            cfg.blockDim = dim3(nthreads<ATMEM>());
             cfg.dynamicSmemBytes = L::TOTAL;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
@@ -533,7 +542,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     ProfScope prof(g.name, st, g.flops);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(gsz);
-    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.blockDim = dim3(nthreads<ATMEM>());
     cfg.dynamicSmemBytes = L::TOTAL;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
