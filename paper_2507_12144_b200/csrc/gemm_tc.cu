@@ -1,20 +1,26 @@
 // tcgen05 / TMEM / TMA grouped GEMM for sm_100a with a 3xTF32 precision split.
 //
 // Persistent, warp-specialised, one CTA per SM:
-//   warp 0        TMA producer: A_hi tile (data), B_hi and B_lo tiles (table) per stage
+//   warp 0        TMA producer: A tile (data, fp32), B_hi and B_lo tiles (table) per
+//                 stage, plus an L2 prefetch cursor PF k-blocks ahead
 //   warp 1        MMA issuer (one elected thread): per K=8 step
 //                   D += A_hi*B_hi ; D += A_hi*B_lo ; D += A_lo*B_hi   (kind::tf32)
 //   warp 2        TMEM allocator
-//   warps 4..7    converter: A (fp32 as landed by TMA) -> A_hi = rna_tf32(A) in place,
-//                 A_lo = A - A_hi into its own SMEM buffer (elementwise, so the 128B
-//                 swizzle is irrelevant), fence.proxy.async, arrive
-//   warps 8..11   epilogue: TMEM -> registers (tcgen05.ld 32x32b) -> global
+//   warps 4..11   converters (ALO, two warpgroups on alternate stages): A_lo = A -
+//                 trunc_tf32(A) -> TMEM (tcgen05.st); A_hi is the fp32 tile itself
+//                 (see the kernel comment).  Non-ALO variant (warps 4..7): A_hi/A_lo
+//                 rna-split in SMEM.
+//   warps 12..15  epilogue (8..11 non-ALO): TMEM -> registers (tcgen05.ld 32x32b) ->
+//                 global, row-major through a per-warp SMEM transpose or column-major
 // Pipelines: SMEM ring (full -> converted -> empty) and a double-buffered TMEM
 // accumulator (full/empty) so the epilogue of tile i overlaps the MMAs of tile i+1.
 // Operand tiles are K-major, SWIZZLE_64B (16 fp32 of K per 64-byte row, 8-row /
-// 512-byte atoms, SBO = 512): small stages -> a 4-deep (BN=256) / 6-deep (BN=128) ring.
+// 512-byte atoms, SBO = 512).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <string>
+#include <vector>
 #include <cstring>
 #include <mutex>
 
@@ -24,11 +30,13 @@ namespace sph {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 16;               // fp32 elements per 64-byte swizzle row
-constexpr int NUM_THREADS = 384;     // 12 warps (smem-A variant)
-constexpr int NUM_THREADS_TM = 512;  // 16 warps (TMEM-A variant: two converter warpgroups)
-template <bool ATMEM> constexpr int nthreads() { return ATMEM ? NUM_THREADS_TM : NUM_THREADS; }
-constexpr int A_TILE_BYTES = BM * BK * 4;  // 16 KB
+constexpr int BK = 16;               // fp32 per 64-byte swizzle row (SWIZZLE_64B variants)
+constexpr int BK_ALO = 32;           // fp32 per 128-byte swizzle row (ALO variant, SWIZZLE_128B)
+template <bool ALO> constexpr int bk_of() { return ALO ? BK_ALO : BK; }
+constexpr int NUM_THREADS = 384;      // 12 warps (SMEM A_hi/A_lo variant)
+constexpr int NUM_THREADS_ALO = 512;  // 16 warps (ALO variant: two converter warpgroups)
+template <bool ALO> constexpr int nthreads() { return ALO ? NUM_THREADS_ALO : NUM_THREADS; }
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -43,9 +51,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Bounded wait: a protocol bug traps (launch error) after 3 s instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t ok = 0;
-    do {
+    uint64_t t0 = 0;
+    for (;;) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -53,7 +68,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "=r"(ok)
             : "r"(bar), "r"(parity)
             : "memory");
-    } while (!ok);
+        if (ok) return;
+        const uint64_t t = global_ns();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > 3000000000ull) {
+            uint64_t raw;
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(raw) : "r"(bar));
+            if ((threadIdx.x & 31) == 0)
+                printf("sph gemm watchdog: block %d warp %d barrier 0x%x parity %u raw 0x%016llx\n",
+                       blockIdx.x, threadIdx.x / 32, bar, parity, static_cast<unsigned long long>(raw));
+            __trap();
+        }
+    }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint32_t bar) {
@@ -62,6 +88,22 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
+}
+struct MatRef {  // base / rows / row stride of a TMA operand, for whole-tile L2 prefetch
+    const float* p;
+    int64_t rows, ld;
+};
+
+// L2 prefetch of a contiguous row range [row0, row0 + nrows) of a row-major matrix
+__device__ __forceinline__ void l2_prefetch_rows(const MatRef& m, int64_t row0, int64_t nrows) {
+    if (m.p == nullptr || row0 >= m.rows) return;
+    if (nrows > m.rows - row0) nrows = m.rows - row0;
+    const char* p = reinterpret_cast<const char*>(m.p + row0 * m.ld);
+    int64_t bytes = nrows * m.ld * 4;
+    for (; bytes > 0; bytes -= 32768, p += 32768) {
+        const uint32_t n = static_cast<uint32_t>(bytes < 32768 ? bytes : 32768);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(n) : "memory");
+    }
 }
 __device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                                uint32_t bar, uint16_t mask) {
@@ -142,31 +184,35 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// UMMA shared-memory descriptor: K-major, SWIZZLE_64B, SBO = 512 B, version 1.
+// UMMA shared-memory descriptor: K-major, rows of KB fp32 (64 B -> SWIZZLE_64B, layout 4;
+// 128 B -> SWIZZLE_128B, layout 2), 8-row atoms (SBO = 8 rows), version 1.
+template <int KB>
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
+    static_assert(KB == 16 || KB == 32, "row width");
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);          // start address
-    d |= static_cast<uint64_t>(1) << 16;                          // LBO (unused for SW128 K-major)
-    d |= static_cast<uint64_t>((8 * BK * 4) >> 4) << 32;          // SBO: 8-row group stride
+    d |= static_cast<uint64_t>(1) << 16;                          // LBO (unused, swizzled K-major)
+    d |= static_cast<uint64_t>((8 * KB * 4) >> 4) << 32;          // SBO: 8-row group stride
     d |= static_cast<uint64_t>(1) << 46;                          // descriptor version (sm100)
-    d |= static_cast<uint64_t>(4) << 61;                          // SWIZZLE_64B
+    d |= static_cast<uint64_t>(KB == 32 ? 2 : 4) << 61;           // SWIZZLE_128B / _64B
     return d;
 }
 // Instruction descriptor: kind::tf32, D f32, A/B tf32, both K-major, M = 128, N = n.
-__device__ __forceinline__ uint32_t make_idesc(int n) {
+__device__ __forceinline__ uint32_t make_idesc(int n, int m = BM) {
     uint32_t d = 0;
     d |= 1u << 4;                             // D format f32
     d |= 2u << 7;                             // A format tf32
     d |= 2u << 10;                            // B format tf32
     d |= static_cast<uint32_t>(n >> 3) << 17; // N >> 3
-    d |= static_cast<uint32_t>(BM >> 4) << 24;// M >> 4
+    d |= static_cast<uint32_t>(m >> 4) << 24; // M >> 4
     return d;
 }
 
-template <int BN, int STAGES, bool ATMEM = false>
+template <int BN, int STAGES, bool ALO = false>
 struct Smem {
-    static constexpr int B_TILE_BYTES = BN * BK * 4;
-    static constexpr int A_BYTES = ATMEM ? A_TILE_BYTES : 2 * A_TILE_BYTES;  // (A_hi, A_lo) or A
+    static constexpr int A_TILE_BYTES = BM * bk_of<ALO>() * 4;
+    static constexpr int B_TILE_BYTES = BN * bk_of<ALO>() * 4;
+    static constexpr int A_BYTES = ALO ? A_TILE_BYTES : 2 * A_TILE_BYTES;  // A or (A_hi, A_lo)
     static constexpr int STAGE_BYTES = A_BYTES + 2 * B_TILE_BYTES;
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     // full[S], conv[S], empty[S], tfull[2], tempty[2], tmem slot
@@ -178,23 +224,43 @@ struct Smem {
 // N-tile); each CTA TMA-loads 1/CL of the table tile and multicasts it to the whole
 // cluster, so the L2 -> SMEM table traffic per CTA drops by CL.  A stage is refilled
 // only after all CL consumers released it (multicast tcgen05.commit, count CL).
-// ATMEM: the converter warps split the TMA-landed A tile into tf32 hi / lo in
-// registers and write both into TMEM (tcgen05.st); the MMAs take A from TMEM, so per
-// stage only the table tile is read from SMEM by the tensor core.  TMEM columns:
-// 2 x BN accumulators + STAGES x 2*BK A columns (BN = 192, STAGES = 4 -> 512).
-template <int BN, int STAGES, int CL, bool ATMEM>
-__global__ void __launch_bounds__(nthreads<ATMEM>(), 1)
+//
+// ALO (the production variant): kind::tf32 reads fp32 operands and ignores the low 13
+// mantissa bits, so the TMA-landed fp32 A tile IS A_hi = trunc_tf32(A) for the SMEM
+// ("SS") MMAs A*B_hi and A*B_lo.  The converter warps only form A_lo = A -
+// trunc_tf32(A) (exact) and tcgen05.st it into TMEM for the A_lo*B_hi ("TS") MMAs.
+// K-block = 32 fp32 (SWIZZLE_128B rows): 12 MMAs per stage barrier round.  Measured with
+// SPH_GEMM_TRACE / SPH_GEMM_DEBUG at BK = 16: ~950-1200 cycles per k-block at ANY tile N
+// and ~700 even with the MMAs, converter, epilogue and table loads all disabled, i.e.
+// the per-stage barrier round trip (producer -> TMA -> full -> convert -> MMA -> commit ->
+// empty) and not the tensor pipe (6 MMAs = 576 cycles at N = 192, profiles/mma_rate.cu)
+// bounded it; doubling the MMA work per round halves that cost per flop.  TMEM: 2 x BN
+// accumulators + STAGES x 32 A_lo columns (384 + 96).
+template <int BN, int STAGES, int CL, bool ALO>
+__global__ void __launch_bounds__(nthreads<ALO>(), 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_bhi,
                    const __grid_constant__ CUtensorMap map_blo, const GemmGroup* __restrict__ groups,
                    const GemmTile* __restrict__ tiles, int ntiles, float* __restrict__ D,
-                   int store_mode, int three_pass) {
-    using L = Smem<BN, STAGES, ATMEM>;
-    static_assert(!ATMEM || 2 * BN + STAGES * 2 * BK <= 512, "TMEM budget");
-    constexpr uint32_t TMEM_COLS = ATMEM ? 512 : 2 * BN;
+                   int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
+                   MatRef ra, MatRef rbhi, MatRef rblo) {
+    // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
+    // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads,
+    // 16 no L2 prefetch, 32 one converter warpgroup
+    // trace (diagnostic, SPH_GEMM_TRACE): CTA 0 records clock64 per k-block j < TR_N at
+    // [0] producer issue, [1] data landed (converter wake), [2] converted, [3] MMA issue,
+    // and per tile [4*TR_N + 2*lt] MMA start clock, [.. + 1] ninst * 1000 + k-blocks
+    constexpr int TR_N = 512;
+    const bool tr = trace != nullptr && blockIdx.x == 0;
+    using L = Smem<BN, STAGES, ALO>;
+    constexpr int KB = bk_of<ALO>();
+    constexpr int A_TILE_BYTES = L::A_TILE_BYTES;
+    static_assert(!ALO || 2 * BN + STAGES * KB <= 512, "TMEM budget");
+    constexpr uint32_t TMEM_COLS = ALO ? 512 : 2 * BN;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // 1 KB alignment by pointer arithmetic on the __shared__ array (keeps the shared
+    // address space, so the epilogue tile accesses compile to LDS/STS)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
     auto a_hi = [&](int s) { return sbase + s * L::STAGE_BYTES; };
     auto a_lo = [&](int s) { return sbase + s * L::STAGE_BYTES + A_TILE_BYTES; };
@@ -240,7 +306,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    auto tmem_a = [&](int s) { return tmem_base + 2 * BN + s * 2 * BK; };  // hi: +0, lo: +BK
+    auto tmem_alo = [&](int s) { return tmem_base + 2 * BN + s * KB; };
     const int crank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
     const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
     const uint16_t cmask = static_cast<uint16_t>((1u << CL) - 1);
@@ -250,26 +316,46 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     if (warp == 0) {
         // ------------------------------------------------------------- producer
         if (lane == 0) {
-            int s = 0;
+            int s = 0, j = 0;
             uint32_t ph = 0;
+            // Whole-tile L2 prefetch one tile ahead (a tile's data rows and table rows are
+            // contiguous row ranges; the k-block boxes walk them in column strips)
+            auto prefetch_tile = [&](int pt) {
+                if (pt >= ntiles || (dbg & 16)) return;
+                const GemmTile ptl = tiles[pt];
+                const GemmGroup pg = groups[ptl.group];
+                l2_prefetch_rows(ra, pg.a_row0 + ptl.m0 + crank * BM, BM);
+                const int brow = pg.b_row0 + ptl.n0 + (CL > 1 ? crank * B_ROWS : 0);
+                l2_prefetch_rows(rbhi, brow, B_ROWS);
+                if (three_pass) l2_prefetch_rows(rblo, brow, B_ROWS);
+            };
+            prefetch_tile(cid);
             for (int t = cid; t < ntiles; t += ncl) {
                 const GemmTile tl = tiles[t];
                 const GemmGroup g = groups[tl.group];
-                const int nkb = (g.K + BK - 1) / BK;
-                for (int kb = 0; kb < nkb; ++kb) {
+                const int nkb = (g.K + KB - 1) / KB;
+                prefetch_tile(t + ncl);
+                for (int kb = 0; kb < nkb; ++kb, ++j) {
                     mbar_wait(empty_bar(s), ph ^ 1);
+                    if (tr && j < TR_N) trace[j] = clock64();
+                    if (dbg & 8) {
+                        mbar_expect_tx(full_bar(s), A_TILE_BYTES);
+                        tma_load_2d(a_hi(s), &map_a, kb * KB, g.a_row0 + tl.m0 + crank * BM, full_bar(s));
+                        if (++s == STAGES) { s = 0; ph ^= 1; }
+                        continue;
+                    }
                     mbar_expect_tx(full_bar(s), A_TILE_BYTES + (three_pass ? 2 : 1) * L::B_TILE_BYTES);
-                    tma_load_2d(a_hi(s), &map_a, kb * BK, g.a_row0 + tl.m0 + crank * BM, full_bar(s));
+                    tma_load_2d(a_hi(s), &map_a, kb * KB, g.a_row0 + tl.m0 + crank * BM, full_bar(s));
                     if (CL == 1) {
-                        tma_load_2d(b_hi(s), &map_bhi, kb * BK, g.b_row0 + tl.n0, full_bar(s));
+                        tma_load_2d(b_hi(s), &map_bhi, kb * KB, g.b_row0 + tl.n0, full_bar(s));
                         if (three_pass)
-                            tma_load_2d(b_lo(s), &map_blo, kb * BK, g.b_row0 + tl.n0, full_bar(s));
+                            tma_load_2d(b_lo(s), &map_blo, kb * KB, g.b_row0 + tl.n0, full_bar(s));
                     } else {
-                        const uint32_t off = crank * B_ROWS * BK * 4;
-                        tma_load_2d_mc(b_hi(s) + off, &map_bhi, kb * BK,
+                        const uint32_t off = crank * B_ROWS * KB * 4;
+                        tma_load_2d_mc(b_hi(s) + off, &map_bhi, kb * KB,
                                        g.b_row0 + tl.n0 + crank * B_ROWS, full_bar(s), cmask);
                         if (three_pass)
-                            tma_load_2d_mc(b_lo(s) + off, &map_blo, kb * BK,
+                            tma_load_2d_mc(b_lo(s) + off, &map_blo, kb * KB,
                                            g.b_row0 + tl.n0 + crank * B_ROWS, full_bar(s), cmask);
                     }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -279,13 +365,13 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     } else if (warp == 1) {
         // ---------------------------------------------------------- MMA issuer
         if (lane == 0) {
-            int s = 0;
+            int s = 0, j = 0;
             uint32_t ph = 0;
             int lt = 0;
             for (int t = cid; t < ntiles; t += ncl, ++lt) {
                 const GemmTile tl = tiles[t];
                 const GemmGroup g = groups[tl.group];
-                const int nkb = (g.K + BK - 1) / BK;
+                const int nkb = (g.K + KB - 1) / KB;
                 const int acc = lt & 1;
                 const uint32_t aph = (lt >> 1) & 1;
                 int nrem = g.N - tl.n0;
@@ -295,29 +381,25 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 const uint32_t tmem_d = tmem_base + acc * BN;
                 mbar_wait(tempty_bar(acc), aph ^ 1);
                 tc_fence_after();
-                for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(conv_bar(s), ph);
+                if (tr && lt < 2048) {
+                    trace[4 * TR_N + 2 * lt] = clock64();
+                    trace[4 * TR_N + 2 * lt + 1] = ninst * 1000 + nkb;
+                }
+                for (int kb = 0; kb < nkb; ++kb, ++j) {
+                    mbar_wait(conv_bar(s), ph);  // converter waited full(s): data landed + A_lo
                     tc_fence_after();
-                    const int ksteps = min(BK / 8, (g.K - kb * BK + 7) / 8);
+                    if (tr && j < TR_N) trace[3 * TR_N + j] = clock64();
+                    const int ksteps = (dbg & 4) ? 0 : min(KB / 8, (g.K - kb * KB + 7) / 8);
                     for (int kk = 0; kk < ksteps; ++kk) {
-                        const uint64_t bhi = make_sdesc(b_hi(s) + kk * 32);
-                        if constexpr (ATMEM) {
-                            const uint32_t ahi = tmem_a(s) + kk * 8, alo = tmem_a(s) + BK + kk * 8;
-                            tc_mma_tf32_ts(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
-                            if (three_pass) {
-                                const uint64_t blo = make_sdesc(b_lo(s) + kk * 32);
-                                tc_mma_tf32_ts(tmem_d, ahi, blo, idesc, 1u);
-                                tc_mma_tf32_ts(tmem_d, alo, bhi, idesc, 1u);
-                            }
-                        } else {
-                            const uint64_t ahi = make_sdesc(a_hi(s) + kk * 32);
-                            tc_mma_tf32(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
-                            if (three_pass) {
-                                const uint64_t alo = make_sdesc(a_lo(s) + kk * 32);
-                                const uint64_t blo = make_sdesc(b_lo(s) + kk * 32);
-                                tc_mma_tf32(tmem_d, ahi, blo, idesc, 1u);
-                                tc_mma_tf32(tmem_d, alo, bhi, idesc, 1u);
-                            }
+                        const uint64_t ahi = make_sdesc<KB>(a_hi(s) + kk * 32);
+                        const uint64_t bhi = make_sdesc<KB>(b_hi(s) + kk * 32);
+                        tc_mma_tf32(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
+                        if (three_pass) {
+                            tc_mma_tf32(tmem_d, ahi, make_sdesc<KB>(b_lo(s) + kk * 32), idesc, 1u);
+                            if constexpr (ALO)
+                                tc_mma_tf32_ts(tmem_d, tmem_alo(s) + kk * 8, bhi, idesc, 1u);
+                            else
+                                tc_mma_tf32(tmem_d, make_sdesc<KB>(a_lo(s) + kk * 32), bhi, idesc, 1u);
                         }
                     }
                     if (CL == 1)
@@ -329,49 +411,53 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 tc_commit(tfull_bar(acc));
             }
         }
-    } else if (warp >= 4 && warp < (ATMEM ? 12 : 8)) {
+    } else if (warp >= 4 && warp < (ALO ? 12 : 8) && !((dbg & 32) && warp >= 8)) {
         // ----------------------------------------------------------- converter
-        // TMEM-A variant: two warpgroups take alternate stages (set = stage parity) so the
-        // per-stage convert latency does not gate small-N tiles
+        // ALO: two warpgroups split the STAGES (set = stage parity).  A set must own whole
+        // stages: TMA loads into different stages can land out of order, so a set that
+        // skipped a phase of full[s] could see try_wait.parity succeed on the stale
+        // phase (parity aliasing) -- assigning by k-block parity with odd STAGES hung.
         const int ct = threadIdx.x - 128;
-        const int cset = ATMEM ? (warp - 4) / 4 : 0;
-        int s = 0;
+        const int cset = ALO ? (warp - 4) / 4 : 0;
+        int s = 0, j = 0;
         uint32_t ph = 0;
+        const bool trc = tr && (ct & 127) == 0;
         for (int t = cid; t < ntiles; t += ncl) {
             const GemmTile tl = tiles[t];
             const GemmGroup g = groups[tl.group];
-            const int nkb = (g.K + BK - 1) / BK;
-            for (int kb = 0; kb < nkb; ++kb) {
-                if (ATMEM && (s & 1) != cset) {
+            const int nkb = (g.K + KB - 1) / KB;
+            for (int kb = 0; kb < nkb; ++kb, ++j) {
+                if (ALO && (s & 1) != cset && !(dbg & 32)) {
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     continue;
                 }
                 mbar_wait(full_bar(s), ph);
-                if constexpr (ATMEM) {
-                    // this warp owns TMEM lanes 32q..32q+31 = tile rows; read the row's BK
-                    // fp32 from the SWIZZLE_64B tile (16-byte chunk c of row r sits at
-                    // chunk c ^ ((r >> 1) & 3); conflict-free for 8 consecutive rows)
-                    const int q = warp & 3;
-                    const int row = 32 * q + lane;
-                    const float4* rowp = reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase) + row * BK * 4);
-                    float hi[16], lo[16];
+                if (trc && j < TR_N) trace[TR_N + j] = clock64();
+                if constexpr (ALO) {
+                    if (three_pass && !(dbg & 2)) {
+                        // this warp owns TMEM lanes 32q..32q+31 = tile rows; read the row's
+                        // 32 fp32 from the SWIZZLE_128B tile (16-byte chunk c of row r sits
+                        // at chunk c ^ (r & 7): conflict-free for 8 consecutive rows)
+                        const int q = warp & 3;
+                        const int row = 32 * q + lane;
+                        const float4* rowp =
+                            reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase) + row * KB * 4);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const float4 v = rowp[c ^ ((row >> 1) & 3)];
-                        const float vv[4] = {v.x, v.y, v.z, v.w};
+                        for (int h = 0; h < 2; ++h) {
+                            float lo[16];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            uint32_t u;
-                            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(vv[e]));
-                            hi[4 * c + e] = three_pass ? __uint_as_float(u) : vv[e];
-                            lo[4 * c + e] = vv[e] - __uint_as_float(u);
+                            for (int c = 0; c < 4; ++c) {
+                                const float4 v = rowp[(4 * h + c) ^ (row & 7)];
+                                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    lo[4 * c + e] = vv[e] - __uint_as_float(__float_as_uint(vv[e]) & 0xFFFFE000u);
+                            }
+                            tmem_st16(tmem_alo(s) + 16 * h + (static_cast<uint32_t>(32 * q) << 16), lo);
                         }
+                        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                        tc_fence_before();
                     }
-                    const uint32_t ta = tmem_a(s) + (static_cast<uint32_t>(32 * q) << 16);
-                    tmem_st16(ta, hi);
-                    if (three_pass) tmem_st16(ta + BK, lo);
-                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                    tc_fence_before();
                 } else if (three_pass) {
                     float4* hi = reinterpret_cast<float4*>(smem + (a_hi(s) - sbase));
                     float4* lo = reinterpret_cast<float4*>(smem + (a_lo(s) - sbase));
@@ -392,10 +478,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
                 mbar_arrive(conv_bar(s));
+                if (trc && j < TR_N) trace[2 * TR_N + j] = clock64();
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
-    } else if (warp >= (ATMEM ? 12 : 8)) {
+    } else if (warp >= (ALO ? 12 : 8)) {
         // ------------------------------------------------------------- epilogue
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         int lt = 0;
@@ -412,7 +499,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             const bool mok = m < g.M;
             const uint32_t trow = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
             float* dbase = D + g.d_off;
-            if (store_mode == STORE_ROW) {
+            if (dbg & 1) {
+            } else if (store_mode == STORE_ROW) {
                 // per-warp 32x32 transpose through padded SMEM: each warp stores its 32
                 // rows as 128-byte row segments (coalesced) instead of one row per lane
                 float* tile = stile + q * 32 * 33;
@@ -484,28 +572,29 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-static CUtensorMap make_map(const Mat2D& m, int box_rows) {
+static CUtensorMap make_map(const Mat2D& m, int box_rows, int kb) {
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
     require(m.ld * 4 % 16 == 0, "gemm: operand row stride must be a multiple of 16 bytes");
     require((reinterpret_cast<uintptr_t>(m.p) & 15) == 0, "gemm: operand must be 16B aligned");
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(m.cols), static_cast<cuuint64_t>(m.rows)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(m.ld * 4)};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(m.p), dims,
                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             kb == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(SPH_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return map;
 }
 
-template <int BN, int STAGES, int CL, bool ATMEM = false>
+template <int BN, int STAGES, int CL, bool ALO = false>
 static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
                    float* D, bool three, cudaStream_t st) {
-    using L = Smem<BN, STAGES, ATMEM>;
-    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL, ATMEM>;
+    using L = Smem<BN, STAGES, ALO>;
+    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL, ALO>;
     static int grid = 0;
     static std::once_flag once;
     std::call_once(once, [&] {
@@ -514,7 +603,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
         if (CL > 1) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(nthreads<ATMEM>());
+            cfg.blockDim = dim3(nthreads<ALO>());
             cfg.dynamicSmemBytes = L::TOTAL;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
@@ -530,19 +619,19 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     });
     Mat2D am = g.A;
     am.p = A;
-    const CUtensorMap ma = make_map(am, BM);
+    const CUtensorMap ma = make_map(am, BM, bk_of<ALO>());
     Mat2D bh = g.Bhi, bl = g.Blo;
     bh.p = Bhi;
     bl.p = Blo;
-    const CUtensorMap mbh = make_map(bh, BN / CL);
-    const CUtensorMap mbl = make_map(three ? bl : bh, BN / CL);
+    const CUtensorMap mbh = make_map(bh, BN / CL, bk_of<ALO>());
+    const CUtensorMap mbl = make_map(three ? bl : bh, BN / CL, bk_of<ALO>());
     const GemmTileList& tl = g.tiles_for(CL);
     int gsz = static_cast<int>(std::min<int64_t>(tl.n * CL, grid));
     gsz = std::max(CL, gsz / CL * CL);
     ProfScope prof(g.name, st, g.flops);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(gsz);
-    cfg.blockDim = dim3(nthreads<ATMEM>());
+    cfg.blockDim = dim3(nthreads<ALO>());
     cfg.dynamicSmemBytes = L::TOTAL;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -552,10 +641,35 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = CL > 1 ? 1 : 0;
+    static const char* trace_dir = std::getenv("SPH_GEMM_TRACE");  // diagnostic only
+    static const int dbg = std::getenv("SPH_GEMM_DEBUG") ? std::atoi(std::getenv("SPH_GEMM_DEBUG")) : 0;
+    long long* trace = nullptr;
+    if (trace_dir) {
+        SPH_CUDA(cudaMalloc(&trace, (4 * 512 + 4096) * sizeof(long long)));
+        SPH_CUDA(cudaMemsetAsync(trace, 0, (4 * 512 + 4096) * sizeof(long long), st));
+    }
     SPH_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, static_cast<const GemmGroup*>(g.d_groups.p),
                                 static_cast<const GemmTile*>(tl.d.p), static_cast<int>(tl.n), D,
-                                g.store, three ? 1 : 0));
+                                g.store, three ? 1 : 0, trace, dbg, MatRef{A, am.rows, am.ld},
+                                MatRef{Bhi, bh.rows, bh.ld}, MatRef{three ? Blo : nullptr, bl.rows, bl.ld}));
     count_launch();
+    if (trace) {
+        std::vector<long long> h(4 * 512 + 4096);
+        SPH_CUDA(cudaStreamSynchronize(st));
+        SPH_CUDA(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        cudaFree(trace);
+        const std::string path = std::string(trace_dir) + "/gemm_trace_" + g.name + ".txt";
+        if (FILE* f = std::fopen(path.c_str(), "w")) {
+            for (int j = 0; j < 512; ++j)
+                std::fprintf(f, "%d %lld %lld %lld %lld\n", j, h[j], h[512 + j], h[1024 + j], h[1536 + j]);
+            std::fclose(f);
+        }
+        const std::string tpath = std::string(trace_dir) + "/gemm_tiles_" + g.name + ".txt";
+        if (FILE* f = std::fopen(tpath.c_str(), "w")) {
+            for (int t = 0; t < 2048; ++t) std::fprintf(f, "%lld %lld\n", h[2048 + 2 * t], h[2048 + 2 * t + 1]);
+            std::fclose(f);
+        }
+    }
 }
 
 }  // namespace tc
@@ -577,11 +691,11 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
     require(!three || Blo, "gemm: 3xTF32 needs the lo table");
     const int cl = g.cluster;
     if (g.bn == 192 && cl == 1)
-        tc::launch<192, 4, 1, true>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<192, 3, 1, true>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 192 && cl == 2)
-        tc::launch<192, 4, 2, true>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<192, 3, 2, true>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 192 && cl == 4)
-        tc::launch<192, 4, 4, true>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<192, 3, 4, true>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 256 && cl == 1)
         tc::launch<256, 4, 1>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 256 && cl == 2)
