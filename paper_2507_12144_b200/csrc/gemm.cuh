@@ -28,8 +28,24 @@ struct GemmTile {
     int32_t group, m0, n0, pad;
 };
 
+// One output tile of the tcgen05 kernel, flattened from (group, m0, n0) on the host so
+// each warp role reads ONE descriptor per tile (and loads the next one a tile ahead)
+// instead of two dependent global loads on the pipeline's critical path.
+struct GemmWork {
+    int32_t a_row;    // group a_row0 + m0
+    int32_t b_row;    // group b_row0 + n0
+    int32_t M;        // group rows (row validity: m < M)
+    int32_t m0, n0;   // tile origin inside the group
+    int32_t nrem;     // min(bn, N - n0): columns computed
+    int32_t K;
+    int32_t ldd;
+    int32_t ncols;    // STORE_ROW columns written incl. the zero fill up to zero_to
+    int32_t dg;       // group index in the 3D [group][rows][ldd] view of D (TMA store)
+    int64_t d_off;    // element offset of D(0,0) of the group
+};
+
 struct GemmTileList {
-    DevBuf<GemmTile> d;
+    DevBuf<GemmWork> d;
     int64_t n = 0;
 };
 
@@ -52,6 +68,11 @@ struct GroupedGemm {
     int store = STORE_ROW;
     int bn = 256;                  // N tile (<= 256, multiple of 16)
     int cluster = 0;               // CTAs per cluster sharing the table tile (0 = auto)
+    bool pair = false;             // cta_group::2 CTA-pair MMA (set by finalize)
+    // TMA-store epilogue (ALO kernel): D is a uniform 3D [d_groups3][d_rows][ldd] view
+    // (every group has the same ldd and row count, d_off a multiple of d_rows * ldd)
+    bool tma_store = false;
+    int64_t d_rows = 0, d_groups3 = 0, d_ldd = 0;
     DevBuf<GemmGroup> d_groups;
     int64_t ntiles = 0;            // tiles at cluster size 1 (0 -> nothing to do)
     mutable std::map<int, std::unique_ptr<GemmTileList>> tile_lists;

@@ -1,21 +1,19 @@
 // tcgen05 / TMEM / TMA grouped GEMM for sm_100a with a 3xTF32 precision split.
 //
-// Persistent, warp-specialised, one CTA per SM:
-//   warp 0        TMA producer: A tile (data, fp32), B_hi and B_lo tiles (table) per
-//                 stage, plus an L2 prefetch cursor PF k-blocks ahead
+// Persistent, warp-specialised, one CTA (or CTA pair) per SM:
+//   warp 0        TMA producer: A tile (data, fp32), B_hi and B_lo tiles (table) per stage
 //   warp 1        MMA issuer (one elected thread): per K=8 step
 //                   D += A_hi*B_hi ; D += A_hi*B_lo ; D += A_lo*B_hi   (kind::tf32)
 //   warp 2        TMEM allocator
-//   warps 4..11   converters (ALO, two warpgroups on alternate stages): A_lo = A -
-//                 trunc_tf32(A) -> TMEM (tcgen05.st); A_hi is the fp32 tile itself
-//                 (see the kernel comment).  Non-ALO variant (warps 4..7): A_hi/A_lo
-//                 rna-split in SMEM.
-//   warps 12..15  epilogue (8..11 non-ALO): TMEM -> registers (tcgen05.ld 32x32b) ->
-//                 global, row-major through a per-warp SMEM transpose or column-major
+//   warps 4..7    converter: ALO -> A_lo = A - trunc_tf32(A) into TMEM (tcgen05.st), A_hi
+//                 is the fp32 tile itself (see the kernel comment); otherwise A_hi/A_lo
+//                 rna-split in SMEM
+//   warps 8..     epilogue (4, or 8 in the pair variant): TMEM -> registers (pipelined
+//                 tcgen05.ld 32x32b.x32) -> global, row-major through a per-warp SMEM
+//                 transpose or column-major
 // Pipelines: SMEM ring (full -> converted -> empty) and a double-buffered TMEM
 // accumulator (full/empty) so the epilogue of tile i overlaps the MMAs of tile i+1.
-// Operand tiles are K-major, SWIZZLE_64B (16 fp32 of K per 64-byte row, 8-row /
-// 512-byte atoms, SBO = 512).
+// Operand tiles are K-major, SWIZZLE_64B (BK = 16) or SWIZZLE_128B (BK = 32, ALO).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -33,9 +31,10 @@ constexpr int BM = 128;
 constexpr int BK = 16;               // fp32 per 64-byte swizzle row (SWIZZLE_64B variants)
 constexpr int BK_ALO = 32;           // fp32 per 128-byte swizzle row (ALO variant, SWIZZLE_128B)
 template <bool ALO> constexpr int bk_of() { return ALO ? BK_ALO : BK; }
-constexpr int NUM_THREADS = 384;      // 12 warps (SMEM A_hi/A_lo variant)
-constexpr int NUM_THREADS_ALO = 512;  // 16 warps (ALO variant: two converter warpgroups)
-template <bool ALO> constexpr int nthreads() { return ALO ? NUM_THREADS_ALO : NUM_THREADS; }
+// warps: 0 producer, 1 MMA, 2 TMEM allocator, 3 idle, 4..7 converter, 8.. epilogue
+// (4 warps, or 8 = two per TMEM lane quarter splitting the columns in the pair variant)
+template <bool PAIR> constexpr int epi_warps() { return PAIR ? 8 : 4; }
+template <bool PAIR> constexpr int nthreads() { return (8 + epi_warps<PAIR>()) * 32; }
 
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -81,6 +80,52 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         }
     }
 }
+// arrive on the barrier at the same SMEM offset in cluster CTA `cta` (default .release.cta
+// semantics, as CUTLASS's ClusterBarrier::arrive; .release.cluster measured ~2k cycles)
+__device__ __forceinline__ void mbar_arrive_cta(uint32_t bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar), "r"(cta)
+        : "memory");
+}
+// CTA-pair TMA: data lands in this CTA's SMEM, completion is signalled on the pair
+// leader's barrier (same offset, peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar & 0xFEFFFFFFu)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(bar), "h"(mask)
+        : "memory");
+}
+// M = 256 over the CTA pair: rows 0..127 from the leader's A (SMEM or TMEM), 128..255
+// from the peer's (same address); the B columns are split in halves between the two
+// CTAs' SMEM (same offset)
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                 uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                    uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint32_t bar) {
     asm volatile(
@@ -89,21 +134,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
 }
-struct MatRef {  // base / rows / row stride of a TMA operand, for whole-tile L2 prefetch
-    const float* p;
-    int64_t rows, ld;
-};
-
-// L2 prefetch of a contiguous row range [row0, row0 + nrows) of a row-major matrix
-__device__ __forceinline__ void l2_prefetch_rows(const MatRef& m, int64_t row0, int64_t nrows) {
-    if (m.p == nullptr || row0 >= m.rows) return;
-    if (nrows > m.rows - row0) nrows = m.rows - row0;
-    const char* p = reinterpret_cast<const char*>(m.p + row0 * m.ld);
-    int64_t bytes = nrows * m.ld * 4;
-    for (; bytes > 0; bytes -= 32768, p += 32768) {
-        const uint32_t n = static_cast<uint32_t>(bytes < 32768 ? bytes : 32768);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(n) : "memory");
-    }
+// TMA tensor store of a [1][32][32] box from SMEM (bulk async-group of this thread)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                                uint32_t bar, uint16_t mask) {
@@ -169,21 +205,32 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
         "r"(__float_as_uint(v[15]))
         : "memory");
 }
-// 32 lanes x 32 bit, 16 consecutive columns per lane
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
+// 32 lanes x 32 bit, 32 consecutive columns per lane, asynchronous: the registers are
+// valid only after tmem_wait32 on the same array (which takes them as "+r" operands so
+// the compiler cannot move their uses above the wait)
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-
+__device__ __forceinline__ void tmem_wait32(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                   "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
+                   "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]),
+                   "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]),
+                   "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]),
+                   "+r"(r[31])
+                 :
+                 : "memory");
+}
 // UMMA shared-memory descriptor: K-major, rows of KB fp32 (64 B -> SWIZZLE_64B, layout 4;
 // 128 B -> SWIZZLE_128B, layout 2), 8-row atoms (SBO = 8 rows), version 1.
 template <int KB>
@@ -198,7 +245,7 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
     return d;
 }
 // Instruction descriptor: kind::tf32, D f32, A/B tf32, both K-major, M = 128, N = n.
-__device__ __forceinline__ uint32_t make_idesc(int n, int m = BM) {
+__device__ __forceinline__ uint32_t make_idesc(int n, int m = BM) {  // m = 256: CTA pair
     uint32_t d = 0;
     d |= 1u << 4;                             // D format f32
     d |= 2u << 7;                             // A format tf32
@@ -208,16 +255,19 @@ __device__ __forceinline__ uint32_t make_idesc(int n, int m = BM) {
     return d;
 }
 
-template <int BN, int STAGES, bool ALO = false>
+template <int BN, int STAGES, bool ALO = false, bool PAIR = false>
 struct Smem {
     static constexpr int A_TILE_BYTES = BM * bk_of<ALO>() * 4;
-    static constexpr int B_TILE_BYTES = BN * bk_of<ALO>() * 4;
+    static constexpr int B_TILE_BYTES = (PAIR ? BN / 2 : BN) * bk_of<ALO>() * 4;  // PAIR: half
     static constexpr int A_BYTES = ALO ? A_TILE_BYTES : 2 * A_TILE_BYTES;  // A or (A_hi, A_lo)
     static constexpr int STAGE_BYTES = A_BYTES + 2 * B_TILE_BYTES;
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     // full[S], conv[S], empty[S], tfull[2], tempty[2], tmem slot
-    static constexpr int TILE_OFF = BAR_OFF + (3 * STAGES + 4) * 8 + 16;
-    static constexpr int TOTAL = TILE_OFF + 4 * 32 * 33 * 4 + 1024;  // + align slack
+    static constexpr int TILE_OFF = (BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1023) / 1024 * 1024;
+    // epilogue staging: ALO -> two 4 KB TMA-store buffers per epilogue warp (also fits the
+    // 32x33 transpose tiles of the plain-store fallback); else the transpose tiles
+    static constexpr int OUT_BYTES = ALO ? epi_warps<PAIR>() * 8192 : epi_warps<PAIR>() * 32 * 33 * 4;
+    static constexpr int TOTAL = TILE_OFF + OUT_BYTES + 1024;  // + align slack
 };
 
 // CL > 1: thread-block cluster of CL CTAs on CL consecutive M-tiles of one (group,
@@ -236,23 +286,35 @@ struct Smem {
 // empty) and not the tensor pipe (6 MMAs = 576 cycles at N = 192, profiles/mma_rate.cu)
 // bounded it; doubling the MMA work per round halves that cost per flop.  TMEM: 2 x BN
 // accumulators + STAGES x 32 A_lo columns (384 + 96).
-template <int BN, int STAGES, int CL, bool ALO>
-__global__ void __launch_bounds__(nthreads<ALO>(), 1)
+//
+// PAIR (ALO, CL = 2): the cluster's two CTAs form one cta_group::2 MMA of M = 256.  Each
+// CTA loads its own 128 data rows and HALF of the table tile (ninst/2 rows at n0 + rank *
+// ninst/2), so per SM and k-block the inbound bytes drop from A + B to A + B/2 -- the
+// measured limit of the single-CTA variant above.  The leader (rank 0) issues the MMAs
+// (both CTAs' A / A_lo / B halves are read at the same SMEM / TMEM offsets); its full
+// barrier also counts the peer's table-half bytes (.cta_group::2 TMA), its conv / tempty
+// barriers take the peer's converter / epilogue arrivals (count 256), and its commits
+// multicast to both CTAs' empty / tfull barriers.
+template <int BN, int STAGES, int CL, bool ALO, bool PAIR = false>
+__global__ void __launch_bounds__(nthreads<PAIR>(), 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_bhi,
-                   const __grid_constant__ CUtensorMap map_blo, const GemmGroup* __restrict__ groups,
-                   const GemmTile* __restrict__ tiles, int ntiles, float* __restrict__ D,
+                   const __grid_constant__ CUtensorMap map_blo, const __grid_constant__ CUtensorMap map_d,
+                   const GemmWork* __restrict__ works,
+                   int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
-                   MatRef ra, MatRef rbhi, MatRef rblo) {
+                   int tma_store) {
     // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
-    // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads,
-    // 16 no L2 prefetch, 32 one converter warpgroup
+    // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads
+    // (a whole-tile cp.async.bulk.prefetch.L2 one tile ahead was measured slower: cfg2
+    // Legendre fwd / inv 5.07M / 4.65M vs 4.44M / 3.81M cycles without)
     // trace (diagnostic, SPH_GEMM_TRACE): CTA 0 records clock64 per k-block j < TR_N at
     // [0] producer issue, [1] data landed (converter wake), [2] converted, [3] MMA issue,
     // and per tile [4*TR_N + 2*lt] MMA start clock, [.. + 1] ninst * 1000 + k-blocks
     constexpr int TR_N = 512;
     const bool tr = trace != nullptr && blockIdx.x == 0;
-    using L = Smem<BN, STAGES, ALO>;
+    using L = Smem<BN, STAGES, ALO, PAIR>;
+    static_assert(!PAIR || (ALO && CL == 2 && BN % 32 == 0), "pair mode: ALO, cluster of 2");
     constexpr int KB = bk_of<ALO>();
     constexpr int A_TILE_BYTES = L::A_TILE_BYTES;
     static_assert(!ALO || 2 * BN + STAGES * KB <= 512, "TMEM budget");
@@ -281,12 +343,12 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(conv_bar(s), 128);
-            mbar_init(empty_bar(s), CL);
+            mbar_init(conv_bar(s), PAIR ? 256 : 128);  // converter warps 4..7 (x2 CTAs)
+            mbar_init(empty_bar(s), PAIR ? 1 : CL);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), 128);
+            mbar_init(tempty_bar(a), (PAIR ? 2 : 1) * epi_warps<PAIR>() * 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -296,11 +358,19 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -310,7 +380,17 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     const int crank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
     const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
     const uint16_t cmask = static_cast<uint16_t>((1u << CL) - 1);
-    constexpr int B_ROWS = BN / CL;  // table rows loaded (and multicast) by this CTA
+    constexpr int B_ROWS = PAIR ? BN / 2 : BN / CL;  // table rows loaded by this CTA
+    // PAIR: instruction N = N rounded up to 32; the peer's half starts at ninst / 2
+    auto pair_half = [](const GemmWork& w) { return (w.nrem + 31) / 32 * 16; };
+    // each role walks tiles cid, cid + ncl, ... and loads the next descriptor one tile ahead
+    GemmWork wnext{};
+    if (cid < ntiles) wnext = works[cid];
+    auto next_work = [&](int t) {
+        const GemmWork w = wnext;
+        if (t + ncl < ntiles) wnext = works[t + ncl];
+        return w;
+    };
     if (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
 
     if (warp == 0) {
@@ -318,45 +398,42 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         if (lane == 0) {
             int s = 0, j = 0;
             uint32_t ph = 0;
-            // Whole-tile L2 prefetch one tile ahead (a tile's data rows and table rows are
-            // contiguous row ranges; the k-block boxes walk them in column strips)
-            auto prefetch_tile = [&](int pt) {
-                if (pt >= ntiles || (dbg & 16)) return;
-                const GemmTile ptl = tiles[pt];
-                const GemmGroup pg = groups[ptl.group];
-                l2_prefetch_rows(ra, pg.a_row0 + ptl.m0 + crank * BM, BM);
-                const int brow = pg.b_row0 + ptl.n0 + (CL > 1 ? crank * B_ROWS : 0);
-                l2_prefetch_rows(rbhi, brow, B_ROWS);
-                if (three_pass) l2_prefetch_rows(rblo, brow, B_ROWS);
-            };
-            prefetch_tile(cid);
             for (int t = cid; t < ntiles; t += ncl) {
-                const GemmTile tl = tiles[t];
-                const GemmGroup g = groups[tl.group];
-                const int nkb = (g.K + KB - 1) / KB;
-                prefetch_tile(t + ncl);
+                const GemmWork w = next_work(t);
+                const int nkb = (w.K + KB - 1) / KB;
                 for (int kb = 0; kb < nkb; ++kb, ++j) {
                     mbar_wait(empty_bar(s), ph ^ 1);
                     if (tr && j < TR_N) trace[j] = clock64();
                     if (dbg & 8) {
                         mbar_expect_tx(full_bar(s), A_TILE_BYTES);
-                        tma_load_2d(a_hi(s), &map_a, kb * KB, g.a_row0 + tl.m0 + crank * BM, full_bar(s));
+                        tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
+                        if (++s == STAGES) { s = 0; ph ^= 1; }
+                        continue;
+                    }
+                    if constexpr (PAIR) {
+                        // leader's full barrier: own A + both CTAs' table halves; peer's: A
+                        const int nb = (three_pass ? 2 : 1) * L::B_TILE_BYTES;
+                        mbar_expect_tx(full_bar(s), A_TILE_BYTES + (crank == 0 ? 2 * nb : 0));
+                        tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
+                        const int brow = w.b_row + crank * pair_half(w);
+                        tma_load_2d_pair(b_hi(s), &map_bhi, kb * KB, brow, full_bar(s));
+                        if (three_pass) tma_load_2d_pair(b_lo(s), &map_blo, kb * KB, brow, full_bar(s));
                         if (++s == STAGES) { s = 0; ph ^= 1; }
                         continue;
                     }
                     mbar_expect_tx(full_bar(s), A_TILE_BYTES + (three_pass ? 2 : 1) * L::B_TILE_BYTES);
-                    tma_load_2d(a_hi(s), &map_a, kb * KB, g.a_row0 + tl.m0 + crank * BM, full_bar(s));
+                    tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
                     if (CL == 1) {
-                        tma_load_2d(b_hi(s), &map_bhi, kb * KB, g.b_row0 + tl.n0, full_bar(s));
+                        tma_load_2d(b_hi(s), &map_bhi, kb * KB, w.b_row, full_bar(s));
                         if (three_pass)
-                            tma_load_2d(b_lo(s), &map_blo, kb * KB, g.b_row0 + tl.n0, full_bar(s));
+                            tma_load_2d(b_lo(s), &map_blo, kb * KB, w.b_row, full_bar(s));
                     } else {
                         const uint32_t off = crank * B_ROWS * KB * 4;
                         tma_load_2d_mc(b_hi(s) + off, &map_bhi, kb * KB,
-                                       g.b_row0 + tl.n0 + crank * B_ROWS, full_bar(s), cmask);
+                                       w.b_row + crank * B_ROWS, full_bar(s), cmask);
                         if (three_pass)
                             tma_load_2d_mc(b_lo(s) + off, &map_blo, kb * KB,
-                                           g.b_row0 + tl.n0 + crank * B_ROWS, full_bar(s), cmask);
+                                           w.b_row + crank * B_ROWS, full_bar(s), cmask);
                     }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
@@ -364,20 +441,18 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------- MMA issuer
-        if (lane == 0) {
+        if (lane == 0 && (!PAIR || crank == 0)) {
             int s = 0, j = 0;
             uint32_t ph = 0;
             int lt = 0;
             for (int t = cid; t < ntiles; t += ncl, ++lt) {
-                const GemmTile tl = tiles[t];
-                const GemmGroup g = groups[tl.group];
-                const int nkb = (g.K + KB - 1) / KB;
+                const GemmWork w = next_work(t);
+                const int nkb = (w.K + KB - 1) / KB;
                 const int acc = lt & 1;
                 const uint32_t aph = (lt >> 1) & 1;
-                int nrem = g.N - tl.n0;
-                if (nrem > BN) nrem = BN;
-                const int ninst = (nrem + 15) / 16 * 16;
-                const uint32_t idesc = make_idesc(ninst);
+                const int nrem = w.nrem;
+                const int ninst = PAIR ? (nrem + 31) / 32 * 32 : (nrem + 15) / 16 * 16;
+                const uint32_t idesc = make_idesc(ninst, PAIR ? 2 * BM : BM);
                 const uint32_t tmem_d = tmem_base + acc * BN;
                 mbar_wait(tempty_bar(acc), aph ^ 1);
                 tc_fence_after();
@@ -389,10 +464,18 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     mbar_wait(conv_bar(s), ph);  // converter waited full(s): data landed + A_lo
                     tc_fence_after();
                     if (tr && j < TR_N) trace[3 * TR_N + j] = clock64();
-                    const int ksteps = (dbg & 4) ? 0 : min(KB / 8, (g.K - kb * KB + 7) / 8);
+                    const int ksteps = (dbg & 4) ? 0 : min(KB / 8, (w.K - kb * KB + 7) / 8);
                     for (int kk = 0; kk < ksteps; ++kk) {
                         const uint64_t ahi = make_sdesc<KB>(a_hi(s) + kk * 32);
                         const uint64_t bhi = make_sdesc<KB>(b_hi(s) + kk * 32);
+                        if constexpr (PAIR) {
+                            tc_mma_tf32_pair(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
+                            if (three_pass) {
+                                tc_mma_tf32_pair(tmem_d, ahi, make_sdesc<KB>(b_lo(s) + kk * 32), idesc, 1u);
+                                tc_mma_tf32_ts_pair(tmem_d, tmem_alo(s) + kk * 8, bhi, idesc, 1u);
+                            }
+                            continue;
+                        }
                         tc_mma_tf32(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
                         if (three_pass) {
                             tc_mma_tf32(tmem_d, ahi, make_sdesc<KB>(b_lo(s) + kk * 32), idesc, 1u);
@@ -402,35 +485,30 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                                 tc_mma_tf32(tmem_d, make_sdesc<KB>(a_lo(s) + kk * 32), bhi, idesc, 1u);
                         }
                     }
-                    if (CL == 1)
+                    if (PAIR)
+                        tc_commit_pair_mc(empty_bar(s), cmask);
+                    else if (CL == 1)
                         tc_commit(empty_bar(s));
                     else
                         tc_commit_mc(empty_bar(s), cmask);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
-                tc_commit(tfull_bar(acc));
+                if (PAIR)
+                    tc_commit_pair_mc(tfull_bar(acc), cmask);
+                else
+                    tc_commit(tfull_bar(acc));
             }
         }
-    } else if (warp >= 4 && warp < (ALO ? 12 : 8) && !((dbg & 32) && warp >= 8)) {
+    } else if (warp >= 4 && warp < 8) {
         // ----------------------------------------------------------- converter
-        // ALO: two warpgroups split the STAGES (set = stage parity).  A set must own whole
-        // stages: TMA loads into different stages can land out of order, so a set that
-        // skipped a phase of full[s] could see try_wait.parity succeed on the stale
-        // phase (parity aliasing) -- assigning by k-block parity with odd STAGES hung.
         const int ct = threadIdx.x - 128;
-        const int cset = ALO ? (warp - 4) / 4 : 0;
         int s = 0, j = 0;
         uint32_t ph = 0;
         const bool trc = tr && (ct & 127) == 0;
         for (int t = cid; t < ntiles; t += ncl) {
-            const GemmTile tl = tiles[t];
-            const GemmGroup g = groups[tl.group];
-            const int nkb = (g.K + KB - 1) / KB;
+            const GemmWork w = next_work(t);
+            const int nkb = (w.K + KB - 1) / KB;
             for (int kb = 0; kb < nkb; ++kb, ++j) {
-                if (ALO && (s & 1) != cset && !(dbg & 32)) {
-                    if (++s == STAGES) { s = 0; ph ^= 1; }
-                    continue;
-                }
                 mbar_wait(full_bar(s), ph);
                 if (trc && j < TR_N) trace[TR_N + j] = clock64();
                 if constexpr (ALO) {
@@ -477,77 +555,132 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
-                mbar_arrive(conv_bar(s));
+                if (PAIR)
+                    mbar_arrive_cta(conv_bar(s), 0);  // the leader's MMA waits both CTAs
+                else
+                    mbar_arrive(conv_bar(s));
                 if (trc && j < TR_N) trace[2 * TR_N + j] = clock64();
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
-    } else if (warp >= (ALO ? 12 : 8)) {
+    } else if (warp >= 8) {
         // ------------------------------------------------------------- epilogue
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        // warp (8 + i): TMEM lane quarter q = warp & 3 (rows 32q..32q+31), 32-column chunks
+        // c = 32 * (i / 4) + 32 * EH * k; the next chunk's tcgen05.ld is in flight while
+        // the current one is stored
+        constexpr int EH = epi_warps<PAIR>() / 4;
+        const int q = warp & 3;
+        const int eh = (warp - 8) / 4;
+        float* tile = stile + (warp - 8) * 32 * 33;  // per-warp 32x32 transpose (STORE_ROW)
+        // TMA-store path (ALO): ping-pong 4 KB staging buffers per warp; lane 0 issues the
+        // 3D tensor store of each 32 x 32 chunk and recycles a buffer after wait_group.read
+        const bool tstore = ALO && tma_store;
+        uint8_t* obase = smem + L::TILE_OFF + (warp - 8) * 8192;
+        int nchunk = 0;
         int lt = 0;
         for (int t = cid; t < ntiles; t += ncl, ++lt) {
-            const GemmTile tl = tiles[t];
-            const GemmGroup g = groups[tl.group];
+            const GemmWork w = next_work(t);
             const int acc = lt & 1;
             const uint32_t aph = (lt >> 1) & 1;
-            int nrem = g.N - tl.n0;
-            if (nrem > BN) nrem = BN;
+            const int nrem = w.nrem;
             mbar_wait(tfull_bar(acc), aph);
             tc_fence_after();
-            const int m = tl.m0 + crank * BM + q * 32 + lane;
-            const bool mok = m < g.M;
+            const int row0 = w.m0 + crank * BM + q * 32;
             const uint32_t trow = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-            float* dbase = D + g.d_off;
-            if (dbg & 1) {
-            } else if (store_mode == STORE_ROW) {
-                // per-warp 32x32 transpose through padded SMEM: each warp stores its 32
-                // rows as 128-byte row segments (coalesced) instead of one row per lane
-                float* tile = stile + q * 32 * 33;
-                const int row0 = tl.m0 + crank * BM + q * 32;
-                const int ncols = max(nrem, min(g.zero_to, tl.n0 + BN) - tl.n0);
-                for (int c = 0; c < ncols; c += 32) {
-                    float v[32];
-                    if (c < nrem) {
-                        tmem_ld16(trow + c, *reinterpret_cast<float(*)[16]>(&v[0]));
-                        tmem_ld16(trow + c + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
-                    }
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = (c + j < nrem) ? v[j] : 0.f;
+            float* dbase = D + w.d_off;
+            const int ncols = store_mode == STORE_ROW ? w.ncols : nrem;
+            uint32_t va[32], vb[32];
+            int c = 32 * eh;
+            if (!(dbg & 1) && c < nrem) {
+                tmem_ld32_async(trow + c, va);
+                tmem_wait32(va);
+            }
+            for (; !(dbg & 1) && c < ncols; c += 32 * EH) {
+                const int cn = c + 32 * EH;
+                const bool more = cn < nrem;
+                if (more) tmem_ld32_async(trow + cn, vb);
+                if (tstore) {
+                    float* ob = reinterpret_cast<float*>(obase + (nchunk & 1) * 4096);
+                    if (lane == 0 && nchunk >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                     __syncwarp();
-                    const int col = tl.n0 + c + lane;
+                    if (store_mode == STORE_ROW) {
+                        // box {32 cols, 32 rows}, SWIZZLE_128B: row = lane, 16-byte chunk k of
+                        // the row at k ^ (row & 7)
+                        float4* orow = reinterpret_cast<float4*>(ob) + lane * 8;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            float e[4];
+#pragma unroll
+                            for (int x = 0; x < 4; ++x)
+                                e[x] = (c + 4 * k + x < nrem) ? __uint_as_float(va[4 * k + x]) : 0.f;
+                            orow[k ^ (lane & 7)] = make_float4(e[0], e[1], e[2], e[3]);
+                        }
+                    } else {
+                        // box {32 rows m (contiguous), 32 cols n}: element (n = jj, m = lane)
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            ob[jj * 32 + lane] = (c + jj < nrem) ? __uint_as_float(va[jj]) : 0.f;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (store_mode == STORE_ROW)
+                            tma_store_3d(&map_d, smem_u32(ob), w.n0 + c, row0, w.dg);
+                        else
+                            tma_store_3d(&map_d, smem_u32(ob), row0, w.n0 + c, w.dg);
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    ++nchunk;
+                } else if (store_mode == STORE_ROW) {
+                    // transpose through padded SMEM: 32 coalesced 128-byte row segments
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj)
+                        tile[lane * 33 + jj] = (c + jj < nrem) ? __uint_as_float(va[jj]) : 0.f;
+                    __syncwarp();
+                    const int col = w.n0 + c + lane;
                     const bool cok = c + lane < ncols;
-#pragma unroll 4
+#pragma unroll 8
                     for (int r = 0; r < 32; ++r) {
                         const int mr = row0 + r;
-                        if (cok && mr < g.M) dbase[static_cast<int64_t>(mr) * g.ldd + col] = tile[r * 33 + lane];
+                        if (cok && mr < w.M) dbase[static_cast<int64_t>(mr) * w.ldd + col] = tile[r * 33 + lane];
                     }
                     __syncwarp();
-                }
-            } else {
-                for (int c = 0; c < nrem; c += 16) {
-                    float v[16];
-                    tmem_ld16(trow + c, v);
-                    const int n = tl.n0 + c;
-                    if (mok) {
+                } else {
+                    const int m = row0 + lane;
+                    if (m < w.M) {
+                        float* dp = dbase + static_cast<int64_t>(w.n0 + c) * w.ldd + m;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (c + j < nrem) dbase[static_cast<int64_t>(n + j) * g.ldd + m] = v[j];
+                        for (int jj = 0; jj < 32; ++jj)
+                            if (c + jj < nrem) dp[static_cast<int64_t>(jj) * w.ldd] = __uint_as_float(va[jj]);
                     }
+                }
+                if (more) {
+                    tmem_wait32(vb);
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) va[jj] = vb[jj];
                 }
             }
             tc_fence_before();
-            mbar_arrive(tempty_bar(acc));
+            if (PAIR)
+                mbar_arrive_cta(tempty_bar(acc), 0);
+            else
+                mbar_arrive(tempty_bar(acc));
         }
+        if (tstore && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
 
     __syncthreads();
     if (CL > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast into it
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(TMEM_COLS)
-                     : "memory");
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS)
+                         : "memory");
     }
 }
 
@@ -590,11 +723,11 @@ static CUtensorMap make_map(const Mat2D& m, int box_rows, int kb) {
     return map;
 }
 
-template <int BN, int STAGES, int CL, bool ALO = false>
+template <int BN, int STAGES, int CL, bool ALO = false, bool PAIR = false>
 static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
                    float* D, bool three, cudaStream_t st) {
-    using L = Smem<BN, STAGES, ALO>;
-    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL, ALO>;
+    using L = Smem<BN, STAGES, ALO, PAIR>;
+    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL, ALO, PAIR>;
     static int grid = 0;
     static std::once_flag once;
     std::call_once(once, [&] {
@@ -603,7 +736,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
         if (CL > 1) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(nthreads<ALO>());
+            cfg.blockDim = dim3(nthreads<PAIR>());
             cfg.dynamicSmemBytes = L::TOTAL;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
@@ -623,15 +756,32 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     Mat2D bh = g.Bhi, bl = g.Blo;
     bh.p = Bhi;
     bl.p = Blo;
-    const CUtensorMap mbh = make_map(bh, BN / CL, bk_of<ALO>());
-    const CUtensorMap mbl = make_map(three ? bl : bh, BN / CL, bk_of<ALO>());
+    const CUtensorMap mbh = make_map(bh, PAIR ? BN / 2 : BN / CL, bk_of<ALO>());
+    const CUtensorMap mbl = make_map(three ? bl : bh, PAIR ? BN / 2 : BN / CL, bk_of<ALO>());
+    CUtensorMap md;
+    std::memset(&md, 0, sizeof(md));
+    const bool tstore = ALO && g.tma_store;
+    if (tstore) {
+        cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.d_ldd), static_cast<cuuint64_t>(g.d_rows),
+                              static_cast<cuuint64_t>(g.d_groups3)};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.d_ldd * 4),
+                                 static_cast<cuuint64_t>(g.d_rows * g.d_ldd * 4)};
+        cuuint32_t box[3] = {32, 32, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        require((reinterpret_cast<uintptr_t>(D) & 15) == 0, "gemm: output must be 16B aligned");
+        CUresult r = encode_fn()(&md, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, D, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 g.store == STORE_ROW ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(SPH_ERR_CUDA, "cuTensorMapEncodeTiled (D) failed: " + std::to_string(r));
+    }
     const GemmTileList& tl = g.tiles_for(CL);
     int gsz = static_cast<int>(std::min<int64_t>(tl.n * CL, grid));
     gsz = std::max(CL, gsz / CL * CL);
     ProfScope prof(g.name, st, g.flops);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(gsz);
-    cfg.blockDim = dim3(nthreads<ALO>());
+    cfg.blockDim = dim3(nthreads<PAIR>());
     cfg.dynamicSmemBytes = L::TOTAL;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -648,10 +798,9 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
         SPH_CUDA(cudaMalloc(&trace, (4 * 512 + 4096) * sizeof(long long)));
         SPH_CUDA(cudaMemsetAsync(trace, 0, (4 * 512 + 4096) * sizeof(long long), st));
     }
-    SPH_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, static_cast<const GemmGroup*>(g.d_groups.p),
-                                static_cast<const GemmTile*>(tl.d.p), static_cast<int>(tl.n), D,
-                                g.store, three ? 1 : 0, trace, dbg, MatRef{A, am.rows, am.ld},
-                                MatRef{Bhi, bh.rows, bh.ld}, MatRef{three ? Blo : nullptr, bl.rows, bl.ld}));
+    SPH_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, md, static_cast<const GemmWork*>(tl.d.p),
+                                static_cast<int>(tl.n), D,
+                                g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0));
     count_launch();
     if (trace) {
         std::vector<long long> h(4 * 512 + 4096);
@@ -690,7 +839,9 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
     const bool three = prec == SPH_PREC_3XTF32;
     require(!three || Blo, "gemm: 3xTF32 needs the lo table");
     const int cl = g.cluster;
-    if (g.bn == 192 && cl == 1)
+    if (g.bn == 192 && g.pair)
+        tc::launch<192, 4, 2, true, true>(g, A, Bhi, Blo, D, three, st);
+    else if (g.bn == 192 && cl == 1)
         tc::launch<192, 3, 1, true>(g, A, Bhi, Blo, D, three, st);
     else if (g.bn == 192 && cl == 2)
         tc::launch<192, 3, 2, true>(g, A, Bhi, Blo, D, three, st);
@@ -726,16 +877,30 @@ static void build_tiles(const GroupedGemm& g, int cl, GemmTileList& out) {
         gorder.push_back(gi);
     }
     std::stable_sort(gorder.begin(), gorder.end(), [&](size_t a, size_t b) { return gcost[a] > gcost[b]; });
-    std::vector<GemmTile> ts;
+    std::vector<GemmWork> ts;
     for (size_t gi : gorder) {
         const GemmGroup& gr = g.groups[gi];
         for (int m0 = 0; m0 < gr.M; m0 += tc::BM * cl)
-            for (int n0 = 0; n0 < gr.N; n0 += g.bn) ts.push_back({static_cast<int32_t>(gi), m0, n0, 0});
+            for (int n0 = 0; n0 < gr.N; n0 += g.bn) {
+                GemmWork w{};
+                w.a_row = gr.a_row0 + m0;
+                w.b_row = gr.b_row0 + n0;
+                w.M = gr.M;
+                w.m0 = m0;
+                w.n0 = n0;
+                w.nrem = std::min(g.bn, gr.N - n0);
+                w.K = gr.K;
+                w.ldd = gr.ldd;
+                w.ncols = std::max(w.nrem, std::min(gr.zero_to, n0 + g.bn) - n0);
+                w.dg = g.tma_store ? static_cast<int32_t>(gr.d_off / (g.d_rows * g.d_ldd)) : 0;
+                w.d_off = gr.d_off;
+                ts.push_back(w);
+            }
     }
     out.n = static_cast<int64_t>(ts.size());
     out.d.alloc(std::max<size_t>(ts.size(), 1), false);
     if (!ts.empty())
-        SPH_CUDA(cudaMemcpy(out.d.p, ts.data(), ts.size() * sizeof(GemmTile), cudaMemcpyHostToDevice));
+        SPH_CUDA(cudaMemcpy(out.d.p, ts.data(), ts.size() * sizeof(GemmWork), cudaMemcpyHostToDevice));
 }
 
 const GemmTileList& GroupedGemm::tiles_for(int cl) const {
@@ -768,6 +933,25 @@ void GroupedGemm::finalize() {
         if (v == 1 || v == 2 || v == 4) cluster = v;
     }
     if (bn == 128 && cluster > 2) cluster = 2;
+    // CTA-pair MMA for the BN = 192 (ALO) GEMMs when there are >= 2 M-tiles per group
+    pair = bn == 192 && mtiles >= 2;
+    if (const char* e = std::getenv("SPH_GEMM_PAIR")) pair = pair && std::atoi(e) != 0;
+    // TMA-store epilogue when D is a uniform [group][rows][ldd] array (the Legendre GEMMs)
+    tma_store = bn == 192 && !groups.empty();
+    d_rows = 0;
+    d_ldd = 0;
+    int64_t gmax = 0;
+    for (const GemmGroup& gr : groups) {
+        if (gr.M <= 0 || gr.N <= 0 || gr.K <= 0) continue;
+        const int64_t rows = store == STORE_ROW ? gr.M : gr.N;
+        if (d_rows == 0) { d_rows = rows; d_ldd = gr.ldd; }
+        if (rows != d_rows || gr.ldd != d_ldd || gr.d_off % (rows * gr.ldd) != 0) tma_store = false;
+        if (d_rows > 0) gmax = std::max<int64_t>(gmax, gr.d_off / (d_rows * d_ldd));
+    }
+    if (d_rows == 0 || d_ldd * 4 % 16 != 0) tma_store = false;
+    d_groups3 = gmax + 1;
+    if (const char* e = std::getenv("SPH_GEMM_TMA_STORE")) tma_store = tma_store && std::atoi(e) != 0;
+    tile_lists.clear();
     ntiles = tiles_for(1).n;
     build_simt_tiles(*this);
 }
