@@ -8,6 +8,7 @@
 //               (fft4.cuh), 256 threads, 256/N1 complex rings per CTA
 //   * stockham  other 2/3/5-smooth n: ping-pong shared-memory radix passes
 //   * direct    anything else: O(n^2) DFT on a global scratch buffer
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <set>
@@ -164,24 +165,46 @@ __device__ __forceinline__ float2* stockham(float2* a, float2* b, int nrings, co
 
 // forward SHT: ring pairs (ia, ib) of field f, folded rows r0.. -> E/O operand.
 // P / n may be std::integral_constant (four-step path) so the index math folds.
+// E/O layout (the forward Legendre GEMM's A operand), k-quad interleaved:
+//   eo[((g * Rq + r / 4) * 2F + row) * 4 + r % 4],  g = 2 m + parity, row = 2 f + re/im,
+//   Rq = Rp / 4 (ring pairs r in [R, Rp) hold zeros)
+// i.e. per (g, quad) a [2F][4] block: a CTA of 4 ring pairs x FB fields writes FB*32-byte
+// runs, and the GEMM loads [8 quads][128 rows][4] boxes (the SWIZZLE_NONE K-major
+// core-matrix layout) with a 4D TMA map.  (The former [g][2F][Rp] layout gave 32-byte
+// runs per CTA and a store phase of 1.56 of 2.86 ms at cfg2, SPH_FFT_DEBUG.)
 struct FoldIO {
+    int dbg;  // diagnostic (SPH_FFT_DEBUG): 1 skip store, 2 skip phase B + store, 4 loads only
     const float* x;
     const int2* rows;
     int R, nlat, mmax;
     float* eo;
-    int64_t ld_eo, twoF;
+    int64_t Rq, twoF;
+    // slot p of a CTA -> (ring pair, field); false if outside [0, R) x [0, F).
+    // P % 4 == 0 (all fast paths): 4 ring pairs x P/4 fields per CTA; otherwise P ring
+    // pairs of one field (small fallback transforms)
+    template <class PT>
+    __device__ __forceinline__ bool slot(PT P, int p, int& r, int& f) const {
+        const int np = static_cast<int>(P);
+        if (np % 4 == 0) {
+            r = 4 * blockIdx.x + (p & 3);
+            f = (np / 4) * blockIdx.y + (p >> 2);
+        } else {
+            r = np * blockIdx.x + p;
+            f = blockIdx.y;
+        }
+        return r < R && f < twoF / 2;
+    }
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
-        const int r0 = blockIdx.x * P, f = blockIdx.y;
-        const int nr = min(static_cast<int>(P), R - r0);
-        const float* xf = x + static_cast<int64_t>(f) * nlat * n;
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
         if ((n & 3) == 0) {
             const int n4 = n / 4;
             for (int j = warp; j < P; j += nw) {  // one ring pair per warp
                 float4* d = reinterpret_cast<float4*>(buf + j * ld);
-                if (j < nr) {
-                    const int2 rw = rows[r0 + j];
+                int rr, f;
+                if (slot(P, j, rr, f)) {
+                    const float* xf = x + static_cast<int64_t>(f) * nlat * n;
+                    const int2 rw = rows[rr];
                     const float4* pa = reinterpret_cast<const float4*>(xf + static_cast<int64_t>(rw.x) * n);
                     const float4* pb = reinterpret_cast<const float4*>(xf + static_cast<int64_t>(rw.y < 0 ? rw.x : rw.y) * n);
                     const bool hb = rw.y >= 0;
@@ -201,8 +224,10 @@ struct FoldIO {
             }
         } else {
             for (int j = warp; j < P; j += nw) {
-                const bool ok = j < nr;
-                const int2 rw = ok ? rows[r0 + j] : make_int2(0, -1);
+                int rr, f;
+                const bool ok = slot(P, j, rr, f);
+                const int2 rw = ok ? rows[rr] : make_int2(0, -1);
+                const float* xf = x + static_cast<int64_t>(ok ? f : 0) * nlat * n;
                 for (int k = lane; k < n; k += 32) {
                     float2 v = make_float2(0.f, 0.f);
                     if (ok) {
@@ -214,71 +239,54 @@ struct FoldIO {
             }
         }
     }
-    // one (m, quad of 4 rings) per thread: all four outputs (E re/im, O re/im) of the
-    // four rings as float4 stores (P % 4 == 0, r0 % 4 == 0, ld_eo % 4 == 0); a partial
-    // tail quad falls back to scalar stores
+    // store: thread (m, row rr of the 2*FB rows [f re, f im, ...]) writes the E and O
+    // float4 of the CTA's 4 ring pairs; the 2*FB lanes of one m cover a contiguous
+    // FB*32-byte run of the quad-interleaved layout
     template <class PT, class NT>
     __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
-        const int r0 = blockIdx.x * P, f = blockIdx.y;
-        const int nr = min(static_cast<int>(P), R - r0);
-        const int64_t so = twoF * ld_eo;      // E -> O row offset
-        const int64_t sm = 2 * so;            // m -> m+1
-        float* e0 = eo + (2 * static_cast<int64_t>(f)) * ld_eo + r0;
-        if (P % 4 == 0 && (ld_eo & 3) == 0) {
-            const int nq = P / 4;
-            const int jq = threadIdx.x % nq;
-            const int mstep = blockDim.x / nq;
-            const int j0 = 4 * jq;
-            if (j0 >= nr) return;
-            float* e = e0 + j0;
-            for (int m = threadIdx.x / nq; m < mmax; m += mstep) {
-                float er[4], ei[4], orr[4], oi[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float2* zr = buf + (j0 + t) * ld;
-                    const float2 z = zr[m];
-                    const float2 zc = zr[m == 0 ? 0 : n - m];
-                    const float ar = 0.5f * (z.x + zc.x), ai = 0.5f * (z.y - zc.y);
-                    const float br = 0.5f * (z.y + zc.y), bi = -0.5f * (z.x - zc.x);
-                    er[t] = ar + br;
-                    ei[t] = ai + bi;
-                    orr[t] = ar - br;
-                    oi[t] = ai - bi;
-                }
-                float* em = e + m * sm;
-                if (j0 + 4 <= nr) {
-                    *reinterpret_cast<float4*>(em) = make_float4(er[0], er[1], er[2], er[3]);
-                    *reinterpret_cast<float4*>(em + ld_eo) = make_float4(ei[0], ei[1], ei[2], ei[3]);
-                    *reinterpret_cast<float4*>(em + so) = make_float4(orr[0], orr[1], orr[2], orr[3]);
-                    *reinterpret_cast<float4*>(em + so + ld_eo) = make_float4(oi[0], oi[1], oi[2], oi[3]);
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        if (j0 + t < nr) {
-                            em[t] = er[t];
-                            em[ld_eo + t] = ei[t];
-                            em[so + t] = orr[t];
-                            em[so + ld_eo + t] = oi[t];
-                        }
-                }
+        const int64_t gstride = Rq * twoF * 4;  // floats per (m, parity) group
+        if (static_cast<int>(P) % 4 != 0) {     // fallback: scalar stores, slot j -> pair
+            const int np = static_cast<int>(P);
+            for (int i = threadIdx.x; i < np * mmax; i += blockDim.x) {
+                const int j = i % np, m = i / np;
+                int r, f;
+                if (!slot(P, j, r, f)) continue;
+                const float2* zr = buf + j * ld;
+                const float2 z = zr[m];
+                const float2 zc = zr[m == 0 ? 0 : static_cast<int>(n) - m];
+                const float ar = 0.5f * (z.x + zc.x), ai = 0.5f * (z.y - zc.y);
+                const float br = 0.5f * (z.y + zc.y), bi = -0.5f * (z.x - zc.x);
+                float* em = eo + (2 * static_cast<int64_t>(m)) * gstride +
+                            ((static_cast<int64_t>(r / 4)) * twoF + 2 * f) * 4 + (r & 3);
+                em[0] = ar + br;
+                em[4] = ai + bi;
+                em[gstride] = ar - br;
+                em[gstride + 4] = ai - bi;
             }
             return;
         }
-        const int j = threadIdx.x % P;
-        const int mstep = blockDim.x / P;
-        if (j >= nr) return;
-        const float2* zr = buf + j * ld;
-        float* e = e0 + j;
-        for (int m = threadIdx.x / P; m < mmax; m += mstep) {
-            const float2 z = zr[m];
-            const float2 zc = zr[m == 0 ? 0 : n - m];
-            const float ar = 0.5f * (z.x + zc.x), ai = 0.5f * (z.y - zc.y);
-            const float br = 0.5f * (z.y + zc.y), bi = -0.5f * (z.x - zc.x);
-            float* em = e + m * sm;
-            em[0] = ar + br;
-            em[ld_eo] = ai + bi;
-            em[so] = ar - br;
-            em[so + ld_eo] = ai - bi;
+        const int FB = static_cast<int>(P) / 4, NR = 2 * FB;
+        const int rr = threadIdx.x % NR;
+        const int mstep = blockDim.x / NR;
+        const int fl = rr >> 1, ri = rr & 1;
+        const int64_t row = 2 * static_cast<int64_t>(FB * blockIdx.y + fl) + ri;
+        if (row >= twoF) return;
+        float* base = eo + (static_cast<int64_t>(blockIdx.x) * twoF + row) * 4;
+        for (int m = threadIdx.x / NR; m < mmax; m += mstep) {
+            float e[4], o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2* zr = buf + (4 * fl + j) * ld;
+                const float2 z = zr[m];
+                const float2 zc = zr[m == 0 ? 0 : static_cast<int>(n) - m];
+                const float ar = 0.5f * (z.x + zc.x), ai = 0.5f * (z.y - zc.y);
+                const float br = 0.5f * (z.y + zc.y), bi = -0.5f * (z.x - zc.x);
+                e[j] = ri ? ai + bi : ar + br;
+                o[j] = ri ? ai - bi : ar - br;
+            }
+            float* em = base + (2 * static_cast<int64_t>(m)) * gstride;
+            *reinterpret_cast<float4*>(em) = make_float4(e[0], e[1], e[2], e[3]);
+            *reinterpret_cast<float4*>(em + gstride) = make_float4(o[0], o[1], o[2], o[3]);
         }
     }
 };
@@ -493,14 +501,13 @@ template <int N1>
 __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_fold_kernel(FoldIO io, const float2* __restrict__ twT) {
     extern __shared__ float2 smf[];
     constexpr int N2 = 45, N = N1 * N2, P = fft4::THREADS / N1, LD = N + 2;
-    const int r0 = blockIdx.x * P, f = blockIdx.y;
-    const int nr = min(P, io.R - r0);
-    const float* xf = io.x + static_cast<int64_t>(f) * io.nlat * N;
     for (int it = threadIdx.x; it < P * N2; it += fft4::THREADS) {
         const int p = it / N2, n2 = it - p * N2;
         float2 a[N1];
-        if (p < nr) {
-            const int2 rw = io.rows[r0 + p];
+        int rr, f;
+        if (io.slot(std::integral_constant<int, P>{}, p, rr, f)) {
+            const float* xf = io.x + static_cast<int64_t>(f) * io.nlat * N;
+            const int2 rw = io.rows[rr];
             const float* pa = xf + static_cast<int64_t>(rw.x) * N + n2;
             const float* pb = xf + static_cast<int64_t>(rw.y < 0 ? rw.x : rw.y) * N + n2;
             const float sb = rw.y < 0 ? 0.f : 1.f;
@@ -510,9 +517,16 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_fold_kernel(FoldIO io, 
 #pragma unroll
             for (int n1 = 0; n1 < N1; ++n1) a[n1] = make_float2(0.f, 0.f);
         }
-        fft4::phase_a_store<N1, N2, LD, false>(a, smf, p, n2, twT);
+        if (io.dbg & 4) {
+            float2* r = smf + p * LD + n2;
+#pragma unroll
+            for (int k1 = 0; k1 < N1; ++k1) r[N2 * k1] = a[k1];
+        } else {
+            fft4::phase_a_store<N1, N2, LD, false>(a, smf, p, n2, twT);
+        }
     }
     __syncthreads();
+    if (io.dbg & 6) return;
     float2 b[N2];
     fft4::phase_b_regs<N1, N2, LD, false>(smf, b);
     __syncthreads();
@@ -523,6 +537,7 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_fold_kernel(FoldIO io, 
         for (int k2 = 0; k2 < N2; ++k2) dst[N1 * k2] = b[k2];
     }
     __syncthreads();
+    if (io.dbg & 1) return;
     io.store(smf, std::integral_constant<int, P>{}, std::integral_constant<int, N>{}, LD);
 }
 
@@ -722,8 +737,18 @@ void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int
     if (F == 0) return;
     require(F <= 65535, "fft: at most 65535 fields per call");
     const int P = rpb_of(fp);
-    FoldIO io{x, fr.d_rows.p, fr.R, nlat, mmax, eo, ld_eo, 2 * F};
-    dim3 grid((fr.R + P - 1) / P, static_cast<unsigned>(F));
+    static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
+    require(ld_eo % 4 == 0, "fft: E/O ring-pair padding must be a multiple of 4");
+    FoldIO io{fft_dbg, x, fr.d_rows.p, fr.R, nlat, mmax, eo, ld_eo / 4, 2 * F};
+    dim3 grid;
+    if (P % 4 == 0) {
+        const int64_t FB = P / 4;
+        grid = dim3((fr.R + 3) / 4, static_cast<unsigned>((F + FB - 1) / FB));
+    } else {  // fallback transforms write pairs < R only: zero the [R, Rp) padding first
+        grid = dim3((fr.R + P - 1) / P, static_cast<unsigned>(F));
+        if (fr.R % 4 != 0)
+            SPH_CUDA(cudaMemsetAsync(eo, 0, sizeof(float) * 2 * F * ld_eo * 2 * mmax, st));
+    }
     const double bytes = 4.0 * F * (static_cast<double>(nlat) * fp.n + 4.0 * mmax * fr.R);
     if (fp.fft4_n1) {
         ProfScope prof("fft_fwd_fold", st, bytes);

@@ -41,6 +41,8 @@ struct GemmWork {
     int32_t ldd;
     int32_t ncols;    // STORE_ROW columns written incl. the zero fill up to zero_to
     int32_t dg;       // group index in the 3D [group][rows][ldd] view of D (TMA store)
+    int32_t ag;       // group index in the 4D quad-interleaved view of A (a_quad)
+    int32_t pad;
     int64_t d_off;    // element offset of D(0,0) of the group
 };
 
@@ -72,6 +74,11 @@ struct GroupedGemm {
     // TMA-store epilogue (ALO kernel): D is a uniform 3D [d_groups3][d_rows][ldd] view
     // (every group has the same ldd and row count, d_off a multiple of d_rows * ldd)
     bool tma_store = false;
+    // a_quad: A is k-quad interleaved per group, element (group g, row, k) at
+    // ((g * a_kq + k / 4) * a_rows_g + row) * 4 + k % 4 (the forward SHT's E/O layout,
+    // fft.cu FoldIO); a_row0 of every group is g * a_rows_g.  Only with bn = 192 (ALO).
+    bool a_quad = false;
+    int64_t a_rows_g = 0, a_groups = 0, a_kq = 0;
     int64_t d_rows = 0, d_groups3 = 0, d_ldd = 0;
     DevBuf<GemmGroup> d_groups;
     int64_t ntiles = 0;            // tiles at cluster size 1 (0 -> nothing to do)

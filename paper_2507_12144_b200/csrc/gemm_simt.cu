@@ -13,7 +13,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
                                                         const float* __restrict__ Blo, int64_t ldb,
                                                         const GemmGroup* __restrict__ groups,
                                                         const GemmTile* __restrict__ tiles,
-                                                        float* __restrict__ D, int store) {
+                                                        float* __restrict__ D, int store,
+                                                        int64_t a_rows_g, int64_t a_kq) {
     __shared__ float As[TK][TM + 4];
     __shared__ float Bs[TK][TN + 4];
     const GemmTile tl = tiles[blockIdx.x];
@@ -27,7 +28,15 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
         for (int i = threadIdx.x; i < TM * TK; i += 256) {
             const int r = i / TK, kk = i % TK;
             const bool ok = (tl.m0 + r < g.M) && (k0 + kk < g.K);
-            As[kk][r] = ok ? Ag[static_cast<int64_t>(r) * lda + k0 + kk] : 0.f;
+            float v = 0.f;
+            if (ok && a_rows_g > 0) {  // quad-interleaved A (GroupedGemm::a_quad)
+                const int64_t grow = g.a_row0 + tl.m0 + r, gi = grow / a_rows_g, row = grow - gi * a_rows_g;
+                const int k = k0 + kk;
+                v = A[((gi * a_kq + k / 4) * a_rows_g + row) * 4 + (k & 3)];
+            } else if (ok) {
+                v = Ag[static_cast<int64_t>(r) * lda + k0 + kk];
+            }
+            As[kk][r] = v;
         }
         for (int i = threadIdx.x; i < TN * TK; i += 256) {
             const int r = i / TK, kk = i % TK;
@@ -93,7 +102,8 @@ void gemm_run_simt(const GroupedGemm& g, const float* A, const float* Bhi, const
     if (g.ntiles_simt == 0) return;
     ProfScope prof("gemm_simt", st, g.flops);
     gemm_simt_kernel<<<static_cast<unsigned>(g.ntiles_simt), 256, 0, st>>>(
-        A, g.A.ld, Bhi, Blo, g.Bhi.ld, g.d_groups.p, g.d_tiles_simt.p, D, g.store);
+        A, g.A.ld, Bhi, Blo, g.Bhi.ld, g.d_groups.p, g.d_tiles_simt.p, D, g.store,
+        g.a_quad ? g.a_rows_g : 0, g.a_kq);
     SPH_LAUNCH_CHECK();
     count_launch();
 }

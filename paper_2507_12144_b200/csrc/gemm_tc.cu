@@ -134,6 +134,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
 // TMA tensor store of a [1][32][32] box from SMEM (bulk async-group of this thread)
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
@@ -244,6 +252,17 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
     d |= static_cast<uint64_t>(KB == 32 ? 2 : 4) << 61;           // SWIZZLE_128B / _64B
     return d;
 }
+// UMMA descriptor for the quad-interleaved A tile (SWIZZLE_NONE K-major): core matrix =
+// 8 rows x 16 B contiguous, 8-row groups 128 B apart (SBO), k-quads 128 rows x 16 B =
+// 2 KB apart (LBO); the TMA box [8 quads][128 rows][4] lands exactly in this layout.
+__device__ __forceinline__ uint64_t make_sdesc_quad(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(2048 >> 4) << 16;  // LBO: next k-quad
+    d |= static_cast<uint64_t>(128 >> 4) << 32;   // SBO: next 8-row group
+    d |= static_cast<uint64_t>(1) << 46;
+    return d;                                     // layout type 0 = SWIZZLE_NONE
+}
 // Instruction descriptor: kind::tf32, D f32, A/B tf32, both K-major, M = 128, N = n.
 __device__ __forceinline__ uint32_t make_idesc(int n, int m = BM) {  // m = 256: CTA pair
     uint32_t d = 0;
@@ -303,7 +322,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const GemmWork* __restrict__ works,
                    int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
-                   int tma_store) {
+                   int tma_store, int a_quad) {  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B
     // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
     // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads
     // (a whole-tile cp.async.bulk.prefetch.L2 one tile ahead was measured slower: cfg2
@@ -383,6 +402,17 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     constexpr int B_ROWS = PAIR ? BN / 2 : BN / CL;  // table rows loaded by this CTA
     // PAIR: instruction N = N rounded up to 32; the peer's half starts at ninst / 2
     auto pair_half = [](const GemmWork& w) { return (w.nrem + 31) / 32 * 16; };
+    auto load_a = [&](int s, const GemmWork& w, int kb) {
+        if (ALO && a_quad == 2)  // wide map: 32-row blocks of 512 B
+            tma_load_4d(a_hi(s), &map_a, 0, (w.m0 + crank * BM) / 32, kb * (KB / 4), w.ag, full_bar(s));
+        else if (ALO && a_quad)
+            tma_load_4d(a_hi(s), &map_a, 0, w.m0 + crank * BM, kb * (KB / 4), w.ag, full_bar(s));
+        else
+            tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
+    };
+    auto adesc = [&](int s, int kk) {  // A operand of k-step kk (8 fp32 of K)
+        return (ALO && a_quad) ? make_sdesc_quad(a_hi(s) + kk * 2 * 2048) : make_sdesc<KB>(a_hi(s) + kk * 32);
+    };
     // each role walks tiles cid, cid + ncl, ... and loads the next descriptor one tile ahead
     GemmWork wnext{};
     if (cid < ntiles) wnext = works[cid];
@@ -406,7 +436,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     if (tr && j < TR_N) trace[j] = clock64();
                     if (dbg & 8) {
                         mbar_expect_tx(full_bar(s), A_TILE_BYTES);
-                        tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
+                        load_a(s, w, kb);
                         if (++s == STAGES) { s = 0; ph ^= 1; }
                         continue;
                     }
@@ -414,7 +444,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                         // leader's full barrier: own A + both CTAs' table halves; peer's: A
                         const int nb = (three_pass ? 2 : 1) * L::B_TILE_BYTES;
                         mbar_expect_tx(full_bar(s), A_TILE_BYTES + (crank == 0 ? 2 * nb : 0));
-                        tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
+                        load_a(s, w, kb);
                         const int brow = w.b_row + crank * pair_half(w);
                         tma_load_2d_pair(b_hi(s), &map_bhi, kb * KB, brow, full_bar(s));
                         if (three_pass) tma_load_2d_pair(b_lo(s), &map_blo, kb * KB, brow, full_bar(s));
@@ -422,7 +452,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                         continue;
                     }
                     mbar_expect_tx(full_bar(s), A_TILE_BYTES + (three_pass ? 2 : 1) * L::B_TILE_BYTES);
-                    tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
+                    load_a(s, w, kb);
                     if (CL == 1) {
                         tma_load_2d(b_hi(s), &map_bhi, kb * KB, w.b_row, full_bar(s));
                         if (three_pass)
@@ -466,7 +496,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     if (tr && j < TR_N) trace[3 * TR_N + j] = clock64();
                     const int ksteps = (dbg & 4) ? 0 : min(KB / 8, (w.K - kb * KB + 7) / 8);
                     for (int kk = 0; kk < ksteps; ++kk) {
-                        const uint64_t ahi = make_sdesc<KB>(a_hi(s) + kk * 32);
+                        const uint64_t ahi = adesc(s, kk);
                         const uint64_t bhi = make_sdesc<KB>(b_hi(s) + kk * 32);
                         if constexpr (PAIR) {
                             tc_mma_tf32_pair(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
@@ -520,12 +550,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                         const int row = 32 * q + lane;
                         const float4* rowp =
                             reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase) + row * KB * 4);
+                        const float4* quadp = reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase)) + row;
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             float lo[16];
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                const float4 v = rowp[(4 * h + c) ^ (row & 7)];
+                                // quad layout: k-quad (4h + c) of the row at quad * 2 KB + row * 16 B
+                                const float4 v = a_quad ? quadp[(4 * h + c) * BM] : rowp[(4 * h + c) ^ (row & 7)];
                                 const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                                 for (int e = 0; e < 4; ++e)
@@ -752,7 +784,30 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     });
     Mat2D am = g.A;
     am.p = A;
-    const CUtensorMap ma = make_map(am, BM, bk_of<ALO>());
+    CUtensorMap ma;
+    const bool quad = ALO && g.a_quad;
+    if (quad) {
+        std::memset(&ma, 0, sizeof(ma));
+        require((reinterpret_cast<uintptr_t>(A) & 15) == 0, "gemm: operand must be 16B aligned");
+        // rows % 32 == 0: dims {32 rows x 4 (512 B contiguous), row blocks, quads, groups},
+        // box {128, 4, 8, 1} -> 512-byte TMA requests; otherwise {4, rows, quads, groups}
+        // with 16-byte requests (measured 3.1 vs 2.4 ms on the cfg2 forward GEMM)
+        const bool wide = g.a_rows_g % 32 == 0;
+        cuuint64_t dims[4] = {wide ? 128u : 4u,
+                              static_cast<cuuint64_t>(wide ? g.a_rows_g / 32 : g.a_rows_g),
+                              static_cast<cuuint64_t>(g.a_kq), static_cast<cuuint64_t>(g.a_groups)};
+        cuuint64_t strides[3] = {static_cast<cuuint64_t>(wide ? 512 : 16), static_cast<cuuint64_t>(g.a_rows_g * 16),
+                                 static_cast<cuuint64_t>(g.a_kq * g.a_rows_g * 16)};
+        cuuint32_t box[4] = {wide ? 128u : 4u, wide ? BM / 32u : static_cast<cuuint32_t>(BM),
+                             static_cast<cuuint32_t>(bk_of<ALO>() / 4), 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = encode_fn()(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(A), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(SPH_ERR_CUDA, "cuTensorMapEncodeTiled (A quad) failed: " + std::to_string(r));
+    } else {
+        ma = make_map(am, BM, bk_of<ALO>());
+    }
     Mat2D bh = g.Bhi, bl = g.Blo;
     bh.p = Bhi;
     bl.p = Blo;
@@ -800,7 +855,8 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     }
     SPH_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, md, static_cast<const GemmWork*>(tl.d.p),
                                 static_cast<int>(tl.n), D,
-                                g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0));
+                                g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0,
+                                quad ? (g.a_rows_g % 32 == 0 ? 2 : 1) : 0));
     count_launch();
     if (trace) {
         std::vector<long long> h(4 * 512 + 4096);
@@ -893,6 +949,7 @@ static void build_tiles(const GroupedGemm& g, int cl, GemmTileList& out) {
                 w.ldd = gr.ldd;
                 w.ncols = std::max(w.nrem, std::min(gr.zero_to, n0 + g.bn) - n0);
                 w.dg = g.tma_store ? static_cast<int32_t>(gr.d_off / (g.d_rows * g.d_ldd)) : 0;
+                w.ag = g.a_quad ? static_cast<int32_t>(gr.a_row0 / g.a_rows_g) : 0;
                 w.d_off = gr.d_off;
                 ts.push_back(w);
             }
@@ -933,6 +990,7 @@ void GroupedGemm::finalize() {
         if (v == 1 || v == 2 || v == 4) cluster = v;
     }
     if (bn == 128 && cluster > 2) cluster = 2;
+    require(!a_quad || (bn == 192 && a_rows_g > 0 && a_kq > 0), "gemm: quad A layout needs the bn=192 kernel");
     // CTA-pair MMA for the BN = 192 (ALO) GEMMs when there are >= 2 M-tiles per group
     pair = bn == 192 && mtiles >= 2;
     if (const char* e = std::getenv("SPH_GEMM_PAIR")) pair = pair && std::atoi(e) != 0;

@@ -156,16 +156,21 @@ __global__ void dense_to_cint_kernel(const float2* __restrict__ dense, int64_t F
     cint[i] = v;
 }
 
-// bins [F][nlat][mcount] complex (scaled by 2pi/nlon) -> EO_loc [mcount][2][2F][Rp]
+// bins [F][nlat][mcount] complex (scaled by 2pi/nlon) -> EO_loc [mcount][2][Rp/4][2F][4]
 __global__ void fold_bins_kernel(const float2* __restrict__ bins, const int2* __restrict__ rows,
                                  int R, int Rp, int64_t F, int64_t nlat, int64_t mcount,
                                  float unscale, float* __restrict__ eo) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t twoF = 2 * F;
-    if (i >= mcount * 2 * twoF * R) return;
-    const int r = static_cast<int>(i % R);
-    const int64_t n = (i / R) % twoF;
-    const int64_t g = i / (static_cast<int64_t>(R) * twoF);
+    if (i >= mcount * 2 * twoF * Rp) return;
+    const int r = static_cast<int>(i % Rp);
+    const int64_t n = (i / Rp) % twoF;
+    const int64_t g = i / (static_cast<int64_t>(Rp) * twoF);
+    float* dst = eo + ((g * (Rp / 4) + r / 4) * twoF + n) * 4 + (r & 3);  // quad-interleaved
+    if (r >= R) {
+        *dst = 0.f;
+        return;
+    }
     const int64_t ml = g >> 1;
     const int p = static_cast<int>(g & 1);
     const int64_t f = n >> 1;
@@ -173,7 +178,7 @@ __global__ void fold_bins_kernel(const float2* __restrict__ bins, const int2* __
     const float2 a = bins[(f * nlat + rw.x) * mcount + ml];
     const float2 b = rw.y >= 0 ? bins[(f * nlat + rw.y) * mcount + ml] : make_float2(0.f, 0.f);
     const float va = (n & 1) ? a.y : a.x, vb = (n & 1) ? b.y : b.x;
-    eo[(g * twoF + n) * Rp + r] = (p == 0 ? va + vb : va - vb) * unscale;
+    *dst = (p == 0 ? va + vb : va - vb) * unscale;
 }
 
 }  // namespace
@@ -285,6 +290,10 @@ const GroupedGemm& ShtPlan::fwd_gemm(int64_t F) {
     if (!slot) {
         auto g = std::make_unique<GroupedGemm>();
         g->A = {nullptr, mmax * 2 * 2 * F, R, Rp};
+        g->a_quad = true;  // E/O from fft_forward_fold: [g][Rp/4][2F][4]
+        g->a_rows_g = 2 * F;
+        g->a_groups = mmax * 2;
+        g->a_kq = Rp / 4;
         g->Bhi = {pf_hi.p, pf_rows, R, Rp};
         g->Blo = {pf_lo.p, pf_rows, R, Rp};
         g->store = STORE_ROW;
@@ -351,6 +360,10 @@ const GroupedGemm& ShtPlan::stage_gemm(int64_t F, int64_t m0, int64_t mcount) {
     if (!slot) {
         auto g = std::make_unique<GroupedGemm>();
         g->A = {nullptr, mcount * 2 * 2 * F, R, Rp};
+        g->a_quad = true;  // E/O from fold_bins_kernel: [g][Rp/4][2F][4]
+        g->a_rows_g = 2 * F;
+        g->a_groups = mcount * 2;
+        g->a_kq = Rp / 4;
         g->Bhi = {pf_hi.p, pf_rows, R, Rp};
         g->Blo = {pf_lo.p, pf_rows, R, Rp};
         g->store = STORE_ROW;
@@ -438,7 +451,7 @@ void ShtPlan::legendre_stage(const float* bins, int64_t F, int64_t m0, int64_t m
     uint8_t* w8 = static_cast<uint8_t*>(workspace(ws, stage_ws_bytes(F, mcount)));
     float* eo = reinterpret_cast<float*>(w8);
     float* cl = reinterpret_cast<float*>(w8 + round_up(4 * mcount * 2 * 2 * F * Rp, 256));
-    const int64_t n = mcount * 2 * 2 * F * R;
+    const int64_t n = mcount * 2 * 2 * F * Rp;
     const double pi = 3.14159265358979323846;
     fold_bins_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const float2*>(bins), fold.d_rows.p, R, Rp, F, nlat, mcount,
