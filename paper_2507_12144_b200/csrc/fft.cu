@@ -292,14 +292,20 @@ struct FoldIO {
 };
 
 // inverse SHT: Ev/Od -> Hermitian spectra of the ring pair -> rings.  Input layout
-// EOi[m][parity][R][2F] (the inverse GEMM's transposed store), so a CTA takes one folded
-// row r and P consecutive fields: per order m it reads 2 x P float2 (64-byte runs).
+// EOi[r][t][g][32] (t = 32-row field tile, g = 2 m + parity, rows 2f + re/im), written by
+// the inverse GEMM's TMA-store epilogue (GroupedGemm::d_mode 1) in 128-byte pieces, so
+// a CTA of one folded row r and P = 8 fields reads 64-byte halves of one contiguous
+// chunk (the neighbouring CTA reads the other halves).  (The former [m][parity][R][2F]
+// layout gave 64-byte runs ~6 MB apart: the load phase alone took 1.56 of 2.4 ms at
+// cfg2, SPH_FFT_DEBUG.)
 struct UnfoldIO {
+    int dbg;  // diagnostic (SPH_FFT_DEBUG, bits << 4): 16 skip stores, 32 loads only
     const float* eoi;
     const int2* rows;
     int R, nlat, msynth, lmax;
     int64_t F, twoF;
     float* y;
+    int64_t T;  // 32-row field tiles
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int r = blockIdx.y;  // field tiles fastest: neighbouring CTAs read adjacent runs
@@ -318,12 +324,14 @@ struct UnfoldIO {
             return;
         }
         const bool pair = rows[r].y >= 0;
-        const float2* e = reinterpret_cast<const float2*>(eoi + static_cast<int64_t>(r) * twoF + 2 * (f0 + j));
-        const int64_t so = static_cast<int64_t>(R) * F;  // parity stride in float2
-        const int64_t sm = 2 * so;                        // order stride in float2
+        const int64_t row = 2 * (f0 + j);  // re row of field f0 + j
+        const float2* e = reinterpret_cast<const float2*>(
+            eoi + ((static_cast<int64_t>(r) * T + row / 32) * 2 * msynth) * 32 + (row & 31));
+        const int64_t so = 16;  // parity stride in float2 (next g)
+        const int64_t sm = 32;  // order stride in float2 (g += 2)
         // batches of UB orders: all 2*UB loads issued before any use (memory-level
         // parallelism for the latency-bound load phase)
-        constexpr int UB = 8;
+        constexpr int UB = 24;
         for (int mb = m0; mb < msynth; mb += UB * mstep) {
             float2 ev[UB], od[UB];
 #pragma unroll
@@ -550,6 +558,7 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_unfold_kernel(UnfoldIO 
     constexpr int N2 = 45, N = N1 * N2, P = fft4::THREADS / N1, LD = N + 2;
     io.load(smu, std::integral_constant<int, P>{}, std::integral_constant<int, N>{}, LD);
     __syncthreads();
+    if (io.dbg & 32) return;
     for (int it = threadIdx.x; it < P * N2; it += fft4::THREADS) {
         const int p = it / N2, n2 = it - p * N2;
         float2 a[N1];
@@ -563,6 +572,10 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_unfold_kernel(UnfoldIO 
     fft4::phase_b_regs<N1, N2, LD, true>(smu, b);
     const int p = threadIdx.x / N1, k1 = threadIdx.x - p * N1;
     const int64_t f = static_cast<int64_t>(blockIdx.x) * P + p;
+    if (io.dbg & 16) {
+        if (b[0].x == 12345.f) io.y[0] = b[N2 - 1].y;  // keep phase B live
+        return;
+    }
     if (f < io.F) {
         const int2 rw = io.rows[blockIdx.y];
         float* yf = io.y + f * io.nlat * N;
@@ -766,7 +779,8 @@ void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi,
     require(F <= 65535, "fft: at most 65535 fields per call");
     const int P = rpb_of(fp);
     (void)ld_eo;  // EOi is [m][parity][R][2F] (transposed GEMM store)
-    UnfoldIO io{eoi, fr.d_rows.p, fr.R, nlat, msynth, lmax, F, 2 * F, y};
+    static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
+    UnfoldIO io{fft_dbg, eoi, fr.d_rows.p, fr.R, nlat, msynth, lmax, F, 2 * F, y, (2 * F + 31) / 32};
     require(fr.R <= 65535, "fft: too many latitude rows");
     dim3 grid(static_cast<unsigned>((F + P - 1) / P), static_cast<unsigned>(fr.R));
     const double bytes = 4.0 * F * (static_cast<double>(nlat) * fp.n + 4.0 * msynth * fr.R);

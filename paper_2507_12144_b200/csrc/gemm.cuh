@@ -79,6 +79,11 @@ struct GroupedGemm {
     // fft.cu FoldIO); a_row0 of every group is g * a_rows_g.  Only with bn = 192 (ALO).
     bool a_quad = false;
     int64_t a_rows_g = 0, a_groups = 0, a_kq = 0;
+    // d_mode 1 (STORE_TRANS only): D element (group dg, n, m) at
+    // ((n * d_t + m / 32) * d_g2 + dg) * 32 + m % 32, dg = d_off / (N * ldd): the inverse
+    // SHT's field-tile-major EOi, so each unfold CTA reads one contiguous chunk (fft.cu)
+    int d_mode = 0;
+    int64_t d_t = 0, d_g2 = 0;
     int64_t d_rows = 0, d_groups3 = 0, d_ldd = 0;
     DevBuf<GemmGroup> d_groups;
     int64_t ntiles = 0;            // tiles at cluster size 1 (0 -> nothing to do)

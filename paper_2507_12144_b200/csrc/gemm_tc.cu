@@ -142,6 +142,13 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2,
+                                             int c3) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
 // TMA tensor store of a [1][32][32] box from SMEM (bulk async-group of this thread)
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
@@ -322,7 +329,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const GemmWork* __restrict__ works,
                    int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
-                   int tma_store, int a_quad) {  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B
+                   int tma_store, int a_quad,  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B
+                   int d_mode, int d_t, int d_g2) {
     // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
     // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads
     // (a whole-tile cp.async.bulk.prefetch.L2 one tile ahead was measured slower: cfg2
@@ -658,6 +666,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     if (lane == 0) {
                         if (store_mode == STORE_ROW)
                             tma_store_3d(&map_d, smem_u32(ob), w.n0 + c, row0, w.dg);
+                        else if (d_mode == 1)  // box {32 rows, group, row tile, 32 n}
+                            tma_store_4d(&map_d, smem_u32(ob), 0, w.dg, row0 / 32, w.n0 + c);
                         else
                             tma_store_3d(&map_d, smem_u32(ob), row0, w.n0 + c, w.dg);
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -679,7 +689,13 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     __syncwarp();
                 } else {
                     const int m = row0 + lane;
-                    if (m < w.M) {
+                    if (m < w.M && d_mode == 1) {
+                        float* dp = D + ((static_cast<int64_t>(w.n0 + c) * d_t + m / 32) * d_g2 + w.dg) * 32 + (m & 31);
+                        const int64_t nstride = static_cast<int64_t>(d_t) * d_g2 * 32;
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            if (c + jj < nrem) dp[jj * nstride] = __uint_as_float(va[jj]);
+                    } else if (m < w.M) {
                         float* dp = dbase + static_cast<int64_t>(w.n0 + c) * w.ldd + m;
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj)
@@ -816,7 +832,21 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     CUtensorMap md;
     std::memset(&md, 0, sizeof(md));
     const bool tstore = ALO && g.tma_store;
-    if (tstore) {
+    if (tstore && g.d_mode == 1) {
+        // [n][row tile of 32][group][32]: box {32, 1, 1, 32} = 128-byte pieces (16-row tiles
+        // with 64-byte pieces measured 3.5 vs 2.1 ms on the cfg2 inverse GEMM)
+        cuuint64_t dims[4] = {32, static_cast<cuuint64_t>(g.d_g2), static_cast<cuuint64_t>(g.d_t),
+                              static_cast<cuuint64_t>(g.d_rows)};
+        cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(g.d_g2 * 128),
+                                 static_cast<cuuint64_t>(g.d_t * g.d_g2 * 128)};
+        cuuint32_t box[4] = {32, 1, 1, 32};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        require((reinterpret_cast<uintptr_t>(D) & 15) == 0, "gemm: output must be 16B aligned");
+        CUresult r = encode_fn()(&md, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(SPH_ERR_CUDA, "cuTensorMapEncodeTiled (D tiles) failed: " + std::to_string(r));
+    } else if (tstore) {
         cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.d_ldd), static_cast<cuuint64_t>(g.d_rows),
                               static_cast<cuuint64_t>(g.d_groups3)};
         cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.d_ldd * 4),
@@ -856,7 +886,8 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     SPH_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, md, static_cast<const GemmWork*>(tl.d.p),
                                 static_cast<int>(tl.n), D,
                                 g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0,
-                                quad ? (g.a_rows_g % 32 == 0 ? 2 : 1) : 0));
+                                quad ? (g.a_rows_g % 32 == 0 ? 2 : 1) : 0, g.d_mode, static_cast<int>(g.d_t),
+                                static_cast<int>(g.d_g2)));
     count_launch();
     if (trace) {
         std::vector<long long> h(4 * 512 + 4096);
@@ -948,7 +979,7 @@ static void build_tiles(const GroupedGemm& g, int cl, GemmTileList& out) {
                 w.K = gr.K;
                 w.ldd = gr.ldd;
                 w.ncols = std::max(w.nrem, std::min(gr.zero_to, n0 + g.bn) - n0);
-                w.dg = g.tma_store ? static_cast<int32_t>(gr.d_off / (g.d_rows * g.d_ldd)) : 0;
+                w.dg = (g.tma_store || g.d_mode == 1) ? static_cast<int32_t>(gr.d_off / (g.d_rows * g.d_ldd)) : 0;
                 w.ag = g.a_quad ? static_cast<int32_t>(gr.a_row0 / g.a_rows_g) : 0;
                 w.d_off = gr.d_off;
                 ts.push_back(w);
@@ -1006,7 +1037,11 @@ void GroupedGemm::finalize() {
         if (rows != d_rows || gr.ldd != d_ldd || gr.d_off % (rows * gr.ldd) != 0) tma_store = false;
         if (d_rows > 0) gmax = std::max<int64_t>(gmax, gr.d_off / (d_rows * d_ldd));
     }
+    const bool uniform = tma_store;
     if (d_rows == 0 || d_ldd * 4 % 16 != 0) tma_store = false;
+    require(d_mode == 0 || (store == STORE_TRANS && bn == 192 && uniform && d_rows > 0),
+            "gemm: tiled D layout needs uniform transposed groups");
+    if (d_mode == 1 && d_rows > 0) tma_store = true;  // the 4D map has no row-stride constraint
     d_groups3 = gmax + 1;
     if (const char* e = std::getenv("SPH_GEMM_TMA_STORE")) tma_store = tma_store && std::atoi(e) != 0;
     tile_lists.clear();

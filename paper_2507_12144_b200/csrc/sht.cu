@@ -329,7 +329,10 @@ const GroupedGemm& ShtPlan::inv_gemm(int64_t F) {
         g->A = {nullptr, mmax * 2 * 2 * F, Lmax_p, Lp};
         g->Bhi = {pi_hi.p, mmax * 2 * R, Lmax_p, Lp};
         g->Blo = {pi_lo.p, mmax * 2 * R, Lmax_p, Lp};
-        g->store = STORE_TRANS;  // EOi[m][parity][R][2F]: coalesced reads for the iFFT
+        g->store = STORE_TRANS;  // EOi[r][2F/32][m, parity][32] (fft.cu UnfoldIO)
+        g->d_mode = 1;
+        g->d_t = (2 * F + 31) / 32;
+        g->d_g2 = 2 * msynth;
         g->bn = 192;  // TMEM-resident A operand variant
         g->name = "gemm_legendre_inv";
         for (int64_t m = 0; m < msynth; ++m)
