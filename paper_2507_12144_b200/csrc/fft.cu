@@ -331,7 +331,7 @@ struct UnfoldIO {
         const int64_t sm = 32;  // order stride in float2 (g += 2)
         // batches of UB orders: all 2*UB loads issued before any use (memory-level
         // parallelism for the latency-bound load phase)
-        constexpr int UB = 24;
+        constexpr int UB = 8;
         for (int mb = m0; mb < msynth; mb += UB * mstep) {
             float2 ev[UB], od[UB];
 #pragma unroll
@@ -505,11 +505,16 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_kernel(IO io, const flo
 // samples of both rings of the pair straight from HBM into registers (a warp reads 32
 // consecutive samples per load -> 128-byte segments, 2*N1 independent loads in flight
 // per thread), so the input never takes a shared-memory staging pass.
+// FOLD_THREADS = 256 (8 ring slots = 4 ring pairs x 2 fields at N1 = 32, 2 CTAs / SM).
+// Measured at cfg2: 512 threads (16 slots, 128-byte E/O runs, 1 CTA / SM) 2.42 ms vs
+// 2.30 ms -- the store phase (~1.0 ms) is not run-length bound; the load / compute /
+// store phases of a CTA serialise (SPH_FFT_DEBUG: loads 0.69, +A+B 1.27 ms).
+constexpr int FOLD_THREADS = 256;
 template <int N1>
-__global__ void __launch_bounds__(fft4::THREADS, 2) fft4_fold_kernel(FoldIO io, const float2* __restrict__ twT) {
+__global__ void __launch_bounds__(FOLD_THREADS, 2) fft4_fold_kernel(FoldIO io, const float2* __restrict__ twT) {
     extern __shared__ float2 smf[];
-    constexpr int N2 = 45, N = N1 * N2, P = fft4::THREADS / N1, LD = N + 2;
-    for (int it = threadIdx.x; it < P * N2; it += fft4::THREADS) {
+    constexpr int N2 = 45, N = N1 * N2, P = FOLD_THREADS / N1, LD = N + 2;
+    for (int it = threadIdx.x; it < P * N2; it += FOLD_THREADS) {
         const int p = it / N2, n2 = it - p * N2;
         float2 a[N1];
         int rr, f;
@@ -655,8 +660,9 @@ void launch_fused(const FftPlan& fp, const FoldIO& fio, const UnfoldIO& uio, dim
         constexpr int N1 = decltype(n1c)::value;
         const size_t sm = static_cast<size_t>(fft4::THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
         if (FWD) {
-            set_smem_once(fft4_fold_kernel<N1>, sm);
-            fft4_fold_kernel<N1><<<grid, fft4::THREADS, sm, st>>>(fio, fp.twT.p);
+            const size_t smf = static_cast<size_t>(FOLD_THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
+            set_smem_once(fft4_fold_kernel<N1>, smf);
+            fft4_fold_kernel<N1><<<grid, FOLD_THREADS, smf, st>>>(fio, fp.twT.p);
         } else {
             set_smem_once(fft4_unfold_kernel<N1>, sm);
             fft4_unfold_kernel<N1><<<grid, fft4::THREADS, sm, st>>>(uio, fp.twT.p);
@@ -749,7 +755,7 @@ void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int
                       int mmax, float* eo, int64_t ld_eo, cudaStream_t st) {
     if (F == 0) return;
     require(F <= 65535, "fft: at most 65535 fields per call");
-    const int P = rpb_of(fp);
+    const int P = fp.fft4_n1 ? FOLD_THREADS / fp.fft4_n1 : rpb_of(fp);
     static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
     require(ld_eo % 4 == 0, "fft: E/O ring-pair padding must be a multiple of 4");
     FoldIO io{fft_dbg, x, fr.d_rows.p, fr.R, nlat, mmax, eo, ld_eo / 4, 2 * F};
