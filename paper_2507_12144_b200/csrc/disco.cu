@@ -14,6 +14,7 @@
 //    output rings.  Parity is by tolerance (summation order differs).
 //  * SPH_PREC_FP32_SIMT anchor: the reference's own operation order (gather t, then
 //    the channel mix) in fp32 FMA.
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include <thread>
@@ -112,11 +113,13 @@ __global__ void split_rows_kernel(const float* __restrict__ src, int64_t rows, i
     lo[i] = x - h;
 }
 
-// Fourier band contraction + stride fold.  Block = (m'-tile of 4, output row h);
-// threads = (m' in tile) x 64 channel lanes; the CTA loops over the batch.  The
-// psi_hat slice of the block (band rows x folds x 4 orders x K) is staged in shared
-// memory once and read as warp-broadcast float4s; the U loads of a band chunk are
-// issued together.  Output S[((b*Hout + h)*nbo + m')*2 + reim][c*K + k].
+// threads = (m' in tile) x 64 channel lanes; the CTA loops over the batch.  The psi_hat
+// slice of the block (band rows x folds x 4 orders x K) and each slot's U row offset +
+// Hermitian-fold flag are staged in shared memory once per slot chunk, so the inner loop
+// is 1 LDG + 5 broadcast LDS.128 + 36 FFMA per slot (the former per-slot integer
+// decoding made it instruction-issue bound: FFMA 13 % of instructions, issue 63 %).
+// Batch register blocking (2 or 4 batches per thread) was measured slower (spills).
+// Output S[((b*Hout + h)*nbo + m')*2 + reim][c*K + k].
 constexpr int BAND_MAX_SLOTS = 64;  // band rows x folds staged per CTA
 __global__ void __launch_bounds__(256) disco_band_kernel(
     const float2* __restrict__ U, const float2* __restrict__ psi_hat, const int32_t* __restrict__ band0,
@@ -126,6 +129,7 @@ __global__ void __launch_bounds__(256) disco_band_kernel(
     // U holds input rows [h_in0, h_in0 + Hin); this launch computes output rows
     // [ho0, ho0 + Hout) (local index h)
     __shared__ float4 ps[BAND_MAX_SLOTS][4][5];  // [band slot][m' in tile][k pairs] (K <= 9 -> 5 float4)
+    __shared__ int32_t uo[BAND_MAX_SLOTS][4];    // (bi * nbi + idx), ~x when folded (conj)
     const int mi = threadIdx.x / 64, cl = threadIdx.x % 64;
     const int64_t mp0 = static_cast<int64_t>(blockIdx.x) * 4;
     const int64_t mp = mp0 + mi;
@@ -144,12 +148,14 @@ __global__ void __launch_bounds__(256) disco_band_kernel(
             const int bi = slot / s, q = slot - bi * s;
             const int64_t m = mp0 + t;
             float2 v = make_float2(0.f, 0.f);
-            if (m < nbo && kk < K) {
-                const int kq = static_cast<int>(m) + wout * q;
-                const int idx = kq > half ? win - kq : kq;
-                v = __ldg(psi_hat + ((po + bi) * nbi + idx) * K + kk);
-            }
+            const int kq = static_cast<int>(m) + wout * q;
+            const int idx = kq > half ? win - kq : kq;
+            if (m < nbo && kk < K) v = __ldg(psi_hat + ((po + bi) * nbi + idx) * K + kk);
             reinterpret_cast<float2*>(&ps[sl][t][0])[kk] = v;
+            if (kk == 0) {
+                const int o = bi * static_cast<int>(nbi) + (m < nbo ? idx : 0);
+                uo[sl][t] = kq > half ? ~o : o;
+            }
         }
         __syncthreads();
         if (mp >= nbo) continue;
@@ -161,20 +167,24 @@ __global__ void __launch_bounds__(256) disco_band_kernel(
 #pragma unroll
                 for (int k = 0; k < 9; ++k) acc[k] = make_float2(0.f, 0.f);
                 const float2* Ub = U + (b * Hin + h0) * nbi * C + c;
-                constexpr int CH = 4;  // slots per load batch
-                for (int sl0 = 0; sl0 < ns; sl0 += CH) {
-                    float2 u[CH];
-                    bool cj[CH];
+                // slots in batches of 4 with the next batch's U loads in flight while the
+                // current batch is consumed (the loop was load-latency bound: long
+                // scoreboard 57 % of stalls)
+                constexpr int CH = 4;
+                float2 ucur[CH], unxt[CH];
+                int ocur[CH], onxt[CH];
+                auto load = [&](int sl0, float2 (&u)[CH], int (&o)[CH]) {
 #pragma unroll
                     for (int j = 0; j < CH; ++j) {
-                        const int slot = slot0 + sl0 + j;
-                        const int bi = slot / s, q = slot - bi * s;
-                        const int kq = static_cast<int>(mp) + wout * q;
-                        cj[j] = kq > half;
-                        const int idx = cj[j] ? win - kq : kq;
-                        u[j] = sl0 + j < ns ? __ldg(Ub + (static_cast<int64_t>(bi) * nbi + idx) * C)
-                                            : make_float2(0.f, 0.f);
+                        const int sl = sl0 + j;
+                        o[j] = sl < ns ? uo[sl][mi] : 0;
+                        const int oo = o[j] < 0 ? ~o[j] : o[j];
+                        u[j] = sl < ns ? __ldg(Ub + static_cast<int64_t>(oo) * C) : make_float2(0.f, 0.f);
                     }
+                };
+                load(0, ucur, ocur);
+                for (int sl0 = 0; sl0 < ns; sl0 += CH) {
+                    if (sl0 + CH < ns) load(sl0 + CH, unxt, onxt);
 #pragma unroll
                     for (int j = 0; j < CH; ++j) {
                         if (sl0 + j >= ns) break;
@@ -186,14 +196,22 @@ __global__ void __launch_bounds__(256) disco_band_kernel(
                             p[2 * k2] = make_float2(t4.x, t4.y);
                             p[2 * k2 + 1] = make_float2(t4.z, t4.w);
                         }
-                        const float2 uu = u[j];
-                        // R = conj(psi) u for kq <= W/2, psi conj(u) above (Hermitian fold)
-                        const float sy = cj[j] ? -1.f : 1.f;
+                        // R = conj(psi) u for kq <= W/2, psi conj(u) = conj(conj(psi) u)
+                        // above (Hermitian fold): re += px ux + py uy, im += px vx - py vy
+                        // with (vx, vy) = sy * (uy, ux)
+                        const bool cj = ocur[j] < 0;
+                        const float ux = ucur[j].x, uy = ucur[j].y;
+                        const float vx = cj ? -uy : uy, vy = cj ? -ux : ux;
 #pragma unroll
                         for (int k = 0; k < 9; ++k) {
-                            acc[k].x += p[k].x * uu.x + p[k].y * uu.y;
-                            acc[k].y += sy * (p[k].x * uu.y - p[k].y * uu.x);
+                            acc[k].x = fmaf(p[k].x, ux, fmaf(p[k].y, uy, acc[k].x));
+                            acc[k].y = fmaf(p[k].x, vx, fmaf(-p[k].y, vy, acc[k].y));
                         }
+                    }
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) {
+                        ucur[j] = unxt[j];
+                        ocur[j] = onxt[j];
                     }
                 }
                 const int64_t row = ((b * Hout + h) * nbo + mp) * 2;
@@ -513,10 +531,9 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
     require(nout <= 65535, "disco: grid too large");
     {
         ProfScope prof("disco_band", st);
-        disco_band_kernel<<<grid, 256, 0, st>>>(U, d_psi_hat.p, d_band0.p, d_bandc.p, d_psi_off.p, nin,
-                                                nbi, nout, nbo, static_cast<int>(win),
-                                                static_cast<int>(wout), static_cast<int>(stride), K,
-                                                cin, w.ldS, S, h_in0, ho0, B);
+        disco_band_kernel<<<grid, 256, 0, st>>>(U, d_psi_hat.p, d_band0.p, d_bandc.p, d_psi_off.p, nin, nbi, nout, nbo,
+                                   static_cast<int>(win), static_cast<int>(wout), static_cast<int>(stride), K,
+                                   cin, w.ldS, S, h_in0, ho0, B);
         SPH_LAUNCH_CHECK();
     }
     count_launch();
