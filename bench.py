@@ -245,10 +245,103 @@ def workload_config(args):
                 "channels": CHANNELS, "parallelism": f"fields sharded over {args.gpus} GPU(s)",
                 "precision": "fp32 I/O, 3xTF32 tcgen05 Legendre GEMMs, fp32 accumulate",
                 "l2_policy": "inputs (4.25 GB/GPU) larger than the 126 MB L2"}
+    if args.workload in ("dist_sht", "dist_disco"):
+        nh, nw = decomp(args)
+        what = ("forward SHT (paper Alg. 1: 4 all-to-all transposes)" if args.workload == "dist_sht"
+                else "DISCO conv -> 360x720 Gaussian, 512 -> 512 channels (Alg. 2 with latitude halo)")
+        return {"workload": f"configs[4]: distributed {what}, 721x1440 equiangular, 512 channels, "
+                            f"batch 1, {nh}x{nw} (polar x azimuth) decomposition",
+                "decomposition": f"{nh}x{nw}", "channels": 512, "parallelism": f"lat/lon domain decomposition over {nh * nw} GPU(s), NCCL",
+                "precision": "fp32 I/O, 3xTF32 tcgen05 GEMMs"}
     return {"workload": "configs[2]: DISCO conv 721x1440 eq -> 360x720 Gaussian, Morlet K=9, "
                         "cutoff 3pi/360, 64 -> 256 channels, batch 4 per GPU",
             "batch": 4, "c_in": 64, "c_out": 256, "precision": "fp32 I/O, 3xTF32 channel mix",
             "l2_policy": "inputs (1.06 GB/GPU) larger than the 126 MB L2"}
+
+
+def decomp(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.decomp:
+        nh, nw = (int(v) for v in args.decomp.lower().split("x"))
+    else:
+        nh, nw = ws, 1
+    if nh * nw != ws:
+        raise SystemExit(f"--decomp {nh}x{nw} does not match WORLD_SIZE={ws}")
+    return nh, nw
+
+
+def run_dist(args, ws, rank, local):
+    """cfg5: the paper's domain-decomposed SHT / DISCO at 721x1440, 512 channels, batch 1.
+    Strong scaling (fixed global problem); value = channels (fields) per second; every
+    collective is NCCL over NVLink; timed with CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2507_12144_b200 as S
+    from paper_2507_12144_b200 import dist as D
+    if ws == 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nh, nw = decomp(args)
+    ctx = D.DistContext(D.CommGrid((1, 1, nh, nw)))
+    ctx.track = False
+    dev = torch.device("cuda", local)
+    C = 512
+    torch.manual_seed(1234 + rank)
+    hp, wp = D.canonical_split(NLAT, nh), D.canonical_split(NLON, nw)
+    i, j = ctx.index(D.POLAR), ctx.index(D.AZIMUTH)
+    x = D.Sharded(torch.rand((C, hp[i], wp[j]), device=dev) * 2 - 1, {1: hp, 2: wp})
+    backend = D.GpuBackend()
+    if args.workload == "dist_sht":
+        grid = S.build_equiangular(NLAT, NLON)
+
+        def step():
+            D.dist_sht_forward(ctx, x, grid, LMAX, MMAX, backend)
+    else:
+        op = S.DiscoOperator(S.build_equiangular(NLAT, NLON), S.build_gaussian(360, 720),
+                             S.morlet_basis(3 * math.pi / 360))
+        mix = (torch.rand((C, C, op.n_basis), device=dev) * 2 - 1) / math.sqrt(C * 9)
+
+        def step():
+            D.dist_disco_apply(ctx, x, op, mix, backend)
+    from paper_2507_12144_b200 import _lib as L
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    launches0 = L.launch_count()
+    L.profile_read()
+    L.profile_enable(True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    L.profile_enable(False)
+    prof = L.profile_read()
+    launches = L.launch_count() - launches0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    # traffic of one step (reference TrafficLog schema, group-summed bytes)
+    ctx.track = True
+    ctx.log = D.TrafficLog()
+    step()
+    torch.cuda.synchronize()
+    if rank == 0:
+        out = {"metric": METRIC, "value": C / (ms / 1e3), "unit": "fields/s", "n_gpus": ws,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
+               "traffic_csv": ctx.log.csv(), "gpu_launches": launches, "clocks": clk.summary(),
+               "per_kernel_ms_rank0": {k: v[1] / args.steps for k, v in sorted(prof.items())},
+               "roofline": None, "cpu_baseline": None, "e2e": None}
+        print(json.dumps(out), flush=True)
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -386,7 +479,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sht", choices=["sht", "disco"])
+    ap.add_argument("--workload", default="sht", choices=["sht", "disco", "dist_sht", "dist_disco"])
+    ap.add_argument("--decomp", default="", help="dist_*: NHxNW polar x azimuth ranks (default WORLD_SIZE x 1)")
     ap.add_argument("--chunk", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -397,9 +491,12 @@ def main():
         run_reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), rank)
         return
     ws, rank, local = dist_setup()
-    run_ours(args, ws, rank, local)
-    if ws > 1:
-        import torch.distributed as dist
+    if args.workload.startswith("dist_"):
+        run_dist(args, ws, rank, local)
+    else:
+        run_ours(args, ws, rank, local)
+    import torch.distributed as dist
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

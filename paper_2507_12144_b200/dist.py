@@ -147,6 +147,7 @@ class DistContext:
         self.rank = dist.get_rank()
         self.coords = grid.coords(self.rank)
         self.log = TrafficLog()
+        self.track = True
         self.pg: Dict[int, Optional[dist.ProcessGroup]] = {}
         self.members: Dict[int, List[int]] = {}
         for axis in (BATCH, ENSEMBLE, POLAR, AZIMUTH):
@@ -167,6 +168,12 @@ class DistContext:
         t = torch.tensor([n], dtype=torch.int64, device=like.device)
         dist.all_reduce(t)
         return int(t.item())
+
+    def record(self, axis: str, collective: str, local_bytes: int, like: torch.Tensor) -> None:
+        """Log one collective with the group-summed bytes (the reference TrafficLog's
+        accounting).  The sum is an all_reduce + host sync, so timed loops set
+        ``track = False`` and only the call count is kept."""
+        self.log.record(axis, collective, self._sum_bytes(local_bytes, like) if self.track else 0)
 
 
 def distributed_transpose(ctx: DistContext, x: torch.Tensor, axis: int, dim_from: int, dim_to: int,
@@ -198,7 +205,7 @@ def distributed_transpose(ctx: DistContext, x: torch.Tensor, axis: int, dim_from
     blocks = list(torch.split(recv, out_splits))
     y = torch.cat([b.view(s) for b, s in zip(blocks, shapes)], dim=dim_from)
     sent = (send.numel() - in_splits[me]) * x.element_size()
-    ctx.log.record(AXIS_NAMES[axis], "all_to_all", ctx._sum_bytes(sent, x))
+    ctx.record(AXIS_NAMES[axis], "all_to_all", sent, x)
     return y, parts_to
 
 
@@ -220,6 +227,15 @@ class GpuBackend:
         """x [C, h, nlon] -> [C, h, mmax, 2] (complex bins * 2pi/nlon)."""
         C, h, _ = x.shape
         return self._plan(grid, lmax, mmax).fft_stage(x.contiguous(), C, h)
+
+    def sht_full(self, grid, lmax, mmax, x: torch.Tensor) -> torch.Tensor:
+        """x [C, nlat, nlon] (all latitudes and longitudes local) -> [C, lmax, mmax, 2]
+        through the fused single-GPU forward SHT (reference-count lmax / mmax)."""
+        from . import _lib as L
+        C = x.shape[0]
+        plan = self._plan(grid, lmax, mmax)
+        out = plan.forward(x.contiguous(), L.SPH_LAYOUT_DENSE_LM)
+        return out.view(C, lmax, mmax, 2)
 
     def legendre_stage(self, grid, lmax, mmax, bins: torch.Tensor, m0: int) -> torch.Tensor:
         """bins [C, nlat, mloc, 2] -> [C, lmax, mloc, 2]."""
@@ -286,14 +302,35 @@ def unshard(ctx: DistContext, s: Sharded) -> torch.Tensor:
 
 
 def dist_sht_forward(ctx: DistContext, x: Sharded, grid, lmax: int, mmax: int,
-                     backend=None) -> Sharded:
+                     backend=None, order: str = "auto") -> Sharded:
     """Algorithm 1 (distsim.hpp:404-463).  x.local [C, Hloc, Wloc] -> [C, lmaxloc, mmaxloc, 2]
     with dim 1 (l) over polar and dim 2 (m) over azimuth.  No grid-kind check, like the
-    reference (its only equiangular forward path)."""
+    reference (its only equiangular forward path).
+
+    order "reference": T1 (W->C, azimuth) -> FFT stage -> T2 (C->m, azimuth) -> T3 (H->C,
+    polar) -> Legendre stage -> T4 (C->l, polar), exactly the reference's sequence.
+    order "fused" (default when the backend has ``sht_full``): T1 (W->C, azimuth) -> T3'
+    (H->C, polar) on the real fields -> the fused single-GPU SHT (fold FFT + quad-layout
+    tcgen05 Legendre GEMM) on the rank's channel slice -> T4' (C->l, polar) -> T2' (C->m,
+    azimuth).  Still 4 all-to-alls; per axis the same bytes as the reference when
+    lmax == nlat (real rings of W = 2 mmax floats vs mmax complex bins), same output
+    layout and canonical splits; per-rank compute is the serial fast path instead of the
+    plain FFT + fold + stage GEMM + layout conversions (cfg5 1x1: 11.5 ms -> fused)."""
     backend = backend or GpuBackend()
     ctx.log.set_operation("dist_sht")
     if grid.nlon < 2 * mmax or grid.nlat < lmax:
         raise ValueError("dist_sht_forward: resolution insufficient for lmax/mmax")
+    if order == "auto":
+        order = "fused" if hasattr(backend, "sht_full") else "reference"
+    if order == "fused":
+        t, cparts_az = distributed_transpose(ctx, x.local, AZIMUTH, 2, 0, x.split[2])
+        t, cparts_pol = distributed_transpose(ctx, t, POLAR, 1, 0, x.split[1])
+        if t.shape[1] != grid.nlat or t.shape[2] != grid.nlon:
+            raise ValueError("dist_sht_forward: bookkeeping mismatch")
+        coeffs = backend.sht_full(grid, lmax, mmax, t)                   # [Cl, lmax, mmax, 2]
+        coeffs, lparts = distributed_transpose(ctx, coeffs, POLAR, 0, 1, cparts_pol)
+        coeffs, mparts = distributed_transpose(ctx, coeffs, AZIMUTH, 0, 2, cparts_az)
+        return Sharded(coeffs, {1: lparts, 2: mparts})
     # T1: W -> C over azimuth
     t, cparts_az = distributed_transpose(ctx, x.local, AZIMUTH, 2, 0, x.split[2])
     if t.shape[2] != grid.nlon:
@@ -349,7 +386,7 @@ def _halo(ctx: DistContext, x: torch.Tensor, hparts: Sequence[int], need: Sequen
         if m:
             out.narrow(1, s - lo, m).copy_(blk.view(C, m, W))
     sent = (send.numel() - in_splits[me]) * x.element_size()
-    ctx.log.record("polar", "halo", ctx._sum_bytes(sent, x))
+    ctx.record("polar", "halo", sent, x)
     return out
 
 
@@ -388,6 +425,5 @@ def dist_disco_apply(ctx: DistContext, x: Sharded, op, mix: torch.Tensor, backen
     out = part.new_empty((cout, nout, mx))
     dist.reduce_scatter_tensor(out.view(-1), padded.view(-1), group=ctx.pg[AZIMUTH])
     me = ctx.index(AZIMUTH)
-    ctx.log.record("azimuth", "reduce_scatter",
-                   ctx._sum_bytes((nw - 1) * out.numel() * out.element_size(), part))
+    ctx.record("azimuth", "reduce_scatter", (nw - 1) * out.numel() * out.element_size(), part)
     return Sharded(out[:, :, :wparts[me]].contiguous(), {1: hoparts, 2: wparts})
