@@ -253,6 +253,10 @@ def workload_config(args):
                             f"batch 1, {nh}x{nw} (polar x azimuth) decomposition",
                 "decomposition": f"{nh}x{nw}", "channels": 512, "parallelism": f"lat/lon domain decomposition over {nh * nw} GPU(s), NCCL",
                 "precision": "fp32 I/O, 3xTF32 tcgen05 GEMMs"}
+    if args.workload == "disco_t":
+        return {"workload": "configs[2] adjoint: disco_transpose_apply 360x720 Gaussian -> 721x1440 eq, "
+                            "Morlet K=9, cutoff 3pi/360, 256 -> 64 channels, batch 4 per GPU",
+                "batch": 4, "c_in": 64, "c_out": 256, "precision": "fp32 I/O, 3xTF32 channel mix"}
     return {"workload": "configs[2]: DISCO conv 721x1440 eq -> 360x720 Gaussian, Morlet K=9, "
                         "cutoff 3pi/360, 64 -> 256 channels, batch 4 per GPU",
             "batch": 4, "c_in": 64, "c_out": 256, "precision": "fp32 I/O, 3xTF32 channel mix",
@@ -372,14 +376,25 @@ def run_ours(args, ws, rank, local):
         go = S.build_gaussian(360, 720)
         op = S.DiscoOperator(gi, go, S.morlet_basis(3 * math.pi / 360))
         B, cin, cout = 4, 64, 256
-        x = torch.rand((B, cin, NLAT, NLON), device=dev) * 2 - 1
         mix = (torch.rand((cout, cin, op.n_basis), device=dev) * 2 - 1) / math.sqrt(cin * 9)
-        y = torch.empty((B, cout, 360, 720), device=dev)
-        wsb = op.workspace(B, cin, cout)
+        if args.workload == "disco":
+            x = torch.rand((B, cin, NLAT, NLON), device=dev) * 2 - 1
+            y = torch.empty((B, cout, 360, 720), device=dev)
+            wsb = op.workspace(B, cin, cout)
 
-        def step():
-            op.apply(x, mix, out=y, ws=wsb)
-        units = B * cout
+            def step():
+                op.apply(x, mix, out=y, ws=wsb)
+            units = B * cout
+        else:  # disco_transpose_apply: v on the 360x720 grid -> 721x1440 (64 channels)
+            v = torch.rand((B, cout, 360, 720), device=dev) * 2 - 1
+            y = torch.empty((B, cin, NLAT, NLON), device=dev)
+            from paper_2507_12144_b200 import _lib as LL
+            wsb = torch.empty(LL.lib.sph_disco_transpose_workspace_bytes(op.h, B, cin, cout),
+                              dtype=torch.uint8, device=dev)
+
+            def step():
+                op.transpose_apply(v, mix, out=y, ws=wsb)
+            units = B * cin
 
     stream = torch.cuda.current_stream(dev)
     for _ in range(max(args.warmup, 3)):
@@ -479,7 +494,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sht", choices=["sht", "disco", "dist_sht", "dist_disco"])
+    ap.add_argument("--workload", default="sht", choices=["sht", "disco", "disco_t", "dist_sht", "dist_disco"])
     ap.add_argument("--decomp", default="", help="dist_*: NHxNW polar x azimuth ranks (default WORLD_SIZE x 1)")
     ap.add_argument("--chunk", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")

@@ -131,6 +131,16 @@ int64_t sph_disco_workspace_bytes(sph_disco_plan plan, int64_t B, int64_t c_in, 
 int sph_disco_apply(sph_disco_plan plan, const float* x, const float* mix, int64_t B,
                     int64_t c_in, int64_t c_out, float* y, void* workspace, void* stream);
 
+/* disco_transpose_apply (convolution.hpp:226-266): the adjoint of sph_disco_apply under
+ * the grids' quadrature inner products (entries re-weighted with the output grid's weight,
+ * :251).  v [B][c_out][out_nlat][out_nlon] on the OUTPUT grid, mix [c_out][c_in][K] (the
+ * forward's mix tensor) -> y [B][c_in][in_nlat][in_nlon] on the input grid.  The
+ * transposed filter tables are built on the first call. */
+int64_t sph_disco_transpose_workspace_bytes(sph_disco_plan plan, int64_t B, int64_t c_in,
+                                            int64_t c_out);
+int sph_disco_transpose_apply(sph_disco_plan plan, const float* v, const float* mix, int64_t B,
+                              int64_t c_in, int64_t c_out, float* y, void* workspace, void* stream);
+
 /* Latitude-shard form used by the distributed DISCO (distsim.hpp:468-547 with a
  * latitude halo instead of the reduce-scatter of K-expanded partials): output rows
  * [h_out0, h_out0+n_out) from the input rows [h_in0, h_in0+n_in) given in

@@ -5,6 +5,7 @@
 //   sphere::sht_forward(field, lmax, mmax)        -> sphere_gpu::sht_forward(...)
 //   sphere::sht_inverse(coeffs, grid)             -> sphere_gpu::sht_inverse(...)
 //   sphere::disco_apply(op, field, mix)           -> sphere_gpu::disco_apply(op, field, mix)
+//   sphere::disco_transpose_apply(op, field, mix) -> sphere_gpu::disco_transpose_apply(...)
 //       with op = sphere_gpu::assemble_disco(in_grid, out_grid, basis)
 //   sphere::spectral_conv(field, kernel)          -> sphere_gpu::spectral_conv(...)
 //
@@ -200,6 +201,27 @@ inline sphere::SphericalField disco_apply(const DiscoOperator& op, const sphere:
                           static_cast<int64_t>(mix.c_out), y.p, nullptr, nullptr));
     const std::vector<float> h = y.download();
     sphere::SphericalField out(op.out_grid, mix.c_out);
+    for (size_t i = 0; i < out.data.size(); ++i) out.data[i] = h[i];
+    return out;
+}
+
+// convolution.hpp:226-266 (field on the output grid -> result on the input grid)
+inline sphere::SphericalField disco_transpose_apply(const DiscoOperator& op,
+                                                    const sphere::SphericalField& field,
+                                                    const sphere::MixTensor& mix) {
+    sphere::require_same_sampling(field, op.out_grid, "disco_transpose_apply");
+    if (mix.c_in == 0 || mix.k != op.n_basis)
+        throw std::invalid_argument("disco_transpose_apply: mix tensor shape mismatch");
+    if (mix.c_out != field.channels)
+        throw std::invalid_argument("disco_transpose_apply: mix tensor shape mismatch");
+    detail::DeviceArray<float> v(field.data.size()), w(mix.w.size()),
+        y(mix.c_in * op.in_grid.nlat * op.in_grid.nlon);
+    v.upload(detail::to_f32(field.data));
+    w.upload(detail::to_f32(mix.w));
+    check(sph_disco_transpose_apply(op.plan.get(), v.p, w.p, 1, static_cast<int64_t>(mix.c_in),
+                                    static_cast<int64_t>(mix.c_out), y.p, nullptr, nullptr));
+    const std::vector<float> h = y.download();
+    sphere::SphericalField out(op.in_grid, mix.c_in);
     for (size_t i = 0; i < out.data.size(); ++i) out.data[i] = h[i];
     return out;
 }

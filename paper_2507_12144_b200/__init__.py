@@ -9,7 +9,7 @@ from ._lib import LIB_PATH, SphError, SphInvalidArgument, launch_count  # noqa: 
 from .sphere import (  # noqa: F401
     EQUIANGULAR, GAUSSIAN, BlockWeights, DiscoOperator, FilterBasis, GridSpec, ShtPlan,
     SpectralCoeffs, SphericalField, assemble_disco, block_apply, block_epilogue,
-    build_equiangular, build_gaussian, default_mmax, disco_apply, get_sht_plan,
+    build_equiangular, build_gaussian, default_mmax, disco_apply, disco_transpose_apply, get_sht_plan,
     isotropic_basis, morlet_basis, require_same_sampling, sht_forward, sht_inverse,
     spectral_conv,
 )

@@ -39,7 +39,8 @@ EXPORTS = [
     "sph_sht_fft_stage", "sph_sht_legendre_stage", "sph_sht_stage_workspace_bytes",
     "sph_disco_plan_create", "sph_disco_plan_destroy", "sph_disco_plan_info",
     "sph_disco_workspace_bytes", "sph_disco_apply", "sph_disco_input_rows",
-    "sph_disco_rows_workspace_bytes", "sph_disco_apply_rows",
+    "sph_disco_rows_workspace_bytes", "sph_disco_apply_rows", "sph_disco_transpose_workspace_bytes",
+    "sph_disco_transpose_apply",
     "sph_spectral_conv", "sph_spectral_conv_workspace_bytes", "sph_block_epilogue",
 ]
 
@@ -91,6 +92,9 @@ def _load():
     L.sph_disco_rows_workspace_bytes.argtypes = [vp, i64, i64, i64, i64, i64]
     L.sph_disco_rows_workspace_bytes.restype = i64
     L.sph_disco_apply_rows.argtypes = [vp, vp, i64, i64, i64, i64, vp, i64, i64, i64, vp, vp, vp]
+    L.sph_disco_transpose_workspace_bytes.argtypes = [vp, i64, i64, i64]
+    L.sph_disco_transpose_workspace_bytes.restype = i64
+    L.sph_disco_transpose_apply.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, vp]
     L.sph_spectral_conv.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp, vp, vp]
     L.sph_spectral_conv_workspace_bytes.argtypes = [vp, i64, i64, i64]
     L.sph_spectral_conv_workspace_bytes.restype = i64

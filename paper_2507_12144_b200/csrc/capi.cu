@@ -274,6 +274,19 @@ int sph_disco_apply(sph_disco_plan plan, const float* x, const float* mix, int64
     });
 }
 
+int64_t sph_disco_transpose_workspace_bytes(sph_disco_plan plan, int64_t B, int64_t c_in,
+                                            int64_t c_out) {
+    return plan ? plan->p.transpose_workspace_bytes(B, c_in, c_out) : -1;
+}
+
+int sph_disco_transpose_apply(sph_disco_plan plan, const float* v, const float* mix, int64_t B,
+                              int64_t c_in, int64_t c_out, float* y, void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "disco_transpose_apply: null plan");
+        plan->p.transpose_apply(v, mix, B, c_in, c_out, y, workspace, S(stream));
+    });
+}
+
 int sph_disco_input_rows(sph_disco_plan plan, int64_t h_out0, int64_t n_out, int64_t* h_in0,
                          int64_t* n_in) {
     return guarded([&] {

@@ -266,6 +266,92 @@ __global__ void __launch_bounds__(256) disco_gather_kernel(
     }
 }
 
+// mix [cout][cin*K] -> transposed tf32 hi/lo table T[n = ci*K + k][co] (row stride ld)
+__global__ void mix_t_split_kernel(const float* __restrict__ mix, int64_t cout, int64_t n, int64_t ld,
+                                   float* __restrict__ hi, float* __restrict__ lo) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n * ld) return;
+    const int64_t r = i / ld, co = i % ld;
+    const float x = co < cout ? mix[co * n + r] : 0.f;
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+    const float h = __uint_as_float(u);
+    hi[i] = h;
+    lo[i] = x - h;
+}
+
+// Transpose band kernel (the adjoint of disco_band_kernel): for input row r and order m
+// (< nbi), channel ci:
+//   U'[b][r][m][ci] = sum_{h : r in band(h)} sum_k psi_t_hat_k[h, r](m) * S_k[b, h](m mod W_out)
+// with S(m') for m' > W_out/2 taken as conj S(W_out - m') (Hermitian extension of the
+// mixed output-ring spectra): zero-insertion upsampling by the stride replicates the
+// spectrum, and the adjoint of the circular correlation is the circular convolution.
+// A CTA owns RT consecutive input rows x 4 orders x 64 channels; it walks the output
+// rows h whose band meets its row tile, loads S_k[b, h](m) (18 floats per thread) ONCE
+// and scatters it into the tile rows of that band (RT complex accumulators per thread),
+// so S is read once per (h, row tile) instead of once per (h, row): measured 20.1 ms at
+// cfg3 B = 4 when each row re-read its S vectors.
+constexpr int TB_RT = 16;
+__global__ void __launch_bounds__(256) disco_band_t_kernel(
+    const float* __restrict__ S, const float2* __restrict__ psi_t, const int32_t* __restrict__ band0,
+    const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, const int32_t* __restrict__ tt_ptr,
+    const int32_t* __restrict__ tt_h, int64_t Hin, int64_t nbi, int64_t Hout, int64_t nbo, int wout, int K,
+    int64_t C, int64_t ldS, float2* __restrict__ Ut, int64_t B) {
+    const int mi = threadIdx.x / 64, cl = threadIdx.x % 64;
+    const int64_t m = static_cast<int64_t>(blockIdx.x) * 4 + mi;
+    const int r0 = blockIdx.y * TB_RT;
+    const int nr = min(TB_RT, static_cast<int>(Hin) - r0);
+    if (m >= nbi) return;
+    const int half = wout / 2;
+    const int mo = static_cast<int>(m % wout);
+    const bool cj = mo > half;
+    const int mp = cj ? wout - mo : mo;
+    const float sg = cj ? -1.f : 1.f;
+    const int t0 = tt_ptr[blockIdx.y], t1 = tt_ptr[blockIdx.y + 1];
+    for (int64_t b = 0; b < B; ++b) {
+        const float* Sb = S + b * Hout * nbo * 2 * ldS;
+        for (int64_t c0 = 0; c0 < C; c0 += 64) {
+            const int64_t c = c0 + cl;
+            if (c >= C) break;
+            float2 acc[TB_RT];
+#pragma unroll
+            for (int i = 0; i < TB_RT; ++i) acc[i] = make_float2(0.f, 0.f);
+            for (int t = t0; t < t1; ++t) {
+                const int h = tt_h[t];
+                const float* sr = Sb + (static_cast<int64_t>(h) * nbo + mp) * 2 * ldS + c * K;
+                const float* si = sr + ldS;
+                float xr[9], xi[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    xr[k] = k < K ? __ldg(sr + k) : 0.f;
+                    xi[k] = k < K ? sg * __ldg(si + k) : 0.f;
+                }
+                const int bl = band0[h], bn = bandc[h];
+                const int lo = max(bl, r0), hi = min(bl + bn, r0 + nr);
+                const float2* pb = psi_t + (psi_off[h] + (lo - bl)) * nbi * K + m * K;
+#pragma unroll
+                for (int i = 0; i < TB_RT; ++i) {
+                    const int r = r0 + i;
+                    if (r < lo || r >= hi) continue;
+                    const float2* pk = pb + static_cast<int64_t>(r - lo) * nbi * K;
+                    float2 a = acc[i];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        if (k >= K) break;
+                        const float2 p = __ldg(pk + k);
+                        a.x = fmaf(p.x, xr[k], fmaf(-p.y, xi[k], a.x));
+                        a.y = fmaf(p.x, xi[k], fmaf(p.y, xr[k], a.y));
+                    }
+                    acc[i] = a;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < TB_RT; ++i)
+                if (i < nr) Ut[((b * Hin + r0 + i) * nbi + m) * C + c] = acc[i];
+        }
+    }
+}
+
 }  // namespace
 
 void split_rows(const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
@@ -303,7 +389,7 @@ void DiscoPlan::create(int in_kind_, int64_t in_nlat, int64_t in_nlon, int out_k
 
     // ---- assemble (convolution.hpp:150-176), per output row in parallel
     std::vector<std::vector<int32_t>> rh(hout), rw(hout);
-    std::vector<std::vector<double>> rv(hout);
+    std::vector<std::vector<double>> rv(hout), rb(hout);
     std::vector<double> lon(win);
     for (int64_t j = 0; j < win; ++j) lon[j] = 2.0 * kPi * static_cast<double>(j) / static_cast<double>(win);
     parallel_for(hout, [&](int64_t h) {
@@ -318,7 +404,11 @@ void DiscoPlan::create(int in_kind_, int64_t in_nlat, int64_t in_nlon, int out_k
                 if (dist >= basis.cutoff) continue;
                 rh[h].push_back(static_cast<int32_t>(hi));
                 rw[h].push_back(static_cast<int32_t>(wj));
-                for (int k = 0; k < K; ++k) rv[h].push_back(basis.eval_real(k, dist, az) * w_in);
+                for (int k = 0; k < K; ++k) {
+                    const double bk = basis.eval_real(k, dist, az);
+                    rv[h].push_back(bk * w_in);
+                    rb[h].push_back(bk);
+                }
             }
         }
     });
@@ -333,10 +423,12 @@ void DiscoPlan::create(int in_kind_, int64_t in_nlat, int64_t in_nlon, int out_k
     h_in.resize(nnz);
     w_rel.resize(nnz);
     vals.resize(nnz * K);
+    bases.resize(nnz * K);
     for (int64_t h = 0; h < hout; ++h) {
         std::copy(rh[h].begin(), rh[h].end(), h_in.begin() + row_ptr[h]);
         std::copy(rw[h].begin(), rw[h].end(), w_rel.begin() + row_ptr[h]);
         std::copy(rv[h].begin(), rv[h].end(), vals.begin() + row_ptr[h] * K);
+        std::copy(rb[h].begin(), rb[h].end(), bases.begin() + row_ptr[h] * K);
     }
     upload(d_row_ptr, row_ptr);
     upload(d_h_in, h_in);
@@ -541,6 +633,162 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
     fft_inverse_plain(fft_out, reinterpret_cast<const float2*>(Yh), B * cout * nout,
                       static_cast<int>(nbo), static_cast<float>(1.0 / static_cast<double>(win)), y,
                       st);
+}
+
+// ------------------------------------------------------------ transpose
+void DiscoPlan::build_transpose() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (t_ready) return;
+    SPH_CUDA(cudaSetDevice(device));
+    // psi_t_hat with weights b_k * w_out[h] (convolution.hpp:251: scale = base * w_out)
+    std::vector<double> cw(win), sw(win);
+    for (int64_t j = 0; j < win; ++j) {
+        const double a = -2.0 * kPi * static_cast<double>(j) / static_cast<double>(win);
+        cw[j] = std::cos(a);
+        sw[j] = std::sin(a);
+    }
+    const int64_t nrow = psi_off[hout];
+    std::vector<float2> ph(static_cast<size_t>(nrow) * nbi * K);
+    parallel_for(hout, [&](int64_t h) {
+        std::vector<double> acc(static_cast<size_t>(bandc[h]) * nbi * K * 2, 0.0);
+        const double wo = out_w[h];
+        for (int64_t e = row_ptr[h]; e < row_ptr[h + 1]; ++e) {
+            const int64_t bi = h_in[e] - band0[h];
+            const int64_t wr = w_rel[e];
+            double* a = acc.data() + bi * nbi * K * 2;
+            int64_t ph_idx = 0;
+            for (int64_t m = 0; m < nbi; ++m) {
+                const double c = cw[ph_idx], s = sw[ph_idx];
+                for (int k = 0; k < K; ++k) {
+                    const double v = bases[e * K + k] * wo;
+                    a[(m * K + k) * 2] += v * c;
+                    a[(m * K + k) * 2 + 1] += v * s;
+                }
+                ph_idx += wr;
+                if (ph_idx >= win) ph_idx -= win;
+            }
+        }
+        float2* out = ph.data() + psi_off[h] * nbi * K;
+        for (size_t i = 0; i < static_cast<size_t>(bandc[h]) * nbi * K; ++i)
+            out[i] = make_float2(static_cast<float>(acc[2 * i]), static_cast<float>(acc[2 * i + 1]));
+    });
+    upload(d_psi_t, ph);
+    // row-tile map: output rows h whose band meets input rows [TB_RT t, TB_RT (t+1))
+    const int64_t ntile = (hin + TB_RT - 1) / TB_RT;
+    std::vector<int32_t> ptr(ntile + 1, 0), hh;
+    for (int64_t t = 0; t < ntile; ++t) {
+        const int64_t r0 = t * TB_RT, r1 = std::min<int64_t>(hin, r0 + TB_RT);
+        for (int64_t h = 0; h < hout; ++h)
+            if (band0[h] < r1 && band0[h] + bandc[h] > r0) hh.push_back(static_cast<int32_t>(h));
+        ptr[t + 1] = static_cast<int32_t>(hh.size());
+    }
+    upload(d_tb_ptr, ptr);
+    upload(d_tb_h, hh);
+    t_ready = true;
+}
+
+namespace {
+struct DiscoTWs {
+    int64_t ldc, ldS, v_off, s_off, u_off, thi_off, tlo_off, total;
+};
+DiscoTWs disco_t_ws(const DiscoPlan& p, int64_t B, int64_t cin, int64_t cout) {
+    DiscoTWs w;
+    w.ldc = static_cast<int64_t>(round_up(cout, 4));
+    w.ldS = static_cast<int64_t>(round_up(cin * p.K, 4));
+    int64_t o = 0;
+    w.thi_off = o;
+    o += round_up(cin * p.K * w.ldc * 4, 256);
+    w.tlo_off = o;
+    o += round_up(cin * p.K * w.ldc * 4, 256);
+    w.v_off = o;  // planar V_hat [(b, h, m', re/im)][ldc]
+    o += round_up(B * p.hout * p.nbo * 2 * w.ldc * 4, 256);
+    w.s_off = o;  // mixed S [(b, h, m', re/im)][ldS]
+    o += round_up(B * p.hout * p.nbo * 2 * w.ldS * 4, 256);
+    w.u_off = o;  // U' [b][r][m][ci] complex
+    o += round_up(B * p.hin * p.nbi * cin * 8, 256);
+    w.total = o + 256;
+    return w;
+}
+}  // namespace
+
+int64_t DiscoPlan::transpose_workspace_bytes(int64_t B, int64_t cin, int64_t cout) const {
+    return disco_t_ws(*this, B, cin, cout).total;
+}
+
+// convolution.hpp:226-266.  v_hat = channel-minor R2C of the output rings (planar re/im
+// rows) -> mix^T GEMM (tcgen05 3xTF32, table mix^T [cin*K][cout]) -> transpose band
+// kernel -> channel-minor C2R of the input rings (scale 1/W_in).
+void DiscoPlan::transpose_apply(const float* v, const float* mix, int64_t B, int64_t cin, int64_t cout,
+                                float* y, void* ws, cudaStream_t st) {
+    require(cin >= 1 && cout >= 1 && B >= 0, "disco_transpose_apply: mix tensor shape mismatch");
+    if (B == 0) return;
+    build_transpose();
+    SPH_CUDA(cudaSetDevice(device));
+    const DiscoTWs w = disco_t_ws(*this, B, cin, cout);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    if (!base) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (own_ws.n < static_cast<size_t>(w.total)) own_ws.alloc(w.total, true);
+        base = own_ws.p;
+    }
+    float* thi = reinterpret_cast<float*>(base + w.thi_off);
+    float* tlo = reinterpret_cast<float*>(base + w.tlo_off);
+    float* V = reinterpret_cast<float*>(base + w.v_off);
+    float* S = reinterpret_cast<float*>(base + w.s_off);
+    float2* Ut = reinterpret_cast<float2*>(base + w.u_off);
+    const int64_t n = cin * K;
+    {
+        const int64_t tot = n * w.ldc;
+        mix_t_split_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(mix, cout, n, w.ldc, thi,
+                                                                                     tlo);
+        SPH_LAUNCH_CHECK();
+        count_launch();
+    }
+    // R2C of v's output rings, planar re/im rows: V[((b*hout + h)*nbo + m')*2 + ri][co]
+    fft_forward_cminor(fft_out, v, B, cout, hout, static_cast<int>(nbo), reinterpret_cast<float2*>(V), st,
+                       /*planar=*/true, w.ldc);
+    const int64_t rows = B * hout * nbo * 2;
+    const GroupedGemm* gp;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto& slot = gemm_t_cache[std::make_tuple(B, cin, cout)];
+        if (!slot) {
+            auto g = std::make_unique<GroupedGemm>();
+            g->A = {nullptr, rows, cout, w.ldc};
+            g->Bhi = {nullptr, n, cout, w.ldc};
+            g->Blo = {nullptr, n, cout, w.ldc};
+            g->store = STORE_ROW;
+            g->bn = n >= 256 ? 256 : 128;
+            g->name = "gemm_disco_mix_t";
+            require(rows < (1LL << 31), "disco_transpose_apply: batch too large for one call");
+            GemmGroup gr;
+            gr.a_row0 = 0;
+            gr.b_row0 = 0;
+            gr.M = static_cast<int32_t>(rows);
+            gr.N = static_cast<int32_t>(n);
+            gr.K = static_cast<int32_t>(cout);
+            gr.ldd = static_cast<int32_t>(w.ldS);
+            gr.zero_to = 0;
+            gr.d_off = 0;
+            g->groups.push_back(gr);
+            g->finalize();
+            slot = std::move(g);
+        }
+        gp = slot.get();
+    }
+    gemm_run(*gp, V, S, prec, st, thi, tlo);
+    require(hin <= 65535, "disco_transpose_apply: grid too large");
+    dim3 grid(static_cast<unsigned>((nbi + 3) / 4), static_cast<unsigned>((hin + TB_RT - 1) / TB_RT));
+    {
+        ProfScope prof("disco_band_t", st);
+        disco_band_t_kernel<<<grid, 256, 0, st>>>(S, d_psi_t.p, d_band0.p, d_bandc.p, d_psi_off.p, d_tb_ptr.p,
+                                                  d_tb_h.p, hin, nbi, hout, nbo, static_cast<int>(wout), K, cin,
+                                                  w.ldS, Ut, B);
+        SPH_LAUNCH_CHECK();
+    }
+    count_launch();
+    fft_inverse_cminor(fft_in, Ut, B, cin, hin, static_cast<int>(nbi),
+                       static_cast<float>(1.0 / static_cast<double>(win)), y, st);
 }
 
 }  // namespace sph

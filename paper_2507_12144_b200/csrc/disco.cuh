@@ -31,6 +31,7 @@ struct DiscoPlan {
     std::vector<int64_t> row_ptr;
     std::vector<int32_t> h_in, w_rel;
     std::vector<double> vals;
+    std::vector<double> bases;  // b_k without the input weight (transpose, convolution.hpp:251)
     // device: direct-gather anchor tables
     DevBuf<int64_t> d_row_ptr;
     DevBuf<int32_t> d_h_in, d_w_rel;
@@ -46,8 +47,18 @@ struct DiscoPlan {
     FftPlan fft_in, fft_out;
     int prec = SPH_PREC_3XTF32;
 
+    // transpose (disco_transpose_apply, convolution.hpp:226-266), built on first use:
+    // psi_t_hat[(psi_off[h] + bi) * nbi + m][k] = sum_e b_k w_out[h] e^{-2 pi i w_rel m / win}
+    // and the row-tile map: input rows [16 t, 16 t + 16) are touched by the output rows
+    // tb_h[tb_ptr[t] .. tb_ptr[t+1]) (those whose band meets the tile)
+    bool t_ready = false;
+    DevBuf<float2> d_psi_t;
+    DevBuf<int32_t> d_tb_ptr, d_tb_h;
+    void build_transpose();
+
     std::mutex mu;
     std::map<std::tuple<int64_t, int64_t, int64_t, int64_t>, std::unique_ptr<GroupedGemm>> gemm_cache;
+    std::map<std::tuple<int64_t, int64_t, int64_t>, std::unique_ptr<GroupedGemm>> gemm_t_cache;
     DevBuf<uint8_t> own_ws;
 
     void create(int in_kind, int64_t in_nlat, int64_t in_nlon, int out_kind, int64_t out_nlat,
@@ -61,6 +72,10 @@ struct DiscoPlan {
                     cudaStream_t st);
     void input_rows(int64_t ho0, int64_t nout, int64_t* lo, int64_t* n) const;
     int64_t rows_workspace_bytes(int64_t B, int64_t cin, int64_t cout, int64_t nin, int64_t nout) const;
+    // v [B][cout][hout][wout] on the output grid -> y [B][cin][hin][win] on the input grid
+    void transpose_apply(const float* v, const float* mix, int64_t B, int64_t cin, int64_t cout,
+                         float* y, void* ws, cudaStream_t st);
+    int64_t transpose_workspace_bytes(int64_t B, int64_t cin, int64_t cout) const;
 };
 
 void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, int64_t cin,

@@ -451,12 +451,16 @@ struct PlainInvIO {
     }
 };
 
-// channel-minor forward (DISCO input): block (c-tile of 2P channels, row hi, batch b)
+// channel-minor forward (DISCO input): block (c-tile of 2P channels, row hi, batch b).
+// planar = 0: U[b][hi][m][c] complex; planar = 1 (DISCO transpose): real planes
+// U[((b*H + hi)*nbins + m)*2 + re/im][c] so a GEMM can take re and im rows with K = c.
 struct CminorIO {
     const float* x;
     int64_t C, H;
     int nbins;
     float2* U;
+    int planar;
+    int64_t ldp;  // planar row stride (floats, >= C)
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
@@ -473,6 +477,7 @@ struct CminorIO {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
         const int64_t hi = blockIdx.y, b = blockIdx.z;
         float2* Ub = U + (b * H + hi) * static_cast<int64_t>(nbins) * C;
+        float* Up = reinterpret_cast<float*>(U) + (b * H + hi) * static_cast<int64_t>(nbins) * 2 * ldp;
         for (int o = threadIdx.x; o < nbins * 2 * P; o += blockDim.x) {
             const int cl = o % (2 * P);
             const int m = o / (2 * P);
@@ -482,7 +487,56 @@ struct CminorIO {
             const float2 zc = buf[j * ld + (m == 0 ? 0 : n - m)];
             const float2 v = (cl & 1) ? make_float2(0.5f * (z.y + zc.y), -0.5f * (z.x - zc.x))
                                       : make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y - zc.y));
-            Ub[static_cast<int64_t>(m) * C + c0 + cl] = v;
+            if (planar) {
+                float* pm = Up + static_cast<int64_t>(m) * 2 * ldp + c0 + cl;
+                pm[0] = v.x;
+                pm[ldp] = v.y;
+            } else {
+                Ub[static_cast<int64_t>(m) * C + c0 + cl] = v;
+            }
+        }
+    }
+};
+
+// channel-minor inverse (DISCO transpose output): half spectra V[b][hi][m][c] (m < nbins)
+// -> rings y[b][c][hi][0..n) * scale; block (c-tile of 2P channels, row hi, batch b), two
+// channels per complex ring (z = A + iB), Im of DC / Nyquist dropped (real synthesis)
+struct CminorInvIO {
+    const float2* V;
+    int64_t C, H;
+    int nbins;
+    float scale;
+    float* y;
+    template <class PT, class NT>
+    __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
+        const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
+        const int64_t hi = blockIdx.y, b = blockIdx.z;
+        const float2* Vb = V + (b * H + hi) * static_cast<int64_t>(nbins) * C;
+        const int half = n / 2;
+        for (int i = threadIdx.x; i < P * n; i += blockDim.x) {
+            const int j = i / n, k = i - j * n;
+            const int64_t ca = c0 + 2 * j, cb = ca + 1;
+            const int kk = k <= half ? k : n - k;
+            float2 ha = make_float2(0.f, 0.f), hb = ha;
+            if (kk < nbins) {
+                if (ca < C) ha = Vb[static_cast<int64_t>(kk) * C + ca];
+                if (cb < C) hb = Vb[static_cast<int64_t>(kk) * C + cb];
+            }
+            if (kk == 0 || 2 * kk == n) { ha.y = 0.f; hb.y = 0.f; }
+            if (k > half) { ha.y = -ha.y; hb.y = -hb.y; }
+            buf[j * ld + k] = make_float2(ha.x - hb.y, ha.y + hb.x);
+        }
+    }
+    template <class PT, class NT>
+    __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
+        const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
+        const int64_t hi = blockIdx.y, b = blockIdx.z;
+        for (int i = threadIdx.x; i < P * n; i += blockDim.x) {
+            const int j = i / n, k = i - j * n;
+            const int64_t ca = c0 + 2 * j, cb = ca + 1;
+            const float2 z = buf[j * ld + k];
+            if (ca < C) y[((b * C + ca) * H + hi) * n + k] = z.x * scale;
+            if (cb < C) y[((b * C + cb) * H + hi) * n + k] = z.y * scale;
         }
     }
 };
@@ -823,14 +877,25 @@ void fft_inverse_plain(const FftPlan& fp, const float2* bins, int64_t nrings, in
 }
 
 void fft_forward_cminor(const FftPlan& fp, const float* x, int64_t B, int64_t C, int64_t H,
-                        int nbins, float2* U, cudaStream_t st) {
+                        int nbins, float2* U, cudaStream_t st, bool planar, int64_t ldp) {
     if (B * C * H == 0) return;
     require(H <= 65535 && B <= 65535, "disco fft: too many rows");
     const int P = rpb_of(fp);
-    CminorIO io{x, C, H, nbins, U};
+    CminorIO io{x, C, H, nbins, U, planar ? 1 : 0, ldp > 0 ? ldp : C};
     dim3 grid(static_cast<unsigned>((C + 2 * P - 1) / (2 * P)), static_cast<unsigned>(H),
               static_cast<unsigned>(B));
     run_transform<false>(fp, io, grid, st, "fft_fwd_cminor", 4.0 * B * C * H * (fp.n + 2.0 * nbins));
+}
+
+void fft_inverse_cminor(const FftPlan& fp, const float2* V, int64_t B, int64_t C, int64_t H, int nbins,
+                        float scale, float* y, cudaStream_t st) {
+    if (B * C * H == 0) return;
+    require(H <= 65535 && B <= 65535, "disco fft: too many rows");
+    const int P = rpb_of(fp);
+    CminorInvIO io{V, C, H, nbins, scale, y};
+    dim3 grid(static_cast<unsigned>((C + 2 * P - 1) / (2 * P)), static_cast<unsigned>(H),
+              static_cast<unsigned>(B));
+    run_transform<true>(fp, io, grid, st, "fft_inv_cminor", 4.0 * B * C * H * (fp.n + 2.0 * nbins));
 }
 
 }  // namespace sph

@@ -63,6 +63,9 @@ void fft_inverse_plain(const FftPlan& fp, const float2* bins, int64_t nrings, in
 // Channel-minor forward transform for DISCO: x [B][C][H][n] ->
 // U [B][H][nbins][C] complex (bins m < nbins, unscaled).
 void fft_forward_cminor(const FftPlan& fp, const float* x, int64_t B, int64_t C, int64_t H,
-                        int nbins, float2* U, cudaStream_t st);
+                        int nbins, float2* U, cudaStream_t st, bool planar = false, int64_t ldp = 0);
+// channel-minor C2R: half spectra V[B][H][nbins][C] -> rings y[B][C][H][n] * scale
+void fft_inverse_cminor(const FftPlan& fp, const float2* V, int64_t B, int64_t C, int64_t H, int nbins,
+                        float scale, float* y, cudaStream_t st);
 
 }  // namespace sph

@@ -354,6 +354,28 @@ class DiscoOperator:
         return out
 
 
+    def transpose_apply(self, v: torch.Tensor, mix: torch.Tensor, out=None, ws=None) -> torch.Tensor:
+        """disco_transpose_apply (convolution.hpp:226-266): v [B, cout, hout, wout] on the
+        output grid -> [B, cin, hin, win] on the input grid; ``mix`` is the forward's
+        [cout, cin, K] tensor."""
+        mix = _dev_f32(mix, "disco_transpose_apply")
+        v = _dev_f32(v, "disco_transpose_apply")
+        cout, cin, K = mix.shape
+        if K != self.n_basis or v.shape[-3] != cout:
+            raise L.SphInvalidArgument(1, "disco_transpose_apply: mix tensor shape mismatch")
+        if v.shape[-2:] != (self.out_grid.nlat, self.out_grid.nlon):
+            raise L.SphInvalidArgument(1, "disco_transpose_apply: field sampling mismatch")
+        B = v.numel() // (cout * self.out_grid.nlat * self.out_grid.nlon)
+        if out is None:
+            out = torch.empty((B, cin, self.in_grid.nlat, self.in_grid.nlon),
+                              dtype=torch.float32, device=v.device)
+        if ws is None:
+            n = L.lib.sph_disco_transpose_workspace_bytes(self.h, B, cin, cout)
+            ws = torch.empty(max(n, 1), dtype=torch.uint8, device=v.device)
+        check(L.lib.sph_disco_transpose_apply(self.h, _ptr(v), _ptr(mix), B, cin, cout, _ptr(out),
+                                              _ptr(ws), _stream(v.device)))
+        return out
+
     def input_rows(self, ho0: int, nout: int):
         """Input latitude rows (h_in0, n_in) covering the filter support of output rows
         [ho0, ho0 + nout) -- the halo a latitude shard needs."""
@@ -404,6 +426,19 @@ def disco_apply(op: DiscoOperator, field: SphericalField, mix: torch.Tensor) -> 
         y = op.apply(field.data, mix)
     return SphericalField(op.out_grid, y.reshape(*lead, mix.shape[0], op.out_grid.nlat,
                                                   op.out_grid.nlon))
+
+
+def disco_transpose_apply(op: DiscoOperator, field: SphericalField, mix: torch.Tensor) -> SphericalField:
+    """convolution.hpp:226-266: the adjoint of disco_apply under the quadrature inner
+    products; ``field`` lives on the output grid, the result on the input grid."""
+    require_same_sampling(field, op.out_grid, "disco_transpose_apply")
+    if mix.shape[0] != field.channels or mix.shape[2] != op.n_basis or mix.shape[1] == 0:
+        raise L.SphInvalidArgument(1, "disco_transpose_apply: mix tensor shape mismatch")
+    lead = tuple(field.data.shape[:-3])
+    with torch.cuda.device(field.data.device):
+        y = op.transpose_apply(field.data, mix)
+    return SphericalField(op.in_grid, y.reshape(*lead, mix.shape[1], op.in_grid.nlat,
+                                                 op.in_grid.nlon))
 
 
 # ----------------------------------------------------------- spectral conv

@@ -14,6 +14,7 @@ int main() {
         sphere_gpu::assemble_disco(g, sphere::build_gaussian(8, 16), sphere::morlet_basis(1.0));
     sphere::MixTensor mix(3, 2, op.n_basis);
     const sphere::SphericalField y = sphere_gpu::disco_apply(op, r, mix);
+    const sphere::SphericalField yt = sphere_gpu::disco_transpose_apply(op, y, mix);
     sphere::SpectralKernel k(2, 2, 16);
     const sphere::SphericalField z = sphere_gpu::spectral_conv(f, k);
     return static_cast<int>(y.data.size() + z.data.size() > 0 ? 0 : 1);

@@ -118,3 +118,73 @@ def test_disco_fourier_vs_direct_anchor_full_size():
     ya, yb = a.apply(x, mix), b.apply(x, mix)
     torch.cuda.synchronize()
     assert float((ya - yb).norm() / yb.norm()) <= TOL
+
+
+# ------------------------------------------------ disco_transpose_apply (convolution.hpp:226-266)
+def transpose(op, v, mix):
+    y = op.transpose_apply(torch.tensor(v, dtype=torch.float32, device=DEV),
+                           torch.tensor(mix, dtype=torch.float32, device=DEV))
+    torch.cuda.synchronize()
+    return y.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("prec", ["3xtf32", "fp32"])
+@pytest.mark.parametrize("name", list(CASES))
+def test_disco_transpose_golden(golden, name, prec):
+    """Reference disco_transpose_apply outputs (tests/golden/make_golden.py)."""
+    ik, ih, iw, ok, oh, ow, cut, cin, cout = CASES[name]
+    op = S.DiscoOperator(grid(ik, ih, iw), grid(ok, oh, ow), S.morlet_basis(cut), prec)
+    mix = oracle.random_field((cout, cin, 9), 77)
+    v = oracle.random_field((cout, oh, ow), 79)
+    yt = transpose(op, v[None], mix)[0]
+    assert rel_l2(yt, golden[f"disco_{name}_yT"]) <= TOL, name
+
+
+def _quad_dot(a, b, w):
+    return float(np.einsum("chw,chw,h->", a, b, w))
+
+
+@pytest.mark.parametrize("case", [
+    (GA, 16, 32, GA, 8, 16, 3 * PI / 8, 2, 3),          # test_convolution.cpp:214-234
+    (EQ, 91, 180, GA, 45, 90, 3 * PI / 45, 4, 8),
+    (EQ, 721, 1440, GA, 360, 720, 3 * PI / 360, 4, 8),  # cfg3 grids, reduced channels
+])
+def test_disco_adjoint_identity(case):
+    """<A u, v>_out == <u, A^T v>_in under the grids' quadrature weights."""
+    ik, ih, iw, ok, oh, ow, cut, cin, cout = case
+    gi, go = grid(ik, ih, iw), grid(ok, oh, ow)
+    op = S.DiscoOperator(gi, go, S.morlet_basis(cut))
+    mix = oracle.random_field((cout, cin, 9), 15)
+    u = oracle.random_field((cin, ih, iw), 16)
+    v = oracle.random_field((cout, oh, ow), 17)
+    au = apply(op, u[None], mix)[0]
+    bv = transpose(op, v[None], mix)[0]
+    lhs = _quad_dot(au, v, np.asarray(go.quad_weights))
+    rhs = _quad_dot(u, bv, np.asarray(gi.quad_weights))
+    assert abs(lhs - rhs) <= 1e-5 * max(1.0, abs(lhs)), (lhs, rhs)
+
+
+def test_disco_isotropic_transpose_equals_forward():
+    """test_convolution.cpp:236-245 (equal Gaussian grids, isotropic basis)."""
+    g = grid(GA, 10, 20)
+    op = S.DiscoOperator(g, g, S.isotropic_basis(3 * PI / 10))
+    mix = np.full((1, 1, 1), 0.7)
+    u = oracle.random_field((1, 10, 20), 21)
+    fwd = apply(op, u[None], mix)[0]
+    tra = transpose(op, u[None], mix)[0]
+    assert rel_l2(tra, fwd) <= TOL
+
+
+def test_disco_transpose_batch_and_rejects():
+    ik, ih, iw, ok, oh, ow, cut, cin, cout = CASES["ga16_ga8"]
+    op = S.DiscoOperator(grid(ik, ih, iw), grid(ok, oh, ow), S.morlet_basis(cut))
+    mix = oracle.random_field((cout, cin, 9), 77)
+    v = oracle.random_field((cout, oh, ow), 79)
+    y = transpose(op, np.stack([v, -3 * v]), mix)
+    assert rel_l2(y[1], -3 * y[0]) <= TOL
+    with pytest.raises(S.SphInvalidArgument):  # convolution.hpp:229-233
+        op.transpose_apply(torch.zeros((1, cout + 1, oh, ow), device=DEV),
+                           torch.zeros((cout, cin, 9), device=DEV))
+    with pytest.raises(S.SphInvalidArgument):
+        op.transpose_apply(torch.zeros((1, cout, oh, ow), device=DEV),
+                           torch.zeros((cout, cin, 5), device=DEV))
