@@ -467,7 +467,7 @@ def run_ours(args, ws, rank, local):
         t = max_over_ranks(t, ws)
         e2e = {"value": ws * F / t, "unit": UNIT, "h2d_bytes_per_step": F * NLAT * NLON * 4,
                "d2h_bytes_per_step": F * NLAT * NLON * 4, "ms_per_step": t * 1e3,
-               "api": "sph_sht_roundtrip_host (pinned host in/out, chunked H2D/compute/D2H)"}
+               "api": "sph_sht_roundtrip_host (pinned host in/out; H2D, compute and D2H streams over 3 chunk buffers)", "chunk_fields": args.chunk}
         del xh, yh
 
     cpu = None
@@ -496,7 +496,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="sht", choices=["sht", "disco", "disco_t", "dist_sht", "dist_disco"])
     ap.add_argument("--decomp", default="", help="dist_*: NHxNW polar x azimuth ranks (default WORLD_SIZE x 1)")
-    ap.add_argument("--chunk", type=int, default=64)
+    ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -169,44 +169,7 @@ int sph_sht_roundtrip_host(sph_sht_plan plan, const float* xh, int64_t F, float*
                            int64_t chunk) {
     return guarded([&] {
         sph::require(plan, "sht roundtrip: null plan");
-        sph::ShtPlan& p = plan->p;
-        SPH_CUDA(cudaSetDevice(p.device));
-        if (F <= 0) return;
-        if (chunk <= 0) chunk = 32;
-        chunk = std::min(chunk, F);
-        const int64_t np = p.nlat * p.nlon;
-        cudaStream_t st[2];
-        cudaEvent_t done[2];
-        for (int i = 0; i < 2; ++i) {
-            SPH_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
-            SPH_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
-        }
-        struct Bufs {
-            sph::DevBuf<float> x, y, c;
-            sph::DevBuf<uint8_t> ws;
-        } b[2];
-        for (int i = 0; i < 2; ++i) {
-            b[i].x.alloc(chunk * np, false);
-            b[i].y.alloc(chunk * np, false);
-            b[i].c.alloc(p.cint_elems(chunk), true);
-            b[i].ws.alloc(p.workspace_bytes(chunk), true);
-        }
-        int it = 0;
-        for (int64_t f0 = 0; f0 < F; f0 += chunk, ++it) {
-            const int s = it & 1;
-            const int64_t n = std::min(chunk, F - f0);
-            SPH_CUDA(cudaMemcpyAsync(b[s].x.p, xh + f0 * np, sizeof(float) * n * np,
-                                     cudaMemcpyHostToDevice, st[s]));
-            p.forward(b[s].x.p, n, b[s].c.p, SPH_LAYOUT_INTERNAL, b[s].ws.p, st[s]);
-            p.inverse(b[s].c.p, n, SPH_LAYOUT_INTERNAL, b[s].y.p, b[s].ws.p, st[s]);
-            SPH_CUDA(cudaMemcpyAsync(yh + f0 * np, b[s].y.p, sizeof(float) * n * np,
-                                     cudaMemcpyDeviceToHost, st[s]));
-        }
-        for (int i = 0; i < 2; ++i) {
-            SPH_CUDA(cudaStreamSynchronize(st[i]));
-            cudaEventDestroy(done[i]);
-            cudaStreamDestroy(st[i]);
-        }
+        plan->p.roundtrip_host(xh, F, yh, chunk);
     });
 }
 

@@ -66,6 +66,13 @@ struct ShtPlan {
     int64_t stage_ws_bytes(int64_t F, int64_t mcount) const {
         return 4 * (mcount * 2 * 2 * F * (int64_t)Rp + mcount * 2 * 2 * F * (int64_t)Lp) + 256;
     }
+    // host round trip: pinned host x -> (H2D | SHT+ISHT | D2H) pipeline -> host y
+    void roundtrip_host(const float* xh, int64_t F, float* yh, int64_t chunk);
+    struct HostPipe;
+    std::unique_ptr<HostPipe> pipe;  // cached streams / events / chunk buffers
+    std::mutex pipe_mu;
+    ShtPlan();
+    ~ShtPlan();
 };
 
 // C_int <-> reference dense [F][lmax][mmax] complex64 conversions
