@@ -265,13 +265,19 @@ struct FoldIO {
             }
             return;
         }
+        store_job(buf, P, n, ld, blockIdx.x, blockIdx.y);
+    }
+    // quad path for the job (quad qx, field group fy)
+    template <class PT, class NT>
+    __device__ __forceinline__ void store_job(const float2* buf, PT P, NT n, int ld, int qx, int fy) const {
+        const int64_t gstride = Rq * twoF * 4;
         const int FB = static_cast<int>(P) / 4, NR = 2 * FB;
         const int rr = threadIdx.x % NR;
         const int mstep = blockDim.x / NR;
         const int fl = rr >> 1, ri = rr & 1;
-        const int64_t row = 2 * static_cast<int64_t>(FB * blockIdx.y + fl) + ri;
+        const int64_t row = 2 * static_cast<int64_t>(FB * fy + fl) + ri;
         if (row >= twoF) return;
-        float* base = eo + (static_cast<int64_t>(blockIdx.x) * twoF + row) * 4;
+        float* base = eo + (static_cast<int64_t>(qx) * twoF + row) * 4;
         for (int m = threadIdx.x / NR; m < mmax; m += mstep) {
             float e[4], o[4];
 #pragma unroll
@@ -562,7 +568,10 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_kernel(IO io, const flo
 // FOLD_THREADS = 256 (8 ring slots = 4 ring pairs x 2 fields at N1 = 32, 2 CTAs / SM).
 // Measured at cfg2: 512 threads (16 slots, 128-byte E/O runs, 1 CTA / SM) 2.42 ms vs
 // 2.30 ms -- the store phase (~1.0 ms) is not run-length bound; the load / compute /
-// store phases of a CTA serialise (SPH_FFT_DEBUG: loads 0.69, +A+B 1.27 ms).
+// store phases of a CTA serialise (SPH_FFT_DEBUG: loads 0.69, +A+B 1.27 ms).  A
+// persistent 1-CTA/SM variant that bulk-copied the next job's rings into a staging
+// buffer during phase B / stores measured 2.50 ms (8 warps per SM for the compute
+// phases cost more than the overlap gained).
 constexpr int FOLD_THREADS = 256;
 template <int N1>
 __global__ void __launch_bounds__(FOLD_THREADS, 2) fft4_fold_kernel(FoldIO io, const float2* __restrict__ twT) {
