@@ -194,6 +194,19 @@ struct FoldIO {
         }
         return r < R && f < twoF / 2;
     }
+    // slot p's ring pair (a, b) for the fused direct-load kernel
+    template <class PT>
+    __device__ __forceinline__ bool rings(PT P, int n, int p, const float*& pa, const float*& pb,
+                                          float& sb) const {
+        int rr, f;
+        if (!slot(P, p, rr, f)) return false;
+        const float* xf = x + static_cast<int64_t>(f) * nlat * n;
+        const int2 rw = rows[rr];
+        pa = xf + static_cast<int64_t>(rw.x) * n;
+        pb = xf + static_cast<int64_t>(rw.y < 0 ? rw.x : rw.y) * n;
+        sb = rw.y < 0 ? 0.f : 1.f;
+        return true;
+    }
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -312,6 +325,25 @@ struct UnfoldIO {
     int64_t F, twoF;
     float* y;
     int64_t T;  // 32-row field tiles
+    template <int N1, int N2>
+    __device__ __forceinline__ void store_b(int P, int N, int p, int k1, const float2 (&b)[N2]) const {
+        const int64_t f = static_cast<int64_t>(blockIdx.x) * P + p;
+        if (dbg & 16) {
+            if (b[0].x == 12345.f) y[0] = b[N2 - 1].y;  // keep phase B live
+            return;
+        }
+        if (f >= F) return;
+        const int2 rw = rows[blockIdx.y];
+        float* yf = y + f * nlat * N;
+        float* pa = yf + static_cast<int64_t>(rw.x) * N + k1;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) pa[N1 * k2] = b[k2].x;
+        if (rw.y >= 0) {
+            float* pb = yf + static_cast<int64_t>(rw.y) * N + k1;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) pb[N1 * k2] = b[k2].y;
+        }
+    }
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int r = blockIdx.y;  // field tiles fastest: neighbouring CTAs read adjacent runs
@@ -420,27 +452,43 @@ struct PlainFwdIO {
 
 // plain inverse: half spectra [nrings][nbins] -> rings [nrings][n] * scale
 struct PlainInvIO {
+    static constexpr bool kRegStore = true;  // fft4_unfold_kernel (register stores)
     const float2* bins;
     int64_t nrings;
     int nbins;
     float scale;
     float* rings;
+    int dbg = 0;
+    template <int N1, int N2>
+    __device__ __forceinline__ void store_b(int P, int n, int p, int k1, const float2 (&b)[N2]) const {
+        const int64_t ra = 2 * (static_cast<int64_t>(blockIdx.x) * P + p), rb = ra + 1;
+        if (ra < nrings) {
+            float* d = rings + ra * n + k1;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) d[N1 * k2] = b[k2].x * scale;
+        }
+        if (rb < nrings) {
+            float* d = rings + rb * n + k1;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) d[N1 * k2] = b[k2].y * scale;
+        }
+    }
+    // each half-spectrum bin k <= n/2 is loaded once and written at k and n - k
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P;
-        const int half = n / 2;
-        for (int i = threadIdx.x; i < P * n; i += blockDim.x) {
-            const int j = i / n, k = i - j * n;
+        const int half = n / 2, nh = half + 1;
+        for (int i = threadIdx.x; i < P * nh; i += blockDim.x) {
+            const int j = i / nh, k = i - j * nh;
             const int64_t ra = 2 * (c0 + j), rb = ra + 1;
-            const int kk = k <= half ? k : n - k;
             float2 ha = make_float2(0.f, 0.f), hb = ha;
-            if (kk < nbins) {
-                if (ra < nrings) ha = bins[ra * nbins + kk];
-                if (rb < nrings) hb = bins[rb * nbins + kk];
+            if (k < nbins) {
+                if (ra < nrings) ha = bins[ra * nbins + k];
+                if (rb < nrings) hb = bins[rb * nbins + k];
             }
-            if (kk == 0 || 2 * kk == n) { ha.y = 0.f; hb.y = 0.f; }
-            if (k > half) { ha.y = -ha.y; hb.y = -hb.y; }
+            if (k == 0 || 2 * k == n) { ha.y = 0.f; hb.y = 0.f; }
             buf[j * ld + k] = make_float2(ha.x - hb.y, ha.y + hb.x);
+            if (k != 0 && 2 * k != n) buf[j * ld + n - k] = make_float2(ha.x + hb.y, hb.x - ha.y);
         }
     }
     template <class PT, class NT>
@@ -467,6 +515,19 @@ struct CminorIO {
     float2* U;
     int planar;
     int64_t ldp;  // planar row stride (floats, >= C)
+    int dbg = 0;
+    // slot p = channels (c0 + 2p, c0 + 2p + 1) of row hi, batch b (fused direct-load kernel)
+    template <class PT>
+    __device__ __forceinline__ bool rings(PT P, int n, int p, const float*& pa, const float*& pb,
+                                          float& sb) const {
+        const int64_t ca = static_cast<int64_t>(blockIdx.x) * 2 * P + 2 * p, cb = ca + 1;
+        const int64_t hi = blockIdx.y, b = blockIdx.z;
+        if (ca >= C) return false;
+        pa = x + ((b * C + ca) * H + hi) * n;
+        pb = cb < C ? x + ((b * C + cb) * H + hi) * n : pa;
+        sb = cb < C ? 1.f : 0.f;
+        return true;
+    }
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
@@ -508,29 +569,46 @@ struct CminorIO {
 // -> rings y[b][c][hi][0..n) * scale; block (c-tile of 2P channels, row hi, batch b), two
 // channels per complex ring (z = A + iB), Im of DC / Nyquist dropped (real synthesis)
 struct CminorInvIO {
+    static constexpr bool kRegStore = true;  // fft4_unfold_kernel (register stores)
     const float2* V;
     int64_t C, H;
     int nbins;
     float scale;
     float* y;
+    int dbg = 0;
+    template <int N1, int N2>
+    __device__ __forceinline__ void store_b(int P, int n, int p, int k1, const float2 (&b)[N2]) const {
+        const int64_t ca = static_cast<int64_t>(blockIdx.x) * 2 * P + 2 * p, cb = ca + 1;
+        const int64_t hi = blockIdx.y, bb = blockIdx.z;
+        if (ca < C) {
+            float* d = y + ((bb * C + ca) * H + hi) * n + k1;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) d[N1 * k2] = b[k2].x * scale;
+        }
+        if (cb < C) {
+            float* d = y + ((bb * C + cb) * H + hi) * n + k1;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) d[N1 * k2] = b[k2].y * scale;
+        }
+    }
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
         const int64_t hi = blockIdx.y, b = blockIdx.z;
         const float2* Vb = V + (b * H + hi) * static_cast<int64_t>(nbins) * C;
-        const int half = n / 2;
-        for (int i = threadIdx.x; i < P * n; i += blockDim.x) {
-            const int j = i / n, k = i - j * n;
+        const int half = n / 2, nh = half + 1;
+        // channel pairs fastest (coalesced channel-minor reads), each bin loaded once
+        for (int i = threadIdx.x; i < P * nh; i += blockDim.x) {
+            const int j = i % P, k = i / P;
             const int64_t ca = c0 + 2 * j, cb = ca + 1;
-            const int kk = k <= half ? k : n - k;
             float2 ha = make_float2(0.f, 0.f), hb = ha;
-            if (kk < nbins) {
-                if (ca < C) ha = Vb[static_cast<int64_t>(kk) * C + ca];
-                if (cb < C) hb = Vb[static_cast<int64_t>(kk) * C + cb];
+            if (k < nbins) {
+                if (ca < C) ha = Vb[static_cast<int64_t>(k) * C + ca];
+                if (cb < C) hb = Vb[static_cast<int64_t>(k) * C + cb];
             }
-            if (kk == 0 || 2 * kk == n) { ha.y = 0.f; hb.y = 0.f; }
-            if (k > half) { ha.y = -ha.y; hb.y = -hb.y; }
+            if (k == 0 || 2 * k == n) { ha.y = 0.f; hb.y = 0.f; }
             buf[j * ld + k] = make_float2(ha.x - hb.y, ha.y + hb.x);
+            if (k != 0 && 2 * k != n) buf[j * ld + n - k] = make_float2(ha.x + hb.y, hb.x - ha.y);
         }
     }
     template <class PT, class NT>
@@ -573,20 +651,20 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_kernel(IO io, const flo
 // buffer during phase B / stores measured 2.50 ms (8 warps per SM for the compute
 // phases cost more than the overlap gained).
 constexpr int FOLD_THREADS = 256;
-template <int N1>
-__global__ void __launch_bounds__(FOLD_THREADS, 2) fft4_fold_kernel(FoldIO io, const float2* __restrict__ twT) {
+// Generic over IO (FoldIO: ring pairs of the SHT; CminorIO: channel pairs of a DISCO
+// input row): IO::rings(P, n, p, pa, pb, sb) gives the two real rings of slot p.
+template <int N1, class IO>
+__global__ void __launch_bounds__(FOLD_THREADS, 2) fft4_fold_kernel(IO io, const float2* __restrict__ twT) {
     extern __shared__ float2 smf[];
     constexpr int N2 = 45, N = N1 * N2, P = FOLD_THREADS / N1, LD = N + 2;
     for (int it = threadIdx.x; it < P * N2; it += FOLD_THREADS) {
         const int p = it / N2, n2 = it - p * N2;
         float2 a[N1];
-        int rr, f;
-        if (io.slot(std::integral_constant<int, P>{}, p, rr, f)) {
-            const float* xf = io.x + static_cast<int64_t>(f) * io.nlat * N;
-            const int2 rw = io.rows[rr];
-            const float* pa = xf + static_cast<int64_t>(rw.x) * N + n2;
-            const float* pb = xf + static_cast<int64_t>(rw.y < 0 ? rw.x : rw.y) * N + n2;
-            const float sb = rw.y < 0 ? 0.f : 1.f;
+        const float *pa, *pb;
+        float sb;
+        if (io.rings(std::integral_constant<int, P>{}, N, p, pa, pb, sb)) {
+            pa += n2;
+            pb += n2;
 #pragma unroll
             for (int n1 = 0; n1 < N1; ++n1) a[n1] = make_float2(__ldg(pa + N2 * n1), sb * __ldg(pb + N2 * n1));
         } else {
@@ -620,8 +698,11 @@ __global__ void __launch_bounds__(FOLD_THREADS, 2) fft4_fold_kernel(FoldIO io, c
 // Inverse SHT ring transform, fused IO: phase B stores the synthesised ring samples
 // straight from registers to HBM (Re -> ring a, Im -> ring b; a warp writes 32
 // consecutive samples per store).
-template <int N1>
-__global__ void __launch_bounds__(fft4::THREADS, 2) fft4_unfold_kernel(UnfoldIO io, const float2* __restrict__ twT) {
+// Generic over IO (UnfoldIO, PlainInvIO, CminorInvIO): IO::load builds the spectra in
+// shared memory, IO::store_b(P, N1, p, k1, b) writes thread (p, k1)'s N2 outputs
+// X[k1 + N1 k2] of ring slot p straight from registers (coalesced over k1).
+template <int N1, class IO>
+__global__ void __launch_bounds__(fft4::THREADS, 2) fft4_unfold_kernel(IO io, const float2* __restrict__ twT) {
     extern __shared__ float2 smu[];
     constexpr int N2 = 45, N = N1 * N2, P = fft4::THREADS / N1, LD = N + 2;
     io.load(smu, std::integral_constant<int, P>{}, std::integral_constant<int, N>{}, LD);
@@ -639,23 +720,7 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_unfold_kernel(UnfoldIO 
     float2 b[N2];
     fft4::phase_b_regs<N1, N2, LD, true>(smu, b);
     const int p = threadIdx.x / N1, k1 = threadIdx.x - p * N1;
-    const int64_t f = static_cast<int64_t>(blockIdx.x) * P + p;
-    if (io.dbg & 16) {
-        if (b[0].x == 12345.f) io.y[0] = b[N2 - 1].y;  // keep phase B live
-        return;
-    }
-    if (f < io.F) {
-        const int2 rw = io.rows[blockIdx.y];
-        float* yf = io.y + f * io.nlat * N;
-        float* pa = yf + static_cast<int64_t>(rw.x) * N + k1;
-#pragma unroll
-        for (int k2 = 0; k2 < N2; ++k2) pa[N1 * k2] = b[k2].x;
-        if (rw.y >= 0) {
-            float* pb = yf + static_cast<int64_t>(rw.y) * N + k1;
-#pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) pb[N1 * k2] = b[k2].y;
-        }
-    }
+    io.template store_b<N1, N2>(P, N, p, k1, b);
 }
 
 template <bool INV, class IO>
@@ -710,9 +775,21 @@ void set_smem_once(K kernel, size_t bytes) {
                                       static_cast<int>(bytes)));
 }
 
+template <class T, class = void>
+struct has_regstore : std::false_type {};
+template <class T>
+struct has_regstore<T, std::void_t<decltype(T::kRegStore)>> : std::true_type {};
+
 template <int N1, bool INV, class IO>
 void launch4(const FftPlan& fp, const IO& io, dim3 grid, cudaStream_t st) {
     const size_t sm = static_cast<size_t>(fft4::THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
+    if constexpr (INV && has_regstore<IO>::value) {
+        // inverse transforms whose IO can store phase B's registers directly (one shared
+        // memory pass fewer than fft4_kernel)
+        set_smem_once(fft4_unfold_kernel<N1, IO>, sm);
+        fft4_unfold_kernel<N1, IO><<<grid, fft4::THREADS, sm, st>>>(io, fp.twT.p);
+        return;
+    }
     set_smem_once(fft4_kernel<N1, INV, IO>, sm);
     fft4_kernel<N1, INV, IO><<<grid, fft4::THREADS, sm, st>>>(io, fp.twT.p);
 }
@@ -724,11 +801,11 @@ void launch_fused(const FftPlan& fp, const FoldIO& fio, const UnfoldIO& uio, dim
         const size_t sm = static_cast<size_t>(fft4::THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
         if (FWD) {
             const size_t smf = static_cast<size_t>(FOLD_THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
-            set_smem_once(fft4_fold_kernel<N1>, smf);
-            fft4_fold_kernel<N1><<<grid, FOLD_THREADS, smf, st>>>(fio, fp.twT.p);
+            set_smem_once(fft4_fold_kernel<N1, FoldIO>, smf);
+            fft4_fold_kernel<N1, FoldIO><<<grid, FOLD_THREADS, smf, st>>>(fio, fp.twT.p);
         } else {
-            set_smem_once(fft4_unfold_kernel<N1>, sm);
-            fft4_unfold_kernel<N1><<<grid, fft4::THREADS, sm, st>>>(uio, fp.twT.p);
+            set_smem_once(fft4_unfold_kernel<N1, UnfoldIO>, sm);
+            fft4_unfold_kernel<N1, UnfoldIO><<<grid, fft4::THREADS, sm, st>>>(uio, fp.twT.p);
         }
     };
     switch (fp.fft4_n1) {
@@ -893,6 +970,26 @@ void fft_forward_cminor(const FftPlan& fp, const float* x, int64_t B, int64_t C,
     CminorIO io{x, C, H, nbins, U, planar ? 1 : 0, ldp > 0 ? ldp : C};
     dim3 grid(static_cast<unsigned>((C + 2 * P - 1) / (2 * P)), static_cast<unsigned>(H),
               static_cast<unsigned>(B));
+    if (fp.fft4_n1 && FOLD_THREADS == fft4::THREADS) {
+        // fused: phase A loads its strided ring samples straight from HBM into registers
+        // (the generic kernel staged the rings through shared memory first)
+        ProfScope prof("fft_fwd_cminor", st, 4.0 * B * C * H * (fp.n + 2.0 * nbins));
+        auto go = [&](auto n1c) {
+            constexpr int N1 = decltype(n1c)::value;
+            const size_t smf = static_cast<size_t>(FOLD_THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
+            set_smem_once(fft4_fold_kernel<N1, CminorIO>, smf);
+            fft4_fold_kernel<N1, CminorIO><<<grid, FOLD_THREADS, smf, st>>>(io, fp.twT.p);
+        };
+        switch (fp.fft4_n1) {
+            case 4: go(std::integral_constant<int, 4>{}); break;
+            case 8: go(std::integral_constant<int, 8>{}); break;
+            case 16: go(std::integral_constant<int, 16>{}); break;
+            default: go(std::integral_constant<int, 32>{}); break;
+        }
+        SPH_LAUNCH_CHECK();
+        count_launch();
+        return;
+    }
     run_transform<false>(fp, io, grid, st, "fft_fwd_cminor", 4.0 * B * C * H * (fp.n + 2.0 * nbins));
 }
 
