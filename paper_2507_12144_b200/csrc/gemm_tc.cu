@@ -156,6 +156,18 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
                  "r"(src), "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                                uint32_t bar, uint16_t mask) {
     asm volatile(
@@ -330,7 +342,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
                    int tma_store, int a_quad,  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B
-                   int d_mode, int d_t, int d_g2) {
+                   int d_mode, int d_t, int d_g2, int pf) {
     // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
     // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads
     // (a whole-tile cp.async.bulk.prefetch.L2 one tile ahead was measured slower: cfg2
@@ -418,6 +430,15 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         else
             tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
     };
+    // L2 prefetch of a data tile k-block (same box as load_a)
+    auto prefetch_a = [&](const GemmWork& w, int kb) {
+        if (ALO && a_quad == 2)
+            tma_prefetch_4d(&map_a, 0, (w.m0 + crank * BM) / 32, kb * (KB / 4), w.ag);
+        else if (ALO && a_quad)
+            tma_prefetch_4d(&map_a, 0, w.m0 + crank * BM, kb * (KB / 4), w.ag);
+        else
+            tma_prefetch_2d(&map_a, kb * KB, w.a_row + crank * BM);
+    };
     auto adesc = [&](int s, int kk) {  // A operand of k-step kk (8 fp32 of K)
         return (ALO && a_quad) ? make_sdesc_quad(a_hi(s) + kk * 2 * 2048) : make_sdesc<KB>(a_hi(s) + kk * 32);
     };
@@ -439,7 +460,19 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             for (int t = cid; t < ntiles; t += ncl) {
                 const GemmWork w = next_work(t);
                 const int nkb = (w.K + KB - 1) / KB;
+                const bool has_next = t + ncl < ntiles;
+                const GemmWork wn = wnext;  // next tile's descriptor (loaded a tile ahead)
+                const int nkb_n = (wn.K + KB - 1) / KB;
                 for (int kb = 0; kb < nkb; ++kb, ++j) {
+                    // data-tile L2 prefetch pf k-blocks ahead (HBM latency dominates the
+                    // ring's round trip; SMEM and TMEM allow no further stages)
+                    if (pf > 0) {
+                        const int kp = kb + pf;
+                        if (kp < nkb)
+                            prefetch_a(w, kp);
+                        else if (has_next && kp - nkb < nkb_n)
+                            prefetch_a(wn, kp - nkb);
+                    }
                     mbar_wait(empty_bar(s), ph ^ 1);
                     if (tr && j < TR_N) trace[j] = clock64();
                     if (dbg & 8) {
@@ -878,6 +911,10 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     cfg.numAttrs = CL > 1 ? 1 : 0;
     static const char* trace_dir = std::getenv("SPH_GEMM_TRACE");  // diagnostic only
     static const int dbg = std::getenv("SPH_GEMM_DEBUG") ? std::atoi(std::getenv("SPH_GEMM_DEBUG")) : 0;
+    static const int pf_env = std::getenv("SPH_GEMM_PF") ? std::atoi(std::getenv("SPH_GEMM_PF")) : -1;
+    // data-tile L2 prefetch distance: off by default (cfg2 Legendre fwd 2.46 ms at 0 vs
+    // 2.52 / 2.52 / 2.57 ms at 2 / 4 / 8 k-blocks ahead, profiles/gemm_pf.sh)
+    const int pf_dist = pf_env >= 0 ? pf_env : 0;
     long long* trace = nullptr;
     if (trace_dir) {
         SPH_CUDA(cudaMalloc(&trace, (4 * 512 + 4096) * sizeof(long long)));
@@ -887,7 +924,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
                                 static_cast<int>(tl.n), D,
                                 g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0,
                                 quad ? (g.a_rows_g % 32 == 0 ? 2 : 1) : 0, g.d_mode, static_cast<int>(g.d_t),
-                                static_cast<int>(g.d_g2)));
+                                static_cast<int>(g.d_g2), pf_dist));
     count_launch();
     if (trace) {
         std::vector<long long> h(4 * 512 + 4096);
