@@ -253,6 +253,11 @@ def workload_config(args):
                             f"batch 1, {nh}x{nw} (polar x azimuth) decomposition",
                 "decomposition": f"{nh}x{nw}", "channels": 512, "parallelism": f"lat/lon domain decomposition over {nh * nw} GPU(s), NCCL",
                 "precision": "fp32 I/O, 3xTF32 tcgen05 GEMMs"}
+    if args.workload == "block":
+        return {"workload": "configs[3]: one global block (SHT -> spectral channel mix -> ISHT -> GeLU/MLP "
+                            "epilogue) + one local block (DISCO 360x720 -> 360x720, Morlet K=9 -> MLP epilogue) "
+                            "at 360x720 Gaussian, 256 channels, MLP hidden 512, batch 1",
+                "batch": 1, "channels": 256, "mlp_hidden": 512, "precision": "fp32 I/O, 3xTF32 GEMMs"}
     if args.workload == "disco_t":
         return {"workload": "configs[2] adjoint: disco_transpose_apply 360x720 Gaussian -> 721x1440 eq, "
                             "Morlet K=9, cutoff 3pi/360, 256 -> 64 channels, batch 4 per GPU",
@@ -371,6 +376,27 @@ def run_ours(args, ws, rank, local):
             plan.forward(x, L.SPH_LAYOUT_INTERNAL, out=cint, ws=wsb)
             plan.inverse(cint, F, L.SPH_LAYOUT_INTERNAL, out=y, ws=wsb)
         units = F
+    elif args.workload == "block":
+        g = S.build_gaussian(360, 720)
+        C, H, B = 256, 512, 1
+        lat = S.SphericalField(g, torch.rand((B, C, 360, 720), device=dev) * 2 - 1)
+        cond = S.SphericalField(g, torch.empty((B, 0, 360, 720), device=dev))
+        sc = 1.0 / math.sqrt(C)
+
+        def wts(conv):
+            return S.BlockWeights(global_=conv.shape[2] != 9, conv=conv,
+                                  w1=(torch.rand((H, C), device=dev) * 2 - 1) * sc,
+                                  b1=torch.rand(H, device=dev) * 0.1,
+                                  w2=(torch.rand((C, H), device=dev) * 2 - 1) / math.sqrt(H),
+                                  b2=torch.rand(C, device=dev) * 0.1, scales=torch.full((C,), 0.1, device=dev))
+        bw_g = wts((torch.rand((C, C, 360), device=dev) * 2 - 1) * sc)
+        block_op = S.DiscoOperator(g, g, S.morlet_basis(3 * math.pi / 360))
+        bw_l = wts((torch.rand((C, C, block_op.n_basis), device=dev) * 2 - 1) * sc / 3)
+
+        def step():
+            S.block_apply(lat, cond, bw_g)
+            S.block_apply(lat, cond, bw_l, block_op)
+        units = B * C
     else:
         gi = S.build_equiangular(NLAT, NLON)
         go = S.build_gaussian(360, 720)
@@ -494,7 +520,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sht", choices=["sht", "disco", "disco_t", "dist_sht", "dist_disco"])
+    ap.add_argument("--workload", default="sht", choices=["sht", "disco", "disco_t", "block", "dist_sht", "dist_disco"])
     ap.add_argument("--decomp", default="", help="dist_*: NHxNW polar x azimuth ranks (default WORLD_SIZE x 1)")
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")

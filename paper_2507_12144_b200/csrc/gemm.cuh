@@ -102,8 +102,19 @@ struct GroupedGemm {
 // A.p of the prepared problem is ignored; the data operand is passed per call so a
 // cached problem can serve concurrent calls on different buffers.
 // Bhi/Blo override the prepared table pointers when non-null (per-call weights).
+// Fused epilogue applied to the accumulator before the store (column n = output
+// column, D element e): mode 1 (STORE_ROW): D = gelu_erfc(acc + bias[n]) -- the MLP's first
+// layer (model.hpp:361-362); mode 2 (STORE_TRANS): D = res[e] + scale[n] * (acc + bias[n])
+// -- the layer-scaled residual (model.hpp:363-368), res laid out like D.
+struct GemmEpi {
+    int mode = 0;
+    const float* bias = nullptr;
+    const float* scale = nullptr;
+    const float* res = nullptr;
+};
+
 void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStream_t stream,
-              const float* Bhi = nullptr, const float* Blo = nullptr);
+              const float* Bhi = nullptr, const float* Blo = nullptr, const GemmEpi* epi = nullptr);
 
 // Host helpers: split fp32 table values into tf32 hi (round-to-nearest) and lo.
 void tf32_split_host(const float* x, size_t n, float* hi, float* lo);

@@ -15,7 +15,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
                                                         const GemmTile* __restrict__ tiles,
                                                         float* __restrict__ D, int store,
                                                         int64_t a_rows_g, int64_t a_kq, int d_mode,
-                                                        int64_t d_t, int64_t d_g2, int64_t d_gsz) {
+                                                        int64_t d_t, int64_t d_g2, int64_t d_gsz,
+                                                        GemmEpi epi) {
     __shared__ float As[TK][TM + 4];
     __shared__ float Bs[TK][TN + 4];
     const GemmTile tl = tiles[blockIdx.x];
@@ -71,14 +72,22 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
             const int n = tl.n0 + tx * 4 + j;
             if (n >= g.N) continue;
             if (store == STORE_ROW) {
-                dbase[static_cast<int64_t>(m) * g.ldd + n] = acc[i][j];
+                float v = acc[i][j];
+                if (epi.mode == 1) {
+                    v += epi.bias[n];
+                    v = v * 0.5f * erfcf(-v * 0.70710678118654752440f);
+                }
+                dbase[static_cast<int64_t>(m) * g.ldd + n] = v;
                 if (n == g.N - 1)
                     for (int z = g.N; z < g.zero_to; ++z)
                         dbase[static_cast<int64_t>(m) * g.ldd + z] = 0.f;
             }
             else if (d_mode == 1)
                 D[((static_cast<int64_t>(n) * d_t + m / 32) * d_g2 + g.d_off / d_gsz) * 32 + (m & 31)] = acc[i][j];
-            else
+            else if (epi.mode == 2) {
+                const int64_t e = g.d_off + static_cast<int64_t>(n) * g.ldd + m;
+                D[e] = epi.res[e] + epi.scale[n] * (acc[i][j] + epi.bias[n]);
+            } else
                 dbase[static_cast<int64_t>(n) * g.ldd + m] = acc[i][j];
         }
     }
@@ -101,13 +110,13 @@ void build_simt_tiles(GroupedGemm& g) {
 }
 
 void gemm_run_simt(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
-                   float* D, cudaStream_t st) {
+                   float* D, cudaStream_t st, const GemmEpi& epi) {
     if (g.ntiles_simt == 0) return;
     ProfScope prof("gemm_simt", st, g.flops);
     gemm_simt_kernel<<<static_cast<unsigned>(g.ntiles_simt), 256, 0, st>>>(
         A, g.A.ld, Bhi, Blo, g.Bhi.ld, g.d_groups.p, g.d_tiles_simt.p, D, g.store,
         g.a_quad ? g.a_rows_g : 0, g.a_kq, g.d_mode, g.d_t, g.d_g2,
-        g.d_mode == 1 ? g.d_rows * g.d_ldd : 1);
+        g.d_mode == 1 ? g.d_rows * g.d_ldd : 1, epi);
     SPH_LAUNCH_CHECK();
     count_launch();
 }

@@ -33,8 +33,10 @@ constexpr int BK_ALO = 32;           // fp32 per 128-byte swizzle row (ALO varia
 template <bool ALO> constexpr int bk_of() { return ALO ? BK_ALO : BK; }
 // warps: 0 producer, 1 MMA, 2 TMEM allocator, 3 idle, 4..7 converter, 8.. epilogue
 // (4 warps, or 8 = two per TMEM lane quarter splitting the columns in the pair variant)
-template <bool PAIR> constexpr int epi_warps() { return PAIR ? 8 : 4; }
-template <bool PAIR> constexpr int nthreads() { return (8 + epi_warps<PAIR>()) * 32; }
+// 8 epilogue warps (two per TMEM lane quarter) except the single-CTA Legendre variant,
+// whose 3 x 64 KB ring leaves SMEM for only 4 warps' TMA-store staging
+template <bool ALO, bool PAIR> constexpr int epi_warps() { return (ALO && !PAIR) ? 4 : 8; }
+template <bool ALO, bool PAIR> constexpr int nthreads() { return (8 + epi_warps<ALO, PAIR>()) * 32; }
 
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -49,6 +51,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ float gelu_erfc_dev(float x) {  // model.hpp:42-44
+    return x * 0.5f * erfcf(-x * 0.70710678118654752440f);
 }
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
@@ -304,7 +309,8 @@ struct Smem {
     static constexpr int TILE_OFF = (BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1023) / 1024 * 1024;
     // epilogue staging: ALO -> two 4 KB TMA-store buffers per epilogue warp (also fits the
     // 32x33 transpose tiles of the plain-store fallback); else the transpose tiles
-    static constexpr int OUT_BYTES = ALO ? epi_warps<PAIR>() * 8192 : epi_warps<PAIR>() * 32 * 33 * 4;
+    // per-warp 32 x 32 transpose tiles (XOR-swizzled, no padding column)
+    static constexpr int OUT_BYTES = ALO ? epi_warps<ALO, PAIR>() * 8192 : epi_warps<ALO, PAIR>() * 32 * 32 * 4;
     static constexpr int TOTAL = TILE_OFF + OUT_BYTES + 1024;  // + align slack
 };
 
@@ -334,7 +340,7 @@ struct Smem {
 // barriers take the peer's converter / epilogue arrivals (count 256), and its commits
 // multicast to both CTAs' empty / tfull barriers.
 template <int BN, int STAGES, int CL, bool ALO, bool PAIR = false>
-__global__ void __launch_bounds__(nthreads<PAIR>(), 1)
+__global__ void __launch_bounds__(nthreads<ALO, PAIR>(), 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_bhi,
                    const __grid_constant__ CUtensorMap map_blo, const __grid_constant__ CUtensorMap map_d,
@@ -342,7 +348,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
                    int tma_store, int a_quad,  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B
-                   int d_mode, int d_t, int d_g2, int pf) {
+                   int d_mode, int d_t, int d_g2, int pf, GemmEpi epi) {
     // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
     // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads
     // (a whole-tile cp.async.bulk.prefetch.L2 one tile ahead was measured slower: cfg2
@@ -387,7 +393,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), (PAIR ? 2 : 1) * epi_warps<PAIR>() * 32);
+            mbar_init(tempty_bar(a), (PAIR ? 2 : 1) * epi_warps<ALO, PAIR>() * 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -641,10 +647,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         // warp (8 + i): TMEM lane quarter q = warp & 3 (rows 32q..32q+31), 32-column chunks
         // c = 32 * (i / 4) + 32 * EH * k; the next chunk's tcgen05.ld is in flight while
         // the current one is stored
-        constexpr int EH = epi_warps<PAIR>() / 4;
+        constexpr int EH = epi_warps<ALO, PAIR>() / 4;
         const int q = warp & 3;
         const int eh = (warp - 8) / 4;
-        float* tile = stile + (warp - 8) * 32 * 33;  // per-warp 32x32 transpose (STORE_ROW)
+        float* tile = stile + (warp - 8) * 32 * 32;  // per-warp 32x32 transpose (STORE_ROW),
+                                                     // element (r, col) at r * 32 + (col ^ r)
         // TMA-store path (ALO): ping-pong 4 KB staging buffers per warp; lane 0 issues the
         // 3D tensor store of each 32 x 32 chunk and recycles a buffer after wait_group.read
         const bool tstore = ALO && tma_store;
@@ -709,15 +716,26 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 } else if (store_mode == STORE_ROW) {
                     // transpose through padded SMEM: 32 coalesced 128-byte row segments
 #pragma unroll
-                    for (int jj = 0; jj < 32; ++jj)
-                        tile[lane * 33 + jj] = (c + jj < nrem) ? __uint_as_float(va[jj]) : 0.f;
+                    if (epi.mode == 1) {  // fused bias + GeLU (erfc form); bias loads batched first
+                        float bv[32];
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) bv[jj] = c + jj < nrem ? __ldg(epi.bias + w.n0 + c + jj) : 0.f;
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            tile[lane * 32 + (jj ^ lane)] =
+                                (c + jj < nrem) ? gelu_erfc_dev(__uint_as_float(va[jj]) + bv[jj]) : 0.f;
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            tile[lane * 32 + (jj ^ lane)] = (c + jj < nrem) ? __uint_as_float(va[jj]) : 0.f;
+                    }
                     __syncwarp();
                     const int col = w.n0 + c + lane;
                     const bool cok = c + lane < ncols;
 #pragma unroll 8
                     for (int r = 0; r < 32; ++r) {
                         const int mr = row0 + r;
-                        if (cok && mr < w.M) dbase[static_cast<int64_t>(mr) * w.ldd + col] = tile[r * 33 + lane];
+                        if (cok && mr < w.M) dbase[static_cast<int64_t>(mr) * w.ldd + col] = tile[r * 32 + (lane ^ r)];
                     }
                     __syncwarp();
                 } else {
@@ -728,6 +746,32 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj)
                             if (c + jj < nrem) dp[jj * nstride] = __uint_as_float(va[jj]);
+                    } else if (m < w.M && epi.mode == 2) {
+                        // fused layer-scaled residual: D = res + scale[n] * (acc + bias[n])
+                        // residual / scale / bias loads issued in groups of 8 before the
+                        // group's stores (the compiler cannot move loads of res past stores
+                        // to D, so one-at-a-time serialised ~32 HBM latencies per chunk)
+                        const int64_t e0 = w.d_off + static_cast<int64_t>(w.n0 + c) * w.ldd + m;
+#pragma unroll
+                        for (int g8 = 0; g8 < 32; g8 += 8) {
+                            float rv[8], sv[8], bv[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const int jj = g8 + u;
+                                const bool ok = c + jj < nrem;
+                                const int n = w.n0 + c + jj;
+                                rv[u] = ok ? __ldg(epi.res + e0 + static_cast<int64_t>(jj) * w.ldd) : 0.f;
+                                sv[u] = ok ? __ldg(epi.scale + n) : 0.f;
+                                bv[u] = ok ? __ldg(epi.bias + n) : 0.f;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const int jj = g8 + u;
+                                if (c + jj < nrem)
+                                    D[e0 + static_cast<int64_t>(jj) * w.ldd] =
+                                        rv[u] + sv[u] * (__uint_as_float(va[jj]) + bv[u]);
+                            }
+                        }
                     } else if (m < w.M) {
                         float* dp = dbase + static_cast<int64_t>(w.n0 + c) * w.ldd + m;
 #pragma unroll
@@ -806,7 +850,9 @@ static CUtensorMap make_map(const Mat2D& m, int box_rows, int kb) {
 
 template <int BN, int STAGES, int CL, bool ALO = false, bool PAIR = false>
 static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
-                   float* D, bool three, cudaStream_t st) {
+                   float* D, bool three, cudaStream_t st, GemmEpi epi) {
+    require(epi.mode == 0 || (!ALO && (epi.mode == 1) == (g.store == STORE_ROW)),
+            "gemm: fused epilogue mode does not match the store mode / variant");
     using L = Smem<BN, STAGES, ALO, PAIR>;
     auto kern = gemm_tf32x3_kernel<BN, STAGES, CL, ALO, PAIR>;
     static int grid = 0;
@@ -817,7 +863,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
         if (CL > 1) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(nthreads<PAIR>());
+            cfg.blockDim = dim3(nthreads<ALO, PAIR>());
             cfg.dynamicSmemBytes = L::TOTAL;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
@@ -899,7 +945,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     ProfScope prof(g.name, st, g.flops);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(gsz);
-    cfg.blockDim = dim3(nthreads<PAIR>());
+    cfg.blockDim = dim3(nthreads<ALO, PAIR>());
     cfg.dynamicSmemBytes = L::TOTAL;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -924,7 +970,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
                                 static_cast<int>(tl.n), D,
                                 g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0,
                                 quad ? (g.a_rows_g % 32 == 0 ? 2 : 1) : 0, g.d_mode, static_cast<int>(g.d_t),
-                                static_cast<int>(g.d_g2), pf_dist));
+                                static_cast<int>(g.d_g2), pf_dist, epi));
     count_launch();
     if (trace) {
         std::vector<long long> h(4 * 512 + 4096);
@@ -948,39 +994,40 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
 }  // namespace tc
 
 void gemm_run_simt(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
-                   float* D, cudaStream_t st);
+                   float* D, cudaStream_t st, const GemmEpi& epi);
 void build_simt_tiles(GroupedGemm& g);                                  // gemm_simt.cu
 
 void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStream_t st,
-              const float* Bhi, const float* Blo) {
+              const float* Bhi, const float* Blo, const GemmEpi* epip) {
+    const GemmEpi epi = epip ? *epip : GemmEpi{};
     if (g.ntiles == 0) return;
     if (!Bhi) Bhi = g.Bhi.p;
     if (!Blo) Blo = g.Blo.p;
     if (prec == SPH_PREC_FP32_SIMT) {
-        gemm_run_simt(g, A, Bhi, Blo, D, st);
+        gemm_run_simt(g, A, Bhi, Blo, D, st, epi);
         return;
     }
     const bool three = prec == SPH_PREC_3XTF32;
     require(!three || Blo, "gemm: 3xTF32 needs the lo table");
     const int cl = g.cluster;
     if (g.bn == 192 && g.pair)
-        tc::launch<192, 4, 2, true, true>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<192, 4, 2, true, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 192 && cl == 1)
-        tc::launch<192, 3, 1, true>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<192, 3, 1, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 192 && cl == 2)
-        tc::launch<192, 3, 2, true>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<192, 3, 2, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 192 && cl == 4)
-        tc::launch<192, 3, 4, true>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<192, 3, 4, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 256 && cl == 1)
-        tc::launch<256, 4, 1>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<256, 4, 1>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 256 && cl == 2)
-        tc::launch<256, 4, 2>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<256, 4, 2>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 256 && cl == 4)
-        tc::launch<256, 4, 4>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<256, 4, 4>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 128 && cl == 1)
-        tc::launch<128, 6, 1>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<128, 6, 1>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 128 && cl == 2)
-        tc::launch<128, 6, 2>(g, A, Bhi, Blo, D, three, st);
+        tc::launch<128, 6, 2>(g, A, Bhi, Blo, D, three, st, epi);
     else
         fail(SPH_ERR_INVALID_ARGUMENT, "gemm: unsupported N tile");
 }
