@@ -154,6 +154,20 @@ int sph_disco_apply_rows(sph_disco_plan plan, const float* x, int64_t h_in0, int
                          int64_t h_out0, int64_t n_out, const float* mix, int64_t B, int64_t c_in,
                          int64_t c_out, float* y, void* workspace, void* stream);
 
+/* ---- grid-to-grid resampling (resample.hpp:20-114) ------------------------------ */
+/* bilinear_resample with pole extension.  Grids are given by their colatitudes (host
+ * fp64, increasing, as GridSpec::colatitudes) and longitude counts (longitudes are
+ * 2*pi*j/nlon for every reference grid).  x [C][in_nlat][in_nlon] -> y [C][out_nlat][out_nlon]
+ * (C = batch x channels fields). */
+typedef struct sph_resample_plan_st* sph_resample_plan;
+int sph_resample_plan_create(const double* in_colat, int64_t in_nlat, int64_t in_nlon,
+                             const double* out_colat, int64_t out_nlat, int64_t out_nlon,
+                             sph_resample_plan* plan);
+int sph_resample_plan_destroy(sph_resample_plan plan);
+int64_t sph_resample_workspace_bytes(sph_resample_plan plan, int64_t C);
+int sph_bilinear_resample(sph_resample_plan plan, const float* x, int64_t C, float* y, void* workspace,
+                          void* stream);
+
 /* ---- spectral convolution + block epilogue ------------------------------------ */
 /* spectral_conv (convolution.hpp:286-304): Gaussian grids only (:287-288);
  * kernel [c_out][c_in][klmax]; x [B][c_in][nlat][nlon] -> y [B][c_out][nlat][nlon].

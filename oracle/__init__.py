@@ -213,6 +213,7 @@ class _Ref:
         L.ref_disco_apply.argtypes = [C.c_int, _sz, _sz, C.c_int, _sz, _sz, C.c_int, C.c_double,
                                       _sz, _sz, _dp, _dp, _dp]
         L.ref_disco_transpose_apply.argtypes = L.ref_disco_apply.argtypes
+        L.ref_bilinear_resample.argtypes = [C.c_int, _sz, _sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp]
         L.ref_spectral_conv.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _sz, _dp, _dp, _dp]
         L.ref_block_apply.argtypes = [_sz, _sz, _sz, _sz, _sz, C.c_int, C.c_double, _sz, _dp,
                                       _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
@@ -316,6 +317,15 @@ class _Ref:
         self._check(self.L.ref_disco_transpose_apply(in_kind, in_nlat, in_nlon, out_kind,
                                                      out_nlat, out_nlon, basis, cutoff, cin,
                                                      cout, _c64(x), mix, y))
+        return y
+
+    def bilinear_resample(self, in_kind, in_nlat, in_nlon, out_kind, out_nlat, out_nlon, x,
+                          in_last_pi=0):
+        x = _c64(x)
+        C = x.shape[0]
+        y = np.zeros((C, out_nlat, out_nlon))
+        self._check(self.L.ref_bilinear_resample(in_kind, in_nlat, in_nlon, in_last_pi, out_kind,
+                                                 out_nlat, out_nlon, C, x, y))
         return y
 
     def spectral_conv(self, kind, nlat, nlon, kernel, x):

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "sphere/convolution.hpp"
+#include "sphere/resample.hpp"
 #include "sphere/distsim.hpp"
 #include "sphere/grid.hpp"
 #include "sphere/harmonics.hpp"
@@ -226,6 +227,19 @@ int ref_disco_transpose_apply(int in_kind, size_t in_nlat, size_t in_nlon, int o
         assemble_disco(make_grid(in_kind, in_nlat, in_nlon), go, make_basis(basis, cutoff));
     const SphericalField out = disco_transpose_apply(op, make_field(go, cout, x),
                                                      make_mix(cout, cin, op.n_basis, mix));
+    std::memcpy(y, out.data.data(), sizeof(double) * out.data.size());
+    REF_CATCH
+}
+
+// resample.hpp:66-114 bilinear_resample (with the pole extension of :20-62);
+// in_last_pi = 1 sets the input grid's last colatitude to pi (test_resample.cpp:46-47)
+int ref_bilinear_resample(int in_kind, size_t in_nlat, size_t in_nlon, int in_last_pi, int out_kind,
+                          size_t out_nlat, size_t out_nlon, size_t C, const double* x, double* y) {
+    REF_TRY
+    GridSpec gi = make_grid(in_kind, in_nlat, in_nlon);
+    if (in_last_pi) gi.colatitudes.back() = pi;
+    const GridSpec go = make_grid(out_kind, out_nlat, out_nlon);
+    const SphericalField out = bilinear_resample(make_field(gi, C, x), go);
     std::memcpy(y, out.data.data(), sizeof(double) * out.data.size());
     REF_CATCH
 }

@@ -40,7 +40,8 @@ EXPORTS = [
     "sph_disco_plan_create", "sph_disco_plan_destroy", "sph_disco_plan_info",
     "sph_disco_workspace_bytes", "sph_disco_apply", "sph_disco_input_rows",
     "sph_disco_rows_workspace_bytes", "sph_disco_apply_rows", "sph_disco_transpose_workspace_bytes",
-    "sph_disco_transpose_apply",
+    "sph_disco_transpose_apply", "sph_resample_plan_create", "sph_resample_plan_destroy",
+    "sph_resample_workspace_bytes", "sph_bilinear_resample",
     "sph_spectral_conv", "sph_spectral_conv_workspace_bytes", "sph_block_epilogue",
 ]
 
@@ -95,6 +96,11 @@ def _load():
     L.sph_disco_transpose_workspace_bytes.argtypes = [vp, i64, i64, i64]
     L.sph_disco_transpose_workspace_bytes.restype = i64
     L.sph_disco_transpose_apply.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, vp]
+    L.sph_resample_plan_create.argtypes = [vp, i64, i64, vp, i64, i64, C.POINTER(vp)]
+    L.sph_resample_plan_destroy.argtypes = [vp]
+    L.sph_resample_workspace_bytes.argtypes = [vp, i64]
+    L.sph_resample_workspace_bytes.restype = i64
+    L.sph_bilinear_resample.argtypes = [vp, vp, i64, vp, vp, vp]
     L.sph_spectral_conv.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp, vp, vp]
     L.sph_spectral_conv_workspace_bytes.argtypes = [vp, i64, i64, i64]
     L.sph_spectral_conv_workspace_bytes.restype = i64

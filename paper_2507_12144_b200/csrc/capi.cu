@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "resample.cuh"
 #include "disco.cuh"
 #include "sht.cuh"
 
@@ -269,6 +270,41 @@ int sph_disco_apply_rows(sph_disco_plan plan, const float* x, int64_t h_in0, int
     return guarded([&] {
         sph::require(plan, "disco_apply: null plan");
         plan->p.apply_rows(x, h_in0, n_in, h_out0, n_out, mix, B, c_in, c_out, y, workspace, S(stream));
+    });
+}
+
+// ------------------------------------------------------------------ resample
+
+int sph_resample_plan_create(const double* in_colat, int64_t in_nlat, int64_t in_nlon,
+                             const double* out_colat, int64_t out_nlat, int64_t out_nlon,
+                             sph_resample_plan* plan) {
+    return guarded([&] {
+        sph::require(plan && in_colat && out_colat, "bilinear_resample: null argument");
+        *plan = nullptr;
+        sph::ResamplePlan* p = sph::resample_new();
+        try {
+            sph::resample_create(*p, in_colat, in_nlat, in_nlon, out_colat, out_nlat, out_nlon);
+        } catch (...) {
+            sph::resample_delete(p);
+            throw;
+        }
+        *plan = reinterpret_cast<sph_resample_plan>(p);
+    });
+}
+
+int sph_resample_plan_destroy(sph_resample_plan plan) {
+    return guarded([&] { sph::resample_delete(reinterpret_cast<sph::ResamplePlan*>(plan)); });
+}
+
+int64_t sph_resample_workspace_bytes(sph_resample_plan plan, int64_t C) {
+    return plan ? sph::resample_workspace_bytes(*reinterpret_cast<sph::ResamplePlan*>(plan), C) : -1;
+}
+
+int sph_bilinear_resample(sph_resample_plan plan, const float* x, int64_t C, float* y, void* workspace,
+                          void* stream) {
+    return guarded([&] {
+        sph::require(plan, "bilinear_resample: null plan");
+        sph::resample_apply(*reinterpret_cast<sph::ResamplePlan*>(plan), x, C, y, workspace, S(stream));
     });
 }
 

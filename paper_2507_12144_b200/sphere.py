@@ -29,7 +29,7 @@ import ctypes as C
 import math
 import threading
 from dataclasses import dataclass, field as dc_field
-from typing import Optional
+from typing import Dict, Optional
 
 import numpy as np
 import torch
@@ -439,6 +439,52 @@ def disco_transpose_apply(op: DiscoOperator, field: SphericalField, mix: torch.T
         y = op.transpose_apply(field.data, mix)
     return SphericalField(op.in_grid, y.reshape(*lead, mix.shape[1], op.in_grid.nlat,
                                                  op.in_grid.nlon))
+
+
+# ------------------------------------------------------------------ resample
+_RESAMPLE_PLANS: Dict[tuple, "ResamplePlan"] = {}
+
+
+class ResamplePlan:
+    """bilinear_resample tables (resample.hpp:66-114) for one (input grid, output grid)
+    pair: fp64 brackets / weights built once on the host, device gather per call."""
+
+    def __init__(self, in_grid: GridSpec, out_grid: GridSpec):
+        self.in_grid, self.out_grid = in_grid, out_grid
+        ci = np.ascontiguousarray(in_grid.colatitudes, dtype=np.float64)
+        co = np.ascontiguousarray(out_grid.colatitudes, dtype=np.float64)
+        h = C.c_void_p()
+        check(L.lib.sph_resample_plan_create(ci.ctypes.data, in_grid.nlat, in_grid.nlon, co.ctypes.data,
+                                             out_grid.nlat, out_grid.nlon, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and L.lib is not None:
+            L.lib.sph_resample_plan_destroy(self.h)
+
+    def apply(self, x: torch.Tensor, out=None) -> torch.Tensor:
+        x = _dev_f32(x, "bilinear_resample")
+        gi, go = self.in_grid, self.out_grid
+        if tuple(x.shape[-2:]) != (gi.nlat, gi.nlon):
+            raise L.SphInvalidArgument(1, "bilinear_resample: field sampling mismatch")
+        Cn = x.numel() // (gi.nlat * gi.nlon)
+        if out is None:
+            out = torch.empty(tuple(x.shape[:-2]) + (go.nlat, go.nlon), dtype=torch.float32, device=x.device)
+        ws = torch.empty(max(1, int(L.lib.sph_resample_workspace_bytes(self.h, Cn))), dtype=torch.uint8,
+                         device=x.device)
+        with torch.cuda.device(x.device):
+            check(L.lib.sph_bilinear_resample(self.h, _ptr(x), Cn, _ptr(out), _ptr(ws), _stream(x.device)))
+        return out
+
+
+def bilinear_resample(field: SphericalField, out_grid: GridSpec) -> SphericalField:
+    """resample.hpp:66-114: four-weight bilinear interpolation with pole extension."""
+    key = (field.grid.kind, field.grid.nlat, field.grid.nlon, tuple(np.asarray(field.grid.colatitudes)[[0, -1]]),
+           out_grid.kind, out_grid.nlat, out_grid.nlon)
+    plan = _RESAMPLE_PLANS.get(key)
+    if plan is None:
+        plan = _RESAMPLE_PLANS[key] = ResamplePlan(field.grid, out_grid)
+    return SphericalField(out_grid, plan.apply(field.data))
 
 
 # ----------------------------------------------------------- spectral conv

@@ -128,6 +128,21 @@ def main():
         G[f"dist_disco_{nh}x{nw}"] = y
         G[f"dist_disco_{nh}x{nw}_csv"] = np.array(csv)
 
+    # bilinear_resample with pole extension (resample.hpp:20-114; test_resample.cpp:12-123)
+    rcases = {
+        "ga8_eq13": (GA, 8, 16, 0, EQ, 13, 20),     # constants / range case
+        "eq9_ga7": (EQ, 9, 12, 0, GA, 7, 9),        # four-weight formula case
+        "eq4_eq4x6": (EQ, 4, 4, 0, EQ, 4, 6),       # longitude wrap-around
+        "ga8_id": (GA, 8, 16, 0, GA, 8, 16),        # identity
+        "eq9_id": (EQ, 9, 16, 0, EQ, 9, 16),
+        "p2p4": (EQ, 4, 4, 1, EQ, 5, 8),            # input already touching both poles
+        "eq91_ga45": (EQ, 91, 180, 0, GA, 45, 90),
+        "ga45_eq91": (GA, 45, 90, 0, EQ, 91, 180),  # decoder direction (Gaussian -> eq)
+    }
+    for name, (ik, ih, iw, lp, ok, oh, ow) in rcases.items():
+        x = r.random_uniform((2, ih, iw), 40)
+        G[f"resample_{name}"] = r.bilinear_resample(ik, ih, iw, ok, oh, ow, x, in_last_pi=lp)
+
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(out, **G)
     print("wrote", out, os.path.getsize(out), "bytes,", len(G), "arrays")
