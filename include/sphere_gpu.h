@@ -168,6 +168,17 @@ int64_t sph_resample_workspace_bytes(sph_resample_plan plan, int64_t C);
 int sph_bilinear_resample(sph_resample_plan plan, const float* x, int64_t C, float* y, void* workspace,
                           void* stream);
 
+/* ---- SHT consumers (metrics.hpp:300-314, loss.hpp:37-81) ---------------------------- */
+/* Reductions over sph_sht_forward's dense output [F][lmax][mmax] complex64:
+ * angular PSD psd[f][l] = |c(l,0)|^2 + 2 sum_{m=1..min(l,mmax-1)} |c(l,m)|^2, and the
+ * spectral CRPS loss out[c] = sum_{1<=l<=lmax_sum, m<=min(l,mmax-1)} (m ? 2 : 1) *
+ * (CRPS(Re) + CRPS(Im)) over E ensemble members (ens [E][C][lmax][mmax], obs [C][lmax][mmax];
+ * variant 0 cdf, 1 spread_skill, 2 fair; out is fp64 [C]). */
+int sph_psd_from_coeffs(const float* coeffs, int64_t F, int64_t lmax, int64_t mmax, float* psd,
+                        void* stream);
+int sph_spectral_crps_from_coeffs(const float* ens, const float* obs, int64_t E, int64_t C, int64_t lmax,
+                                  int64_t mmax, int64_t lmax_sum, int variant, double* out, void* stream);
+
 /* ---- spectral convolution + block epilogue ------------------------------------ */
 /* spectral_conv (convolution.hpp:286-304): Gaussian grids only (:287-288);
  * kernel [c_out][c_in][klmax]; x [B][c_in][nlat][nlon] -> y [B][c_out][nlat][nlon].

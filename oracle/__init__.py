@@ -214,6 +214,8 @@ class _Ref:
                                       _sz, _sz, _dp, _dp, _dp]
         L.ref_disco_transpose_apply.argtypes = L.ref_disco_apply.argtypes
         L.ref_bilinear_resample.argtypes = [C.c_int, _sz, _sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp]
+        L.ref_angular_psd.argtypes = [C.c_int, _sz, _sz, _sz, _dp, _dp]
+        L.ref_spectral_crps_loss.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _dp, _dp, _sz, C.c_int, _dp]
         L.ref_spectral_conv.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _sz, _dp, _dp, _dp]
         L.ref_block_apply.argtypes = [_sz, _sz, _sz, _sz, _sz, C.c_int, C.c_double, _sz, _dp,
                                       _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
@@ -327,6 +329,19 @@ class _Ref:
         self._check(self.L.ref_bilinear_resample(in_kind, in_nlat, in_nlon, in_last_pi, out_kind,
                                                  out_nlat, out_nlon, C, x, y))
         return y
+
+    def angular_psd(self, kind, nlat, nlon, x):
+        x = _c64(x)
+        out = np.zeros((x.shape[0], nlat))
+        self._check(self.L.ref_angular_psd(kind, nlat, nlon, x.shape[0], x, out))
+        return out
+
+    def spectral_crps_loss(self, kind, nlat, nlon, ens, obs, lmax_sum, variant):
+        ens, obs = _c64(ens), _c64(obs)
+        E, Cc = ens.shape[:2]
+        out = np.zeros(Cc)
+        self._check(self.L.ref_spectral_crps_loss(kind, nlat, nlon, E, Cc, ens, obs, lmax_sum, variant, out))
+        return out
 
     def spectral_conv(self, kind, nlat, nlon, kernel, x):
         kernel = _c64(kernel)

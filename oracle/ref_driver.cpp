@@ -23,6 +23,8 @@
 
 #include "sphere/convolution.hpp"
 #include "sphere/resample.hpp"
+#include "sphere/loss.hpp"
+#include "sphere/metrics.hpp"
 #include "sphere/distsim.hpp"
 #include "sphere/grid.hpp"
 #include "sphere/harmonics.hpp"
@@ -241,6 +243,28 @@ int ref_bilinear_resample(int in_kind, size_t in_nlat, size_t in_nlon, int in_la
     const GridSpec go = make_grid(out_kind, out_nlat, out_nlon);
     const SphericalField out = bilinear_resample(make_field(gi, C, x), go);
     std::memcpy(y, out.data.data(), sizeof(double) * out.data.size());
+    REF_CATCH
+}
+
+// metrics.hpp:300-314 angular_psd -> psd [C][nlat]
+int ref_angular_psd(int kind, size_t nlat, size_t nlon, size_t C, const double* x, double* psd) {
+    REF_TRY
+    const GridSpec g = make_grid(kind, nlat, nlon);
+    const auto out = angular_psd(make_field(g, C, x));
+    for (size_t c = 0; c < C; ++c) std::memcpy(psd + c * nlat, out[c].data(), sizeof(double) * nlat);
+    REF_CATCH
+}
+
+// loss.hpp:37-81 spectral_crps_loss; ens [E][C][H][W], obs [C][H][W]; variant 0 cdf,
+// 1 spread_skill, 2 fair -> out [C]
+int ref_spectral_crps_loss(int kind, size_t nlat, size_t nlon, size_t E, size_t C, const double* ens,
+                           const double* obs, size_t lmax_sum, int variant, double* out) {
+    REF_TRY
+    const GridSpec g = make_grid(kind, nlat, nlon);
+    EnsembleField ef(g, E, C);
+    std::memcpy(ef.values.data(), ens, sizeof(double) * ef.values.size());
+    const auto r = spectral_crps_loss(ef, make_field(g, C, obs), lmax_sum, static_cast<CrpsVariant>(variant));
+    std::memcpy(out, r.data(), sizeof(double) * C);
     REF_CATCH
 }
 

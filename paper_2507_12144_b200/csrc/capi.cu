@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "metrics.cuh"
 #include "resample.cuh"
 #include "disco.cuh"
 #include "sht.cuh"
@@ -305,6 +306,17 @@ int sph_bilinear_resample(sph_resample_plan plan, const float* x, int64_t C, flo
     return guarded([&] {
         sph::require(plan, "bilinear_resample: null plan");
         sph::resample_apply(*reinterpret_cast<sph::ResamplePlan*>(plan), x, C, y, workspace, S(stream));
+    });
+}
+
+int sph_psd_from_coeffs(const float* coeffs, int64_t F, int64_t lmax, int64_t mmax, float* psd, void* stream) {
+    return guarded([&] { sph::psd_from_coeffs(coeffs, F, lmax, mmax, psd, S(stream)); });
+}
+
+int sph_spectral_crps_from_coeffs(const float* ens, const float* obs, int64_t E, int64_t C, int64_t lmax,
+                                  int64_t mmax, int64_t lmax_sum, int variant, double* out, void* stream) {
+    return guarded([&] {
+        sph::spectral_crps_from_coeffs(ens, obs, E, C, lmax, mmax, lmax_sum, variant, out, S(stream));
     });
 }
 

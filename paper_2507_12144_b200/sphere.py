@@ -487,6 +487,57 @@ def bilinear_resample(field: SphericalField, out_grid: GridSpec) -> SphericalFie
     return SphericalField(out_grid, plan.apply(field.data))
 
 
+# ------------------------------------------------------------ SHT consumers
+CRPS_VARIANTS = {"cdf": 0, "spread_skill": 1, "fair": 2}
+
+
+def angular_psd(field: SphericalField, precision: str = "3xtf32") -> torch.Tensor:
+    """metrics.hpp:300-314: PSD(l) = sum_{|m|<=l} |uhat_l^m|^2 per channel, lmax = nlat
+    (Gaussian grids only, through sht_forward like the reference).  Returns [..., C, nlat]."""
+    g = field.grid
+    if g.kind != GAUSSIAN:
+        raise L.SphInvalidArgument(1, "sht_forward: requires a gaussian grid")
+    lmax = g.nlat
+    mmax = max(min(default_mmax(lmax, g.nlon), g.nlon // 2), 1)
+    plan = get_sht_plan(g, lmax, mmax, precision)
+    x = _dev_f32(field.data, "angular_psd")
+    F = x.numel() // (g.nlat * g.nlon)
+    with torch.cuda.device(x.device):
+        c = plan.forward(x, L.SPH_LAYOUT_DENSE_LM)
+        psd = torch.empty((F, lmax), dtype=torch.float32, device=x.device)
+        check(L.lib.sph_psd_from_coeffs(_ptr(c), F, lmax, mmax, _ptr(psd), _stream(x.device)))
+    return psd.reshape(tuple(x.shape[:-2]) + (lmax,))
+
+
+def spectral_crps_loss(ens: torch.Tensor, obs: SphericalField, lmax_sum: int = 0,
+                       variant: str = "spread_skill", precision: str = "3xtf32") -> torch.Tensor:
+    """loss.hpp:37-81: ens [E][C][H][W] members on obs.grid (Gaussian), obs [C][H][W];
+    sum over 1 <= l <= lmax_sum and stored orders of the CRPS of Re and Im, per channel
+    (fp64 [C])."""
+    g = obs.grid
+    if g.kind != GAUSSIAN:
+        raise L.SphInvalidArgument(1, "spectral_crps_loss: requires a gaussian grid")
+    E, Cc = ens.shape[0], ens.shape[1]
+    if tuple(ens.shape[2:]) != (g.nlat, g.nlon) or obs.channels != Cc:
+        raise L.SphInvalidArgument(1, "spectral_crps_loss: shape mismatch")
+    if lmax_sum == 0:
+        lmax_sum = g.nlat // 2
+    if lmax_sum + 1 > g.nlat:
+        raise L.SphInvalidArgument(1, "spectral_crps_loss: lmax_sum exceeds grid capacity")
+    lmax = lmax_sum + 1
+    mmax = min(lmax, g.nlon // 2)
+    plan = get_sht_plan(g, lmax, mmax, precision)
+    ens = _dev_f32(ens, "spectral_crps_loss")
+    o = _dev_f32(obs.data, "spectral_crps_loss")
+    with torch.cuda.device(ens.device):
+        ce = plan.forward(ens.reshape(E * Cc, g.nlat, g.nlon), L.SPH_LAYOUT_DENSE_LM)
+        co = plan.forward(o.reshape(Cc, g.nlat, g.nlon), L.SPH_LAYOUT_DENSE_LM)
+        out = torch.empty(Cc, dtype=torch.float64, device=ens.device)
+        check(L.lib.sph_spectral_crps_from_coeffs(_ptr(ce), _ptr(co), E, Cc, lmax, mmax, lmax_sum,
+                                                  CRPS_VARIANTS[variant], _ptr(out), _stream(ens.device)))
+    return out
+
+
 # ----------------------------------------------------------- spectral conv
 def spectral_conv(field: SphericalField, kernel: torch.Tensor,
                   precision: str = "3xtf32") -> SphericalField:

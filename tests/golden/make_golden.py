@@ -143,6 +143,19 @@ def main():
         x = r.random_uniform((2, ih, iw), 40)
         G[f"resample_{name}"] = r.bilinear_resample(ik, ih, iw, ok, oh, ow, x, in_last_pi=lp)
 
+    # SHT consumers (metrics.hpp:300-314 angular_psd, loss.hpp:37-81 spectral_crps_loss)
+    x = r.random_uniform((3, 16, 32), 60)
+    G["psd_ga16"] = r.angular_psd(GA, 16, 32, x)
+    x = r.random_uniform((2, 45, 90), 61)
+    G["psd_ga45"] = r.angular_psd(GA, 45, 90, x)
+    ens = r.random_uniform((5, 2, 16, 32), 62)
+    obs = r.random_uniform((2, 16, 32), 63)
+    for v in range(3):
+        G[f"scrps_ga16_v{v}"] = r.spectral_crps_loss(GA, 16, 32, ens, obs, 0, v)
+    ens = r.random_uniform((8, 3, 45, 90), 64)
+    obs = r.random_uniform((3, 45, 90), 65)
+    G["scrps_ga45_v2_l20"] = r.spectral_crps_loss(GA, 45, 90, ens, obs, 20, 2)
+
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(out, **G)
     print("wrote", out, os.path.getsize(out), "bytes,", len(G), "arrays")
