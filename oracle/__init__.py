@@ -215,6 +215,7 @@ class _Ref:
         L.ref_disco_transpose_apply.argtypes = L.ref_disco_apply.argtypes
         L.ref_bilinear_resample.argtypes = [C.c_int, _sz, _sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp]
         L.ref_angular_psd.argtypes = [C.c_int, _sz, _sz, _sz, _dp, _dp]
+        L.ref_noise_stream.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _dp, C.c_uint64, _sz, _dp, _dp]
         L.ref_spectral_crps_loss.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _dp, _dp, _sz, C.c_int, _dp]
         L.ref_spectral_conv.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _sz, _dp, _dp, _dp]
         L.ref_block_apply.argtypes = [_sz, _sz, _sz, _sz, _sz, C.c_int, C.c_double, _sz, _dp,
@@ -342,6 +343,14 @@ class _Ref:
         out = np.zeros(Cc)
         self._check(self.L.ref_spectral_crps_loss(kind, nlat, nlon, E, Cc, ens, obs, lmax_sum, variant, out))
         return out
+
+    def noise_stream(self, kind, nlat, nlon, lmax, kts, seed, steps):
+        kts = _c64(kts)
+        Cc = kts.shape[0]
+        field = np.zeros((Cc, nlat, nlon))
+        coeffs = np.zeros((Cc, lmax, lmax, 2))
+        self._check(self.L.ref_noise_stream(kind, nlat, nlon, lmax, Cc, kts, seed, steps, field, coeffs))
+        return field, coeffs
 
     def spectral_conv(self, kind, nlat, nlon, kernel, x):
         kernel = _c64(kernel)

@@ -23,6 +23,7 @@
 
 #include "sphere/convolution.hpp"
 #include "sphere/resample.hpp"
+#include "sphere/noise.hpp"
 #include "sphere/loss.hpp"
 #include "sphere/metrics.hpp"
 #include "sphere/distsim.hpp"
@@ -265,6 +266,33 @@ int ref_spectral_crps_loss(int kind, size_t nlat, size_t nlon, size_t E, size_t 
     std::memcpy(ef.values.data(), ens, sizeof(double) * ef.values.size());
     const auto r = spectral_crps_loss(ef, make_field(g, C, obs), lmax_sum, static_cast<CrpsVariant>(variant));
     std::memcpy(out, r.data(), sizeof(double) * C);
+    REF_CATCH
+}
+
+// noise.hpp:95-97 + :113-140: `steps` steps of a NoiseStream (lambda = sigma = 1, the
+// given k_T per channel) -> the final synthesized field [C][H][W] and the channels'
+// spectral states [C][lmax][lmax] complex (interleaved re/im)
+int ref_noise_stream(int kind, size_t nlat, size_t nlon, size_t lmax, size_t C, const double* kts,
+                     uint64_t seed, size_t steps, double* field, double* coeffs) {
+    REF_TRY
+    const GridSpec g = make_grid(kind, nlat, nlon);
+    std::vector<DiffusionParams> ps;
+    for (size_t c = 0; c < C; ++c) ps.push_back(diffusion_params(1.0, 1.0, kts[c], lmax));
+    Rng rng(seed);
+    std::vector<NoiseState> st;
+    for (auto& p : ps) st.push_back(make_noise_state(p));
+    for (size_t s = 0; s < steps; ++s)
+        for (size_t c = 0; c < C; ++c) st[c] = diffusion_step(st[c], ps[c], rng);
+    for (size_t c = 0; c < C; ++c) {
+        const SphericalField f = noise_field(st[c], g);
+        std::memcpy(field + c * f.npoints(), f.data.data(), sizeof(double) * f.npoints());
+        for (size_t l = 0; l < lmax; ++l)
+            for (size_t m = 0; m < lmax; ++m) {
+                const std::complex<double> v = st[c].coeffs.at(0, l, m);
+                coeffs[((c * lmax + l) * lmax + m) * 2] = v.real();
+                coeffs[((c * lmax + l) * lmax + m) * 2 + 1] = v.imag();
+            }
+    }
     REF_CATCH
 }
 

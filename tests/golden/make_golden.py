@@ -156,6 +156,13 @@ def main():
     obs = r.random_uniform((3, 45, 90), 65)
     G["scrps_ga45_v2_l20"] = r.spectral_crps_loss(GA, 45, 90, ens, obs, 20, 2)
 
+    # noise_field synthesis (noise.hpp:95-97) of the reference's own AR(1) noise states
+    kts = np.array([3.08e-5, 1.97e-3, 1.26e-1])
+    f, c = r.noise_stream(GA, 24, 48, 24, kts, 1234, 3)
+    G["noise_ga24_field"], G["noise_ga24_coeffs"] = f, c
+    f, c = r.noise_stream(EQ, 33, 64, 32, kts, 99, 2)
+    G["noise_eq33_field"], G["noise_eq33_coeffs"] = f, c
+
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(out, **G)
     print("wrote", out, os.path.getsize(out), "bytes,", len(G), "arrays")

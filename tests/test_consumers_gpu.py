@@ -52,3 +52,15 @@ def test_spectral_crps_larger_lmax_sum(golden):
     got = S.spectral_crps_loss(torch.tensor(ens, dtype=torch.float32, device=DEV), field(obs, 45, 90),
                                20, "fair").cpu().numpy()
     assert rel_l2(got, golden["scrps_ga45_v2_l20"]) <= TOL
+
+
+@pytest.mark.parametrize("name,kind,nlat,nlon,lmax", [("ga24", 1, 24, 48, 24), ("eq33", 0, 33, 64, 32)])
+def test_noise_field_synthesis(golden, name, kind, nlat, nlon, lmax):
+    """noise.hpp:95-97: noise_field(state) = sht_inverse(state.coeffs); the GPU synthesizes
+    the reference's own AR(1) noise states (3 channels) in one batched inverse SHT."""
+    g = S.build_equiangular(nlat, nlon) if kind == 0 else S.build_gaussian(nlat, nlon)
+    c = golden[f"noise_{name}_coeffs"]  # [C][lmax][lmax][2]
+    p = S.ShtPlan(g, lmax, lmax, "3xtf32", allow_equiangular_forward=True)
+    y = p.inverse(torch.tensor(c, dtype=torch.float32, device=DEV), c.shape[0])
+    torch.cuda.synchronize()
+    assert rel_l2(y.cpu().numpy().astype(np.float64), golden[f"noise_{name}_field"]) <= TOL
