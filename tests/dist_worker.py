@@ -124,6 +124,15 @@ def main():
     if key + "_csv" in G.files:
         rep["ref_sht_csv"] = str(G[key + "_csv"])
 
+    # ---- fused order pipelined over 3 channel chunks (GPU backend only)
+    if cuda:
+        x = torch.tensor(oracle.random_field((7, 16, 32), 36), dtype=dt, device=dev)
+        out = D.dist_sht_forward(ctx, D.shard_field(ctx, x), grid, 16, 16, backend, chunks=3)
+        glob = D.unshard(ctx, out).cpu().numpy()
+        got = glob[..., 0] + 1j * glob[..., 1]
+        want = oracle.orc().sht_forward(1, 16, 32, 16, 16, x.cpu().numpy())
+        rep["sht_chunked_err"] = float(np.abs(got - want).max() / np.abs(want).max())
+
     # ---- equiangular 91x180 (cfg1 grid) dist SHT vs the oracle (reference equiangular path)
     if cuda:
         grid = S.build_equiangular(91, 180)

@@ -72,3 +72,4 @@ def test_dist_nccl_gpu(tmp_path):
         assert rep["sht_eq_rel"] <= 1e-5, rep
         assert rep["disco_err"] <= 1e-5, rep
         assert rep["sht_a2a_calls"] == 4
+        assert rep["sht_chunked_err"] <= 1e-5, rep
