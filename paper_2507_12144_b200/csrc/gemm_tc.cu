@@ -357,6 +357,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     // [0] producer issue, [1] data landed (converter wake), [2] converted, [3] MMA issue,
     // and per tile [4*TR_N + 2*lt] MMA start clock, [.. + 1] ninst * 1000 + k-blocks
     constexpr int TR_N = 512;
+    const int tr_off = dbg >> 8;  // k-block window start (SPH_GEMM_DEBUG high bits)
     const bool tr = trace != nullptr && blockIdx.x == 0;
     using L = Smem<BN, STAGES, ALO, PAIR>;
     static_assert(!PAIR || (ALO && CL == 2 && BN % 32 == 0), "pair mode: ALO, cluster of 2");
@@ -388,12 +389,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(conv_bar(s), PAIR ? 256 : 128);  // converter warps 4..7 (x2 CTAs)
+            // PAIR: one aggregated arrival per CTA (named barrier + elected thread; 128
+            // individual remote arrivals per stage cost ~2k cycles on the critical path)
+            mbar_init(conv_bar(s), PAIR ? 2 : 128);
             mbar_init(empty_bar(s), PAIR ? 1 : CL);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), (PAIR ? 2 : 1) * epi_warps<ALO, PAIR>() * 32);
+            mbar_init(tempty_bar(a), PAIR ? 2 : epi_warps<ALO, PAIR>() * 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -480,7 +483,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                             prefetch_a(wn, kp - nkb);
                     }
                     mbar_wait(empty_bar(s), ph ^ 1);
-                    if (tr && j < TR_N) trace[j] = clock64();
+                    if (tr && j >= tr_off && j - tr_off < TR_N) trace[j - tr_off] = clock64();
                     if (dbg & 8) {
                         mbar_expect_tx(full_bar(s), A_TILE_BYTES);
                         load_a(s, w, kb);
@@ -540,7 +543,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 for (int kb = 0; kb < nkb; ++kb, ++j) {
                     mbar_wait(conv_bar(s), ph);  // converter waited full(s): data landed + A_lo
                     tc_fence_after();
-                    if (tr && j < TR_N) trace[3 * TR_N + j] = clock64();
+                    if (tr && j >= tr_off && j - tr_off < TR_N) trace[3 * TR_N + j - tr_off] = clock64();
                     const int ksteps = (dbg & 4) ? 0 : min(KB / 8, (w.K - kb * KB + 7) / 8);
                     for (int kk = 0; kk < ksteps; ++kk) {
                         const uint64_t ahi = adesc(s, kk);
@@ -587,7 +590,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             const int nkb = (w.K + KB - 1) / KB;
             for (int kb = 0; kb < nkb; ++kb, ++j) {
                 mbar_wait(full_bar(s), ph);
-                if (trc && j < TR_N) trace[TR_N + j] = clock64();
+                if (trc && j >= tr_off && j - tr_off < TR_N) trace[TR_N + j - tr_off] = clock64();
                 if constexpr (ALO) {
                     if (three_pass && !(dbg & 2)) {
                         // this warp owns TMEM lanes 32q..32q+31 = tile rows; read the row's
@@ -634,11 +637,18 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
-                if (PAIR)
-                    mbar_arrive_cta(conv_bar(s), 0);  // the leader's MMA waits both CTAs
-                else
+                if (PAIR) {
+                    // all 4 converter warps done (their tcgen05.st fenced) -> one arrival on
+                    // the leader's conv barrier for this CTA
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (ct == 0) mbar_arrive_cta(conv_bar(s), 0);
+                    // trace: global-timer stamps of both CTAs' conversions (cross-SM comparable)
+                    if (trace != nullptr && blockIdx.x < 2 && ct == 0 && j >= tr_off && j - tr_off < TR_N)
+                        trace[4 * TR_N + 4096 + blockIdx.x * TR_N + (j - tr_off)] = static_cast<long long>(global_ns());
+                } else {
                     mbar_arrive(conv_bar(s));
-                if (trc && j < TR_N) trace[2 * TR_N + j] = clock64();
+                }
+                if (trc && j >= tr_off && j - tr_off < TR_N) trace[2 * TR_N + j - tr_off] = clock64();
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
@@ -786,10 +796,12 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 }
             }
             tc_fence_before();
-            if (PAIR)
-                mbar_arrive_cta(tempty_bar(acc), 0);
-            else
+            if (PAIR) {  // one aggregated arrival per CTA on the leader's tempty barrier
+                asm volatile("bar.sync 2, %0;" ::"n"(epi_warps<ALO, PAIR>() * 32) : "memory");
+                if (warp == 8 && lane == 0) mbar_arrive_cta(tempty_bar(acc), 0);
+            } else {
                 mbar_arrive(tempty_bar(acc));
+            }
         }
         if (tstore && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
@@ -963,8 +975,8 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     const int pf_dist = pf_env >= 0 ? pf_env : 0;
     long long* trace = nullptr;
     if (trace_dir) {
-        SPH_CUDA(cudaMalloc(&trace, (4 * 512 + 4096) * sizeof(long long)));
-        SPH_CUDA(cudaMemsetAsync(trace, 0, (4 * 512 + 4096) * sizeof(long long), st));
+        SPH_CUDA(cudaMalloc(&trace, (6 * 512 + 4096) * sizeof(long long)));
+        SPH_CUDA(cudaMemsetAsync(trace, 0, (6 * 512 + 4096) * sizeof(long long), st));
     }
     SPH_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, md, static_cast<const GemmWork*>(tl.d.p),
                                 static_cast<int>(tl.n), D,
@@ -973,7 +985,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
                                 static_cast<int>(g.d_g2), pf_dist, epi));
     count_launch();
     if (trace) {
-        std::vector<long long> h(4 * 512 + 4096);
+        std::vector<long long> h(6 * 512 + 4096);
         SPH_CUDA(cudaStreamSynchronize(st));
         SPH_CUDA(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
         cudaFree(trace);
@@ -981,6 +993,11 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
         if (FILE* f = std::fopen(path.c_str(), "w")) {
             for (int j = 0; j < 512; ++j)
                 std::fprintf(f, "%d %lld %lld %lld %lld\n", j, h[j], h[512 + j], h[1024 + j], h[1536 + j]);
+            std::fclose(f);
+        }
+        const std::string gpath = std::string(trace_dir) + "/gemm_pairconv_" + g.name + ".txt";
+        if (FILE* f = std::fopen(gpath.c_str(), "w")) {  // global-ns conversion stamps, CTA 0 / 1
+            for (int j = 0; j < 512; ++j) std::fprintf(f, "%d %lld %lld\n", j, h[2048 + 4096 + j], h[2048 + 4096 + 512 + j]);
             std::fclose(f);
         }
         const std::string tpath = std::string(trace_dir) + "/gemm_tiles_" + g.name + ".txt";
