@@ -215,6 +215,9 @@ class _Ref:
         L.ref_disco_transpose_apply.argtypes = L.ref_disco_apply.argtypes
         L.ref_bilinear_resample.argtypes = [C.c_int, _sz, _sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp]
         L.ref_angular_psd.argtypes = [C.c_int, _sz, _sz, _sz, _dp, _dp]
+        L.ref_write_sfd.argtypes = [C.c_char_p, C.c_int, _sz, _sz, _sz, _dp]
+        L.ref_write_weights.argtypes = [C.c_char_p, _sz, _sz, _dp, _dp]
+        L.ref_read_sfd.argtypes = [C.c_char_p, _dp, _sz, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz)]
         L.ref_noise_stream.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _dp, C.c_uint64, _sz, _dp, _dp]
         L.ref_spectral_crps_loss.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _dp, _dp, _sz, C.c_int, _dp]
         L.ref_spectral_conv.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _sz, _dp, _dp, _dp]
@@ -351,6 +354,23 @@ class _Ref:
         coeffs = np.zeros((Cc, lmax, lmax, 2))
         self._check(self.L.ref_noise_stream(kind, nlat, nlon, lmax, Cc, kts, seed, steps, field, coeffs))
         return field, coeffs
+
+    def write_sfd(self, path, kind, x):
+        x = _c64(x)
+        self._check(self.L.ref_write_sfd(str(path).encode(), kind, x.shape[1], x.shape[2], x.shape[0], x))
+
+    def write_weights(self, path, w1, b1):
+        w1, b1 = _c64(w1), _c64(b1)
+        self._check(self.L.ref_write_weights(str(path).encode(), w1.shape[0], w1.shape[1], w1, b1))
+
+    def read_sfd(self, path, cap=1 << 22):
+        """-> (code, array or None); code 0 ok, else 1 + sphere::IoErrorCode."""
+        buf = np.zeros(cap)
+        c, h, w = _sz(0), _sz(0), _sz(0)
+        rc = self.L.ref_read_sfd(str(path).encode(), buf, cap, C.byref(c), C.byref(h), C.byref(w))
+        if rc:
+            return rc, None
+        return 0, buf[: c.value * h.value * w.value].reshape(c.value, h.value, w.value)
 
     def spectral_conv(self, kind, nlat, nlon, kernel, x):
         kernel = _c64(kernel)

@@ -23,6 +23,7 @@
 
 #include "sphere/convolution.hpp"
 #include "sphere/resample.hpp"
+#include "sphere/sfd.hpp"
 #include "sphere/noise.hpp"
 #include "sphere/loss.hpp"
 #include "sphere/metrics.hpp"
@@ -294,6 +295,36 @@ int ref_noise_stream(int kind, size_t nlat, size_t nlon, size_t lmax, size_t C, 
             }
     }
     REF_CATCH
+}
+
+// sfd.hpp:107-131 write_sfd (default channel names) and :183-206 write_weights of two
+// tensors ("w1" [a][b], "b1" [a]) with meta {"model": "fcn3", "version": 3}
+int ref_write_sfd(const char* path, int kind, size_t nlat, size_t nlon, size_t C, const double* data) {
+    REF_TRY
+    write_sfd(path, make_field(make_grid(kind, nlat, nlon), C, data));
+    REF_CATCH
+}
+
+int ref_write_weights(const char* path, size_t a, size_t b, const double* w1, const double* b1) {
+    REF_TRY
+    NamedTensor t1{"w1", {a, b}, std::vector<double>(w1, w1 + a * b)};
+    NamedTensor t2{"b1", {a}, std::vector<double>(b1, b1 + a)};
+    write_weights(path, {t1, t2}, nlohmann::json{{"model", "fcn3"}, {"version", 3}});
+    REF_CATCH
+}
+
+// read back through the reference readers: returns the io error code + 1 on IoError
+int ref_read_sfd(const char* path, double* data, size_t cap, size_t* C, size_t* nlat, size_t* nlon) {
+    try {
+        const SfdContents c = read_sfd(path);
+        *C = c.field.channels;
+        *nlat = c.field.grid.nlat;
+        *nlon = c.field.grid.nlon;
+        if (c.field.data.size() <= cap) std::memcpy(data, c.field.data.data(), 8 * c.field.data.size());
+        return 0;
+    } catch (const IoError& e) {
+        return 1 + static_cast<int>(e.code());
+    }
 }
 
 // convolution.hpp:286 (Gaussian only)
