@@ -178,6 +178,10 @@ int sph_psd_from_coeffs(const float* coeffs, int64_t F, int64_t lmax, int64_t mm
                         void* stream);
 int sph_spectral_crps_from_coeffs(const float* ens, const float* obs, int64_t E, int64_t C, int64_t lmax,
                                   int64_t mmax, int64_t lmax_sum, int variant, double* out, void* stream);
+/* dist_crps local kernel (distsim.hpp:591-618): out[c] = sum_k w[k] CRPS(f[.][c][k], o[c][k]) / (4 pi)
+ * over E members; f [E][C][ns], o [C][ns], w [ns] (latitude quadrature weight per sample). */
+int sph_weighted_crps(const float* f, const float* o, const float* w, int64_t E, int64_t C, int64_t ns,
+                      int variant, double* out, void* stream);
 
 /* ---- spectral convolution + block epilogue ------------------------------------ */
 /* spectral_conv (convolution.hpp:286-304): Gaussian grids only (:287-288);

@@ -215,6 +215,7 @@ class _Ref:
         L.ref_disco_transpose_apply.argtypes = L.ref_disco_apply.argtypes
         L.ref_bilinear_resample.argtypes = [C.c_int, _sz, _sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp]
         L.ref_angular_psd.argtypes = [C.c_int, _sz, _sz, _sz, _dp, _dp]
+        L.ref_crps_field.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _dp, _dp, C.c_int, _dp]
         L.ref_write_sfd.argtypes = [C.c_char_p, C.c_int, _sz, _sz, _sz, _dp]
         L.ref_write_weights.argtypes = [C.c_char_p, _sz, _sz, _dp, _dp]
         L.ref_read_sfd.argtypes = [C.c_char_p, _dp, _sz, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz)]
@@ -371,6 +372,13 @@ class _Ref:
         if rc:
             return rc, None
         return 0, buf[: c.value * h.value * w.value].reshape(c.value, h.value, w.value)
+
+    def crps_field(self, kind, nlat, nlon, ens, obs, variant):
+        ens, obs = _c64(ens), _c64(obs)
+        E, Cc = ens.shape[:2]
+        out = np.zeros(Cc)
+        self._check(self.L.ref_crps_field(kind, nlat, nlon, E, Cc, ens, obs, variant, out))
+        return out
 
     def spectral_conv(self, kind, nlat, nlon, kernel, x):
         kernel = _c64(kernel)

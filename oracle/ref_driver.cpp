@@ -327,6 +327,18 @@ int ref_read_sfd(const char* path, double* data, size_t cap, size_t* C, size_t* 
     }
 }
 
+// metrics.hpp:212-231 crps_field (the serial target of dist_crps, test_distsim.cpp:250-275)
+int ref_crps_field(int kind, size_t nlat, size_t nlon, size_t E, size_t C, const double* ens,
+                   const double* obs, int variant, double* out) {
+    REF_TRY
+    const GridSpec g = make_grid(kind, nlat, nlon);
+    EnsembleField ef(g, E, C);
+    std::memcpy(ef.values.data(), ens, sizeof(double) * ef.values.size());
+    const auto r = crps_field(ef, make_field(g, C, obs), g, static_cast<CrpsVariant>(variant));
+    std::memcpy(out, r.data(), sizeof(double) * C);
+    REF_CATCH
+}
+
 // convolution.hpp:286 (Gaussian only)
 int ref_spectral_conv(int kind, size_t nlat, size_t nlon, size_t cin, size_t cout, size_t klmax,
                       const double* kernel, const double* x, double* y) {

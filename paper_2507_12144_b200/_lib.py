@@ -42,7 +42,7 @@ EXPORTS = [
     "sph_disco_rows_workspace_bytes", "sph_disco_apply_rows", "sph_disco_transpose_workspace_bytes",
     "sph_disco_transpose_apply", "sph_resample_plan_create", "sph_resample_plan_destroy",
     "sph_resample_workspace_bytes", "sph_bilinear_resample", "sph_psd_from_coeffs",
-    "sph_spectral_crps_from_coeffs",
+    "sph_spectral_crps_from_coeffs", "sph_weighted_crps",
     "sph_spectral_conv", "sph_spectral_conv_workspace_bytes", "sph_block_epilogue",
 ]
 
@@ -104,6 +104,7 @@ def _load():
     L.sph_bilinear_resample.argtypes = [vp, vp, i64, vp, vp, vp]
     L.sph_psd_from_coeffs.argtypes = [vp, i64, i64, i64, vp, vp]
     L.sph_spectral_crps_from_coeffs.argtypes = [vp, vp, i64, i64, i64, i64, i64, C.c_int, vp, vp]
+    L.sph_weighted_crps.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int, vp, vp]
     L.sph_spectral_conv.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp, vp, vp]
     L.sph_spectral_conv_workspace_bytes.argtypes = [vp, i64, i64, i64]
     L.sph_spectral_conv_workspace_bytes.restype = i64

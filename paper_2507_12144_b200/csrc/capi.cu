@@ -309,6 +309,11 @@ int sph_bilinear_resample(sph_resample_plan plan, const float* x, int64_t C, flo
     });
 }
 
+int sph_weighted_crps(const float* f, const float* o, const float* w, int64_t E, int64_t C, int64_t ns,
+                      int variant, double* out, void* stream) {
+    return guarded([&] { sph::weighted_crps(f, o, w, E, C, ns, variant, out, S(stream)); });
+}
+
 int sph_psd_from_coeffs(const float* coeffs, int64_t F, int64_t lmax, int64_t mmax, float* psd, void* stream) {
     return guarded([&] { sph::psd_from_coeffs(coeffs, F, lmax, mmax, psd, S(stream)); });
 }

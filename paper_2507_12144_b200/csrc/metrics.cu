@@ -65,7 +65,48 @@ __global__ void spectral_crps_kernel(const float2* __restrict__ ens, const float
     if ((threadIdx.x & 31) == 0 && v != 0.0) atomicAdd(out + c, v);
 }
 
+// dist_crps local kernel (distsim.hpp:591-618): thread per (channel, spatial sample k):
+// ensemble CRPS of f[e][c][k] against o[c][k], times w[k] (quadrature weight of the
+// sample's latitude), summed per channel in fp64 and divided by 4 pi.
+__global__ void weighted_crps_kernel(const float* __restrict__ f, const float* __restrict__ o,
+                                     const float* __restrict__ w, int E, int64_t C, int64_t ns, int fair,
+                                     double* __restrict__ out) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t c = blockIdx.y;
+    double v = 0.0;
+    if (k < ns) {
+        constexpr int EMAX = 64;
+        float u[EMAX];
+        for (int e = 0; e < E; ++e) u[e] = f[(e * C + c) * ns + k];
+        const double ob = o[c * ns + k];
+        double skill = 0.0, pair = 0.0;
+        for (int e = 0; e < E; ++e) {
+            skill += fabs(static_cast<double>(u[e]) - ob);
+            for (int q = e + 1; q < E; ++q) pair += fabs(static_cast<double>(u[e]) - static_cast<double>(u[q]));
+        }
+        const double n = E;
+        const double denom = fair ? 2.0 * n * (n - 1.0) : 2.0 * n * n;
+        v = static_cast<double>(w[k]) * (skill / n - 2.0 * pair / denom) / (4.0 * 3.14159265358979323846);
+    }
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+    if ((threadIdx.x & 31) == 0 && v != 0.0) atomicAdd(out + c, v);
+}
+
 }  // namespace
+
+void weighted_crps(const float* f, const float* o, const float* w, int64_t E, int64_t C, int64_t ns, int variant,
+                   double* out, cudaStream_t st) {
+    require(E >= 1 && E <= 64, "dist_crps: 1..64 ensemble members supported");
+    require(variant >= 0 && variant <= 2, "dist_crps: unknown CRPS variant");
+    require(variant != 2 || E >= 2, "crps_pointwise: fair variant needs E >= 2");
+    require(C <= 65535, "dist_crps: too many channels");
+    SPH_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * C, st));
+    if (C == 0 || ns == 0) return;
+    dim3 grid(static_cast<unsigned>((ns + 255) / 256), static_cast<unsigned>(C));
+    weighted_crps_kernel<<<grid, 256, 0, st>>>(f, o, w, static_cast<int>(E), C, ns, variant == 2 ? 1 : 0, out);
+    SPH_LAUNCH_CHECK();
+    count_launch();
+}
 
 void psd_from_coeffs(const float* coeffs, int64_t F, int64_t lmax, int64_t mmax, float* psd, cudaStream_t st) {
     require(F >= 0 && lmax >= 1 && mmax >= 1, "angular_psd: bad shapes");

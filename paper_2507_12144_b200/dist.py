@@ -23,6 +23,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -160,6 +161,15 @@ class DistContext:
                 pg = dist.new_group(g)
                 if self.rank in g:
                     self.pg[axis] = pg
+        # ranks sharing this rank's batch coordinate (the ensemble+polar+azimuth
+        # all-reduce of dist_crps); built by every rank in the same order
+        self.pg_nonbatch: Optional[dist.ProcessGroup] = None
+        nb = grid.axis_size(BATCH)
+        for b in range(nb):
+            members = [r for r in range(grid.world()) if grid.coords(r)[BATCH] == b]
+            pg = dist.new_group(members) if len(members) > 1 and nb > 1 else None
+            if self.coords[BATCH] == b:
+                self.pg_nonbatch = pg  # None with a single batch coordinate: the world group
 
     def index(self, axis: int) -> int:
         return self.coords[axis]
@@ -257,6 +267,19 @@ class GpuBackend:
         plan = self._plan(grid, lmax, mmax)
         out = plan.forward(x.contiguous(), L.SPH_LAYOUT_DENSE_LM)
         return out.view(C, lmax, mmax, 2)
+
+    def weighted_crps(self, f: torch.Tensor, o: torch.Tensor, w, variant: str) -> torch.Tensor:
+        """dist_crps local kernel in libsphgpu.so: f [E, C, ns], o [C, ns], w [ns]."""
+        from . import _lib as L
+        E, C, ns = f.shape
+        f = f.contiguous().float()
+        o = o.contiguous().float()
+        wt = torch.as_tensor(np.asarray(w, dtype=np.float32), device=f.device)
+        out = torch.empty(C, dtype=torch.float64, device=f.device)
+        L.check(L.lib.sph_weighted_crps(f.data_ptr(), o.data_ptr(), wt.data_ptr(), E, C, ns,
+                                        {"cdf": 0, "spread_skill": 1, "fair": 2}[variant], out.data_ptr(),
+                                        torch.cuda.current_stream(f.device).cuda_stream))
+        return out
 
     def legendre_stage(self, grid, lmax, mmax, bins: torch.Tensor, m0: int) -> torch.Tensor:
         """bins [C, nlat, mloc, 2] -> [C, lmax, mloc, 2]."""
@@ -404,6 +427,42 @@ def _dist_sht_fused(ctx: DistContext, x: Sharded, grid, lmax: int, mmax: int, ba
     outs.append(pend_t2.finish()[0])
     out = outs[0] if len(outs) == 1 else torch.cat(outs, dim=0)
     return Sharded(out, {1: lparts, 2: mparts})
+
+
+def dist_crps(ctx: DistContext, f: Sharded, o: Sharded, grid, variant: str = "fair",
+              backend=None) -> torch.Tensor:
+    """Algorithm 3 (distsim.hpp:548-629): ensemble-transposed CRPS.  f.local [Eloc, C, Hloc,
+    Wloc] (dim 0 over the ensemble axis, dims 2/3 over polar/azimuth, split in f.split),
+    o.local [C, Hloc, Wloc] replicated over the ensemble axis.  Flattens space, transposes
+    the ensemble dimension against it (all-to-all over ensemble), scatters the observation
+    over the ensemble axis (replicated input: the rank's canonical chunk, bytes logged as
+    the reference's root scatter), runs the quadrature-weighted local CRPS kernel and
+    all-reduces over ensemble+polar+azimuth.  Returns this rank's batch scores [C] (fp64)."""
+    backend = backend or GpuBackend()
+    ctx.log.set_operation("dist_crps")
+    g = ctx.grid
+    nH, nW = g.axis_size(POLAR), g.axis_size(AZIMUTH)
+    hparts, wparts = canonical_split(grid.nlat, nH), canonical_split(grid.nlon, nW)
+    if 0 not in f.split or len(f.split[0]) != g.axis_size(ENSEMBLE):
+        raise ValueError("dist_crps: ensemble split bookkeeping missing")
+    Eloc, C, Hloc, Wloc = f.local.shape
+    ff = f.local.reshape(Eloc, C, Hloc * Wloc)
+    oo = o.local.reshape(C, Hloc * Wloc)
+    t, sparts = distributed_transpose(ctx, ff, ENSEMBLE, 0, 2, f.split[0])   # [E, C, SlocE]
+    me = ctx.index(ENSEMBLE)
+    soff = split_offset(sparts, me)
+    ochunk = oo.narrow(1, soff, sparts[me]).contiguous()
+    ctx.record("ensemble", "scatter", ochunk.numel() * ochunk.element_size() if me != 0 else 0, oo)
+    h0 = split_offset(hparts, ctx.index(POLAR))
+    k = np.arange(sparts[me]) + soff
+    w = np.asarray(grid.quad_weights, dtype=np.float64)[h0 + k // Wloc]
+    part = backend.weighted_crps(t, ochunk, w, variant)                    # [C] fp64
+    if g.world() > 1:
+        dist.all_reduce(part, group=ctx.pg_nonbatch)
+    members = g.world() // g.axis_size(BATCH)
+    ctx.record("ensemble+polar+azimuth", "all_reduce", (members - 1) * part.numel() * part.element_size()
+               if me == 0 and ctx.index(POLAR) == 0 and ctx.index(AZIMUTH) == 0 else 0, part)
+    return part
 
 
 def _halo(ctx: DistContext, x: torch.Tensor, hparts: Sequence[int], need: Sequence[Tuple[int, int]]

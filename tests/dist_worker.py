@@ -62,6 +62,29 @@ class OracleBackend:
             out[:, :, ml, 0], out[:, :, ml, 1] = acc.real, acc.imag
         return torch.from_numpy(out)
 
+    def weighted_crps(self, f, o, w, variant):
+        """distsim.hpp:598-616 with crps_pointwise (metrics.hpp:160-209), fp64."""
+        fn, on = f.numpy(), o.numpy()
+        E, C, ns = fn.shape
+        out = np.zeros(C)
+        n = float(E)
+        for c in range(C):
+            acc = 0.0
+            for k in range(ns):
+                u = np.sort(fn[:, c, k])
+                ob = on[c, k]
+                if variant == "cdf":
+                    e = np.arange(1, E + 1)
+                    v = np.where(u <= ob, (2 * e - 1) / (n * n) * (ob - u), (2 * n + 1 - 2 * e) / (n * n) * (u - ob)).sum()
+                else:
+                    skill = np.abs(u - ob).sum() / n
+                    pair = 2.0 * ((2 * np.arange(1, E + 1) - 1 - n) * u).sum()
+                    denom = 2 * n * (n - 1) if variant == "fair" else 2 * n * n
+                    v = skill - pair / denom
+                acc += w[k] * v
+            out[c] = acc / (4 * PI)
+        return torch.from_numpy(out)
+
     def disco_rows(self, op, x, h_in0, ho0, nout, mix):
         xn = x.numpy()
         full = np.zeros((xn.shape[0], op.in_grid.nlat, op.in_grid.nlon))
@@ -84,8 +107,42 @@ class OracleDiscoOp:
         return lo, hi - lo
 
 
+def run_crps(args, cuda, dev, G):
+    """dist_crps (Alg. 3) vs the serial crps_field (test_distsim.cpp:250-300)."""
+    ctx = D.DistContext(D.CommGrid((1, args.ne, args.nh, args.nw)))
+    rep = {}
+    for key, nlat, nlon in (("crps_ga8_E8", 8, 16), ("crps_ga5_E8", 5, 8)):
+        ens, obs, want = G[key + "_ens"], G[key + "_obs"], G[key]
+        E = ens.shape[0]
+        ep = D.canonical_split(E, args.ne)
+        hp, wp = D.canonical_split(nlat, args.nh), D.canonical_split(nlon, args.nw)
+        e, i, j = ctx.index(D.ENSEMBLE), ctx.index(D.POLAR), ctx.index(D.AZIMUTH)
+        fl = ens[D.split_offset(ep, e):D.split_offset(ep, e) + ep[e], :,
+                 D.split_offset(hp, i):D.split_offset(hp, i) + hp[i],
+                 D.split_offset(wp, j):D.split_offset(wp, j) + wp[j]]
+        ol = obs[:, D.split_offset(hp, i):D.split_offset(hp, i) + hp[i],
+                 D.split_offset(wp, j):D.split_offset(wp, j) + wp[j]]
+        dt = torch.float32 if cuda else torch.float64
+        f = D.Sharded(torch.tensor(np.ascontiguousarray(fl), dtype=dt, device=dev), {0: ep, 2: hp, 3: wp})
+        o = D.Sharded(torch.tensor(np.ascontiguousarray(ol), dtype=dt, device=dev), {1: hp, 2: wp})
+        if cuda:
+            import paper_2507_12144_b200 as S
+            grid, backend = S.build_gaussian(nlat, nlon), D.GpuBackend()
+        else:
+            backend = OracleBackend()
+            colat, w = oracle.orc().grid(1, nlat, nlon)
+            grid = _Grid(1, nlat, nlon)
+            grid.quad_weights = w
+        ctx.log = D.TrafficLog()
+        got = D.dist_crps(ctx, f, o, grid, "fair", backend).cpu().numpy()
+        rep[key] = float(np.abs(got - want).max() / max(1.0, np.abs(want).max()))
+        rep[key + "_calls"] = {c: ctx.log.calls("dist_crps", c) for c in ("all_to_all", "scatter", "all_reduce")}
+    return rep
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--ne", type=int, default=0, help="dist_crps mode with this many ensemble ranks")
     ap.add_argument("--device", default="cpu")
     ap.add_argument("--nh", type=int, required=True)
     ap.add_argument("--nw", type=int, required=True)
@@ -100,8 +157,16 @@ def main():
     else:
         dist.init_process_group("gloo")
         dev = torch.device("cpu")
-    ctx = D.DistContext(D.CommGrid((1, 1, args.nh, args.nw)))
     G = np.load(os.path.join(ROOT, "tests", "golden", "golden.npz"))
+    if args.ne:
+        rep = run_crps(args, cuda, dev, G)
+        if dist.get_rank() == 0:
+            with open(args.out, "w") as f:
+                json.dump(rep, f)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    ctx = D.DistContext(D.CommGrid((1, 1, args.nh, args.nw)))
     rep = {}
     dt = torch.float32 if cuda else torch.float64
 

@@ -163,6 +163,14 @@ def main():
     f, c = r.noise_stream(EQ, 33, 64, 32, kts, 99, 2)
     G["noise_eq33_field"], G["noise_eq33_coeffs"] = f, c
 
+    # dist_crps targets: the serial crps_field (test_distsim.cpp:250-300)
+    ens = r.random_uniform((8, 2, 8, 16), 66)
+    obs = r.random_uniform((2, 8, 16), 67)
+    G["crps_ga8_E8"], G["crps_ga8_E8_ens"], G["crps_ga8_E8_obs"] = r.crps_field(GA, 8, 16, ens, obs, 2), ens, obs
+    ens = r.random_uniform((8, 1, 5, 8), 68)
+    obs = r.random_uniform((1, 5, 8), 69)
+    G["crps_ga5_E8"], G["crps_ga5_E8_ens"], G["crps_ga5_E8_obs"] = r.crps_field(GA, 5, 8, ens, obs, 2), ens, obs
+
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(out, **G)
     print("wrote", out, os.path.getsize(out), "bytes,", len(G), "arrays")

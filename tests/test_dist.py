@@ -25,12 +25,12 @@ def _free_port():
     return p
 
 
-def _run(nh, nw, device, tmp_path):
-    out = tmp_path / f"rep_{nh}x{nw}_{device}.json"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nh * nw}",
+def _run(nh, nw, device, tmp_path, ne=0):
+    out = tmp_path / f"rep_{ne}x{nh}x{nw}_{device}.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={max(ne, 1) * nh * nw}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), "--device", device, "--nh", str(nh),
-           "--nw", str(nw), "--out", str(out)]
+           "--nw", str(nw), "--ne", str(ne), "--out", str(out)]
     env = dict(os.environ, OMP_NUM_THREADS="1")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
@@ -58,6 +58,27 @@ def test_dist_gloo_matches_reference_simulator(nh, nw, tmp_path):
     if nh == 2:
         assert rep["odd_split"] == [5, 4]
         assert rep["odd_err"] <= 1e-12
+
+
+@pytest.mark.parametrize("ne,nh,nw", [(2, 1, 1), (4, 1, 1), (1, 2, 2), (2, 1, 2)])
+def test_dist_crps_gloo_matches_serial(ne, nh, nw, tmp_path):
+    """Alg. 3 (distsim.hpp:548-629) vs the reference's serial crps_field, incl. spatial
+    shards not divisible by the ensemble axis (test_distsim.cpp:277-303)."""
+    rep = _run(nh, nw, "cpu", tmp_path, ne=ne)
+    for key in ("crps_ga8_E8", "crps_ga5_E8"):
+        assert rep[key] <= 1e-12, rep
+        assert rep[key + "_calls"] == {"all_to_all": 1, "scatter": 1, "all_reduce": 1}
+
+
+@pytest.mark.gpu
+def test_dist_crps_nccl_gpu(tmp_path):
+    torch = pytest.importorskip("torch")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    for ne, nh, nw in [(2, 1, 1), (1, 2, 1)]:
+        rep = _run(nh, nw, "cuda", tmp_path, ne=ne)
+        for key in ("crps_ga8_E8", "crps_ga5_E8"):
+            assert rep[key] <= 1e-5, rep
 
 
 @pytest.mark.gpu
