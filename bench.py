@@ -258,6 +258,11 @@ def workload_config(args):
                             "epilogue) + one local block (DISCO 360x720 -> 360x720, Morlet K=9 -> MLP epilogue) "
                             "at 360x720 Gaussian, 256 channels, MLP hidden 512, batch 1",
                 "batch": 1, "channels": 256, "mlp_hidden": 512, "precision": "fp32 I/O, 3xTF32 GEMMs"}
+    if args.workload == "decoder":
+        return {"workload": "§8f decoder group (model.hpp:372-394): bilinear upsample 360x720 Gaussian -> "
+                            "721x1440 eq fused into DISCO 721x1440 -> 721x1440 (Morlet K=9, cutoff 3pi/720), "
+                            "64 -> 64 channels, batch 4 per GPU",
+                "batch": 4, "c_in": 64, "c_out": 64, "precision": "fp32 I/O, 3xTF32 channel mix"}
     if args.workload == "disco_t":
         return {"workload": "configs[2] adjoint: disco_transpose_apply 360x720 Gaussian -> 721x1440 eq, "
                             "Morlet K=9, cutoff 3pi/360, 256 -> 64 channels, batch 4 per GPU",
@@ -362,6 +367,7 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     hbm, bf16, bf16_sus, peak_src = peaks()
     torch.manual_seed(1234 + rank)
+    extra = {}
 
     if args.workload == "sht":
         g = S.build_equiangular(NLAT, NLON)
@@ -397,6 +403,38 @@ def run_ours(args, ws, rank, local):
             S.block_apply(lat, cond, bw_g)
             S.block_apply(lat, cond, bw_l, block_op)
         units = B * C
+    elif args.workload == "decoder":
+        # decode_preclamp group (model.hpp:372-394): 360x720 Gaussian latent -> bilinear
+        # upsample to 721x1440 -> DISCO 721x1440 -> 721x1440, 64 -> 64 channels, batch 4
+        gl, go = S.build_gaussian(360, 720), S.build_equiangular(NLAT, NLON)
+        op = S.DiscoOperator(go, go, S.morlet_basis(3 * math.pi / 720))
+        dplan = S.DecoderPlan(op, gl)
+        B, cin, cout = 4, 64, 64
+        mix = (torch.rand((cout, cin, op.n_basis), device=dev) * 2 - 1) / math.sqrt(cin * 9)
+        lat = torch.rand((B, cin, 360, 720), device=dev) * 2 - 1
+        y = torch.empty((B, cout, NLAT, NLON), device=dev)
+        wsb = torch.empty(L.lib.sph_decoder_workspace_bytes(dplan.h, B, cin, cout), dtype=torch.uint8, device=dev)
+        # unfused two-stage path for comparison (reported as extra["unfused_ms"])
+        up = torch.empty((B, cin, NLAT, NLON), device=dev)
+        rplan = S.ResamplePlan(gl, go)
+        wsd = op.workspace(B, cin, cout)
+
+        def unfused():
+            rplan.apply(lat, out=up)
+            op.apply(up, mix, out=y, ws=wsd)
+        for _ in range(3):
+            unfused()
+        ue0, ue1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ue0.record()
+        for _ in range(args.steps):
+            unfused()
+        ue1.record()
+        torch.cuda.synchronize()
+        extra["unfused_ms"] = ue0.elapsed_time(ue1) / args.steps
+
+        def step():
+            dplan.apply(lat, mix, out=y, ws=wsb)
+        units = B * cout
     else:
         gi = S.build_equiangular(NLAT, NLON)
         go = S.build_gaussian(360, 720)
@@ -499,6 +537,8 @@ def run_ours(args, ws, rank, local):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
+            if args.workload == "decoder":
+                raise RuntimeError("no CPU baseline for the decoder workload")
             cpu = cpu_reference_sht(1) if args.workload == "sht" else cpu_reference_disco()
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # noqa: BLE001
@@ -511,6 +551,7 @@ def run_ours(args, ws, rank, local):
                "data": "synthetic (uniform(-1,1) fields of the named shape)",
                "config": workload_config(args), "roofline": roof, "cpu_baseline": cpu,
                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
+        out.update(extra)
         print(json.dumps(out), flush=True)
 
 
@@ -520,7 +561,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sht", choices=["sht", "disco", "disco_t", "block", "dist_sht", "dist_disco"])
+    ap.add_argument("--workload", default="sht", choices=["sht", "disco", "disco_t", "block", "decoder", "dist_sht", "dist_disco"])
     ap.add_argument("--decomp", default="", help="dist_*: NHxNW polar x azimuth ranks (default WORLD_SIZE x 1)")
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")

@@ -168,6 +168,21 @@ int64_t sph_resample_workspace_bytes(sph_resample_plan plan, int64_t C);
 int sph_bilinear_resample(sph_resample_plan plan, const float* x, int64_t C, float* y, void* workspace,
                           void* stream);
 
+/* ---- fused decoder (model.hpp:372-394, decode_preclamp per channel group) -------- */
+/* y [B][c_out][out_nlat][out_nlon] = disco_apply(dec_op, bilinear_resample(latent, out_grid), mix)
+ * for latent [B][c_in][latent_nlat][latent_nlon] (latent colatitudes as in
+ * sph_resample_plan_create).  `disco` is the decoder's out_grid -> out_grid operator and
+ * must outlive the decoder plan.  When out_nlon is an integer multiple of latent_nlon the
+ * upsampling is applied to the latent's ring spectra inside the convolution (the
+ * upsampled field is never materialized); otherwise the two stages run back to back. */
+typedef struct sph_decoder_plan_st* sph_decoder_plan;
+int sph_decoder_plan_create(sph_disco_plan disco, const double* latent_colat, int64_t latent_nlat,
+                            int64_t latent_nlon, sph_decoder_plan* plan);
+int sph_decoder_plan_destroy(sph_decoder_plan plan);
+int64_t sph_decoder_workspace_bytes(sph_decoder_plan plan, int64_t B, int64_t c_in, int64_t c_out);
+int sph_decoder_apply(sph_decoder_plan plan, const float* latent, const float* mix, int64_t B,
+                      int64_t c_in, int64_t c_out, float* y, void* workspace, void* stream);
+
 /* ---- SHT consumers (metrics.hpp:300-314, loss.hpp:37-81) ---------------------------- */
 /* Reductions over sph_sht_forward's dense output [F][lmax][mmax] complex64:
  * angular PSD psd[f][l] = |c(l,0)|^2 + 2 sum_{m=1..min(l,mmax-1)} |c(l,m)|^2, and the

@@ -214,6 +214,7 @@ class _Ref:
                                       _sz, _sz, _dp, _dp, _dp]
         L.ref_disco_transpose_apply.argtypes = L.ref_disco_apply.argtypes
         L.ref_bilinear_resample.argtypes = [C.c_int, _sz, _sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp]
+        L.ref_spectral_resample.argtypes = [C.c_int, _sz, _sz, C.c_int, _sz, _sz, _sz, _dp, _dp]
         L.ref_angular_psd.argtypes = [C.c_int, _sz, _sz, _sz, _dp, _dp]
         L.ref_crps_field.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _dp, _dp, C.c_int, _dp]
         L.ref_write_sfd.argtypes = [C.c_char_p, C.c_int, _sz, _sz, _sz, _dp]
@@ -333,6 +334,14 @@ class _Ref:
         y = np.zeros((C, out_nlat, out_nlon))
         self._check(self.L.ref_bilinear_resample(in_kind, in_nlat, in_nlon, in_last_pi, out_kind,
                                                  out_nlat, out_nlon, C, x, y))
+        return y
+
+    def spectral_resample(self, in_kind, in_nlat, in_nlon, out_kind, out_nlat, out_nlon, x):
+        x = _c64(x)
+        C = x.shape[0]
+        y = np.zeros((C, out_nlat, out_nlon))
+        self._check(self.L.ref_spectral_resample(in_kind, in_nlat, in_nlon, out_kind, out_nlat,
+                                                 out_nlon, C, x, y))
         return y
 
     def angular_psd(self, kind, nlat, nlon, x):

@@ -248,6 +248,17 @@ int ref_bilinear_resample(int in_kind, size_t in_nlat, size_t in_nlon, int in_la
     REF_CATCH
 }
 
+// resample.hpp:120-132 spectral_resample -> y [C][out_nlat][out_nlon]
+int ref_spectral_resample(int in_kind, size_t in_nlat, size_t in_nlon, int out_kind, size_t out_nlat,
+                          size_t out_nlon, size_t C, const double* x, double* y) {
+    REF_TRY
+    const GridSpec gi = make_grid(in_kind, in_nlat, in_nlon);
+    const GridSpec go = make_grid(out_kind, out_nlat, out_nlon);
+    const SphericalField out = spectral_resample(make_field(gi, C, x), go);
+    std::memcpy(y, out.data.data(), sizeof(double) * out.data.size());
+    REF_CATCH
+}
+
 // metrics.hpp:300-314 angular_psd -> psd [C][nlat]
 int ref_angular_psd(int kind, size_t nlat, size_t nlon, size_t C, const double* x, double* psd) {
     REF_TRY

@@ -10,7 +10,7 @@ from .sphere import (  # noqa: F401
     EQUIANGULAR, GAUSSIAN, BlockWeights, DiscoOperator, FilterBasis, GridSpec, ShtPlan,
     SpectralCoeffs, SphericalField, assemble_disco, block_apply, block_epilogue,
     build_equiangular, build_gaussian, default_mmax, disco_apply, disco_transpose_apply, get_sht_plan,
-    bilinear_resample, ResamplePlan, angular_psd, spectral_crps_loss,
+    bilinear_resample, spectral_resample, ResamplePlan, DecoderPlan, decode_preclamp, angular_psd, spectral_crps_loss,
     isotropic_basis, morlet_basis, require_same_sampling, sht_forward, sht_inverse,
     spectral_conv,
 )

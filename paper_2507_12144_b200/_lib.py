@@ -41,7 +41,8 @@ EXPORTS = [
     "sph_disco_workspace_bytes", "sph_disco_apply", "sph_disco_input_rows",
     "sph_disco_rows_workspace_bytes", "sph_disco_apply_rows", "sph_disco_transpose_workspace_bytes",
     "sph_disco_transpose_apply", "sph_resample_plan_create", "sph_resample_plan_destroy",
-    "sph_resample_workspace_bytes", "sph_bilinear_resample", "sph_psd_from_coeffs",
+    "sph_resample_workspace_bytes", "sph_bilinear_resample", "sph_decoder_plan_create",
+    "sph_decoder_plan_destroy", "sph_decoder_workspace_bytes", "sph_decoder_apply", "sph_psd_from_coeffs",
     "sph_spectral_crps_from_coeffs", "sph_weighted_crps",
     "sph_spectral_conv", "sph_spectral_conv_workspace_bytes", "sph_block_epilogue",
 ]
@@ -102,6 +103,11 @@ def _load():
     L.sph_resample_workspace_bytes.argtypes = [vp, i64]
     L.sph_resample_workspace_bytes.restype = i64
     L.sph_bilinear_resample.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.sph_decoder_plan_create.argtypes = [vp, vp, i64, i64, C.POINTER(vp)]
+    L.sph_decoder_plan_destroy.argtypes = [vp]
+    L.sph_decoder_workspace_bytes.argtypes = [vp, i64, i64, i64]
+    L.sph_decoder_workspace_bytes.restype = i64
+    L.sph_decoder_apply.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, vp]
     L.sph_psd_from_coeffs.argtypes = [vp, i64, i64, i64, vp, vp]
     L.sph_spectral_crps_from_coeffs.argtypes = [vp, vp, i64, i64, i64, i64, i64, C.c_int, vp, vp]
     L.sph_weighted_crps.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int, vp, vp]

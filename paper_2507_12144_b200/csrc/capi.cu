@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "metrics.cuh"
+#include "decoder.cuh"
 #include "resample.cuh"
 #include "disco.cuh"
 #include "sht.cuh"
@@ -306,6 +307,39 @@ int sph_bilinear_resample(sph_resample_plan plan, const float* x, int64_t C, flo
     return guarded([&] {
         sph::require(plan, "bilinear_resample: null plan");
         sph::resample_apply(*reinterpret_cast<sph::ResamplePlan*>(plan), x, C, y, workspace, S(stream));
+    });
+}
+
+// ------------------------------------------------------------------ decoder
+int sph_decoder_plan_create(sph_disco_plan disco, const double* latent_colat, int64_t latent_nlat,
+                            int64_t latent_nlon, sph_decoder_plan* plan) {
+    return guarded([&] {
+        sph::require(plan && disco && latent_colat, "decode: null argument");
+        *plan = nullptr;
+        auto* p = new sph::DecoderPlan();
+        try {
+            p->create(&disco->p, latent_colat, latent_nlat, latent_nlon);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *plan = reinterpret_cast<sph_decoder_plan>(p);
+    });
+}
+
+int sph_decoder_plan_destroy(sph_decoder_plan plan) {
+    return guarded([&] { delete reinterpret_cast<sph::DecoderPlan*>(plan); });
+}
+
+int64_t sph_decoder_workspace_bytes(sph_decoder_plan plan, int64_t B, int64_t c_in, int64_t c_out) {
+    return plan ? reinterpret_cast<sph::DecoderPlan*>(plan)->workspace_bytes(B, c_in, c_out) : -1;
+}
+
+int sph_decoder_apply(sph_decoder_plan plan, const float* latent, const float* mix, int64_t B,
+                      int64_t c_in, int64_t c_out, float* y, void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "decode: null plan");
+        reinterpret_cast<sph::DecoderPlan*>(plan)->apply(latent, mix, B, c_in, c_out, y, workspace, S(stream));
     });
 }
 

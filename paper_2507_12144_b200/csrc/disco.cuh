@@ -2,6 +2,7 @@
 // (convolution.hpp:286-304) + block epilogue (model.hpp:355-368).
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "fft.cuh"
@@ -67,9 +68,11 @@ struct DiscoPlan {
     void apply(const float* x, const float* mix, int64_t B, int64_t cin, int64_t cout, float* y,
                void* ws, cudaStream_t st);
     // output rows [ho0, ho0+nout) from input rows [h_in0, h_in0+nin) (latitude shards)
+    // make_u (optional): produces the channel-minor input spectrum U[B][nin][nbi][cin]
+    // instead of the R2C of x (the fused decoder builds it from the latent's spectrum)
     void apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t ho0, int64_t nout,
                     const float* mix, int64_t B, int64_t cin, int64_t cout, float* y, void* ws,
-                    cudaStream_t st);
+                    cudaStream_t st, const std::function<void(float2*)>* make_u = nullptr);
     void input_rows(int64_t ho0, int64_t nout, int64_t* lo, int64_t* n) const;
     int64_t rows_workspace_bytes(int64_t B, int64_t cin, int64_t cout, int64_t nin, int64_t nout) const;
     // v [B][cout][hout][wout] on the output grid -> y [B][cin][hin][win] on the input grid

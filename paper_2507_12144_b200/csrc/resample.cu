@@ -16,14 +16,6 @@
 
 namespace sph {
 
-struct ResamplePlan {
-    int device = 0;
-    int64_t in_nlat = 0, in_nlon = 0, out_nlat = 0, out_nlon = 0;
-    bool ext = false, add_north = false, add_south = false;
-    int64_t ext_nlat = 0;
-    DevBuf<int32_t> d_i0, d_i1, d_j0, d_j1;
-    DevBuf<float> d_wt, d_wp;
-};
 
 namespace {
 constexpr double kPi = 3.14159265358979323846;
@@ -97,8 +89,14 @@ void resample_create(ResamplePlan& p, const double* in_colat, int64_t in_nlat, i
     if (p.add_south) ec.push_back(kPi);
     p.ext_nlat = static_cast<int64_t>(ec.size());
     const int64_t n = p.ext_nlat;
-    std::vector<int32_t> i0(out_nlat), i1(out_nlat), j0(out_nlon), j1(out_nlon);
-    std::vector<float> wt(out_nlat), wp(out_nlon);
+    std::vector<int32_t>&i0 = p.i0, &i1 = p.i1, &j0 = p.j0, &j1 = p.j1;
+    std::vector<double>&wt = p.wt, &wp = p.wp;
+    i0.assign(out_nlat, 0);
+    i1.assign(out_nlat, 0);
+    j0.assign(out_nlon, 0);
+    j1.assign(out_nlon, 0);
+    wt.assign(out_nlat, 0.0);
+    wp.assign(out_nlon, 0.0);
     for (int64_t oi = 0; oi < out_nlat; ++oi) {  // :81-90
         const double theta = out_colat[oi];
         const int64_t u = std::upper_bound(ec.begin(), ec.end(), theta) - ec.begin();
@@ -108,7 +106,7 @@ void resample_create(ResamplePlan& p, const double* in_colat, int64_t in_nlat, i
         const double w = (a1 == a0 || theta <= t0) ? 0.0 : (theta - t0) / (t1 - t0);
         i0[oi] = static_cast<int32_t>(a0);
         i1[oi] = static_cast<int32_t>(a1);
-        wt[oi] = static_cast<float>(w);
+        wt[oi] = w;
     }
     const double dphi = 2.0 * kPi / static_cast<double>(in_nlon);
     for (int64_t oj = 0; oj < out_nlon; ++oj) {  // :92-105
@@ -124,14 +122,14 @@ void resample_create(ResamplePlan& p, const double* in_colat, int64_t in_nlat, i
         }
         j0[oj] = static_cast<int32_t>(a0);
         j1[oj] = static_cast<int32_t>((a0 + 1) % in_nlon);
-        wp[oj] = static_cast<float>(w);
+        wp[oj] = w;
     }
     upload(p.d_i0, i0);
     upload(p.d_i1, i1);
-    upload(p.d_wt, wt);
+    upload(p.d_wt, std::vector<float>(wt.begin(), wt.end()));
     upload(p.d_j0, j0);
     upload(p.d_j1, j1);
-    upload(p.d_wp, wp);
+    upload(p.d_wp, std::vector<float>(wp.begin(), wp.end()));
 }
 
 ResamplePlan* resample_new() { return new ResamplePlan(); }

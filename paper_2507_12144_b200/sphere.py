@@ -487,6 +487,89 @@ def bilinear_resample(field: SphericalField, out_grid: GridSpec) -> SphericalFie
     return SphericalField(out_grid, plan.apply(field.data))
 
 
+def spectral_resample(field: SphericalField, out_grid: GridSpec, precision: str = "3xtf32") -> SphericalField:
+    """resample.hpp:120-132: alias-free resampling, forward SHT truncated to the smaller
+    grid's capacity then synthesis on ``out_grid``; non-Gaussian inputs are first moved
+    to the Gaussian grid of the same size by bilinear interpolation."""
+    src = field
+    if field.grid.kind != GAUSSIAN:
+        src = bilinear_resample(field, build_gaussian(field.grid.nlat, field.grid.nlon))
+    lmax = min(src.grid.nlat, out_grid.nlat)
+    mmax = min(lmax, src.grid.nlon // 2, (out_grid.nlon - 1) // 2 + 1)
+    return sht_inverse(sht_forward(src, lmax, mmax, precision), out_grid, precision)
+
+
+# ------------------------------------------------------------------ decoder
+class DecoderPlan:
+    """decode_preclamp's per-group body (model.hpp:372-394): disco_apply(op,
+    bilinear_resample(latent, op.in_grid), mix) with the upsampling applied to the latent's
+    ring spectra inside the convolution when op.in_grid.nlon is a multiple of the latent's."""
+
+    def __init__(self, op: DiscoOperator, latent_grid: GridSpec):
+        if (op.in_grid.kind, op.in_grid.nlat, op.in_grid.nlon) != (op.out_grid.kind, op.out_grid.nlat,
+                                                                    op.out_grid.nlon):
+            raise L.SphInvalidArgument(1, "decode: the decoder convolution maps the output grid onto itself")
+        self.op, self.latent_grid = op, latent_grid
+        ci = np.ascontiguousarray(latent_grid.colatitudes, dtype=np.float64)
+        h = C.c_void_p()
+        check(L.lib.sph_decoder_plan_create(op.h, ci.ctypes.data, latent_grid.nlat, latent_grid.nlon, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and L.lib is not None:
+            L.lib.sph_decoder_plan_destroy(self.h)
+            self.h = None
+
+    def apply(self, latent: torch.Tensor, mix: torch.Tensor, out=None, ws=None) -> torch.Tensor:
+        """latent [B, cin, latent_nlat, latent_nlon] -> y [B, cout, out_nlat, out_nlon]."""
+        mix = _dev_f32(mix, "decode")
+        latent = _dev_f32(latent, "decode")
+        cout, cin, K = mix.shape
+        gl, go = self.latent_grid, self.op.out_grid
+        if K != self.op.n_basis or latent.shape[-3] != cin:
+            raise L.SphInvalidArgument(1, "decode: mix tensor shape mismatch")
+        if tuple(latent.shape[-2:]) != (gl.nlat, gl.nlon):
+            raise L.SphInvalidArgument(1, "decode: latent sampling mismatch")
+        B = latent.numel() // (cin * gl.nlat * gl.nlon)
+        if out is None:
+            out = torch.empty((B, cout, go.nlat, go.nlon), dtype=torch.float32, device=latent.device)
+        if ws is None:
+            ws = torch.empty(int(L.lib.sph_decoder_workspace_bytes(self.h, B, cin, cout)), dtype=torch.uint8,
+                             device=latent.device)
+        with torch.cuda.device(latent.device):
+            check(L.lib.sph_decoder_apply(self.h, _ptr(latent), _ptr(mix), B, cin, cout, _ptr(out), _ptr(ws),
+                                          _stream(latent.device)))
+        return out
+
+
+_DECODER_PLANS: Dict[tuple, DecoderPlan] = {}
+
+
+def decode_preclamp(op: DiscoOperator, latent: SphericalField, mixes) -> SphericalField:
+    """model.hpp:372-394: the latent channels split into consecutive groups, group g of
+    mixes[g].shape[1] channels decoded by disco_apply(op, upsampled group, mixes[g]); the
+    outputs are concatenated along channels.  Upsampling and convolution run fused."""
+    if isinstance(mixes, torch.Tensor) and mixes.dim() == 3:
+        mixes = [mixes]
+    key = (id(op), latent.grid.kind, latent.grid.nlat, latent.grid.nlon,
+           tuple(np.asarray(latent.grid.colatitudes)[[0, -1]]))
+    plan = _DECODER_PLANS.get(key)
+    if plan is None or plan.op is not op:
+        plan = _DECODER_PLANS[key] = DecoderPlan(op, latent.grid)
+    x = latent.data
+    if sum(int(m.shape[1]) for m in mixes) != x.shape[-3]:
+        raise L.SphInvalidArgument(1, "decode: channel groups do not cover the latent channels")
+    lead = tuple(x.shape[:-3])
+    x = x.reshape(-1, *x.shape[-3:])
+    outs, c0 = [], 0
+    for m in mixes:
+        cin = int(m.shape[1])
+        outs.append(plan.apply(x[:, c0:c0 + cin].contiguous(), m))
+        c0 += cin
+    y = torch.cat(outs, dim=1)
+    return SphericalField(op.out_grid, y.reshape(*lead, y.shape[1], op.out_grid.nlat, op.out_grid.nlon))
+
+
 # ------------------------------------------------------------ SHT consumers
 CRPS_VARIANTS = {"cdf": 0, "spread_skill": 1, "fair": 2}
 

@@ -143,6 +143,30 @@ def main():
         x = r.random_uniform((2, ih, iw), 40)
         G[f"resample_{name}"] = r.bilinear_resample(ik, ih, iw, ok, oh, ow, x, in_last_pi=lp)
 
+    # spectral_resample (resample.hpp:120-132): Gaussian / equiangular inputs, up and down
+    for name, (ik, ih, iw, ok, oh, ow) in {"ga8_ga12": (GA, 8, 16, GA, 12, 24),
+                                           "ga12_eq9": (GA, 12, 24, EQ, 9, 16),
+                                           "eq9_ga8": (EQ, 9, 16, GA, 8, 16),
+                                           "ga45_eq91": (GA, 45, 90, EQ, 91, 180)}.items():
+        x = r.random_uniform((2, ih, iw), 41)
+        G[f"sresample_{name}"] = r.spectral_resample(ik, ih, iw, ok, oh, ow, x)
+
+    # decoder group (model.hpp:372-394): disco_apply(dec_op, bilinear_resample(latent, out))
+    dcases = {
+        "ga8_eq17": (GA, 8, 16, EQ, 17, 32, 3 * PI / 16, 3, 2),    # r = 2, both poles extended
+        "ga6_ga12": (GA, 6, 12, GA, 12, 36, 3 * PI / 12, 2, 3),    # r = 3, Gaussian -> Gaussian
+        "eq5_eq9": (EQ, 5, 8, EQ, 9, 16, 3 * PI / 9, 2, 1),        # latent touches the north pole
+        "eq9_eq9x24": (EQ, 9, 16, EQ, 9, 24, 3 * PI / 9, 2, 2),    # ratio 1.5: unfused path
+        "ga45_eq91": (GA, 45, 90, EQ, 91, 180, 3 * PI / 90, 4, 1),
+    }
+    for name, (lk, lh, lw, ok, oh, ow, cut, cin, cout) in dcases.items():
+        lat = r.random_uniform((cin, lh, lw), 90)
+        up = r.bilinear_resample(lk, lh, lw, ok, oh, ow, lat)
+        mix = r.random_uniform((cout, cin, 9), 91)
+        G[f"decoder_{name}_latent"] = lat
+        G[f"decoder_{name}_mix"] = mix
+        G[f"decoder_{name}_y"] = r.disco_apply(ok, oh, ow, ok, oh, ow, cut, up, mix)
+
     # SHT consumers (metrics.hpp:300-314 angular_psd, loss.hpp:37-81 spectral_crps_loss)
     x = r.random_uniform((3, 16, 32), 60)
     G["psd_ga16"] = r.angular_psd(GA, 16, 32, x)

@@ -80,3 +80,18 @@ def test_resample_batched_cfg_size():
     if want is not None:
         assert rel_l2(y[:2], want) <= TOL
     assert y.shape == (3, 721, 1440)
+
+
+SCASES = {"ga8_ga12": (GA, 8, 16, GA, 12, 24), "ga12_eq9": (GA, 12, 24, EQ, 9, 16),
+          "eq9_ga8": (EQ, 9, 16, GA, 8, 16), "ga45_eq91": (GA, 45, 90, EQ, 91, 180)}
+
+
+@pytest.mark.parametrize("name", list(SCASES))
+def test_spectral_resample_golden(golden, name):
+    """resample.hpp:120-132 through the SHT kernels (fp32 / 3xTF32 tolerance)."""
+    ik, ih, iw, ok, oh, ow = SCASES[name]
+    x = oracle.random_field((2, ih, iw), 41)
+    f = S.SphericalField(grid(ik, ih, iw), torch.tensor(x, dtype=torch.float32, device=DEV))
+    y = S.spectral_resample(f, grid(ok, oh, ow)).data
+    torch.cuda.synchronize()
+    assert rel_l2(y.cpu().numpy().astype(np.float64), golden[f"sresample_{name}"]) <= 1e-5, name
