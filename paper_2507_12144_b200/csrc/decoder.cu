@@ -23,11 +23,12 @@ namespace sph {
 namespace {
 constexpr double kPi = 3.14159265358979323846;
 
-// thread per (bin m, channel group): V = float4 carries two consecutive channels' complex
-// values (even channel counts), float2 one
+// thread per (bin m, channel group): V = float4 carries a channel pair (even channel
+// counts, both spectra in the pair-interleaved layout), float2 one channel
 __device__ __forceinline__ float4 vzero(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
 __device__ __forceinline__ float2 vzero(float2) { return make_float2(0.f, 0.f); }
-__device__ __forceinline__ void vconj(float4& v) { v.y = -v.y; v.w = -v.w; }
+// float4 = channel pair in DISCO's pair-interleaved layout (re c, re c+1, im c, im c+1)
+__device__ __forceinline__ void vconj(float4& v) { v.z = -v.z; v.w = -v.w; }
 __device__ __forceinline__ void vconj(float2& v) { v.y = -v.y; }
 __device__ __forceinline__ float4 vaxpby(float a, float4 p, float b, float4 q) {
     return make_float4(fmaf(b, q.x, a * p.x), fmaf(b, q.y, a * p.y), fmaf(b, q.z, a * p.z), fmaf(b, q.w, a * p.w));
@@ -151,8 +152,8 @@ void DecoderPlan::apply(const float* latent, const float* mix, int64_t B, int64_
     const int row0 = rs.add_north ? 1 : 0;
     const int north = rs.add_north ? 0 : -1, south = rs.add_south ? static_cast<int>(rs.ext_nlat - 1) : -1;
     const std::function<void(float2*)> make_u = [&](float2* U) {
-        fft_forward_cminor(fft_lat, latent, B, cin, HL, static_cast<int>(nbl), UL, st);
-        const bool pairs = cin % 2 == 0;
+        const bool pairs = disco->pair_layout(cin);
+        fft_forward_cminor(fft_lat, latent, B, cin, HL, static_cast<int>(nbl), UL, st, pairs ? 2 : 0);
         const int CV = static_cast<int>(pairs ? cin / 2 : cin);
         const int64_t n = disco->nbi * CV;
         dim3 grid(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(HO), static_cast<unsigned>(B));

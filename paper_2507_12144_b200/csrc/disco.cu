@@ -263,30 +263,25 @@ __global__ void __launch_bounds__(256) disco_band_kernel(
 
 // Even channel counts: each thread owns a channel pair (c, c+1) and accumulates both in
 // packed fp32x2 registers with FFMA2 (fma.rn.f32x2, the psi value as a broadcast scalar
-// operand), so a slot costs 36 FFMA2 for 2 channels instead of 72 FFMA; U comes in as one
-// float4 per slot, double-buffered in two named register sets (no per-slot moves).
-// threads = 4 orders x LANES lanes, 2 * LANES channels per pass.
-typedef unsigned long long f2x;
-__device__ __forceinline__ f2x pk2(float a, float b) {
-    f2x r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void ffma2(f2x& d, float a, f2x b) {
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(pk2(a, a)), "l"(b));
-}
-__device__ __forceinline__ float lo2(f2x v) { return __uint_as_float(static_cast<uint32_t>(v)); }
-__device__ __forceinline__ float hi2(f2x v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+// operand): a slot costs 1 LDG.128 + 9 broadcast LDS.128 + 36 FFMA2 for 2 channels
+// (the scalar kernel: 2 x (1 LDG + 5 LDS + 36 FFMA + selects)).  U arrives in the
+// pair-interleaved layout (re c, re c+1, im c, im c+1), so one float4 is directly the two
+// packed operands; the Hermitian-fold sign is folded into the staged psi values:
+// per (slot, order, k) smem holds (px, py, s px, -s py) with
+//     re += px ux + py uy,   im += s (px uy - py ux),   s = -1 for folded bins.
+// threads = 4 orders x 32 lanes, 64 channels per pass.
+// acc += a * b for a float2 pair with a broadcast scalar (FFMA2 R.F32 operand)
+__device__ __forceinline__ void ffma2(float2& d, float a, float2 b) { d = __ffma2_rn(make_float2(a, a), b, d); }
 
-template <int LANES>
-__global__ void __launch_bounds__(4 * LANES) disco_band2_kernel(
-    const float2* __restrict__ U, const float2* __restrict__ psi_hat, const int32_t* __restrict__ band0,
+constexpr int BAND2_SLOTS = 32;
+__global__ void __launch_bounds__(128) disco_band2_kernel(
+    const float4* __restrict__ U, const float2* __restrict__ psi_hat, const int32_t* __restrict__ band0,
     const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, int64_t Hin, int64_t nbi,
     int64_t Hout, int64_t nbo, int win, int wout, int s, int K, int64_t C, int64_t ldS,
     float* __restrict__ S, int64_t h_in0, int64_t ho0, int64_t B) {
-    constexpr int CP = 2 * LANES;
-    __shared__ float4 ps[BAND_MAX_SLOTS][4][5];
-    __shared__ int32_t uo[BAND_MAX_SLOTS][4];
+    constexpr int LANES = 32, CP = 64;
+    __shared__ float4 ps[BAND2_SLOTS][4][9];
+    __shared__ int32_t uo[BAND2_SLOTS][4];
     __shared__ __align__(16) float so[4][2][CP * 9];
     const int mi = threadIdx.x / LANES, cl = threadIdx.x % LANES;
     const int64_t mp0 = static_cast<int64_t>(blockIdx.x) * 4;
@@ -297,24 +292,28 @@ __global__ void __launch_bounds__(4 * LANES) disco_band2_kernel(
     const int64_t po = psi_off[hg];
     const int half = win / 2;
     const int nslot = nb * s;
-    const int64_t C2 = C / 2;  // float4 stride of one U row (C even)
-    for (int slot0 = 0; slot0 < nslot; slot0 += BAND_MAX_SLOTS) {
-        const int ns = min(BAND_MAX_SLOTS, nslot - slot0);
+    const int64_t C2 = C / 2;  // float4 per U bin row
+    const int nt = static_cast<int>(nbo - mp0 < 4 ? nbo - mp0 : 4);
+    for (int slot0 = 0; slot0 < nslot; slot0 += BAND2_SLOTS) {
+        const int ns = min(BAND2_SLOTS, nslot - slot0);
         __syncthreads();
-        for (int i = threadIdx.x; i < ns * 4 * 10; i += blockDim.x) {
-            const int kk = i % 10, t = (i / 10) % 4, sl = i / 40;
+        for (int i = threadIdx.x; i < ns * 4; i += blockDim.x) {
+            const int sl = i >> 2, t = i & 3;
             const int slot = slot0 + sl;
             const int bi = slot / s, q = slot - bi * s;
             const int64_t m = mp0 + t;
-            float2 v = make_float2(0.f, 0.f);
             const int kq = static_cast<int>(m) + wout * q;
-            const int idx = kq > half ? win - kq : kq;
-            if (m < nbo && kk < K) v = __ldg(psi_hat + ((po + bi) * nbi + idx) * K + kk);
-            reinterpret_cast<float2*>(&ps[sl][t][0])[kk] = v;
-            if (kk == 0) {
-                const int o = bi * static_cast<int>(nbi) + (m < nbo ? idx : 0);
-                uo[sl][t] = kq > half ? ~o : o;
+            const bool fold = kq > half;
+            const int idx = fold ? win - kq : kq;
+            const float sg = fold ? -1.f : 1.f;
+            const float2* src = psi_hat + ((po + bi) * nbi + idx) * K;
+#pragma unroll
+            for (int kk = 0; kk < 9; ++kk) {
+                float2 v = make_float2(0.f, 0.f);
+                if (m < nbo && kk < K) v = __ldg(src + kk);
+                ps[sl][t][kk] = make_float4(v.x, v.y, sg * v.x, -sg * v.y);
             }
+            uo[sl][t] = bi * static_cast<int>(nbi) + (m < nbo ? idx : 0);
         }
         __syncthreads();
         const bool mact = mp < nbo;
@@ -322,95 +321,79 @@ __global__ void __launch_bounds__(4 * LANES) disco_band2_kernel(
             for (int64_t c0 = 0; c0 < C; c0 += CP) {
                 const int64_t c = c0 + 2 * cl;
                 const int cn = static_cast<int>(C - c0 < CP ? C - c0 : CP);
-                f2x re[9], im[9];
+                float2 re[9], im[9];
 #pragma unroll
-                for (int k = 0; k < 9; ++k) re[k] = im[k] = 0ull;
+                for (int k = 0; k < 9; ++k) re[k] = im[k] = make_float2(0.f, 0.f);
                 if (mact && c < C) {
-                    const float4* Ub = reinterpret_cast<const float4*>(U + (b * Hin + h0) * nbi * C + c);
+                    const float4* Ub = U + ((b * Hin + h0) * nbi * C + c) / 2;
                     constexpr int CH = 4;
                     float4 ua[CH], ub[CH];
-                    int oa[CH], ob[CH];
-                    auto load = [&](int sl0, float4 (&u)[CH], int (&o)[CH]) {
+                    auto load = [&](int sl0, float4 (&u)[CH]) {
 #pragma unroll
                         for (int j = 0; j < CH; ++j) {
                             const int sl = sl0 + j;
-                            o[j] = sl < ns ? uo[sl][mi] : 0;
-                            const int oo = o[j] < 0 ? ~o[j] : o[j];
-                            u[j] = sl < ns ? __ldg(Ub + static_cast<int64_t>(oo) * C2) : make_float4(0.f, 0.f, 0.f, 0.f);
+                            u[j] = sl < ns ? __ldg(Ub + static_cast<int64_t>(uo[sl][mi]) * C2)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
                         }
                     };
-                    auto consume = [&](int sl0, const float4 (&u)[CH], const int (&o)[CH]) {
+                    auto consume = [&](int sl0, const float4 (&u)[CH]) {
 #pragma unroll
                         for (int j = 0; j < CH; ++j) {
                             if (sl0 + j >= ns) break;
                             const float4* pp = &ps[sl0 + j][mi][0];
-                            float2 p[10];
-#pragma unroll
-                            for (int k2 = 0; k2 < 5; ++k2) {
-                                const float4 t4 = pp[k2];
-                                p[2 * k2] = make_float2(t4.x, t4.y);
-                                p[2 * k2 + 1] = make_float2(t4.z, t4.w);
-                            }
-                            // re += px ux + py uy; im += px vx - py vy, (vx, vy) = sy (uy, ux)
-                            const bool cj = o[j] < 0;
-                            const f2x UX = pk2(u[j].x, u[j].z), UY = pk2(u[j].y, u[j].w);
-                            const f2x V1 = cj ? pk2(-u[j].y, -u[j].w) : UY;
-                            const f2x V2 = cj ? UX : pk2(-u[j].x, -u[j].z);
+                            const float2 UX = make_float2(u[j].x, u[j].y), UY = make_float2(u[j].z, u[j].w);
 #pragma unroll
                             for (int k = 0; k < 9; ++k) {
-                                ffma2(re[k], p[k].y, UY);
-                                ffma2(re[k], p[k].x, UX);
-                                ffma2(im[k], p[k].y, V2);
-                                ffma2(im[k], p[k].x, V1);
+                                const float4 qv = pp[k];
+                                ffma2(re[k], qv.y, UY);
+                                ffma2(re[k], qv.x, UX);
+                                ffma2(im[k], qv.z, UY);
+                                ffma2(im[k], qv.w, UX);
                             }
                         }
                     };
-                    load(0, ua, oa);
+                    load(0, ua);
                     for (int sl0 = 0; sl0 < ns; sl0 += 2 * CH) {
-                        if (sl0 + CH < ns) load(sl0 + CH, ub, ob);
-                        consume(sl0, ua, oa);
+                        if (sl0 + CH < ns) load(sl0 + CH, ub);
+                        consume(sl0, ua);
                         if (sl0 + CH >= ns) break;
-                        if (sl0 + 2 * CH < ns) load(sl0 + 2 * CH, ua, oa);
-                        consume(sl0 + CH, ub, ob);
+                        if (sl0 + 2 * CH < ns) load(sl0 + 2 * CH, ua);
+                        consume(sl0 + CH, ub);
                     }
                 }
                 __syncthreads();
 #pragma unroll
                 for (int k = 0; k < 9; ++k)
                     if (k < K) {
-                        so[mi][0][(2 * cl) * K + k] = lo2(re[k]);
-                        so[mi][0][(2 * cl + 1) * K + k] = hi2(re[k]);
-                        so[mi][1][(2 * cl) * K + k] = lo2(im[k]);
-                        so[mi][1][(2 * cl + 1) * K + k] = hi2(im[k]);
+                        so[mi][0][(2 * cl) * K + k] = re[k].x;
+                        so[mi][0][(2 * cl + 1) * K + k] = re[k].y;
+                        so[mi][1][(2 * cl) * K + k] = im[k].x;
+                        so[mi][1][(2 * cl + 1) * K + k] = im[k].y;
                     }
                 __syncthreads();
+                // contiguous rows of cn * K floats per (order, re/im)
                 const int rowlen = cn * K;
-                const int nt = static_cast<int>(nbo - mp0 < 4 ? nbo - mp0 : 4);
-                if ((rowlen & 3) == 0 && (ldS & 3) == 0 && ((c0 * K) & 3) == 0) {
-                    const int q4 = rowlen >> 2;
-                    for (int i = threadIdx.x; i < nt * 2 * q4; i += blockDim.x) {
-                        const int r = i / q4, j = i - r * q4;
-                        const int t = r >> 1, ri = r & 1;
-                        const int64_t row = ((b * Hout + h) * nbo + mp0 + t) * 2 + ri;
-                        float4* dst = reinterpret_cast<float4*>(S + row * ldS + c0 * K) + j;
-                        float4 v = reinterpret_cast<const float4*>(&so[t][ri][0])[j];
-                        if (slot0 != 0) {
-                            const float4 o = *dst;
-                            v.x += o.x;
-                            v.y += o.y;
-                            v.z += o.z;
-                            v.w += o.w;
+                const bool vec = (rowlen & 3) == 0 && (ldS & 3) == 0 && ((c0 * K) & 3) == 0;
+                for (int r = 0; r < nt * 2; ++r) {
+                    const int t = r >> 1, ri = r & 1;
+                    float* drow = S + (((b * Hout + h) * nbo + mp0 + t) * 2 + ri) * ldS + c0 * K;
+                    const float* srow = &so[t][ri][0];
+                    if (vec) {
+                        for (int j = threadIdx.x; j < (rowlen >> 2); j += blockDim.x) {
+                            float4 v = reinterpret_cast<const float4*>(srow)[j];
+                            float4* dst = reinterpret_cast<float4*>(drow) + j;
+                            if (slot0 != 0) {
+                                const float4 o = *dst;
+                                v.x += o.x;
+                                v.y += o.y;
+                                v.z += o.z;
+                                v.w += o.w;
+                            }
+                            *dst = v;
                         }
-                        *dst = v;
-                    }
-                } else {
-                    for (int i = threadIdx.x; i < nt * 2 * rowlen; i += blockDim.x) {
-                        const int r = i / rowlen, j = i - r * rowlen;
-                        const int t = r >> 1, ri = r & 1;
-                        const int64_t row = ((b * Hout + h) * nbo + mp0 + t) * 2 + ri;
-                        float* dst = S + row * ldS + c0 * K + j;
-                        const float v = so[t][ri][j];
-                        *dst = slot0 != 0 ? *dst + v : v;
+                    } else {
+                        for (int j = threadIdx.x; j < rowlen; j += blockDim.x)
+                            drow[j] = slot0 != 0 ? drow[j] + srow[j] : srow[j];
                     }
                 }
             }
@@ -724,6 +707,14 @@ void DiscoPlan::input_rows(int64_t ho0, int64_t nout, int64_t* lo, int64_t* n) c
     *n = b - a;
 }
 
+bool DiscoPlan::pair_layout(int64_t cin) const {
+    static const int band_mode = [] {
+        const char* e = std::getenv("SPH_DISCO_BAND");
+        return e ? std::atoi(e) : 2;
+    }();
+    return cin % 2 == 0 && band_mode == 2;
+}
+
 void DiscoPlan::apply(const float* x, const float* mix, int64_t B, int64_t cin, int64_t cout,
                       float* y, void* ws, cudaStream_t st) {
     apply_rows(x, 0, hin, 0, hout, mix, B, cin, cout, y, ws, st);
@@ -802,20 +793,17 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
     if (make_u)
         (*make_u)(U);
     else
-        fft_forward_cminor(fft_in, x, B, cin, nin, static_cast<int>(nbi), U, st);
+        fft_forward_cminor(fft_in, x, B, cin, nin, static_cast<int>(nbi), U, st, pair_layout(cin) ? 2 : 0);
     dim3 grid(static_cast<unsigned>((nbo + 3) / 4), static_cast<unsigned>(nout));
     require(nout <= 65535, "disco: grid too large");
     {
         // algorithmic bytes: U read once, S written once
         ProfScope prof("disco_band", st, 8.0 * B * nin * nbi * cin + 4.0 * B * nout * nbo * 2 * cin * K);
-        static const int band_mode = [] {
-            const char* e = std::getenv("SPH_DISCO_BAND");
-            return e ? std::atoi(e) : 2;
-        }();
-        if (cin % 2 == 0 && band_mode == 2)
-            disco_band2_kernel<32><<<grid, 128, 0, st>>>(U, d_psi_hat.p, d_band0.p, d_bandc.p, d_psi_off.p, nin, nbi,
-                                                         nout, nbo, static_cast<int>(win), static_cast<int>(wout),
-                                                         static_cast<int>(stride), K, cin, w.ldS, S, h_in0, ho0, B);
+        if (pair_layout(cin))
+            disco_band2_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const float4*>(U), d_psi_hat.p, d_band0.p,
+                                                     d_bandc.p, d_psi_off.p, nin, nbi, nout, nbo,
+                                                     static_cast<int>(win), static_cast<int>(wout),
+                                                     static_cast<int>(stride), K, cin, w.ldS, S, h_in0, ho0, B);
         else
             disco_band_kernel<<<grid, 256, 0, st>>>(U, d_psi_hat.p, d_band0.p, d_bandc.p, d_psi_off.p, nin, nbi, nout,
                                                     nbo, static_cast<int>(win), static_cast<int>(wout),

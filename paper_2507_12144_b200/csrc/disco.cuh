@@ -73,6 +73,8 @@ struct DiscoPlan {
     void apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t ho0, int64_t nout,
                     const float* mix, int64_t B, int64_t cin, int64_t cout, float* y, void* ws,
                     cudaStream_t st, const std::function<void(float2*)>* make_u = nullptr);
+    // U layout of the band stage: channel pairs interleaved (FFMA2 band kernel) for even cin
+    bool pair_layout(int64_t cin) const;
     void input_rows(int64_t ho0, int64_t nout, int64_t* lo, int64_t* n) const;
     int64_t rows_workspace_bytes(int64_t B, int64_t cin, int64_t cout, int64_t nin, int64_t nout) const;
     // v [B][cout][hout][wout] on the output grid -> y [B][cin][hin][win] on the input grid

@@ -507,7 +507,8 @@ struct PlainInvIO {
 
 // channel-minor forward (DISCO input): block (c-tile of 2P channels, row hi, batch b).
 // planar = 0: U[b][hi][m][c] complex; planar = 1 (DISCO transpose): real planes
-// U[((b*H + hi)*nbins + m)*2 + re/im][c] so a GEMM can take re and im rows with K = c.
+// U[((b*H + hi)*nbins + m)*2 + re/im][c] so a GEMM can take re and im rows with K = c;
+// planar = 2 (DISCO band, even C): per bin, channel pairs as (re c, re c+1, im c, im c+1).
 struct CminorIO {
     const float* x;
     int64_t C, H;
@@ -554,7 +555,13 @@ struct CminorIO {
             const float2 zc = buf[j * ld + (m == 0 ? 0 : n - m)];
             const float2 v = (cl & 1) ? make_float2(0.5f * (z.y + zc.y), -0.5f * (z.x - zc.x))
                                       : make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y - zc.y));
-            if (planar) {
+            if (planar == 2) {
+                // channel-pair interleaved: (re c, re c+1, im c, im c+1) per even c
+                const int64_t cc = c0 + cl;
+                float* pu = reinterpret_cast<float*>(Ub) + (static_cast<int64_t>(m) * C + (cc & ~1LL)) * 2 + (cc & 1);
+                pu[0] = v.x;
+                pu[2] = v.y;
+            } else if (planar) {
                 float* pm = Up + static_cast<int64_t>(m) * 2 * ldp + c0 + cl;
                 pm[0] = v.x;
                 pm[ldp] = v.y;
@@ -963,11 +970,12 @@ void fft_inverse_plain(const FftPlan& fp, const float2* bins, int64_t nrings, in
 }
 
 void fft_forward_cminor(const FftPlan& fp, const float* x, int64_t B, int64_t C, int64_t H,
-                        int nbins, float2* U, cudaStream_t st, bool planar, int64_t ldp) {
+                        int nbins, float2* U, cudaStream_t st, int planar, int64_t ldp) {
     if (B * C * H == 0) return;
+    require(planar != 2 || C % 2 == 0, "disco fft: pair-interleaved layout needs an even channel count");
     require(H <= 65535 && B <= 65535, "disco fft: too many rows");
     const int P = rpb_of(fp);
-    CminorIO io{x, C, H, nbins, U, planar ? 1 : 0, ldp > 0 ? ldp : C};
+    CminorIO io{x, C, H, nbins, U, planar, ldp > 0 ? ldp : C};
     dim3 grid(static_cast<unsigned>((C + 2 * P - 1) / (2 * P)), static_cast<unsigned>(H),
               static_cast<unsigned>(B));
     if (fp.fft4_n1 && FOLD_THREADS == fft4::THREADS) {

@@ -61,9 +61,10 @@ void fft_inverse_plain(const FftPlan& fp, const float2* bins, int64_t nrings, in
                        float scale, float* rings, cudaStream_t st);
 
 // Channel-minor forward transform for DISCO: x [B][C][H][n] ->
-// U [B][H][nbins][C] complex (bins m < nbins, unscaled).
+// U [B][H][nbins][C] complex (bins m < nbins, unscaled).  planar = 1: real planes
+// [(b, h, m, re/im)][ldp]; planar = 2: channel pairs interleaved (re c, re c+1, im c, im c+1).
 void fft_forward_cminor(const FftPlan& fp, const float* x, int64_t B, int64_t C, int64_t H,
-                        int nbins, float2* U, cudaStream_t st, bool planar = false, int64_t ldp = 0);
+                        int nbins, float2* U, cudaStream_t st, int planar = 0, int64_t ldp = 0);
 // channel-minor C2R: half spectra V[B][H][nbins][C] -> rings y[B][C][H][n] * scale
 void fft_inverse_cminor(const FftPlan& fp, const float2* V, int64_t B, int64_t C, int64_t H, int nbins,
                         float scale, float* y, cudaStream_t st);
