@@ -754,6 +754,17 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
             g->Blo = {nullptr, cout, cin * K, w.ldS};
             g->store = STORE_TRANS;
             g->bn = cout >= 256 ? 256 : 128;
+            static const int alo_mode = [] {
+                const char* e = std::getenv("SPH_DISCO_ALO");
+                return e ? std::atoi(e) : 1;
+            }();
+            if (alo_mode == 1 && prec != SPH_PREC_FP32_SIMT && cout <= 128) {
+                // BK = 32 kernel: half the k-block rounds of the BK = 16 one at K = cin * 9
+                // (decoder 64 -> 64: 4.26 -> 3.23 ms); with two N tiles (cout 256) the
+                // BN = 256 BK = 16 kernel stays faster (1.42 vs 1.63 ms at cfg3)
+                g->alo = true;
+                g->bn = cout <= 64 ? 64 : 128;
+            }
             g->name = "gemm_disco_mix";
             require(B * rows_per_b < (1LL << 31), "disco: batch too large for one call");
             for (int64_t b = 0; b < B; ++b) {

@@ -1035,6 +1035,14 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
         tc::launch<192, 3, 2, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 192 && cl == 4)
         tc::launch<192, 3, 4, true>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.alo && g.bn == 128 && cl == 1)
+        tc::launch<128, 3, 1, true>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.alo && g.bn == 128 && cl == 2)
+        tc::launch<128, 3, 2, true>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.alo && g.bn == 64 && cl == 1)
+        tc::launch<64, 4, 1, true>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.alo && g.bn == 64 && cl == 2)
+        tc::launch<64, 4, 2, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 256 && cl == 1)
         tc::launch<256, 4, 1>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 256 && cl == 2)
@@ -1121,13 +1129,14 @@ void GroupedGemm::finalize() {
         const int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) cluster = v;
     }
-    if (bn == 128 && cluster > 2) cluster = 2;
+    if (alo && bn != 64 && bn != 128) alo = false;
+    if ((bn == 128 || alo) && cluster > 2) cluster = 2;
     require(!a_quad || (bn == 192 && a_rows_g > 0 && a_kq > 0), "gemm: quad A layout needs the bn=192 kernel");
     // CTA-pair MMA for the BN = 192 (ALO) GEMMs when there are >= 2 M-tiles per group
     pair = bn == 192 && mtiles >= 2;
     if (const char* e = std::getenv("SPH_GEMM_PAIR")) pair = pair && std::atoi(e) != 0;
     // TMA-store epilogue when D is a uniform [group][rows][ldd] array (the Legendre GEMMs)
-    tma_store = bn == 192 && !groups.empty();
+    tma_store = (bn == 192 || alo) && !groups.empty();
     d_rows = 0;
     d_ldd = 0;
     int64_t gmax = 0;
