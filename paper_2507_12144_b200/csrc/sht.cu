@@ -119,41 +119,69 @@ void upload(DevBuf<T>& d, const std::vector<T>& h) {
 }
 
 // ---------------------------------------------------------------- kernels
-__global__ void cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int64_t lmax,
-                                     int64_t m0, int64_t mcount, int64_t out_mcount, int Lp,
-                                     float2* __restrict__ dense) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= F * lmax * out_mcount) return;
-    const int64_t ml = i % out_mcount;
-    const int64_t l = (i / out_mcount) % lmax;
-    const int64_t f = i / (out_mcount * lmax);
-    float2 v = make_float2(0.f, 0.f);
-    const int64_t m = m0 + ml;
-    if (ml < mcount && l >= m) {
-        const int64_t p = (l - m) & 1, lp = (l - m) >> 1;
-        const int64_t row = (ml * 2 + p) * 2 * F + 2 * f;
-        v = make_float2(cint[row * Lp + lp], cint[(row + 1) * Lp + lp]);
+// Internal coefficient layout cint[(ml*2 + p)][2F (f, re/im)][Lp] (l = m + p + 2 lp,
+// lp contiguous) <-> dense [F][lmax][mcols] complex (m contiguous): tiled transposes
+// through shared memory so both sides are read / written in contiguous runs (the
+// element-wise form read cint with a stride of 2F*Lp floats: 3 ms at 512 x 721 x 720).
+// CTA (32 orders, 64 degrees, field f): the (m, p, re/im) rows are read as 33-lane runs
+// of lp covering the tile's degrees, the dense rows written as 32-order runs.
+template <int LT>
+__global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int64_t lmax,
+                                                            int64_t m0, int64_t mcount, int64_t out_mcount, int Lp,
+                                                            float2* __restrict__ dense, int64_t f0) {
+    __shared__ float2 tile[LT][33];
+    const int mt = blockIdx.x * 32, lt = blockIdx.y * LT;
+    const int64_t f = f0 + blockIdx.z;
+    for (int e = threadIdx.x; e < LT * 32; e += blockDim.x) tile[e >> 5][e & 31] = make_float2(0.f, 0.f);
+    __syncthreads();
+    constexpr int NLP = LT / 2 + 1;
+    for (int e = threadIdx.x; e < 32 * 2 * 2 * NLP; e += blockDim.x) {
+        const int lpl = e % NLP, r = e / NLP;
+        const int ri = r & 1, p = (r >> 1) & 1, mlt = r >> 2;
+        const int ml = mt + mlt;
+        if (ml >= mcount) continue;
+        const int m = static_cast<int>(m0) + ml;
+        const int d = lt - m - p;
+        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lpl;
+        const int l = m + p + 2 * lp;
+        if (lp >= Lp || l >= lmax || l >= lt + LT) continue;
+        const int64_t row = (static_cast<int64_t>(ml) * 2 + p) * 2 * F + 2 * f + ri;
+        reinterpret_cast<float*>(&tile[l - lt][mlt])[ri] = cint[row * Lp + lp];
     }
-    dense[i] = v;
+    __syncthreads();
+    for (int e = threadIdx.x; e < LT * 32; e += blockDim.x) {
+        const int ll = e >> 5, mlt = e & 31;
+        const int64_t l = lt + ll;
+        const int oc = mt + mlt;
+        if (l < lmax && oc < out_mcount) dense[(f * lmax + l) * out_mcount + oc] = tile[ll][mlt];
+    }
 }
 
-__global__ void dense_to_cint_kernel(const float2* __restrict__ dense, int64_t F, int64_t lmax,
-                                     int64_t mmax, int Lp, float* __restrict__ cint) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t twoF = 2 * F;
-    if (i >= mmax * 2 * twoF * Lp) return;
-    const int64_t lp = i % Lp;
-    const int64_t n = (i / Lp) % twoF;
-    const int64_t g = i / (Lp * twoF);
-    const int64_t m = g >> 1, p = g & 1;
-    const int64_t l = m + p + 2 * lp;
-    float v = 0.f;
-    if (l < lmax) {
-        const int64_t f = n >> 1;
-        const float2 c = dense[(f * lmax + l) * mmax + m];
-        v = (n & 1) ? c.y : c.x;
+// CTA (32 orders, 32 lp, field f): the degrees l = m + p + 2 lp of the tile span 96 dense
+// rows, loaded as 32-order runs; the cint rows are written as 32-lp runs.
+__global__ void __launch_bounds__(256) dense_to_cint_kernel(const float2* __restrict__ dense, int64_t F, int64_t lmax,
+                                                            int64_t mmax, int Lp, float* __restrict__ cint,
+                                                            int64_t f0) {
+    __shared__ float2 tile[96][33];
+    const int mt = blockIdx.x * 32, lpt = blockIdx.y * 32;
+    const int64_t f = f0 + blockIdx.z;
+    const int lbase = mt + 2 * lpt;
+    for (int e = threadIdx.x; e < 96 * 32; e += blockDim.x) {
+        const int ll = e >> 5, mlt = e & 31;
+        const int64_t l = lbase + ll;
+        const int m = mt + mlt;
+        tile[ll][mlt] = (l < lmax && m < mmax) ? dense[(f * lmax + l) * mmax + m] : make_float2(0.f, 0.f);
     }
-    cint[i] = v;
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 2 * 2 * 32; e += blockDim.x) {
+        const int lpl = e & 31, r = e >> 5;
+        const int ri = r & 1, p = (r >> 1) & 1, mlt = r >> 2;
+        const int m = mt + mlt, lp = lpt + lpl;
+        if (m >= mmax || lp >= Lp) continue;
+        const int l = m + p + 2 * lp;
+        const float v = l < lmax ? reinterpret_cast<const float*>(&tile[mlt + p + 2 * lpl][mlt])[ri] : 0.f;
+        cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp] = v;
+    }
 }
 
 // bins [F][nlat][mcount] complex (scaled by 2pi/nlon) -> EO_loc [mcount][2][Rp/4][2F][4]
@@ -185,21 +213,30 @@ __global__ void fold_bins_kernel(const float2* __restrict__ bins, const int2* __
 
 void cint_to_dense(const ShtPlan& p, const float* cint, int64_t F, int64_t m0, int64_t mcount,
                    int64_t out_mcount, float* dense, cudaStream_t st) {
-    const int64_t n = F * p.lmax * out_mcount;
-    if (n == 0) return;
-    cint_to_dense_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
-        cint, F, p.lmax, m0, mcount, out_mcount, p.Lp, reinterpret_cast<float2*>(dense));
-    SPH_LAUNCH_CHECK();
-    count_launch();
+    if (F * p.lmax * out_mcount == 0) return;
+    ProfScope prof("sht_to_dense", st, 16.0 * F * p.lmax * out_mcount);
+    for (int64_t f0 = 0; f0 < F; f0 += 65535) {
+        constexpr int LT = 128;
+        dim3 grid(static_cast<unsigned>((out_mcount + 31) / 32), static_cast<unsigned>((p.lmax + LT - 1) / LT),
+                  static_cast<unsigned>(std::min<int64_t>(65535, F - f0)));
+        cint_to_dense_kernel<LT><<<grid, 256, 0, st>>>(cint, F, p.lmax, m0, mcount, out_mcount, p.Lp,
+                                                       reinterpret_cast<float2*>(dense), f0);
+        SPH_LAUNCH_CHECK();
+        count_launch();
+    }
 }
 
 void dense_to_cint(const ShtPlan& p, const float* dense, int64_t F, float* cint, cudaStream_t st) {
-    const int64_t n = p.mmax * 2 * 2 * F * p.Lp;
-    if (n == 0) return;
-    dense_to_cint_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
-        reinterpret_cast<const float2*>(dense), F, p.lmax, p.mmax, p.Lp, cint);
-    SPH_LAUNCH_CHECK();
-    count_launch();
+    if (p.mmax * F * p.Lp == 0) return;
+    ProfScope prof("sht_from_dense", st, 8.0 * F * p.lmax * p.mmax + 16.0 * F * p.mmax * p.Lp);
+    for (int64_t f0 = 0; f0 < F; f0 += 65535) {
+        dim3 grid(static_cast<unsigned>((p.mmax + 31) / 32), static_cast<unsigned>((p.Lp + 31) / 32),
+                  static_cast<unsigned>(std::min<int64_t>(65535, F - f0)));
+        dense_to_cint_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(dense), F, p.lmax, p.mmax,
+                                                   p.Lp, cint, f0);
+        SPH_LAUNCH_CHECK();
+        count_launch();
+    }
 }
 
 void ShtPlan::create(int kind_, int64_t nlat_, int64_t nlon_, int64_t lmax_, int64_t mmax_,
