@@ -197,6 +197,11 @@ class _Pending:
         if self.y is not None:
             return self.y, self.parts_to
         self.work.wait()  # the current stream waits for the NCCL stream
+        if self.dim_from == 0:
+            # blocks stacked along the outermost dimension: the receive buffer is the result
+            full = list(self.shapes[0])
+            full[0] = sum(s[0] for s in self.shapes)
+            return self.recv.view(full), self.parts_to
         out_splits = [int(torch.Size(s).numel()) for s in self.shapes]
         blocks = list(torch.split(self.recv, out_splits))
         y = torch.cat([b.view(s) for b, s in zip(blocks, self.shapes)], dim=self.dim_from)
@@ -215,9 +220,14 @@ def distributed_transpose_start(ctx: DistContext, x: torch.Tensor, axis: int, di
         ctx.log.record(AXIS_NAMES[axis], "all_to_all", 0)
         return _Pending(y=x, parts_to=parts_to)
     me = ctx.index(axis)
-    chunks = [x.narrow(dim_to, split_offset(parts_to, j), parts_to[j]).contiguous() for j in range(p)]
-    send = torch.cat([c.reshape(-1) for c in chunks])
-    in_splits = [c.numel() for c in chunks]
+    views = [x.narrow(dim_to, split_offset(parts_to, j), parts_to[j]) for j in range(p)]
+    in_splits = [v.numel() for v in views]
+    if dim_to == 0 and x.is_contiguous():
+        send = x.reshape(-1)  # outermost split: the chunks are already contiguous and in order
+    else:  # one packing pass straight into the send buffer
+        send = torch.empty(sum(in_splits), dtype=x.dtype, device=x.device)
+        for v, blk in zip(views, torch.split(send, in_splits)):
+            blk.view(v.shape).copy_(v)
     shapes = []
     for i in range(p):
         s = list(x.shape)
