@@ -298,10 +298,14 @@ __device__ __forceinline__ uint32_t make_idesc(int n, int m = BM) {  // m = 256:
     return d;
 }
 
-template <int BN, int STAGES, bool ALO = false, bool PAIR = false>
+// KS (ALO only): 32-wide SWIZZLE_128B atoms per pipeline stage.  The loads, conversions
+// and MMAs of a stage run per atom; its barrier waits, fences and commit once per stage.
+template <int BN, int STAGES, bool ALO = false, bool PAIR = false, int KS = 1>
 struct Smem {
-    static constexpr int A_TILE_BYTES = BM * bk_of<ALO>() * 4;
-    static constexpr int B_TILE_BYTES = (PAIR ? BN / 2 : BN) * bk_of<ALO>() * 4;  // PAIR: half
+    static constexpr int A_ATOM = BM * bk_of<ALO>() * 4;
+    static constexpr int B_ATOM = (PAIR ? BN / 2 : BN) * bk_of<ALO>() * 4;  // PAIR: half
+    static constexpr int A_TILE_BYTES = KS * A_ATOM;
+    static constexpr int B_TILE_BYTES = KS * B_ATOM;
     static constexpr int A_BYTES = ALO ? A_TILE_BYTES : 2 * A_TILE_BYTES;  // A or (A_hi, A_lo)
     static constexpr int STAGE_BYTES = A_BYTES + 2 * B_TILE_BYTES;
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
@@ -339,7 +343,7 @@ struct Smem {
 // barrier also counts the peer's table-half bytes (.cta_group::2 TMA), its conv / tempty
 // barriers take the peer's converter / epilogue arrivals (count 256), and its commits
 // multicast to both CTAs' empty / tfull barriers.
-template <int BN, int STAGES, int CL, bool ALO, bool PAIR = false>
+template <int BN, int STAGES, int CL, bool ALO, bool PAIR = false, int KS = 1>
 __global__ void __launch_bounds__(nthreads<ALO, PAIR>(), 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_bhi,
@@ -359,11 +363,13 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     constexpr int TR_N = 512;
     const int tr_off = dbg >> 8;  // k-block window start (SPH_GEMM_DEBUG high bits)
     const bool tr = trace != nullptr && blockIdx.x == 0;
-    using L = Smem<BN, STAGES, ALO, PAIR>;
+    using L = Smem<BN, STAGES, ALO, PAIR, KS>;
     static_assert(!PAIR || (ALO && CL == 2 && BN % 32 == 0), "pair mode: ALO, cluster of 2");
-    constexpr int KB = bk_of<ALO>();
+    static_assert(KS == 1 || ALO, "multi-atom stages: ALO variant");
+    constexpr int KB = bk_of<ALO>();   // atom width (fp32 of K)
+    constexpr int KST = KB * KS;       // K per pipeline stage
     constexpr int A_TILE_BYTES = L::A_TILE_BYTES;
-    static_assert(!ALO || 2 * BN + STAGES * KB <= 512, "TMEM budget");
+    static_assert(!ALO || 2 * BN + STAGES * KST <= 512, "TMEM budget");
     constexpr uint32_t TMEM_COLS = ALO ? 512 : 2 * BN;
     extern __shared__ uint8_t smem_raw[];
     // 1 KB alignment by pointer arithmetic on the __shared__ array (keeps the shared
@@ -424,20 +430,27 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    auto tmem_alo = [&](int s) { return tmem_base + 2 * BN + s * KB; };
+    auto tmem_alo = [&](int s) { return tmem_base + 2 * BN + s * KST; };
     const int crank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
     const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
     const uint16_t cmask = static_cast<uint16_t>((1u << CL) - 1);
     constexpr int B_ROWS = PAIR ? BN / 2 : BN / CL;  // table rows loaded by this CTA
     // PAIR: instruction N = N rounded up to 32; the peer's half starts at ninst / 2
     auto pair_half = [](const GemmWork& w) { return (w.nrem + 31) / 32 * 16; };
-    auto load_a = [&](int s, const GemmWork& w, int kb) {
+    // atom ka (K offset ka * KB) of the data tile into atom slot a of stage s
+    auto load_a1 = [&](int s, int a, const GemmWork& w, int ka) {
+        const uint32_t dst = a_hi(s) + a * L::A_ATOM;
         if (ALO && a_quad == 2)  // wide map: 32-row blocks of 512 B
-            tma_load_4d(a_hi(s), &map_a, 0, (w.m0 + crank * BM) / 32, kb * (KB / 4), w.ag, full_bar(s));
+            tma_load_4d(dst, &map_a, 0, (w.m0 + crank * BM) / 32, ka * (KB / 4), w.ag, full_bar(s));
         else if (ALO && a_quad)
-            tma_load_4d(a_hi(s), &map_a, 0, w.m0 + crank * BM, kb * (KB / 4), w.ag, full_bar(s));
+            tma_load_4d(dst, &map_a, 0, w.m0 + crank * BM, ka * (KB / 4), w.ag, full_bar(s));
         else
-            tma_load_2d(a_hi(s), &map_a, kb * KB, w.a_row + crank * BM, full_bar(s));
+            tma_load_2d(dst, &map_a, ka * KB, w.a_row + crank * BM, full_bar(s));
+    };
+    // atoms of stage k-block kb that hold K (the last stage of a tile may be partial)
+    auto natoms_of = [&](const GemmWork& w, int kb) { return min(KS, (w.K - kb * KST + KB - 1) / KB); };
+    auto load_a = [&](int s, const GemmWork& w, int kb, int na) {
+        for (int a = 0; a < na; ++a) load_a1(s, a, w, kb * KS + a);
     };
     // L2 prefetch of a data tile k-block (same box as load_a)
     auto prefetch_a = [&](const GemmWork& w, int kb) {
@@ -448,8 +461,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         else
             tma_prefetch_2d(&map_a, kb * KB, w.a_row + crank * BM);
     };
-    auto adesc = [&](int s, int kk) {  // A operand of k-step kk (8 fp32 of K)
-        return (ALO && a_quad) ? make_sdesc_quad(a_hi(s) + kk * 2 * 2048) : make_sdesc<KB>(a_hi(s) + kk * 32);
+    // operands of k-step kk (8 fp32 of K) of a stage: atom kk / 4, 32-byte step kk % 4
+    // (quad layout: the atoms' k-quads are contiguous 2 KB blocks)
+    auto adesc = [&](int s, int kk) {
+        return (ALO && a_quad) ? make_sdesc_quad(a_hi(s) + kk * 2 * 2048)
+                               : make_sdesc<KB>(a_hi(s) + (kk / (KB / 8)) * L::A_ATOM + (kk % (KB / 8)) * 32);
+    };
+    auto bdesc = [&](uint32_t base, int kk) {
+        return make_sdesc<KB>(base + (kk / (KB / 8)) * L::B_ATOM + (kk % (KB / 8)) * 32);
     };
     // each role walks tiles cid, cid + ncl, ... and loads the next descriptor one tile ahead
     GemmWork wnext{};
@@ -468,52 +487,60 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             uint32_t ph = 0;
             for (int t = cid; t < ntiles; t += ncl) {
                 const GemmWork w = next_work(t);
-                const int nkb = (w.K + KB - 1) / KB;
+                const int nkb = (w.K + KST - 1) / KST;
                 const bool has_next = t + ncl < ntiles;
                 const GemmWork wn = wnext;  // next tile's descriptor (loaded a tile ahead)
-                const int nkb_n = (wn.K + KB - 1) / KB;
+                const int nkb_n = (wn.K + KST - 1) / KST;
                 for (int kb = 0; kb < nkb; ++kb, ++j) {
                     // data-tile L2 prefetch pf k-blocks ahead (HBM latency dominates the
                     // ring's round trip; SMEM and TMEM allow no further stages)
                     if (pf > 0) {
                         const int kp = kb + pf;
                         if (kp < nkb)
-                            prefetch_a(w, kp);
+                            prefetch_a(w, kp * KS);
                         else if (has_next && kp - nkb < nkb_n)
-                            prefetch_a(wn, kp - nkb);
+                            prefetch_a(wn, (kp - nkb) * KS);
                     }
                     mbar_wait(empty_bar(s), ph ^ 1);
                     if (tr && j >= tr_off && j - tr_off < TR_N) trace[j - tr_off] = clock64();
+                    const int na = natoms_of(w, kb);
                     if (dbg & 8) {
-                        mbar_expect_tx(full_bar(s), A_TILE_BYTES);
-                        load_a(s, w, kb);
+                        mbar_expect_tx(full_bar(s), na * L::A_ATOM);
+                        load_a(s, w, kb, na);
                         if (++s == STAGES) { s = 0; ph ^= 1; }
                         continue;
                     }
                     if constexpr (PAIR) {
                         // leader's full barrier: own A + both CTAs' table halves; peer's: A
-                        const int nb = (three_pass ? 2 : 1) * L::B_TILE_BYTES;
-                        mbar_expect_tx(full_bar(s), A_TILE_BYTES + (crank == 0 ? 2 * nb : 0));
-                        load_a(s, w, kb);
+                        const int nb = (three_pass ? 2 : 1) * na * L::B_ATOM;
+                        mbar_expect_tx(full_bar(s), na * L::A_ATOM + (crank == 0 ? 2 * nb : 0));
+                        load_a(s, w, kb, na);
                         const int brow = w.b_row + crank * pair_half(w);
-                        tma_load_2d_pair(b_hi(s), &map_bhi, kb * KB, brow, full_bar(s));
-                        if (three_pass) tma_load_2d_pair(b_lo(s), &map_blo, kb * KB, brow, full_bar(s));
+                        for (int a = 0; a < na; ++a) {
+                            const int kx = (kb * KS + a) * KB;
+                            tma_load_2d_pair(b_hi(s) + a * L::B_ATOM, &map_bhi, kx, brow, full_bar(s));
+                            if (three_pass)
+                                tma_load_2d_pair(b_lo(s) + a * L::B_ATOM, &map_blo, kx, brow, full_bar(s));
+                        }
                         if (++s == STAGES) { s = 0; ph ^= 1; }
                         continue;
                     }
-                    mbar_expect_tx(full_bar(s), A_TILE_BYTES + (three_pass ? 2 : 1) * L::B_TILE_BYTES);
-                    load_a(s, w, kb);
-                    if (CL == 1) {
-                        tma_load_2d(b_hi(s), &map_bhi, kb * KB, w.b_row, full_bar(s));
-                        if (three_pass)
-                            tma_load_2d(b_lo(s), &map_blo, kb * KB, w.b_row, full_bar(s));
-                    } else {
-                        const uint32_t off = crank * B_ROWS * KB * 4;
-                        tma_load_2d_mc(b_hi(s) + off, &map_bhi, kb * KB,
-                                       w.b_row + crank * B_ROWS, full_bar(s), cmask);
-                        if (three_pass)
-                            tma_load_2d_mc(b_lo(s) + off, &map_blo, kb * KB,
-                                           w.b_row + crank * B_ROWS, full_bar(s), cmask);
+                    mbar_expect_tx(full_bar(s), na * (L::A_ATOM + (three_pass ? 2 : 1) * L::B_ATOM));
+                    load_a(s, w, kb, na);
+                    for (int a = 0; a < na; ++a) {
+                        const int kx = (kb * KS + a) * KB;
+                        if (CL == 1) {
+                            tma_load_2d(b_hi(s) + a * L::B_ATOM, &map_bhi, kx, w.b_row, full_bar(s));
+                            if (three_pass)
+                                tma_load_2d(b_lo(s) + a * L::B_ATOM, &map_blo, kx, w.b_row, full_bar(s));
+                        } else {
+                            const uint32_t off = a * L::B_ATOM + crank * B_ROWS * KB * 4;
+                            tma_load_2d_mc(b_hi(s) + off, &map_bhi, kx, w.b_row + crank * B_ROWS, full_bar(s),
+                                           cmask);
+                            if (three_pass)
+                                tma_load_2d_mc(b_lo(s) + off, &map_blo, kx, w.b_row + crank * B_ROWS,
+                                               full_bar(s), cmask);
+                        }
                     }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
@@ -527,7 +554,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
             int lt = 0;
             for (int t = cid; t < ntiles; t += ncl, ++lt) {
                 const GemmWork w = next_work(t);
-                const int nkb = (w.K + KB - 1) / KB;
+                const int nkb = (w.K + KST - 1) / KST;
                 const int acc = lt & 1;
                 const uint32_t aph = (lt >> 1) & 1;
                 const int nrem = w.nrem;
@@ -544,21 +571,21 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     mbar_wait(conv_bar(s), ph);  // converter waited full(s): data landed + A_lo
                     tc_fence_after();
                     if (tr && j >= tr_off && j - tr_off < TR_N) trace[3 * TR_N + j - tr_off] = clock64();
-                    const int ksteps = (dbg & 4) ? 0 : min(KB / 8, (w.K - kb * KB + 7) / 8);
+                    const int ksteps = (dbg & 4) ? 0 : min(KST / 8, (w.K - kb * KST + 7) / 8);
                     for (int kk = 0; kk < ksteps; ++kk) {
                         const uint64_t ahi = adesc(s, kk);
-                        const uint64_t bhi = make_sdesc<KB>(b_hi(s) + kk * 32);
+                        const uint64_t bhi = bdesc(b_hi(s), kk);
                         if constexpr (PAIR) {
                             tc_mma_tf32_pair(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
                             if (three_pass) {
-                                tc_mma_tf32_pair(tmem_d, ahi, make_sdesc<KB>(b_lo(s) + kk * 32), idesc, 1u);
+                                tc_mma_tf32_pair(tmem_d, ahi, bdesc(b_lo(s), kk), idesc, 1u);
                                 tc_mma_tf32_ts_pair(tmem_d, tmem_alo(s) + kk * 8, bhi, idesc, 1u);
                             }
                             continue;
                         }
                         tc_mma_tf32(tmem_d, ahi, bhi, idesc, (kb | kk) ? 1u : 0u);
                         if (three_pass) {
-                            tc_mma_tf32(tmem_d, ahi, make_sdesc<KB>(b_lo(s) + kk * 32), idesc, 1u);
+                            tc_mma_tf32(tmem_d, ahi, bdesc(b_lo(s), kk), idesc, 1u);
                             if constexpr (ALO)
                                 tc_mma_tf32_ts(tmem_d, tmem_alo(s) + kk * 8, bhi, idesc, 1u);
                             else
@@ -587,7 +614,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
         const bool trc = tr && (ct & 127) == 0;
         for (int t = cid; t < ntiles; t += ncl) {
             const GemmWork w = next_work(t);
-            const int nkb = (w.K + KB - 1) / KB;
+            const int nkb = (w.K + KST - 1) / KST;
             for (int kb = 0; kb < nkb; ++kb, ++j) {
                 mbar_wait(full_bar(s), ph);
                 if (trc && j >= tr_off && j - tr_off < TR_N) trace[TR_N + j - tr_off] = clock64();
@@ -598,9 +625,12 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                         // at chunk c ^ (r & 7): conflict-free for 8 consecutive rows)
                         const int q = warp & 3;
                         const int row = 32 * q + lane;
-                        const float4* rowp =
-                            reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase) + row * KB * 4);
-                        const float4* quadp = reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase)) + row;
+                        const int na = natoms_of(w, kb);
+                        for (int at = 0; at < na; ++at) {
+                        const float4* rowp = reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase) +
+                                                                             at * L::A_ATOM + row * KB * 4);
+                        const float4* quadp =
+                            reinterpret_cast<const float4*>(smem + (a_hi(s) - sbase) + at * L::A_ATOM) + row;
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             float lo[16];
@@ -613,7 +643,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                                 for (int e = 0; e < 4; ++e)
                                     lo[4 * c + e] = vv[e] - __uint_as_float(__float_as_uint(vv[e]) & 0xFFFFE000u);
                             }
-                            tmem_st16(tmem_alo(s) + 16 * h + (static_cast<uint32_t>(32 * q) << 16), lo);
+                            tmem_st16(tmem_alo(s) + at * KB + 16 * h + (static_cast<uint32_t>(32 * q) << 16), lo);
+                        }
                         }
                         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                         tc_fence_before();
@@ -860,13 +891,14 @@ static CUtensorMap make_map(const Mat2D& m, int box_rows, int kb) {
     return map;
 }
 
-template <int BN, int STAGES, int CL, bool ALO = false, bool PAIR = false>
+template <int BN, int STAGES, int CL, bool ALO = false, bool PAIR = false, int KS = 1>
 static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
                    float* D, bool three, cudaStream_t st, GemmEpi epi) {
     require(epi.mode == 0 || (!ALO && (epi.mode == 1) == (g.store == STORE_ROW)),
             "gemm: fused epilogue mode does not match the store mode / variant");
-    using L = Smem<BN, STAGES, ALO, PAIR>;
-    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL, ALO, PAIR>;
+    using L = Smem<BN, STAGES, ALO, PAIR, KS>;
+    static_assert(L::TOTAL <= 232448, "gemm: shared memory budget");
+    auto kern = gemm_tf32x3_kernel<BN, STAGES, CL, ALO, PAIR, KS>;
     static int grid = 0;
     static std::once_flag once;
     std::call_once(once, [&] {
@@ -1027,7 +1059,9 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
     const bool three = prec == SPH_PREC_3XTF32;
     require(!three || Blo, "gemm: 3xTF32 needs the lo table");
     const int cl = g.cluster;
-    if (g.bn == 192 && g.pair)
+    if (g.bn == 192 && g.pair && g.ks == 2)
+        tc::launch<192, 2, 2, true, true, 2>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.bn == 192 && g.pair)
         tc::launch<192, 4, 2, true, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 192 && cl == 1)
         tc::launch<192, 3, 1, true>(g, A, Bhi, Blo, D, three, st, epi);
@@ -1035,6 +1069,14 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
         tc::launch<192, 3, 2, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.bn == 192 && cl == 4)
         tc::launch<192, 3, 4, true>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.alo && g.ks == 2 && g.bn == 128 && cl == 1)
+        tc::launch<128, 2, 1, true, false, 2>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.alo && g.ks == 2 && g.bn == 128 && cl == 2)
+        tc::launch<128, 2, 2, true, false, 2>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.alo && g.ks == 2 && g.bn == 64 && cl == 1)
+        tc::launch<64, 3, 1, true, false, 2>(g, A, Bhi, Blo, D, three, st, epi);
+    else if (g.alo && g.ks == 2 && g.bn == 64 && cl == 2)
+        tc::launch<64, 3, 2, true, false, 2>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.alo && g.bn == 128 && cl == 1)
         tc::launch<128, 3, 1, true>(g, A, Bhi, Blo, D, three, st, epi);
     else if (g.alo && g.bn == 128 && cl == 2)
@@ -1130,6 +1172,9 @@ void GroupedGemm::finalize() {
         if (v == 1 || v == 2 || v == 4) cluster = v;
     }
     if (alo && bn != 64 && bn != 128) alo = false;
+    // two 32-wide atoms per pipeline stage (half the barrier rounds) for the pair and the
+    // narrow A_lo-in-TMEM kernels
+    if (const char* e = std::getenv("SPH_GEMM_KS")) ks = std::atoi(e) == 2 ? 2 : 1;
     if ((bn == 128 || alo) && cluster > 2) cluster = 2;
     require(!a_quad || (bn == 192 && a_rows_g > 0 && a_kq > 0), "gemm: quad A layout needs the bn=192 kernel");
     // CTA-pair MMA for the BN = 192 (ALO) GEMMs when there are >= 2 M-tiles per group
