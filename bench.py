@@ -507,8 +507,10 @@ def run_ours(args, ws, rank, local):
         try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
             with open(os.path.join(ROOT, "profiles", "ncu_traffic_sht.json")) as f:
                 tj = json.load(f)
-            if args.workload == "sht" and name in tj["dram_bytes_per_launch"]:
-                roof["traffic"] = tj["dram_bytes_per_launch"][name]
+            tw = tj["dram_bytes_per_launch"] if args.workload == "sht" else \
+                tj.get("by_workload", {}).get(args.workload, {}).get("dram_bytes_per_launch", {})
+            if name in tw:
+                roof["traffic"] = tw[name]
                 roof["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write)"
                 roof["algorithmic_per_launch"] = work / cnt
         except Exception:
