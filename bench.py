@@ -536,6 +536,50 @@ def run_ours(args, ws, rank, local):
                "api": "sph_sht_roundtrip_host (pinned host in/out; H2D, compute and D2H streams over 3 chunk buffers)", "chunk_fields": args.chunk}
         del xh, yh
 
+    if args.workload == "disco" and not args.no_e2e:
+        # per batch item: pinned host -> device (H2D stream), sph_disco_apply (compute
+        # stream), device -> pinned host (D2H stream), 3 slots in flight
+        xh = torch.empty((B, cin, NLAT, NLON), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        yh = torch.empty((B, cout, 360, 720), dtype=torch.float32, pin_memory=True)
+        NS = 3
+        xd = [torch.empty((1, cin, NLAT, NLON), device=dev) for _ in range(NS)]
+        yd = [torch.empty((1, cout, 360, 720), device=dev) for _ in range(NS)]
+        ws1 = op.workspace(1, cin, cout)
+        s_up, s_cp, s_dn = (torch.cuda.Stream(dev) for _ in range(3))
+        ev_up = [torch.cuda.Event() for _ in range(NS)]
+        ev_cp = [torch.cuda.Event() for _ in range(NS)]
+        ev_dn = [torch.cuda.Event() for _ in range(NS)]
+
+        def e2e_step():
+            for b in range(B):
+                k = b % NS
+                with torch.cuda.stream(s_up):
+                    s_up.wait_event(ev_cp[k])          # slot's input consumed
+                    xd[k].copy_(xh[b:b + 1], non_blocking=True)
+                    ev_up[k].record(s_up)
+                with torch.cuda.stream(s_cp):
+                    s_cp.wait_event(ev_up[k])
+                    s_cp.wait_event(ev_dn[k])          # slot's output downloaded
+                    op.apply(xd[k], mix, out=yd[k], ws=ws1)
+                    ev_cp[k].record(s_cp)
+                with torch.cuda.stream(s_dn):
+                    s_dn.wait_event(ev_cp[k])
+                    yh[b:b + 1].copy_(yd[k], non_blocking=True)
+                    ev_dn[k].record(s_dn)
+            torch.cuda.synchronize()
+        e2e_step()
+        barrier(ws)
+        t0 = time.perf_counter()
+        n_e2e = max(1, min(args.steps, 3))
+        for _ in range(n_e2e):
+            e2e_step()
+        t = max_over_ranks((time.perf_counter() - t0) / n_e2e, ws)
+        e2e = {"value": ws * units / t, "unit": "output fields/s", "h2d_bytes_per_step": xh.numel() * 4,
+               "d2h_bytes_per_step": yh.numel() * 4, "ms_per_step": t * 1e3,
+               "api": "sph_disco_apply per batch item (pinned host in/out; H2D, compute and D2H streams, 3 slots)"}
+        del xh, yh
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
