@@ -50,6 +50,13 @@ extern "C" {
  * (harmonics.hpp:129-130); the reference's equiangular forward is dist_sht_forward
  * (distsim.hpp:404).  Plans created without this flag reject equiangular forwards. */
 #define SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD 0x10
+/* adjoint plan (the SHT's backward pass; no reference counterpart):
+ * under the real inner product <c, d> = sum Re(conj(c) d) over the stored m >= 0,
+ * sph_sht_forward computes the adjoint of sht_inverse (grid field -> coefficients:
+ * unweighted analysis, m >= 1 doubled; any grid kind) and sph_sht_inverse computes the
+ * adjoint of sht_forward (coefficients -> field: quadrature-weighted synthesis with
+ * m >= 1 halved).  Same kernels, different tables. */
+#define SPH_FLAG_ADJOINT 0x20
 
 /* coefficient layouts */
 #define SPH_LAYOUT_DENSE_LM 0 /* reference [F][lmax][mmax] complex64 */

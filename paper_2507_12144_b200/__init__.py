@@ -12,5 +12,6 @@ from .sphere import (  # noqa: F401
     build_equiangular, build_gaussian, default_mmax, disco_apply, disco_transpose_apply, get_sht_plan,
     bilinear_resample, spectral_resample, ResamplePlan, DecoderPlan, decode_preclamp, angular_psd, spectral_crps_loss,
     isotropic_basis, morlet_basis, require_same_sampling, sht_forward, sht_inverse,
+    sht_forward_adjoint, sht_inverse_adjoint,
     spectral_conv,
 )

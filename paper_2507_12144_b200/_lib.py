@@ -25,6 +25,7 @@ SPH_PREC_3XTF32 = 0
 SPH_PREC_TF32 = 1
 SPH_PREC_FP32_SIMT = 2
 SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD = 0x10
+SPH_FLAG_ADJOINT = 0x20
 SPH_LAYOUT_DENSE_LM = 0
 SPH_LAYOUT_INTERNAL = 1
 SPH_BASIS_MORLET = 0

@@ -249,6 +249,7 @@ void ShtPlan::create(int kind_, int64_t nlat_, int64_t nlon_, int64_t lmax_, int
     mmax = mmax_;
     flags = flags_;
     prec = flags & SPH_FLAG_PREC_MASK;
+    const bool adjoint = (flags & SPH_FLAG_ADJOINT) != 0;
     require(prec <= SPH_PREC_FP32_SIMT, "sht plan: unknown precision mode");
     require(lmax >= 1 && mmax >= 1, "sht plan: lmax and mmax must be >= 1");
     require(mmax <= lmax, "SpectralCoeffs: mmax must be <= lmax");
@@ -301,8 +302,19 @@ void ShtPlan::create(int kind_, int64_t nlat_, int64_t nlon_, int64_t lmax_, int
                 const int64_t Lmp = L(m, p);
                 for (int64_t lp = 0; lp < Lmp; ++lp) {
                     const double v = col[m + p + 2 * lp];
-                    pf[(pf_off[m * 2 + p] + lp) * Rp + r] = static_cast<float>(v * w[ia]);
-                    pit[((m * 2 + p) * R + r) * static_cast<int64_t>(Lp) + lp] = static_cast<float>(v);
+                    if (adjoint) {
+                        // analysis A: c = sum_ij w_i P x e^{-im phi}; synthesis S doubles m >= 1
+                        // (Hermitian C2R).  Under <c, d> = sum Re(conj(c) d) over stored m >= 0:
+                        //   S^T z = unweighted analysis of z, m >= 1 doubled   ("forward" tables)
+                        //   A^T d = w_i * synthesis of d with m >= 1 halved    ("inverse" tables)
+                        const double dm = m ? 2.0 : 1.0;
+                        pf[(pf_off[m * 2 + p] + lp) * Rp + r] = static_cast<float>(v * dm);
+                        pit[((m * 2 + p) * R + r) * static_cast<int64_t>(Lp) + lp] =
+                            static_cast<float>(v * w[ia] / dm);
+                    } else {
+                        pf[(pf_off[m * 2 + p] + lp) * Rp + r] = static_cast<float>(v * w[ia]);
+                        pit[((m * 2 + p) * R + r) * static_cast<int64_t>(Lp) + lp] = static_cast<float>(v);
+                    }
                 }
             }
         }
@@ -438,7 +450,7 @@ void* ShtPlan::workspace(void* ws, int64_t bytes) {
 }
 
 void ShtPlan::forward(const float* x, int64_t F, float* out, int layout, void* ws, cudaStream_t st) {
-    require(kind == SPH_GAUSSIAN || (flags & SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD),
+    require(kind == SPH_GAUSSIAN || (flags & (SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD | SPH_FLAG_ADJOINT)),
             "sht_forward: requires a gaussian grid");
     require(nlat >= lmax && nlon >= 2 * mmax, "sht_forward: resolution insufficient for lmax/mmax");
     require(layout == SPH_LAYOUT_DENSE_LM || layout == SPH_LAYOUT_INTERNAL, "sht_forward: bad layout");

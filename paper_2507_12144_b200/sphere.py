@@ -145,12 +145,14 @@ class ShtPlan:
     per-call table builds of harmonics.hpp:159-162 / :202-205."""
 
     def __init__(self, grid: GridSpec, lmax: int, mmax: int, precision: str = "3xtf32",
-                 allow_equiangular_forward: bool = False, device=None):
+                 allow_equiangular_forward: bool = False, device=None, adjoint: bool = False):
         self.grid, self.lmax, self.mmax = grid, int(lmax), int(mmax)
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None
                                    else torch.device(device).index or 0)
         flags = PRECISIONS[precision] | (L.SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD
                                          if allow_equiangular_forward else 0)
+        if adjoint:  # forward / inverse compute the adjoints of inverse / forward
+            flags |= L.SPH_FLAG_ADJOINT
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             check(L.lib.sph_sht_plan_create(grid.kind, grid.nlat, grid.nlon, self.lmax,
@@ -224,13 +226,13 @@ class ShtPlan:
 
 
 def get_sht_plan(grid: GridSpec, lmax: int, mmax: int, precision: str = "3xtf32",
-                 allow_equiangular_forward: bool = False) -> ShtPlan:
+                 allow_equiangular_forward: bool = False, adjoint: bool = False) -> ShtPlan:
     dev = torch.cuda.current_device()
-    key = (grid.kind, grid.nlat, grid.nlon, lmax, mmax, precision, allow_equiangular_forward, dev)
+    key = (grid.kind, grid.nlat, grid.nlon, lmax, mmax, precision, allow_equiangular_forward, dev, adjoint)
     with _plan_lock:
         p = _sht_plans.get(key)
         if p is None:
-            p = ShtPlan(grid, lmax, mmax, precision, allow_equiangular_forward)
+            p = ShtPlan(grid, lmax, mmax, precision, allow_equiangular_forward, adjoint=adjoint)
             _sht_plans[key] = p
         return p
 
@@ -278,6 +280,40 @@ def sht_inverse(coeffs: SpectralCoeffs, grid: GridSpec,
     with torch.cuda.device(c.device):
         y = plan.inverse(c.to(torch.complex64), F)
     return SphericalField(grid, y.reshape(*lead, grid.nlat, grid.nlon))
+
+
+# ----------------------------------------------------------- SHT adjoints
+# The SHT's backward pass ("SHT adjoints come next"; the reference has no
+# counterpart).  Inner products: sum Re(conj(c) d) over the stored m >= 0 coefficients and
+# the plain sum over grid samples; pinned by the adjoint identities (tests/test_sht_gpu.py)
+# and by the fp64 oracle restatement of the same formulas (tests/test_oracle.py).
+def sht_forward_adjoint(coeffs: SpectralCoeffs, grid: GridSpec, precision: str = "3xtf32") -> SphericalField:
+    """Adjoint of sht_forward on ``grid`` (Gaussian): coefficients [..., lmax, mmax] ->
+    field, y_ij = w_i * sum_lm P_lm(theta_i) Re(d_lm e^{i m phi_j})."""
+    if grid.kind != GAUSSIAN:
+        raise L.SphInvalidArgument(1, "sht_forward: requires a gaussian grid")
+    c = coeffs.coeffs
+    lead = tuple(c.shape[:-2])
+    F = int(np.prod(lead)) if lead else 1
+    plan = get_sht_plan(grid, coeffs.lmax, coeffs.mmax, precision, adjoint=True)
+    with torch.cuda.device(c.device):
+        y = plan.inverse(c.to(torch.complex64), F)
+    return SphericalField(grid, y.reshape(*lead, grid.nlat, grid.nlon))
+
+
+def sht_inverse_adjoint(field: SphericalField, lmax: int, mmax: int, precision: str = "3xtf32") -> SpectralCoeffs:
+    """Adjoint of sht_inverse(., field.grid) for (lmax, mmax) coefficients: field ->
+    coefficients c_lm = (m ? 2 : 1) sum_ij P_lm(theta_i) z_ij e^{-i m phi_j} (any grid kind)."""
+    g = field.grid
+    if g.nlat < lmax or g.nlon < 2 * mmax:
+        raise L.SphInvalidArgument(1, "sht_forward: resolution insufficient for lmax/mmax")
+    if mmax > lmax:
+        raise L.SphInvalidArgument(1, "SpectralCoeffs: mmax must be <= lmax")
+    lead = tuple(field.data.shape[:-2])
+    plan = get_sht_plan(g, lmax, mmax, precision, adjoint=True)
+    with torch.cuda.device(field.data.device):
+        out = plan.forward(field.data)
+    return SpectralCoeffs(lmax, mmax, torch.view_as_complex(out).reshape(*lead, lmax, mmax))
 
 
 # ------------------------------------------------------------------- DISCO

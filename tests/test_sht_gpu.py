@@ -218,3 +218,55 @@ def test_gemm_cluster_multicast_matches_simt(monkeypatch, cluster):
     ya = inv(pa, a, 512)
     yb = inv(plan(0, 91, 180, 91, 90, "fp32"), a, 512)
     assert rel_l2(ya, yb) <= 2e-6
+
+
+# ------------------------------------------------------------- SHT adjoints
+def _grid(kind, nlat, nlon):
+    return S.build_gaussian(nlat, nlon) if kind == 1 else S.build_equiangular(nlat, nlon)
+
+
+@pytest.mark.parametrize("kind,nlat,nlon,lmax,mmax", [(1, 12, 24, 12, 9), (0, 9, 16, 9, 8), (1, 45, 90, 45, 45)])
+def test_sht_adjoints_vs_oracle(kind, nlat, nlon, lmax, mmax):
+    """SPH_FLAG_ADJOINT plans against the fp64 oracle restatement of the adjoint formulas
+    (tests/test_oracle.py::test_sht_adjoint_formulas pins those by the adjoint identity)."""
+    dev = torch.device("cuda", 0)
+    o = oracle.orc()
+    colat, w = o.grid(kind, nlat, nlon)
+    rng = np.random.default_rng(3)
+    z = rng.standard_normal((3, nlat, nlon))
+    d = (rng.standard_normal((3, lmax, mmax)) + 1j * rng.standard_normal((3, lmax, mmax))) * \
+        (np.tril(np.ones((lmax, mmax))) > 0)
+    g = _grid(kind, nlat, nlon)
+    # S^T z
+    c = S.sht_inverse_adjoint(S.SphericalField(g, torch.tensor(z, dtype=torch.float32, device=dev)), lmax, mmax)
+    out = np.zeros((3, lmax, mmax, 2))
+    assert o.L.orc_sht_forward(nlat, nlon, colat, np.ones(nlat), lmax, mmax, 3, np.ascontiguousarray(z), out) == 0
+    ref = (out[..., 0] + 1j * out[..., 1]) * np.where(np.arange(mmax) >= 1, 2.0, 1.0)
+    assert rel_l2(c.coeffs.cpu().numpy().astype(np.complex128), ref) <= TOL
+    if kind == 1:  # A^T d
+        y = S.sht_forward_adjoint(S.SpectralCoeffs(lmax, mmax, torch.tensor(d, dtype=torch.complex64, device=dev)), g)
+        ref = w[None, :, None] * o.sht_inverse(kind, nlat, nlon, d * np.where(np.arange(mmax) >= 1, 0.5, 1.0))
+        assert rel_l2(y.data.cpu().numpy().astype(np.float64), ref) <= TOL
+
+
+def test_sht_adjoint_identities_latent_size():
+    """<A x, d> = <x, A^T d> and <S c, z> = <c, S^T z> through the kernels at the
+    360x720 Gaussian latent grid (lmax = mmax = 360), fp32 tolerance."""
+    dev = torch.device("cuda", 0)
+    g = S.build_gaussian(360, 720)
+    gen = torch.Generator(device="cpu").manual_seed(11)
+    x = torch.randn(2, 360, 720, generator=gen).to(dev)
+    z = torch.randn(2, 360, 720, generator=gen).to(dev)
+    tri = torch.tril(torch.ones(360, 360)).to(dev)
+    d = torch.complex(torch.randn(2, 360, 360, generator=gen), torch.randn(2, 360, 360, generator=gen)).to(dev) * tri
+    c = torch.complex(torch.randn(2, 360, 360, generator=gen), torch.randn(2, 360, 360, generator=gen)).to(dev) * tri
+    Ax = S.sht_forward(S.SphericalField(g, x), 360, 360).coeffs
+    ATd = S.sht_forward_adjoint(S.SpectralCoeffs(360, 360, d), g).data
+    lhs = (Ax.conj() * d).real.double().sum().item()
+    rhs = (x.double() * ATd.double()).sum().item()
+    assert abs(lhs - rhs) <= 2e-5 * (Ax.abs().double().pow(2).sum().sqrt() * d.abs().double().pow(2).sum().sqrt()).item()
+    Sc = S.sht_inverse(S.SpectralCoeffs(360, 360, c), g).data
+    STz = S.sht_inverse_adjoint(S.SphericalField(g, z), 360, 360).coeffs
+    lhs = (Sc.double() * z.double()).sum().item()
+    rhs = (c.conj() * STz).real.double().sum().item()
+    assert abs(lhs - rhs) <= 2e-5 * (Sc.double().pow(2).sum().sqrt() * z.double().pow(2).sum().sqrt()).item()
