@@ -451,6 +451,41 @@ struct PlainFwdIO {
 };
 
 // plain inverse: half spectra [nrings][nbins] -> rings [nrings][n] * scale
+// Hermitian half-spectrum load into the complex ring buffer of a C2R pair (z = A + iB):
+// element i of the P x (n/2+1) block is (slot j, bin k) = at(i) with spectra ha (ring A),
+// hb (ring B).  Batches of 4 elements per thread issue all their global loads before
+// any shared-memory store (one load pair in flight per thread was latency-bound: 62 %
+// long-scoreboard stalls at the DISCO C2R).
+template <class PT, class NT, class At, class Get>
+__device__ __forceinline__ void load_half_spectra(float2* buf, PT P, NT n, int ld, At at, Get get) {
+    constexpr int U = 4;
+    const int half = n / 2, nh = half + 1;
+    const int total = P * nh;
+    for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+        float2 ha[U], hb[U];
+        int jj[U], kk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * blockDim.x;
+            jj[u] = -1;
+            ha[u] = hb[u] = make_float2(0.f, 0.f);
+            if (i < total) {
+                at(i, jj[u], kk[u]);
+                get(jj[u], kk[u], ha[u], hb[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (jj[u] < 0) continue;
+            const int j = jj[u], k = kk[u];
+            float2 a = ha[u], b = hb[u];
+            if (k == 0 || 2 * k == n) { a.y = 0.f; b.y = 0.f; }
+            buf[j * ld + k] = make_float2(a.x - b.y, a.y + b.x);
+            if (k != 0 && 2 * k != n) buf[j * ld + n - k] = make_float2(a.x + b.y, b.x - a.y);
+        }
+    }
+}
+
 struct PlainInvIO {
     static constexpr bool kRegStore = true;  // fft4_unfold_kernel (register stores)
     const float2* bins;
@@ -477,19 +512,16 @@ struct PlainInvIO {
     template <class PT, class NT>
     __device__ __forceinline__ void load(float2* buf, PT P, NT n, int ld) const {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * P;
-        const int half = n / 2, nh = half + 1;
-        for (int i = threadIdx.x; i < P * nh; i += blockDim.x) {
-            const int j = i / nh, k = i - j * nh;
-            const int64_t ra = 2 * (c0 + j), rb = ra + 1;
-            float2 ha = make_float2(0.f, 0.f), hb = ha;
-            if (k < nbins) {
-                if (ra < nrings) ha = bins[ra * nbins + k];
-                if (rb < nrings) hb = bins[rb * nbins + k];
-            }
-            if (k == 0 || 2 * k == n) { ha.y = 0.f; hb.y = 0.f; }
-            buf[j * ld + k] = make_float2(ha.x - hb.y, ha.y + hb.x);
-            if (k != 0 && 2 * k != n) buf[j * ld + n - k] = make_float2(ha.x + hb.y, hb.x - ha.y);
-        }
+        const int nh = n / 2 + 1;
+        load_half_spectra(
+            buf, P, n, ld, [&](int i, int& j, int& k) { j = i / nh; k = i - j * nh; },
+            [&](int j, int k, float2& ha, float2& hb) {
+                const int64_t ra = 2 * (c0 + j), rb = ra + 1;
+                if (k < nbins) {
+                    if (ra < nrings) ha = __ldg(bins + ra * nbins + k);
+                    if (rb < nrings) hb = __ldg(bins + rb * nbins + k);
+                }
+            });
     }
     template <class PT, class NT>
     __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
@@ -603,20 +635,16 @@ struct CminorInvIO {
         const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 2 * P;
         const int64_t hi = blockIdx.y, b = blockIdx.z;
         const float2* Vb = V + (b * H + hi) * static_cast<int64_t>(nbins) * C;
-        const int half = n / 2, nh = half + 1;
         // channel pairs fastest (coalesced channel-minor reads), each bin loaded once
-        for (int i = threadIdx.x; i < P * nh; i += blockDim.x) {
-            const int j = i % P, k = i / P;
-            const int64_t ca = c0 + 2 * j, cb = ca + 1;
-            float2 ha = make_float2(0.f, 0.f), hb = ha;
-            if (k < nbins) {
-                if (ca < C) ha = Vb[static_cast<int64_t>(k) * C + ca];
-                if (cb < C) hb = Vb[static_cast<int64_t>(k) * C + cb];
-            }
-            if (k == 0 || 2 * k == n) { ha.y = 0.f; hb.y = 0.f; }
-            buf[j * ld + k] = make_float2(ha.x - hb.y, ha.y + hb.x);
-            if (k != 0 && 2 * k != n) buf[j * ld + n - k] = make_float2(ha.x + hb.y, hb.x - ha.y);
-        }
+        load_half_spectra(
+            buf, P, n, ld, [&](int i, int& j, int& k) { j = i % P; k = i / P; },
+            [&](int j, int k, float2& ha, float2& hb) {
+                const int64_t ca = c0 + 2 * j, cb = ca + 1;
+                if (k < nbins) {
+                    if (ca < C) ha = __ldg(Vb + static_cast<int64_t>(k) * C + ca);
+                    if (cb < C) hb = __ldg(Vb + static_cast<int64_t>(k) * C + cb);
+                }
+            });
     }
     template <class PT, class NT>
     __device__ __forceinline__ void store(const float2* buf, PT P, NT n, int ld) const {
