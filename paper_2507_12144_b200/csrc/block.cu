@@ -2,6 +2,8 @@
 // epilogue (model.hpp:355-368), both on the shared tcgen05 grouped-GEMM engine.
 #include <algorithm>
 
+#include <mutex>
+
 #include "disco.cuh"
 
 namespace sph {
@@ -260,6 +262,21 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
     // workspace: G [B*P][ldc], Hm [B*P][ldh], W1 hi/lo [H][ldc], W2 hi/lo [C][ldh]
     const int64_t nG = B * P * ldc, nH = B * P * ldh, nW1 = H * ldc, nW2 = C * ldh;
     float* wsp = nullptr;
+    {
+        // stream-ordered workspace from the device's default pool; keep the pool's memory
+        // resident across synchronisations (release threshold 0 would return the ~0.8 GB
+        // to the OS at every sync and remap it on the next call)
+        static std::once_flag once[64];
+        int dev = 0;
+        SPH_CUDA(cudaGetDevice(&dev));
+        std::call_once(once[dev & 63], [dev] {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        });
+    }
     SPH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wsp), 4 * (nG + nH + 2 * nW1 + 2 * nW2) + 1024, st));
     float* G = wsp;
     float* Hm = G + round_up(nG, 64);
