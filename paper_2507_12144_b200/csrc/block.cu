@@ -87,29 +87,59 @@ __global__ void spec_scatter_kernel(const float* __restrict__ Yg, const int64_t*
 }
 
 // G[(b*P + p)][c] = gelu(conv[b][c][p])  (tiled transpose)
+// 32 x 32 tiles, GELU_PT consecutive point tiles per CTA (amortises the CTA set-up of a
+// 4-element-per-thread tile over 4x the bytes)
+constexpr int GELU_PT = 4;
 __global__ void gelu_transpose_kernel(const float* __restrict__ conv, int64_t C, int64_t P,
                                       int64_t ldc, float* __restrict__ G) {
     __shared__ float tile[32][33];
     const int64_t b = blockIdx.z;
-    const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int64_t c = c0 + r, p = p0 + threadIdx.x;
-        tile[r][threadIdx.x] = (c < C && p < P) ? gelu_erfc(conv[(b * C + c) * P + p]) : 0.f;
-    }
-    __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int64_t p = p0 + r, c = c0 + threadIdx.x;
-        if (p < P && c < ldc) G[(b * P + p) * ldc + c] = c < C ? tile[threadIdx.x][r] : 0.f;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 32;
+    const float* cb = conv + (b * C + c0) * P;
+    float* gb = G + b * P * ldc + c0;
+    for (int pt = 0; pt < GELU_PT; ++pt) {
+        const int64_t p0 = (static_cast<int64_t>(blockIdx.x) * GELU_PT + pt) * 32;
+        if (p0 >= P) break;
+        if (pt) __syncthreads();
+#pragma unroll
+        for (int r = threadIdx.y; r < 32; r += 8) {
+            const int64_t p = p0 + threadIdx.x;
+            tile[r][threadIdx.x] = (c0 + r < C && p < P) ? gelu_erfc(__ldg(cb + r * P + p)) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = threadIdx.y; r < 32; r += 8) {
+            const int64_t p = p0 + r;
+            const int64_t c = c0 + threadIdx.x;
+            if (p < P && c < ldc) gb[p * ldc + threadIdx.x] = c < C ? tile[threadIdx.x][r] : 0.f;
+        }
     }
 }
 
+// y = x + scale[c] (y + b2[c]); grid (point chunks, c, b), float4 when P % 4 == 0
 __global__ void residual_kernel(float* __restrict__ y, const float* __restrict__ x, int64_t B,
                                 int64_t C, int64_t P, const float* __restrict__ b2,
                                 const float* __restrict__ scales) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= B * C * P) return;
-    const int64_t c = (i / P) % C;
-    y[i] = x[i] + scales[c] * (y[i] + b2[c]);
+    const int64_t c = blockIdx.y, b = blockIdx.z;
+    const float s = scales[c], bb = b2[c];
+    const int64_t base = (b * C + c) * P;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if ((P & 3) == 0) {
+        float4* y4 = reinterpret_cast<float4*>(y + base);
+        const float4* x4 = reinterpret_cast<const float4*>(x + base);
+        for (int64_t i = t0; i < P / 4; i += stride) {
+            const float4 xv = __ldg(x4 + i);
+            float4 yv = y4[i];
+            yv.x = xv.x + s * (yv.x + bb);
+            yv.y = xv.y + s * (yv.y + bb);
+            yv.z = xv.z + s * (yv.z + bb);
+            yv.w = xv.w + s * (yv.w + bb);
+            y4[i] = yv;
+        }
+    } else {
+        for (int64_t i = t0; i < P; i += stride) y[base + i] = x[base + i] + s * (y[base + i] + bb);
+    }
 }
 
 inline unsigned nblk(int64_t n) { return static_cast<unsigned>((n + 255) / 256); }
@@ -323,7 +353,8 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
     }
     split_rows(w1, H, C, ldc, w1h, w1l, st);
     split_rows(w2, C, H, ldh, w2h, w2l, st);
-    dim3 grid(static_cast<unsigned>((P + 31) / 32), static_cast<unsigned>((ldc + 31) / 32),
+    require(B <= 65535 && C <= 65535, "block_apply: too many channels / batches");
+    dim3 grid(static_cast<unsigned>((P + 32 * GELU_PT - 1) / (32 * GELU_PT)), static_cast<unsigned>((ldc + 31) / 32),
               static_cast<unsigned>(B));
     {
         ProfScope prof("mlp_gelu_transpose", st);
@@ -342,7 +373,9 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
     gemm_run(*g2, Hm, y, prec, st, w2h, w2l);
     {
         ProfScope prof("mlp_residual", st);
-        residual_kernel<<<nblk(B * C * P), 256, 0, st>>>(y, x, B, C, P, b2, scales);
+        const int64_t chunks = std::min<int64_t>((P / 4 + 255) / 256 + 1, 64);
+        residual_kernel<<<dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(C), static_cast<unsigned>(B)), 256, 0,
+                          st>>>(y, x, B, C, P, b2, scales);
         SPH_LAUNCH_CHECK();
     }
     count_launch();
