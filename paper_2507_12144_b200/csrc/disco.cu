@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <thread>
 
 #include "disco.cuh"
@@ -516,6 +517,103 @@ __global__ void __launch_bounds__(256) disco_band_t_kernel(
     }
 }
 
+// Same contraction with the CTA's psi_t slice staged in shared memory once per CTA
+// (reused over the batch and channel passes): the per-thread global psi loads of the
+// kernel above (one LDG.64 per 4 FMA) made it load-bound (9.0 ms at cfg3 vs 1.8 ms for the
+// forward band kernel, which stages psi the same way).  Dynamic SMEM psm[pair][4 orders][9]
+// over the tile's (output row h, input row r) pairs in (h, r) order.
+constexpr int TB_MAXH = 64;
+__global__ void __launch_bounds__(256) disco_band_t2_kernel(
+    const float* __restrict__ S, const float2* __restrict__ psi_t, const int32_t* __restrict__ band0,
+    const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, const int32_t* __restrict__ tt_ptr,
+    const int32_t* __restrict__ tt_h, int64_t Hin, int64_t nbi, int64_t Hout, int64_t nbo, int wout, int K,
+    int64_t C, int64_t ldS, float2* __restrict__ Ut, int64_t B) {
+    extern __shared__ float2 psm[];
+    __shared__ int s_q0[TB_MAXH + 1], s_lo[TB_MAXH], s_hi[TB_MAXH];
+    const int mi = threadIdx.x / 64, cl = threadIdx.x % 64;
+    const int64_t mbase = static_cast<int64_t>(blockIdx.x) * 4;
+    const int64_t m = mbase + mi;
+    const int r0 = blockIdx.y * TB_RT;
+    const int nr = min(TB_RT, static_cast<int>(Hin) - r0);
+    const int t0 = tt_ptr[blockIdx.y], nt = tt_ptr[blockIdx.y + 1] - t0;
+    if (threadIdx.x == 0) {
+        int q = 0;
+        for (int t = 0; t < nt; ++t) {
+            const int h = tt_h[t0 + t];
+            const int lo = max(band0[h], r0), hi = min(band0[h] + bandc[h], r0 + nr);
+            s_q0[t] = q;
+            s_lo[t] = lo;
+            s_hi[t] = hi;
+            q += max(0, hi - lo);
+        }
+        s_q0[nt] = q;
+    }
+    __syncthreads();
+    const int nm = static_cast<int>(nbi - mbase < 4 ? nbi - mbase : 4);
+    for (int t = 0; t < nt; ++t) {
+        const int h = tt_h[t0 + t];
+        const int lo = s_lo[t], n = s_hi[t] - lo;
+        if (n <= 0) continue;
+        // rows lo .. lo+n of h's band, orders mbase .. mbase+3, k < K: contiguous per row
+        const float2* src = psi_t + (psi_off[h] + (lo - band0[h])) * nbi * K + mbase * K;
+        for (int e = threadIdx.x; e < n * 4 * K; e += blockDim.x) {
+            const int rr = e / (4 * K), rem = e - rr * 4 * K;
+            const int mm = rem / K, k = rem - mm * K;
+            psm[((s_q0[t] + rr) * 4 + mm) * 9 + k] =
+                mm < nm ? __ldg(src + static_cast<int64_t>(rr) * nbi * K + rem) : make_float2(0.f, 0.f);
+        }
+    }
+    __syncthreads();
+    if (m >= nbi) return;
+    const int half = wout / 2;
+    const int mo = static_cast<int>(m % wout);
+    const bool cj = mo > half;
+    const int mp = cj ? wout - mo : mo;
+    const float sg = cj ? -1.f : 1.f;
+    for (int64_t b = 0; b < B; ++b) {
+        const float* Sb = S + b * Hout * nbo * 2 * ldS;
+        for (int64_t c0 = 0; c0 < C; c0 += 64) {
+            const int64_t c = c0 + cl;
+            if (c >= C) break;
+            float2 acc[TB_RT];
+#pragma unroll
+            for (int i = 0; i < TB_RT; ++i) acc[i] = make_float2(0.f, 0.f);
+            for (int t = 0; t < nt; ++t) {
+                const int h = tt_h[t0 + t];
+                const int lo = s_lo[t], hi = s_hi[t];
+                if (hi <= lo) continue;
+                const float* sr = Sb + (static_cast<int64_t>(h) * nbo + mp) * 2 * ldS + c * K;
+                const float* si = sr + ldS;
+                float xr[9], xi[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    xr[k] = k < K ? __ldg(sr + k) : 0.f;
+                    xi[k] = k < K ? sg * __ldg(si + k) : 0.f;
+                }
+                const float2* pq = psm + (s_q0[t] - lo + r0) * 36 + mi * 9;  // pair of row r: pq + (r - r0) * 36
+#pragma unroll
+                for (int i = 0; i < TB_RT; ++i) {
+                    const int r = r0 + i;
+                    if (r < lo || r >= hi) continue;
+                    const float2* pk = pq + i * 36;
+                    float2 a = acc[i];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        if (k >= K) break;
+                        const float2 p = pk[k];
+                        a.x = fmaf(p.x, xr[k], fmaf(-p.y, xi[k], a.x));
+                        a.y = fmaf(p.x, xi[k], fmaf(p.y, xr[k], a.y));
+                    }
+                    acc[i] = a;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < TB_RT; ++i)
+                if (i < nr) Ut[((b * Hin + r0 + i) * nbi + m) * C + c] = acc[i];
+        }
+    }
+}
+
 }  // namespace
 
 void split_rows(const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
@@ -877,6 +975,18 @@ void DiscoPlan::build_transpose() {
     }
     upload(d_tb_ptr, ptr);
     upload(d_tb_h, hh);
+    t_max_pairs = 0;
+    t_max_h = 0;
+    for (int64_t t = 0; t < ntile; ++t) {
+        const int64_t r0 = t * TB_RT, r1 = std::min<int64_t>(hin, r0 + TB_RT);
+        int64_t q = 0;
+        for (int32_t i = ptr[t]; i < ptr[t + 1]; ++i) {
+            const int64_t h = hh[i];
+            q += std::max<int64_t>(0, std::min<int64_t>(band0[h] + bandc[h], r1) - std::max<int64_t>(band0[h], r0));
+        }
+        t_max_pairs = std::max(t_max_pairs, q);
+        t_max_h = std::max<int64_t>(t_max_h, ptr[t + 1] - ptr[t]);
+    }
     t_ready = true;
 }
 
@@ -975,9 +1085,22 @@ void DiscoPlan::transpose_apply(const float* v, const float* mix, int64_t B, int
     {
         // algorithmic bytes: S read once, the input-grid spectrum written once
         ProfScope prof("disco_band_t", st, 4.0 * B * hout * nbo * 2 * cin * K + 8.0 * B * hin * nbi * cin);
-        disco_band_t_kernel<<<grid, 256, 0, st>>>(S, d_psi_t.p, d_band0.p, d_bandc.p, d_psi_off.p, d_tb_ptr.p,
-                                                  d_tb_h.p, hin, nbi, hout, nbo, static_cast<int>(wout), K, cin,
-                                                  w.ldS, Ut, B);
+        // psi_t staged per CTA when the tile's (h, r) pairs fit in shared memory
+        const size_t psm_bytes = static_cast<size_t>(t_max_pairs) * 36 * sizeof(float2);
+        if (t_max_h <= TB_MAXH && psm_bytes <= 200 * 1024) {
+            static std::once_flag once;  // opt-in cap (the launch passes the actual size)
+            std::call_once(once, [] {
+                SPH_CUDA(cudaFuncSetAttribute(disco_band_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              200 * 1024));
+            });
+            disco_band_t2_kernel<<<grid, 256, psm_bytes, st>>>(S, d_psi_t.p, d_band0.p, d_bandc.p, d_psi_off.p,
+                                                               d_tb_ptr.p, d_tb_h.p, hin, nbi, hout, nbo,
+                                                               static_cast<int>(wout), K, cin, w.ldS, Ut, B);
+        } else {
+            disco_band_t_kernel<<<grid, 256, 0, st>>>(S, d_psi_t.p, d_band0.p, d_bandc.p, d_psi_off.p, d_tb_ptr.p,
+                                                      d_tb_h.p, hin, nbi, hout, nbo, static_cast<int>(wout), K, cin,
+                                                      w.ldS, Ut, B);
+        }
         SPH_LAUNCH_CHECK();
     }
     count_launch();

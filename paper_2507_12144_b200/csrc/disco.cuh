@@ -55,6 +55,7 @@ struct DiscoPlan {
     bool t_ready = false;
     DevBuf<float2> d_psi_t;
     DevBuf<int32_t> d_tb_ptr, d_tb_h;
+    int64_t t_max_pairs = 0, t_max_h = 0;  // per row tile: (h, r) band pairs, output rows
     void build_transpose();
 
     std::mutex mu;
