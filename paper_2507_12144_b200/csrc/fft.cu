@@ -179,6 +179,9 @@ struct FoldIO {
     int R, nlat, mmax;
     float* eo;
     int64_t Rq, twoF;
+    int fy_fast = 0;  // grid (field group, ring quad): concurrent CTAs fill adjacent E/O runs
+    __device__ __forceinline__ int qx_of() const { return fy_fast ? blockIdx.y : blockIdx.x; }
+    __device__ __forceinline__ int fy_of() const { return fy_fast ? blockIdx.x : blockIdx.y; }
     // slot p of a CTA -> (ring pair, field); false if outside [0, R) x [0, F).
     // P % 4 == 0 (all fast paths): 4 ring pairs x P/4 fields per CTA; otherwise P ring
     // pairs of one field (small fallback transforms)
@@ -186,8 +189,8 @@ struct FoldIO {
     __device__ __forceinline__ bool slot(PT P, int p, int& r, int& f) const {
         const int np = static_cast<int>(P);
         if (np % 4 == 0) {
-            r = 4 * blockIdx.x + (p & 3);
-            f = (np / 4) * blockIdx.y + (p >> 2);
+            r = 4 * qx_of() + (p & 3);
+            f = (np / 4) * fy_of() + (p >> 2);
         } else {
             r = np * blockIdx.x + p;
             f = blockIdx.y;
@@ -278,7 +281,7 @@ struct FoldIO {
             }
             return;
         }
-        store_job(buf, P, n, ld, blockIdx.x, blockIdx.y);
+        store_job(buf, P, n, ld, qx_of(), fy_of());
     }
     // quad path for the job (quad qx, field group fy)
     template <class PT, class NT>
@@ -934,10 +937,16 @@ void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int
     static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
     require(ld_eo % 4 == 0, "fft: E/O ring-pair padding must be a multiple of 4");
     FoldIO io{fft_dbg, x, fr.d_rows.p, fr.R, nlat, mmax, eo, ld_eo / 4, 2 * F};
+    // field groups fastest (measured at cfg2: 2.21 -> 2.11 ms): concurrently running CTAs
+    // write adjacent 64-byte runs of the same (m, parity, quad) E/O row instead of runs
+    // 32 KB apart; SPH_FFT_FY_FAST=0 restores quad-fastest
+    static const int fy_fast = std::getenv("SPH_FFT_FY_FAST") ? std::atoi(std::getenv("SPH_FFT_FY_FAST")) : 1;
     dim3 grid;
     if (P % 4 == 0) {
         const int64_t FB = P / 4;
-        grid = dim3((fr.R + 3) / 4, static_cast<unsigned>((F + FB - 1) / FB));
+        io.fy_fast = fy_fast;
+        grid = fy_fast ? dim3(static_cast<unsigned>((F + FB - 1) / FB), (fr.R + 3) / 4)
+                       : dim3((fr.R + 3) / 4, static_cast<unsigned>((F + FB - 1) / FB));
     } else {  // fallback transforms write pairs < R only: zero the [R, Rp) padding first
         grid = dim3((fr.R + P - 1) / P, static_cast<unsigned>(F));
         if (fr.R % 4 != 0)
