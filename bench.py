@@ -36,7 +36,7 @@ sys.path.insert(0, ROOT)
 NLAT, NLON, LMAX, MMAX = 721, 1440, 721, 720
 BATCH, CHANNELS = 4, 256
 FIELDS = BATCH * CHANNELS
-METRIC = "SHT+ISHT & DISCO-conv fields/sec at 721x1440, % of roofline, at 1/2/4/8 GPUs"
+METRIC = "SHT+ISHT & DISCO-conv fields/sec at 721\u00d71440, % of roofline, at 1/2/4/8 GPUs"  # BASELINE.json metric
 UNIT = "fields/s"
 
 
