@@ -1,5 +1,9 @@
 """cfg2 SHT round trip (1024 fields): forward-then-inverse vs the pipelined device round trip
-(sph_sht_roundtrip) over chunk sizes and GEMM CTA caps; checks the results agree."""
+(sph_sht_roundtrip) over chunk sizes and GEMM CTA caps; checks the results agree.
+
+Record of a reverted experiment: ShtPlan.roundtrip / sph_sht_roundtrip
+were removed after this measured slower than forward-then-inverse, so the script no
+longer runs against the current library."""
 import sys
 import torch
 import paper_2507_12144_b200 as S
