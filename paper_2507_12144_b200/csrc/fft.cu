@@ -581,6 +581,22 @@ struct CminorIO {
         const int64_t hi = blockIdx.y, b = blockIdx.z;
         float2* Ub = U + (b * H + hi) * static_cast<int64_t>(nbins) * C;
         float* Up = reinterpret_cast<float*>(U) + (b * H + hi) * static_cast<int64_t>(nbins) * 2 * ldp;
+        if (planar == 2) {
+            // channel-pair interleaved (re c, re c+1, im c, im c+1): one thread per (bin,
+            // pair) forms both channels from the pair's complex ring and stores one float4
+            // (C even, so a pair never straddles the channel range)
+            for (int o = threadIdx.x; o < nbins * P; o += blockDim.x) {
+                const int j = o % P;
+                const int m = o / P;
+                if (c0 + 2 * j >= C) continue;
+                const float2 z = buf[j * ld + m];
+                const float2 zc = buf[j * ld + (m == 0 ? 0 : n - m)];
+                const float4 v = make_float4(0.5f * (z.x + zc.x), 0.5f * (z.y + zc.y), 0.5f * (z.y - zc.y),
+                                             -0.5f * (z.x - zc.x));
+                reinterpret_cast<float4*>(Ub)[(static_cast<int64_t>(m) * C + c0 + 2 * j) >> 1] = v;
+            }
+            return;
+        }
         for (int o = threadIdx.x; o < nbins * 2 * P; o += blockDim.x) {
             const int cl = o % (2 * P);
             const int m = o / (2 * P);
