@@ -755,28 +755,61 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     }
                     ++nchunk;
                 } else if (store_mode == STORE_ROW) {
-                    // transpose through padded SMEM: 32 coalesced 128-byte row segments
+                    // transpose through the per-warp 32 x 32 SMEM tile in 16-byte chunks:
+                    // chunk q of row r sits at q ^ (r & 7) (conflict-free STS.128 by rows,
+                    // LDS.128 by 8-lane row groups), stored as 4 rows of 128 coalesced bytes
+                    // per STG.128 (the word-wise form issued 32 LDG + 32 STS + 32 LDS +
+                    // 32 STG per chunk: the cfg4 MLP GEMM was epilogue-bound)
+                    float4* t4 = reinterpret_cast<float4*>(tile);
+                    float bv[32];
 #pragma unroll
-                    if (epi.mode == 1) {  // fused bias + GeLU (erfc form); bias loads batched first
-                        float bv[32];
+                    for (int jj = 0; jj < 32; ++jj) bv[jj] = 0.f;
+                    if (epi.mode == 1) {  // fused bias + GeLU (erfc form); bias chunks are warp-uniform
+                        const float* bsrc = epi.bias + w.n0 + c;
+                        if (c + 32 <= nrem && (reinterpret_cast<uintptr_t>(bsrc) & 15) == 0) {
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) bv[jj] = c + jj < nrem ? __ldg(epi.bias + w.n0 + c + jj) : 0.f;
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 b4 = __ldg(reinterpret_cast<const float4*>(bsrc) + q);
+                                bv[4 * q] = b4.x;
+                                bv[4 * q + 1] = b4.y;
+                                bv[4 * q + 2] = b4.z;
+                                bv[4 * q + 3] = b4.w;
+                            }
+                        } else {
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj)
-                            tile[lane * 32 + (jj ^ lane)] =
-                                (c + jj < nrem) ? gelu_erfc_dev(__uint_as_float(va[jj]) + bv[jj]) : 0.f;
-                    } else {
+                            for (int jj = 0; jj < 32; ++jj) bv[jj] = c + jj < nrem ? __ldg(bsrc + jj) : 0.f;
+                        }
+                    }
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj)
-                            tile[lane * 32 + (jj ^ lane)] = (c + jj < nrem) ? __uint_as_float(va[jj]) : 0.f;
+                    for (int q = 0; q < 8; ++q) {
+                        float e[4];
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            const int jj = 4 * q + x;
+                            const float v = __uint_as_float(va[jj]);
+                            e[x] = (c + jj < nrem) ? (epi.mode == 1 ? gelu_erfc_dev(v + bv[jj]) : v) : 0.f;
+                        }
+                        t4[lane * 8 + (q ^ (lane & 7))] = make_float4(e[0], e[1], e[2], e[3]);
                     }
                     __syncwarp();
-                    const int col = w.n0 + c + lane;
-                    const bool cok = c + lane < ncols;
-#pragma unroll 8
-                    for (int r = 0; r < 32; ++r) {
+                    const int qq = lane & 7;
+                    const int colq = w.n0 + c + 4 * qq;
+                    const bool vec = (w.ldd & 3) == 0 && (reinterpret_cast<uintptr_t>(dbase) & 15) == 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int r = 4 * k + (lane >> 3);
                         const int mr = row0 + r;
-                        if (cok && mr < w.M) dbase[static_cast<int64_t>(mr) * w.ldd + col] = tile[r * 32 + (lane ^ r)];
+                        const float4 v = t4[r * 8 + (qq ^ (r & 7))];
+                        if (mr >= w.M) continue;
+                        float* dst = dbase + static_cast<int64_t>(mr) * w.ldd + colq;
+                        if (vec && c + 4 * qq + 4 <= ncols) {
+                            *reinterpret_cast<float4*>(dst) = v;
+                        } else {
+                            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int x = 0; x < 4; ++x)
+                                if (c + 4 * qq + x < ncols) dst[x] = vv[x];
+                        }
                     }
                     __syncwarp();
                 } else {
