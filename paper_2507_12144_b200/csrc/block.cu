@@ -41,49 +41,66 @@ __global__ void kernel_transpose_split(const float* __restrict__ k, int64_t cout
 }
 
 // C_int (F = B*cin fields) -> Xg[row_off[l] + (m*2 + reim)*B + b][i]
+// C_int [(m*2+p)][2F (b, i, re/im)][Lp] <-> per-l GEMM rows: 32 x 32 tiled transposes over
+// (channel, lp) for one (m, p, b, re/im) -- both sides in 128-byte runs (the element-wise
+// forms read with a stride of 2*Lp resp. ldy floats).  blockIdx.z = ((m*2 + p)*B + b)*2 + re/im.
+// Xg[row_off[l] + (m*2+reim)*B + b][i] = C_int(l, m; b, i, reim)  (l = m + p + 2 lp)
 __global__ void spec_gather_kernel(const float* __restrict__ cint, const int64_t* __restrict__ row_off,
-                                   int64_t lmax, int64_t mmax, int64_t B, int64_t cin, int Lp,
-                                   int64_t ldx, int64_t nrows, float* __restrict__ Xg,
-                                   const int32_t* __restrict__ row_l) {
-    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= nrows * ldx) return;
-    const int64_t i = idx % ldx, row = idx / ldx;
-    float v = 0.f;
-    if (i < cin) {
-        const int64_t l = row_l[row];
-        const int64_t r = row - row_off[l];
-        const int64_t b = r % B;
-        const int64_t reim = (r / B) & 1;
-        const int64_t m = r / (2 * B);
-        const int64_t p = (l - m) & 1, lp = (l - m) >> 1;
-        const int64_t twoF = 2 * B * cin;
-        v = cint[((m * 2 + p) * twoF + 2 * (b * cin + i) + reim) * Lp + lp];
+                                   int64_t lmax, int64_t B, int64_t cin, int Lp, int64_t ldx,
+                                   float* __restrict__ Xg) {
+    __shared__ float t[32][33];
+    int64_t z = blockIdx.z;
+    const int reim = static_cast<int>(z & 1);
+    z >>= 1;
+    const int64_t b = z % B;
+    z /= B;
+    const int p = static_cast<int>(z & 1);
+    const int64_t m = z >> 1;
+    const int64_t twoF = 2 * B * cin;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, lp0 = static_cast<int64_t>(blockIdx.y) * 32;
+    const int64_t nlp = (lmax - m - p + 1) / 2;  // lp with l = m + p + 2 lp < lmax
+    if (lp0 >= nlp) return;                      // no GEMM rows in this tile (the triangle)
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int64_t i = i0 + r, lp = lp0 + threadIdx.x;
+        t[r][threadIdx.x] =
+            (i < cin && lp < nlp) ? __ldg(cint + ((m * 2 + p) * twoF + 2 * (b * cin + i) + reim) * Lp + lp) : 0.f;
     }
-    Xg[idx] = v;
-    (void)lmax;
-    (void)mmax;
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int64_t lp = lp0 + r, l = m + p + 2 * lp;
+        const int64_t i = i0 + threadIdx.x;
+        if (lp >= Lp || l >= lmax || i >= ldx) continue;
+        const int64_t row = row_off[l] + (m * 2 + reim) * B + b;
+        Xg[row * ldx + i] = i < cin ? t[threadIdx.x][r] : 0.f;
+    }
 }
 
 // Yg[row_off[l] + (m*2+reim)*B + b][o] -> C_int (F = B*cout) incl. zero padding
 __global__ void spec_scatter_kernel(const float* __restrict__ Yg, const int64_t* __restrict__ row_off,
-                                    int64_t lmax, int64_t mmax, int64_t B, int64_t cout, int Lp,
-                                    int64_t ldy, float* __restrict__ cint) {
+                                    int64_t lmax, int64_t B, int64_t cout, int Lp, int64_t ldy,
+                                    float* __restrict__ cint) {
+    __shared__ float t[32][33];
+    int64_t z = blockIdx.z;
+    const int reim = static_cast<int>(z & 1);
+    z >>= 1;
+    const int64_t b = z % B;
+    z /= B;
+    const int p = static_cast<int>(z & 1);
+    const int64_t m = z >> 1;
     const int64_t twoF = 2 * B * cout;
-    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= mmax * 2 * twoF * Lp) return;
-    const int64_t lp = idx % Lp;
-    const int64_t n = (idx / Lp) % twoF;
-    const int64_t g = idx / (Lp * twoF);
-    const int64_t m = g >> 1, p = g & 1;
-    const int64_t l = m + p + 2 * lp;
-    float v = 0.f;
-    if (l < lmax) {
-        const int64_t f = n >> 1, reim = n & 1;
-        const int64_t b = f / cout, o = f % cout;
-        const int64_t row = row_off[l] + (m * 2 + reim) * B + b;
-        v = Yg[row * ldy + o];
+    const int64_t o0 = static_cast<int64_t>(blockIdx.x) * 32, lp0 = static_cast<int64_t>(blockIdx.y) * 32;
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int64_t lp = lp0 + r, l = m + p + 2 * lp;
+        const int64_t o = o0 + threadIdx.x;
+        float v = 0.f;
+        if (lp < Lp && l < lmax && o < cout) v = __ldg(Yg + (row_off[l] + (m * 2 + reim) * B + b) * ldy + o);
+        t[r][threadIdx.x] = v;
     }
-    cint[idx] = v;
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int64_t o = o0 + r, lp = lp0 + threadIdx.x;
+        if (o < cout && lp < Lp) cint[((m * 2 + p) * twoF + 2 * (b * cout + o) + reim) * Lp + lp] = t[threadIdx.x][r];
+    }
 }
 
 // G[(b*P + p)][c] = gelu(conv[b][c][p])  (tiled transpose)
@@ -263,16 +280,19 @@ void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, i
         }
         {
             ProfScope prof("spectral_gather", st);
-            spec_gather_kernel<<<nblk(sp->nrows * w.ldx), 256, 0, st>>>(
-                cin_i, sp->d_row_off.p, lmax, mmax, B, cin, p.Lp, w.ldx, sp->nrows, Xg, sp->d_row_l.p);
+            require(mmax * 4 * B <= 65535, "spectral_conv: too many orders x batches for the gather grid");
+            dim3 tg(static_cast<unsigned>((w.ldx + 31) / 32), static_cast<unsigned>((p.Lp + 31) / 32),
+                    static_cast<unsigned>(mmax * 4 * B));
+            spec_gather_kernel<<<tg, dim3(32, 8), 0, st>>>(cin_i, sp->d_row_off.p, lmax, B, cin, p.Lp, w.ldx, Xg);
             SPH_LAUNCH_CHECK();
         }
         count_launch(2);
         gemm_run(sp->gemm, Xg, Yg, p.prec, st, khi, klo);
         {
             ProfScope prof("spectral_scatter", st);
-            spec_scatter_kernel<<<nblk(mmax * 2 * 2 * B * cout * p.Lp), 256, 0, st>>>(
-                Yg, sp->d_row_off.p, lmax, mmax, B, cout, p.Lp, w.ldy, cout_i);
+            dim3 ts(static_cast<unsigned>((cout + 31) / 32), static_cast<unsigned>((p.Lp + 31) / 32),
+                    static_cast<unsigned>(mmax * 4 * B));
+            spec_scatter_kernel<<<ts, dim3(32, 8), 0, st>>>(Yg, sp->d_row_off.p, lmax, B, cout, p.Lp, w.ldy, cout_i);
             SPH_LAUNCH_CHECK();
         }
         count_launch();
