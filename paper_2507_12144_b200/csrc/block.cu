@@ -134,6 +134,46 @@ __global__ void gelu_transpose_kernel(const float* __restrict__ conv, int64_t C,
 }
 
 // y = x + scale[c] (y + b2[c]); grid (point chunks, c, b), float4 when P % 4 == 0
+// P % 4 == 0: one 32-channel x 128-point tile per CTA, float4 point loads (all four per
+// thread in flight), a single barrier, float4 channel stores of the transposed rows; tile
+// pitch 129 keeps the column reads conflict-free
+__global__ void __launch_bounds__(256) gelu_transpose4_kernel(const float* __restrict__ conv, int64_t C, int64_t P,
+                                                              int64_t ldc, float* __restrict__ G) {
+    __shared__ float tile[32][129];
+    const int64_t b = blockIdx.z;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 32, p0 = static_cast<int64_t>(blockIdx.x) * 128;
+    const int t = threadIdx.x;
+    float4 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int idx = t + 256 * i;
+        const int c = idx >> 5, p4 = 4 * (idx & 31);
+        v[i] = (c0 + c < C && p0 + p4 < P)
+                   ? __ldg(reinterpret_cast<const float4*>(conv + (b * C + c0 + c) * P + p0 + p4))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int idx = t + 256 * i;
+        const int c = idx >> 5, p4 = 4 * (idx & 31);
+        const bool ok = c0 + c < C;
+        tile[c][p4] = ok ? gelu_erfc(v[i].x) : 0.f;
+        tile[c][p4 + 1] = ok ? gelu_erfc(v[i].y) : 0.f;
+        tile[c][p4 + 2] = ok ? gelu_erfc(v[i].z) : 0.f;
+        tile[c][p4 + 3] = ok ? gelu_erfc(v[i].w) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int idx = t + 256 * i;
+        const int pr = idx >> 3, q = idx & 7;
+        const int64_t p = p0 + pr;
+        if (p >= P || c0 + 4 * q >= ldc) continue;
+        const float4 o = make_float4(tile[4 * q][pr], tile[4 * q + 1][pr], tile[4 * q + 2][pr], tile[4 * q + 3][pr]);
+        *reinterpret_cast<float4*>(G + (b * P + p) * ldc + c0 + 4 * q) = o;
+    }
+}
+
 __global__ void residual_kernel(float* __restrict__ y, const float* __restrict__ x, int64_t B,
                                 int64_t C, int64_t P, const float* __restrict__ b2,
                                 const float* __restrict__ scales) {
@@ -378,7 +418,12 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
               static_cast<unsigned>(B));
     {
         ProfScope prof("mlp_gelu_transpose", st);
-        gelu_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(conv, C, P, ldc, G);
+        if (P % 4 == 0 && ldc % 32 == 0 && (reinterpret_cast<uintptr_t>(conv) & 15) == 0) {
+            dim3 g4(static_cast<unsigned>((P + 127) / 128), static_cast<unsigned>(ldc / 32), static_cast<unsigned>(B));
+            gelu_transpose4_kernel<<<g4, 256, 0, st>>>(conv, C, P, ldc, G);
+        } else {
+            gelu_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(conv, C, P, ldc, G);
+        }
         SPH_LAUNCH_CHECK();
     }
     count_launch();
