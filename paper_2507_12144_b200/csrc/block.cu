@@ -386,6 +386,8 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
             g->store = STORE_ROW;
             g->bn = H >= 256 ? 256 : 128;
             g->name = "gemm_mlp1";
+            static const int row_tma = std::getenv("SPH_MLP_ROW_TMA") ? std::atoi(std::getenv("SPH_MLP_ROW_TMA")) : 1;
+            g->row_tma = row_tma != 0;
             require(B * P < (1LL << 31), "block: too many points");
             g->groups.push_back({0, 0, static_cast<int32_t>(B * P), static_cast<int32_t>(H),
                                  static_cast<int32_t>(C), static_cast<int32_t>(ldh), 0, 0});

@@ -72,6 +72,7 @@ struct GroupedGemm {
     int cluster = 0;               // CTAs per cluster sharing the table tile (0 = auto)
     bool alo = false;              // bn 64 / 128: the BK = 32 A_lo-in-TMEM kernel (bn 192 always is)
     int ks = 1;                    // 32-wide atoms per pipeline stage (1 or 2; A_lo-in-TMEM kernels)
+    bool row_tma = false;          // non-ALO STORE_ROW: TMA-store epilogue (uniform D groups)
     bool pair = false;             // cta_group::2 CTA-pair MMA (set by finalize)
     // TMA-store epilogue (ALO kernel): D is a uniform 3D [d_groups3][d_rows][ldd] view
     // (every group has the same ldd and row count, d_off a multiple of d_rows * ldd)

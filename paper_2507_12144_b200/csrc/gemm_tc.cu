@@ -695,8 +695,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                                                      // element (r, col) at r * 32 + (col ^ r)
         // TMA-store path (ALO): ping-pong 4 KB staging buffers per warp; lane 0 issues the
         // 3D tensor store of each 32 x 32 chunk and recycles a buffer after wait_group.read
-        const bool tstore = ALO && tma_store;
-        uint8_t* obase = smem + L::TILE_OFF + (warp - 8) * 8192;
+        // TMA-store path: ALO kernels ping-pong two 4 KB staging buffers per warp; the
+        // non-ALO row-store kernels (row_tma) use one (their SMEM ring leaves 4 KB per warp)
+        const bool tstore = tma_store && (ALO || store_mode == STORE_ROW);
+        uint8_t* obase = smem + L::TILE_OFF + (warp - 8) * (ALO ? 8192 : 4096);
         int nchunk = 0;
         int lt = 0;
         for (int t = cid; t < ntiles; t += ncl, ++lt) {
@@ -721,19 +723,45 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 const bool more = cn < nrem;
                 if (more) tmem_ld32_async(trow + cn, vb);
                 if (tstore) {
-                    float* ob = reinterpret_cast<float*>(obase + (nchunk & 1) * 4096);
-                    if (lane == 0 && nchunk >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    float* ob = reinterpret_cast<float*>(obase + (ALO ? (nchunk & 1) * 4096 : 0));
+                    if (ALO) {
+                        if (lane == 0 && nchunk >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    } else {
+                        if (lane == 0 && nchunk >= 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    }
                     __syncwarp();
                     if (store_mode == STORE_ROW) {
                         // box {32 cols, 32 rows}, SWIZZLE_128B: row = lane, 16-byte chunk k of
-                        // the row at k ^ (row & 7)
+                        // the row at k ^ (row & 7); fused bias + GeLU (epi mode 1) on the way
+                        float bv[32];
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) bv[jj] = 0.f;
+                        if (epi.mode == 1) {
+                            const float* bsrc = epi.bias + w.n0 + c;
+                            if (c + 32 <= nrem && (reinterpret_cast<uintptr_t>(bsrc) & 15) == 0) {
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(bsrc) + q);
+                                    bv[4 * q] = b4.x;
+                                    bv[4 * q + 1] = b4.y;
+                                    bv[4 * q + 2] = b4.z;
+                                    bv[4 * q + 3] = b4.w;
+                                }
+                            } else {
+#pragma unroll
+                                for (int jj = 0; jj < 32; ++jj) bv[jj] = c + jj < nrem ? __ldg(bsrc + jj) : 0.f;
+                            }
+                        }
                         float4* orow = reinterpret_cast<float4*>(ob) + lane * 8;
 #pragma unroll
                         for (int k = 0; k < 8; ++k) {
                             float e[4];
 #pragma unroll
-                            for (int x = 0; x < 4; ++x)
-                                e[x] = (c + 4 * k + x < nrem) ? __uint_as_float(va[4 * k + x]) : 0.f;
+                            for (int x = 0; x < 4; ++x) {
+                                const int jj = 4 * k + x;
+                                const float v = __uint_as_float(va[jj]);
+                                e[x] = (c + jj < nrem) ? (epi.mode == 1 ? gelu_erfc_dev(v + bv[jj]) : v) : 0.f;
+                            }
                             orow[k ^ (lane & 7)] = make_float4(e[0], e[1], e[2], e[3]);
                         }
                     } else {
@@ -987,7 +1015,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     const CUtensorMap mbl = make_map(three ? bl : bh, PAIR ? BN / 2 : BN / CL, bk_of<ALO>());
     CUtensorMap md;
     std::memset(&md, 0, sizeof(md));
-    const bool tstore = ALO && g.tma_store;
+    const bool tstore = g.tma_store && (ALO || g.store == STORE_ROW);
     if (tstore && g.d_mode == 1) {
         // [n][row tile of 32][group][32]: box {32, 1, 1, 32} = 128-byte pieces (16-row tiles
         // with 64-byte pieces measured 3.5 vs 2.1 ms on the cfg2 inverse GEMM)
@@ -1214,7 +1242,7 @@ void GroupedGemm::finalize() {
     pair = bn == 192 && mtiles >= 2;
     if (const char* e = std::getenv("SPH_GEMM_PAIR")) pair = pair && std::atoi(e) != 0;
     // TMA-store epilogue when D is a uniform [group][rows][ldd] array (the Legendre GEMMs)
-    tma_store = (bn == 192 || alo) && !groups.empty();
+    tma_store = (bn == 192 || alo || (row_tma && store == STORE_ROW)) && !groups.empty();
     d_rows = 0;
     d_ldd = 0;
     int64_t gmax = 0;
