@@ -372,29 +372,29 @@ __global__ void __launch_bounds__(128) disco_band2_kernel(
                         so[mi][1][(2 * cl + 1) * K + k] = im[k].y;
                     }
                 __syncthreads();
-                // contiguous rows of cn * K floats per (order, re/im)
+                // contiguous rows of cn * K floats per (order, re/im), flattened over
+                // (row, float4) so every pass keeps all threads busy
                 const int rowlen = cn * K;
                 const bool vec = (rowlen & 3) == 0 && (ldS & 3) == 0 && ((c0 * K) & 3) == 0;
-                for (int r = 0; r < nt * 2; ++r) {
-                    const int t = r >> 1, ri = r & 1;
-                    float* drow = S + (((b * Hout + h) * nbo + mp0 + t) * 2 + ri) * ldS + c0 * K;
-                    const float* srow = &so[t][ri][0];
+                const int q4 = vec ? rowlen >> 2 : rowlen;
+                float* sbase = S + (((b * Hout + h) * nbo + mp0) * 2) * ldS + c0 * K;
+                for (int i = threadIdx.x; i < nt * 2 * q4; i += blockDim.x) {
+                    const int r = i / q4, j = i - r * q4;
+                    float* drow = sbase + static_cast<int64_t>(r) * ldS;
+                    const float* srow = &so[r >> 1][r & 1][0];
                     if (vec) {
-                        for (int j = threadIdx.x; j < (rowlen >> 2); j += blockDim.x) {
-                            float4 v = reinterpret_cast<const float4*>(srow)[j];
-                            float4* dst = reinterpret_cast<float4*>(drow) + j;
-                            if (slot0 != 0) {
-                                const float4 o = *dst;
-                                v.x += o.x;
-                                v.y += o.y;
-                                v.z += o.z;
-                                v.w += o.w;
-                            }
-                            *dst = v;
+                        float4 v = reinterpret_cast<const float4*>(srow)[j];
+                        float4* dst = reinterpret_cast<float4*>(drow) + j;
+                        if (slot0 != 0) {
+                            const float4 o = *dst;
+                            v.x += o.x;
+                            v.y += o.y;
+                            v.z += o.z;
+                            v.w += o.w;
                         }
+                        *dst = v;
                     } else {
-                        for (int j = threadIdx.x; j < rowlen; j += blockDim.x)
-                            drow[j] = slot0 != 0 ? drow[j] + srow[j] : srow[j];
+                        drow[j] = slot0 != 0 ? drow[j] + srow[j] : srow[j];
                     }
                 }
             }
