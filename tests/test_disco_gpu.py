@@ -188,3 +188,20 @@ def test_disco_transpose_batch_and_rejects():
     with pytest.raises(S.SphInvalidArgument):
         op.transpose_apply(torch.zeros((1, cout, oh, ow), device=DEV),
                            torch.zeros((cout, cin, 5), device=DEV))
+
+
+@pytest.mark.parametrize("cin,cout,B", [(66, 5, 2), (130, 3, 1), (7, 4, 3), (2, 1, 1)])
+def test_disco_channel_counts_vs_oracle(cin, cout, B):
+    """Band kernels across channel-pass boundaries: more than 64 channels (a partial second
+    64-channel pass), odd counts (the scalar kernel, channel-major U), and tiny counts;
+    stride-2 grids, against the fp64 restatement."""
+    op = S.DiscoOperator(grid(EQ, 12, 24), grid(GA, 6, 12), S.morlet_basis(3 * PI / 12))
+    oop = oracle.orc().disco_assemble(EQ, 12, 24, GA, 6, 12, 3 * PI / 12)
+    u = oracle.random_field((B, cin, 12, 24), 31)
+    mix = oracle.random_field((cout, cin, 9), 32) / math.sqrt(cin)
+    y = op.apply(torch.tensor(u, dtype=torch.float32, device=DEV), torch.tensor(mix, dtype=torch.float32, device=DEV))
+    torch.cuda.synchronize()
+    y = y.cpu().numpy().astype(np.float64)
+    for b in range(B):
+        ref = oracle.orc().disco_apply(oop, u[b], mix)
+        assert rel_l2(y[b], ref) <= TOL, (cin, cout, b)
