@@ -80,3 +80,19 @@ def test_decoder_errors():
     other = S.DiscoOperator(grid(EQ, 17, 32), grid(EQ, 9, 16), S.morlet_basis(3 * PI / 9))
     with pytest.raises(S.SphInvalidArgument):
         S.DecoderPlan(other, grid(GA, 8, 16))  # not an output-grid self map
+
+
+@pytest.mark.parametrize("cin", [66, 5])
+def test_decoder_channel_counts(cin):
+    """Fused decoder across the band kernel's 64-channel passes (66) and an odd count (the
+    channel-major spectrum): equal to bilinear_resample followed by disco_apply."""
+    gl, go = grid(GA, 8, 16), grid(EQ, 17, 32)
+    op = S.DiscoOperator(go, go, S.morlet_basis(3 * PI / 16))
+    g = torch.Generator(device="cpu").manual_seed(9)
+    lat = torch.randn(2, cin, 8, 16, generator=g).to(DEV)
+    mix = (torch.randn(3, cin, op.n_basis, generator=g) / math.sqrt(cin)).to(DEV)
+    y = S.decode_preclamp(op, S.SphericalField(gl, lat), mix).data
+    ref = op.apply(S.bilinear_resample(S.SphericalField(gl, lat), go).data, mix)
+    torch.cuda.synchronize()
+    err = (torch.linalg.vector_norm(y - ref) / torch.linalg.vector_norm(ref)).item()
+    assert err <= 2e-6, err
