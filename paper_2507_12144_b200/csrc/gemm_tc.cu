@@ -464,10 +464,12 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     // operands of k-step kk (8 fp32 of K) of a stage: atom kk / 4, 32-byte step kk % 4
     // (quad layout: the atoms' k-quads are contiguous 2 KB blocks)
     auto adesc = [&](int s, int kk) {
-        return (ALO && a_quad) ? make_sdesc_quad(a_hi(s) + kk * 2 * 2048)
-                               : make_sdesc<KB>(a_hi(s) + (kk / (KB / 8)) * L::A_ATOM + (kk % (KB / 8)) * 32);
+        if (ALO && a_quad) return make_sdesc_quad(a_hi(s) + kk * 2 * 2048);
+        if constexpr (KS == 1) return make_sdesc<KB>(a_hi(s) + kk * 32);  // one atom: no split
+        return make_sdesc<KB>(a_hi(s) + (kk / (KB / 8)) * L::A_ATOM + (kk % (KB / 8)) * 32);
     };
     auto bdesc = [&](uint32_t base, int kk) {
+        if constexpr (KS == 1) return make_sdesc<KB>(base + kk * 32);
         return make_sdesc<KB>(base + (kk / (KB / 8)) * L::B_ATOM + (kk % (KB / 8)) * 32);
     };
     // each role walks tiles cid, cid + ncl, ... and loads the next descriptor one tile ahead
@@ -1227,7 +1229,9 @@ void GroupedGemm::finalize() {
                             cudaMemcpyHostToDevice));
     // table-tile multicast over clusters on neighbouring M-tiles (measured at cfg2,
     // cluster 1 / 2 / 4: Legendre fwd 4.6 / 3.5 / 3.4 ms, inv 4.9 / 4.1 / 3.55 ms)
-    if (cluster == 0) cluster = mtiles >= 8 ? 4 : mtiles >= 4 ? 2 : 1;
+    // (the pair-mode Legendre GEMMs ignore this; the non-pair GEMMs measured best at 2:
+    // cfg4 MLP1 1.36 -> 1.24 ms, MLP2 0.69 -> 0.64 ms, cfg3 DISCO mix 1.445 -> 1.386 ms vs 4)
+    if (cluster == 0) cluster = mtiles >= 4 ? 2 : 1;
     if (const char* e = std::getenv("SPH_GEMM_CLUSTER")) {  // test / tuning override
         const int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) cluster = v;
