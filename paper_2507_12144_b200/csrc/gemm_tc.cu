@@ -735,36 +735,47 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     if (store_mode == STORE_ROW) {
                         // box {32 cols, 32 rows}, SWIZZLE_128B: row = lane, 16-byte chunk k of
                         // the row at k ^ (row & 7); fused bias + GeLU (epi mode 1) on the way
-                        float bv[32];
-#pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) bv[jj] = 0.f;
-                        if (epi.mode == 1) {
-                            const float* bsrc = epi.bias + w.n0 + c;
-                            if (c + 32 <= nrem && (reinterpret_cast<uintptr_t>(bsrc) & 15) == 0) {
-#pragma unroll
-                                for (int q = 0; q < 8; ++q) {
-                                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(bsrc) + q);
-                                    bv[4 * q] = b4.x;
-                                    bv[4 * q + 1] = b4.y;
-                                    bv[4 * q + 2] = b4.z;
-                                    bv[4 * q + 3] = b4.w;
-                                }
-                            } else {
-#pragma unroll
-                                for (int jj = 0; jj < 32; ++jj) bv[jj] = c + jj < nrem ? __ldg(bsrc + jj) : 0.f;
-                            }
-                        }
                         float4* orow = reinterpret_cast<float4*>(ob) + lane * 8;
+                        if constexpr (ALO) {  // no fused epilogue in the A_lo-in-TMEM kernels
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            float e[4];
+                            for (int k = 0; k < 8; ++k) {
+                                float e[4];
 #pragma unroll
-                            for (int x = 0; x < 4; ++x) {
-                                const int jj = 4 * k + x;
-                                const float v = __uint_as_float(va[jj]);
-                                e[x] = (c + jj < nrem) ? (epi.mode == 1 ? gelu_erfc_dev(v + bv[jj]) : v) : 0.f;
+                                for (int x = 0; x < 4; ++x)
+                                    e[x] = (c + 4 * k + x < nrem) ? __uint_as_float(va[4 * k + x]) : 0.f;
+                                orow[k ^ (lane & 7)] = make_float4(e[0], e[1], e[2], e[3]);
                             }
-                            orow[k ^ (lane & 7)] = make_float4(e[0], e[1], e[2], e[3]);
+                        } else {
+                            float bv[32];
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj) bv[jj] = 0.f;
+                            if (epi.mode == 1) {
+                                const float* bsrc = epi.bias + w.n0 + c;
+                                if (c + 32 <= nrem && (reinterpret_cast<uintptr_t>(bsrc) & 15) == 0) {
+#pragma unroll
+                                    for (int q = 0; q < 8; ++q) {
+                                        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bsrc) + q);
+                                        bv[4 * q] = b4.x;
+                                        bv[4 * q + 1] = b4.y;
+                                        bv[4 * q + 2] = b4.z;
+                                        bv[4 * q + 3] = b4.w;
+                                    }
+                                } else {
+#pragma unroll
+                                    for (int jj = 0; jj < 32; ++jj) bv[jj] = c + jj < nrem ? __ldg(bsrc + jj) : 0.f;
+                                }
+                            }
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                float e[4];
+#pragma unroll
+                                for (int x = 0; x < 4; ++x) {
+                                    const int jj = 4 * k + x;
+                                    const float v = __uint_as_float(va[jj]);
+                                    e[x] = (c + jj < nrem) ? (epi.mode == 1 ? gelu_erfc_dev(v + bv[jj]) : v) : 0.f;
+                                }
+                                orow[k ^ (lane & 7)] = make_float4(e[0], e[1], e[2], e[3]);
+                            }
                         }
                     } else {
                         // box {32 rows m (contiguous), 32 cols n}: element (n = jj, m = lane)
