@@ -28,6 +28,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-pthread",
                 "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
                 "-Xptxas", "-warn-spills"]
+if os.environ.get("SPH_DEBUG") == "1":  # bounded barrier waits in the GEMM (watchdog trap)
+    FLAGS += ["-DSPH_GEMM_WATCHDOG"]
 
 
 def _deps_newer(obj: str, src: str) -> bool:

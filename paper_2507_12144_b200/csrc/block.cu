@@ -250,7 +250,7 @@ void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, i
     require(p.lmax == lmax && p.mmax == mmax,
             "spectral_conv: plan truncation must be lmax=min(klmax,nlat), mmax=min(lmax,nlon/2)");
     if (B == 0) return;
-    SPH_CUDA(cudaSetDevice(p.device));
+    DeviceGuard dguard(p.device);
     const SpecWs w = spec_ws(p, B, cin, cout);
     uint8_t* base = static_cast<uint8_t*>(ws);
     DevBuf<uint8_t> tmp;
@@ -352,23 +352,14 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
     const int64_t ldc = static_cast<int64_t>(round_up(C, 4)), ldh = static_cast<int64_t>(round_up(H, 4));
     // workspace: G [B*P][ldc], Hm [B*P][ldh], W1 hi/lo [H][ldc], W2 hi/lo [C][ldh]
     const int64_t nG = B * P * ldc, nH = B * P * ldh, nW1 = H * ldc, nW2 = C * ldh;
-    float* wsp = nullptr;
-    {
-        // stream-ordered workspace from the device's default pool; keep the pool's memory
-        // resident across synchronisations (release threshold 0 would return the ~0.8 GB
-        // to the OS at every sync and remap it on the next call)
-        static std::once_flag once[64];
-        int dev = 0;
-        SPH_CUDA(cudaGetDevice(&dev));
-        std::call_once(once[dev & 63], [dev] {
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t thr = ~0ull;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-            }
-        });
-    }
-    SPH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wsp), 4 * (nG + nH + 2 * nW1 + 2 * nW2) + 1024, st));
+    require(B <= 65535 && C <= 65535, "block_apply: too many channels / batches");
+    require(B * P < (1LL << 31), "block: too many points");
+    // stream-ordered workspace from the library's own pool (release threshold UINT64_MAX
+    // keeps the ~0.8 GB resident across synchronisations; the device's default pool,
+    // which other cudaMallocAsync users share, is left untouched).  The guard returns
+    // it to the pool on every exit path, errors included.
+    StreamBuf wsb(4 * (nG + nH + 2 * nW1 + 2 * nW2) + 1024, st);
+    float* wsp = static_cast<float*>(wsb.p);
     float* G = wsp;
     float* Hm = G + round_up(nG, 64);
     float* w1h = Hm + round_up(nH, 64);
@@ -389,7 +380,6 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
             g->name = "gemm_mlp1";
             static const int row_tma = std::getenv("SPH_MLP_ROW_TMA") ? std::atoi(std::getenv("SPH_MLP_ROW_TMA")) : 1;
             g->row_tma = row_tma != 0;
-            require(B * P < (1LL << 31), "block: too many points");
             g->groups.push_back({0, 0, static_cast<int32_t>(B * P), static_cast<int32_t>(H),
                                  static_cast<int32_t>(C), static_cast<int32_t>(ldh), 0, 0});
             g->finalize();
@@ -416,7 +406,6 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
     }
     split_rows(w1, H, C, ldc, w1h, w1l, st);
     split_rows(w2, C, H, ldh, w2h, w2l, st);
-    require(B <= 65535 && C <= 65535, "block_apply: too many channels / batches");
     dim3 grid(static_cast<unsigned>((P + 32 * GELU_PT - 1) / (32 * GELU_PT)), static_cast<unsigned>((ldc + 31) / 32),
               static_cast<unsigned>(B));
     {
@@ -447,7 +436,6 @@ void block_epilogue(const float* conv, const float* x, const float* w1, const fl
         SPH_LAUNCH_CHECK();
     }
     count_launch();
-    SPH_CUDA(cudaFreeAsync(wsp, st));
 }
 
 }  // namespace sph

@@ -36,20 +36,40 @@ std::atomic<bool> g_prof_on{false};
 std::vector<ProfRec> g_prof;
 }  // namespace
 
-ProfScope::ProfScope(const char* name, cudaStream_t s, double work) : st(s) {
+ProfScope::ProfScope(const char* n, cudaStream_t s, double w) : name(n), work(w), st(s) {
     if (!g_prof_on.load(std::memory_order_relaxed)) return;
-    ProfRec r{name, nullptr, nullptr, work};
-    cudaEventCreate(&r.e0);
-    cudaEventCreate(&r.e1);
-    cudaEventRecord(r.e0, st);
-    std::lock_guard<std::mutex> lk(g_prof_mu);
-    slot = static_cast<int>(g_prof.size());
-    g_prof.push_back(r);
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        if (e0) cudaEventDestroy(e0);
+        e0 = e1 = nullptr;
+        return;
+    }
+    cudaEventRecord(e0, st);
 }
 ProfScope::~ProfScope() {
-    if (slot < 0) return;
+    if (!e0) return;
+    cudaEventRecord(e1, st);
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    cudaEventRecord(g_prof[slot].e1, st);
+    g_prof.push_back(ProfRec{name, e0, e1, work});
+}
+
+cudaMemPool_t lib_pool() {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    int dev = 0;
+    SPH_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    SPH_CUDA(cudaMemPoolCreate(&pool, &props));
+    uint64_t thr = ~0ull;
+    SPH_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    pools[dev] = pool;
+    return pool;
 }
 }  // namespace sph
 

@@ -77,7 +77,7 @@ void DecoderPlan::create(DiscoPlan* d, const double* lat_colat, int64_t lat_nlat
     require(d->hin == d->hout && d->win == d->wout && d->stride == 1,
             "decode: the decoder convolution maps the output grid onto itself");
     disco = d;
-    SPH_CUDA(cudaSetDevice(d->device));
+    DeviceGuard dguard(d->device);
     resample_create(rs, lat_colat, lat_nlat, lat_nlon, d->in_colat.data(), d->hin, d->win);
     ratio = static_cast<int>(d->win / lat_nlon);
     fourier = d->prec != SPH_PREC_FP32_SIMT && d->win % lat_nlon == 0 && lat_nlon <= (1 << 30);
@@ -130,7 +130,7 @@ void DecoderPlan::apply(const float* latent, const float* mix, int64_t B, int64_
                         void* ws, cudaStream_t st) {
     require(B >= 0 && cin >= 1 && cout >= 1, "decode: mix tensor shape mismatch");
     if (B == 0) return;
-    SPH_CUDA(cudaSetDevice(disco->device));
+    DeviceGuard dguard(disco->device);
     const DecWs w = dec_ws(*this, B, cin, cout);
     uint8_t* base = static_cast<uint8_t*>(ws);
     if (!base) {

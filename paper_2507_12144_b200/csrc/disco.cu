@@ -828,7 +828,9 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
         require(band0[h] >= h_in0 && band0[h] + bandc[h] <= h_in0 + nin,
                 "disco_apply: input rows do not cover the filter support of the output rows");
     if (B == 0) return;
-    SPH_CUDA(cudaSetDevice(device));
+    DeviceGuard dguard(device);
+    require_on_device(x, device, "disco_apply");
+    require_on_device(y, device, "disco_apply");
     const DiscoWs w = disco_ws(*this, B, cin, cout, nin, nout);
     uint8_t* base = static_cast<uint8_t*>(ws);
     if (!base) {
@@ -932,7 +934,7 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
 void DiscoPlan::build_transpose() {
     std::lock_guard<std::mutex> lk(mu);
     if (t_ready) return;
-    SPH_CUDA(cudaSetDevice(device));
+    DeviceGuard dguard(device);
     // psi_t_hat with weights b_k * w_out[h] (convolution.hpp:251: scale = base * w_out)
     std::vector<double> cw(win), sw(win);
     for (int64_t j = 0; j < win; ++j) {
@@ -1028,7 +1030,7 @@ void DiscoPlan::transpose_apply(const float* v, const float* mix, int64_t B, int
     require(cin >= 1 && cout >= 1 && B >= 0, "disco_transpose_apply: mix tensor shape mismatch");
     if (B == 0) return;
     build_transpose();
-    SPH_CUDA(cudaSetDevice(device));
+    DeviceGuard dguard(device);
     const DiscoTWs w = disco_t_ws(*this, B, cin, cout);
     uint8_t* base = static_cast<uint8_t*>(ws);
     if (!base) {

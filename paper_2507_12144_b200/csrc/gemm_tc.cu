@@ -60,10 +60,15 @@ __device__ __forceinline__ uint64_t global_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// Bounded wait: a protocol bug traps (launch error) after 3 s instead of hanging the GPU.
+// Barrier wait.  Debug builds (SPH_DEBUG=1 python paper_2507_12144_b200/build.py defines
+// SPH_GEMM_WATCHDOG) bound it: a protocol bug then prints the barrier state and traps after
+// 3 s instead of hanging.  Release builds spin without the bound, so a correct kernel
+// preempted or time-sliced for longer than that is never killed.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t ok = 0;
+#ifdef SPH_GEMM_WATCHDOG
     uint64_t t0 = 0;
+#endif
     for (;;) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -73,6 +78,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "r"(bar), "r"(parity)
             : "memory");
         if (ok) return;
+#ifdef SPH_GEMM_WATCHDOG
         const uint64_t t = global_ns();
         if (t0 == 0) t0 = t;
         else if (t - t0 > 3000000000ull) {
@@ -83,6 +89,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
                        blockIdx.x, threadIdx.x / 32, bar, parity, static_cast<unsigned long long>(raw));
             __trap();
         }
+#endif
     }
 }
 // arrive on the barrier at the same SMEM offset in cluster CTA `cta` (default .release.cta

@@ -143,7 +143,7 @@ void resample_apply(const ResamplePlan& p, const float* x, int64_t C, float* y, 
     require(C >= 0, "bilinear_resample: negative field count");
     require(C <= 65535, "bilinear_resample: at most 65535 fields per call");
     if (C == 0) return;
-    SPH_CUDA(cudaSetDevice(p.device));
+    DeviceGuard dguard(p.device);
     float* means = static_cast<float*>(ws);
     if (p.add_north || p.add_south) {
         require(means != nullptr, "bilinear_resample: workspace required for the pole extension");

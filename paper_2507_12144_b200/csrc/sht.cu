@@ -456,7 +456,9 @@ void ShtPlan::forward(const float* x, int64_t F, float* out, int layout, void* w
     require(layout == SPH_LAYOUT_DENSE_LM || layout == SPH_LAYOUT_INTERNAL, "sht_forward: bad layout");
     require(F >= 0, "sht_forward: negative field count");
     if (F == 0) return;
-    SPH_CUDA(cudaSetDevice(device));
+    DeviceGuard dguard(device);
+    require_on_device(x, device, "sht_forward");
+    require_on_device(out, device, "sht_forward");
     uint8_t* w8 = static_cast<uint8_t*>(workspace(ws, workspace_bytes(F)));
     float* eo = reinterpret_cast<float*>(w8);
     float* ctmp = reinterpret_cast<float*>(w8 + round_up(4 * eo_elems(F), 256));
@@ -471,7 +473,9 @@ void ShtPlan::inverse(const float* coeffs, int64_t F, int layout, float* y, void
     require(layout == SPH_LAYOUT_DENSE_LM || layout == SPH_LAYOUT_INTERNAL, "sht_inverse: bad layout");
     require(F >= 0, "sht_inverse: negative field count");
     if (F == 0) return;
-    SPH_CUDA(cudaSetDevice(device));
+    DeviceGuard dguard(device);
+    require_on_device(coeffs, device, "sht_inverse");
+    require_on_device(y, device, "sht_inverse");
     uint8_t* w8 = static_cast<uint8_t*>(workspace(ws, workspace_bytes(F)));
     float* eoi = reinterpret_cast<float*>(w8);
     float* ctmp = reinterpret_cast<float*>(w8 + round_up(4 * eo_elems(F), 256));
@@ -487,7 +491,7 @@ void ShtPlan::inverse(const float* coeffs, int64_t F, int layout, float* y, void
 
 void ShtPlan::fft_stage(const float* rings, int64_t F, int64_t h, float* bins, cudaStream_t st) {
     require(nlon >= 2 * mmax, "dist_sht_forward: resolution insufficient for mmax");
-    SPH_CUDA(cudaSetDevice(device));
+    DeviceGuard dguard(device);
     const double pi = 3.14159265358979323846;
     fft_forward_plain(fft, rings, F * h, static_cast<int>(mmax),
                       static_cast<float>(2.0 * pi / static_cast<double>(nlon)),
@@ -499,7 +503,7 @@ void ShtPlan::legendre_stage(const float* bins, int64_t F, int64_t m0, int64_t m
     require(m0 >= 0 && mcount >= 0 && m0 + mcount <= mmax, "legendre stage: order range");
     require(nlat >= lmax, "dist_sht_forward: resolution insufficient for lmax");
     if (F == 0 || mcount == 0) return;
-    SPH_CUDA(cudaSetDevice(device));
+    DeviceGuard dguard(device);
     uint8_t* w8 = static_cast<uint8_t*>(workspace(ws, stage_ws_bytes(F, mcount)));
     float* eo = reinterpret_cast<float*>(w8);
     float* cl = reinterpret_cast<float*>(w8 + round_up(4 * mcount * 2 * 2 * F * Rp, 256));
@@ -561,7 +565,7 @@ ShtPlan::~ShtPlan() = default;
 
 void ShtPlan::roundtrip_host(const float* xh, int64_t F, float* yh, int64_t chunk) {
     if (F <= 0) return;
-    SPH_CUDA(cudaSetDevice(device));
+    DeviceGuard dguard(device);
     if (chunk <= 0) chunk = 32;
     chunk = std::min(chunk, F);
     std::lock_guard<std::mutex> lk(pipe_mu);  // one round trip per plan at a time

@@ -262,7 +262,8 @@ class GpuBackend:
         self.precision = precision
 
     def _plan(self, grid, lmax, mmax):
-        return self.S.get_sht_plan(grid, lmax, mmax, self.precision, allow_equiangular_forward=True)
+        return self.S.get_sht_plan(grid, lmax, mmax, self.precision, allow_equiangular_forward=True,
+                                   device=torch.cuda.current_device())
 
     def fft_stage(self, grid, lmax, mmax, x: torch.Tensor) -> torch.Tensor:
         """x [C, h, nlon] -> [C, h, mmax, 2] (complex bins * 2pi/nlon)."""
@@ -467,9 +468,12 @@ def dist_crps(ctx: DistContext, f: Sharded, o: Sharded, grid, variant: str = "fa
     k = np.arange(sparts[me]) + soff
     w = np.asarray(grid.quad_weights, dtype=np.float64)[h0 + k // Wloc]
     part = backend.weighted_crps(t, ochunk, w, variant)                    # [C] fp64
-    if g.world() > 1:
-        dist.all_reduce(part, group=ctx.pg_nonbatch)
+    # reduce over ensemble+polar+azimuth only (distsim.hpp:620): ranks of other batch
+    # items score other samples.  With one member per batch group there is nothing to
+    # reduce (pg_nonbatch is None then, which would mean the whole world).
     members = g.world() // g.axis_size(BATCH)
+    if members > 1:
+        dist.all_reduce(part, group=ctx.pg_nonbatch)
     ctx.record("ensemble+polar+azimuth", "all_reduce", (members - 1) * part.numel() * part.element_size()
                if me == 0 and ctx.index(POLAR) == 0 and ctx.index(AZIMUTH) == 0 else 0, part)
     return part

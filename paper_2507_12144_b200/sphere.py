@@ -147,8 +147,7 @@ class ShtPlan:
     def __init__(self, grid: GridSpec, lmax: int, mmax: int, precision: str = "3xtf32",
                  allow_equiangular_forward: bool = False, device=None, adjoint: bool = False):
         self.grid, self.lmax, self.mmax = grid, int(lmax), int(mmax)
-        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
-                                   else torch.device(device).index or 0)
+        self.device = torch.device("cuda", _dev_index(device))
         flags = PRECISIONS[precision] | (L.SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD
                                          if allow_equiangular_forward else 0)
         if adjoint:  # forward / inverse compute the adjoints of inverse / forward
@@ -225,14 +224,23 @@ class ShtPlan:
         return out
 
 
+def _dev_index(device) -> int:
+    if device is None:
+        return torch.cuda.current_device()
+    d = torch.device(device)
+    return torch.cuda.current_device() if d.index is None else d.index
+
+
 def get_sht_plan(grid: GridSpec, lmax: int, mmax: int, precision: str = "3xtf32",
-                 allow_equiangular_forward: bool = False, adjoint: bool = False) -> ShtPlan:
-    dev = torch.cuda.current_device()
+                 allow_equiangular_forward: bool = False, adjoint: bool = False, device=None) -> ShtPlan:
+    """Plan cache keyed by the device of the data (``device``, default the current one):
+    a tensor on cuda:1 gets a cuda:1 plan whatever device is current."""
+    dev = _dev_index(device)
     key = (grid.kind, grid.nlat, grid.nlon, lmax, mmax, precision, allow_equiangular_forward, dev, adjoint)
     with _plan_lock:
         p = _sht_plans.get(key)
         if p is None:
-            p = ShtPlan(grid, lmax, mmax, precision, allow_equiangular_forward, adjoint=adjoint)
+            p = ShtPlan(grid, lmax, mmax, precision, allow_equiangular_forward, device=dev, adjoint=adjoint)
             _sht_plans[key] = p
         return p
 
@@ -262,7 +270,7 @@ def _forward(field: SphericalField, lmax: int, mmax: int, precision: str,
              allow_eq: bool) -> SpectralCoeffs:
     g = field.grid
     lead = tuple(field.data.shape[:-2])
-    plan = get_sht_plan(g, lmax, mmax, precision, allow_eq)
+    plan = get_sht_plan(g, lmax, mmax, precision, allow_eq, device=field.data.device)
     with torch.cuda.device(field.data.device):
         out = plan.forward(field.data)
     return SpectralCoeffs(lmax, mmax, torch.view_as_complex(out).reshape(*lead, lmax, mmax))
@@ -276,7 +284,7 @@ def sht_inverse(coeffs: SpectralCoeffs, grid: GridSpec,
     c = coeffs.coeffs
     lead = tuple(c.shape[:-2])
     F = int(np.prod(lead)) if lead else 1
-    plan = get_sht_plan(grid, coeffs.lmax, coeffs.mmax, precision)
+    plan = get_sht_plan(grid, coeffs.lmax, coeffs.mmax, precision, device=c.device)
     with torch.cuda.device(c.device):
         y = plan.inverse(c.to(torch.complex64), F)
     return SphericalField(grid, y.reshape(*lead, grid.nlat, grid.nlon))
@@ -295,7 +303,7 @@ def sht_forward_adjoint(coeffs: SpectralCoeffs, grid: GridSpec, precision: str =
     c = coeffs.coeffs
     lead = tuple(c.shape[:-2])
     F = int(np.prod(lead)) if lead else 1
-    plan = get_sht_plan(grid, coeffs.lmax, coeffs.mmax, precision, adjoint=True)
+    plan = get_sht_plan(grid, coeffs.lmax, coeffs.mmax, precision, adjoint=True, device=c.device)
     with torch.cuda.device(c.device):
         y = plan.inverse(c.to(torch.complex64), F)
     return SphericalField(grid, y.reshape(*lead, grid.nlat, grid.nlon))
@@ -310,7 +318,7 @@ def sht_inverse_adjoint(field: SphericalField, lmax: int, mmax: int, precision: 
     if mmax > lmax:
         raise L.SphInvalidArgument(1, "SpectralCoeffs: mmax must be <= lmax")
     lead = tuple(field.data.shape[:-2])
-    plan = get_sht_plan(g, lmax, mmax, precision, adjoint=True)
+    plan = get_sht_plan(g, lmax, mmax, precision, adjoint=True, device=field.data.device)
     with torch.cuda.device(field.data.device):
         out = plan.forward(field.data)
     return SpectralCoeffs(lmax, mmax, torch.view_as_complex(out).reshape(*lead, lmax, mmax))
@@ -350,14 +358,15 @@ class DiscoOperator:
     """convolution.hpp:105-123: the assembled operator lives on the device."""
 
     def __init__(self, in_grid: GridSpec, out_grid: GridSpec, basis: FilterBasis,
-                 precision: str = "3xtf32"):
+                 precision: str = "3xtf32", device=None):
         self.in_grid, self.out_grid, self.basis = in_grid, out_grid, basis
-        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device("cuda", _dev_index(device))
         h = C.c_void_p()
-        check(L.lib.sph_disco_plan_create(in_grid.kind, in_grid.nlat, in_grid.nlon,
-                                          out_grid.kind, out_grid.nlat, out_grid.nlon,
-                                          basis.kind, basis.theta_cutoff, PRECISIONS[precision],
-                                          C.byref(h)))
+        with torch.cuda.device(self.device):
+            check(L.lib.sph_disco_plan_create(in_grid.kind, in_grid.nlat, in_grid.nlon,
+                                              out_grid.kind, out_grid.nlat, out_grid.nlon,
+                                              basis.kind, basis.theta_cutoff, PRECISIONS[precision],
+                                              C.byref(h)))
         self.h = h
         k, s, nnz = C.c_int64(), C.c_int64(), C.c_int64()
         check(L.lib.sph_disco_plan_info(h, C.byref(k), C.byref(s), C.byref(nnz)))
@@ -439,14 +448,15 @@ class DiscoOperator:
 
 
 def assemble_disco(in_grid: GridSpec, out_grid: GridSpec, basis: FilterBasis,
-                   precision: str = "3xtf32") -> DiscoOperator:
-    """convolution.hpp:141-177."""
+                   precision: str = "3xtf32", device=None) -> DiscoOperator:
+    """convolution.hpp:141-177 (the operator lives on ``device``, default the current one)."""
+    dev = _dev_index(device)
     key = (in_grid.kind, in_grid.nlat, in_grid.nlon, out_grid.kind, out_grid.nlat,
-           out_grid.nlon, basis, precision, torch.cuda.current_device())
+           out_grid.nlon, basis, precision, dev)
     with _plan_lock:
         op = _disco_plans.get(key)
     if op is None:
-        op = DiscoOperator(in_grid, out_grid, basis, precision)
+        op = DiscoOperator(in_grid, out_grid, basis, precision, device=dev)
         with _plan_lock:
             _disco_plans[key] = op
     return op
@@ -618,8 +628,8 @@ def angular_psd(field: SphericalField, precision: str = "3xtf32") -> torch.Tenso
         raise L.SphInvalidArgument(1, "sht_forward: requires a gaussian grid")
     lmax = g.nlat
     mmax = max(min(default_mmax(lmax, g.nlon), g.nlon // 2), 1)
-    plan = get_sht_plan(g, lmax, mmax, precision)
     x = _dev_f32(field.data, "angular_psd")
+    plan = get_sht_plan(g, lmax, mmax, precision, device=x.device)
     F = x.numel() // (g.nlat * g.nlon)
     with torch.cuda.device(x.device):
         c = plan.forward(x, L.SPH_LAYOUT_DENSE_LM)
@@ -645,8 +655,8 @@ def spectral_crps_loss(ens: torch.Tensor, obs: SphericalField, lmax_sum: int = 0
         raise L.SphInvalidArgument(1, "spectral_crps_loss: lmax_sum exceeds grid capacity")
     lmax = lmax_sum + 1
     mmax = min(lmax, g.nlon // 2)
-    plan = get_sht_plan(g, lmax, mmax, precision)
     ens = _dev_f32(ens, "spectral_crps_loss")
+    plan = get_sht_plan(g, lmax, mmax, precision, device=ens.device)
     o = _dev_f32(obs.data, "spectral_crps_loss")
     with torch.cuda.device(ens.device):
         ce = plan.forward(ens.reshape(E * Cc, g.nlat, g.nlon), L.SPH_LAYOUT_DENSE_LM)
@@ -669,8 +679,8 @@ def spectral_conv(field: SphericalField, kernel: torch.Tensor,
         raise L.SphInvalidArgument(1, "spectral_conv: kernel channel mismatch")
     lmax = min(klmax, g.nlat)
     mmax = min(lmax, g.nlon // 2)
-    plan = get_sht_plan(g, lmax, mmax, precision)
     x = _dev_f32(field.data, "spectral_conv")
+    plan = get_sht_plan(g, lmax, mmax, precision, device=x.device)
     lead = tuple(x.shape[:-3])
     B = x.numel() // (cin * g.nlat * g.nlon)
     kernel = _dev_f32(kernel, "spectral_conv")

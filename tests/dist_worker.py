@@ -109,10 +109,14 @@ class OracleDiscoOp:
 
 def run_crps(args, cuda, dev, G):
     """dist_crps (Alg. 3) vs the serial crps_field (test_distsim.cpp:250-300)."""
-    ctx = D.DistContext(D.CommGrid((1, args.ne, args.nh, args.nw)))
+    ctx = D.DistContext(D.CommGrid((args.nb, args.ne, args.nh, args.nw)))
     rep = {}
+    # batch item b scores the golden sample scaled by (1 + b): CRPS is positively
+    # homogeneous, so its score is (1 + b) * golden -- a rank that mixed in another batch
+    # item's partial sums would be off by a whole sample's score.
+    scale = 1.0 + ctx.index(D.BATCH)
     for key, nlat, nlon in (("crps_ga8_E8", 8, 16), ("crps_ga5_E8", 5, 8)):
-        ens, obs, want = G[key + "_ens"], G[key + "_obs"], G[key]
+        ens, obs, want = G[key + "_ens"] * scale, G[key + "_obs"] * scale, G[key] * scale
         E = ens.shape[0]
         ep = D.canonical_split(E, args.ne)
         hp, wp = D.canonical_split(nlat, args.nh), D.canonical_split(nlon, args.nw)
@@ -135,7 +139,10 @@ def run_crps(args, cuda, dev, G):
             grid.quad_weights = w
         ctx.log = D.TrafficLog()
         got = D.dist_crps(ctx, f, o, grid, "fair", backend).cpu().numpy()
-        rep[key] = float(np.abs(got - want).max() / max(1.0, np.abs(want).max()))
+        err = torch.tensor([float(np.abs(got - want).max() / max(1.0, np.abs(want).max()))],
+                           dtype=torch.float64, device=dev)
+        dist.all_reduce(err, op=dist.ReduceOp.MAX)   # worst rank, every batch item
+        rep[key] = float(err.item())
         rep[key + "_calls"] = {c: ctx.log.calls("dist_crps", c) for c in ("all_to_all", "scatter", "all_reduce")}
     return rep
 
@@ -143,6 +150,7 @@ def run_crps(args, cuda, dev, G):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ne", type=int, default=0, help="dist_crps mode with this many ensemble ranks")
+    ap.add_argument("--nb", type=int, default=1, help="dist_crps: batch ranks")
     ap.add_argument("--device", default="cpu")
     ap.add_argument("--nh", type=int, required=True)
     ap.add_argument("--nw", type=int, required=True)

@@ -25,14 +25,19 @@ def _free_port():
     return p
 
 
-def _run(nh, nw, device, tmp_path, ne=0):
-    out = tmp_path / f"rep_{ne}x{nh}x{nw}_{device}.json"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={max(ne, 1) * nh * nw}",
+def _run(nh, nw, device, tmp_path, ne=0, nb=1):
+    out = tmp_path / f"rep_{nb}x{ne}x{nh}x{nw}_{device}.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nb * max(ne, 1) * nh * nw}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), "--device", device, "--nh", str(nh),
-           "--nw", str(nw), "--ne", str(ne), "--out", str(out)]
+           "--nw", str(nw), "--ne", str(ne), "--nb", str(nb), "--out", str(out)]
     env = dict(os.environ, OMP_NUM_THREADS="1")
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    for _ in range(4):  # the probed free port can be taken before the rendezvous binds it
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            break
+        cmd[cmd.index("--master-port") + 1] = str(_free_port())
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
     return json.loads(out.read_text())
 
@@ -60,11 +65,13 @@ def test_dist_gloo_matches_reference_simulator(nh, nw, tmp_path):
         assert rep["odd_err"] <= 1e-12
 
 
-@pytest.mark.parametrize("ne,nh,nw", [(2, 1, 1), (4, 1, 1), (1, 2, 2), (2, 1, 2)])
-def test_dist_crps_gloo_matches_serial(ne, nh, nw, tmp_path):
+@pytest.mark.parametrize("nb,ne,nh,nw", [(1, 2, 1, 1), (1, 4, 1, 1), (1, 1, 2, 2), (1, 2, 1, 2),
+                                         (2, 1, 1, 1), (2, 2, 1, 1)])
+def test_dist_crps_gloo_matches_serial(nb, ne, nh, nw, tmp_path):
     """Alg. 3 (distsim.hpp:548-629) vs the reference's serial crps_field, incl. spatial
-    shards not divisible by the ensemble axis (test_distsim.cpp:277-303)."""
-    rep = _run(nh, nw, "cpu", tmp_path, ne=ne)
+    shards not divisible by the ensemble axis (test_distsim.cpp:277-303) and batch ranks
+    (each batch item reduces over ensemble+polar+azimuth only, distsim.hpp:620)."""
+    rep = _run(nh, nw, "cpu", tmp_path, ne=ne, nb=nb)
     for key in ("crps_ga8_E8", "crps_ga5_E8"):
         assert rep[key] <= 1e-12, rep
         assert rep[key + "_calls"] == {"all_to_all": 1, "scatter": 1, "all_reduce": 1}
