@@ -1,16 +1,24 @@
 """Benchmark of the spherical-operator hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload sht|disco]
+                    [--workload all|sht|disco|disco_t|block|decoder|dist_sht|dist_disco]
 
-Default workload (N=1): configs[1] -- forward + inverse SHT on the 721x1440
-equiangular grid, lmax=721 (count) / mmax=720, 256 channels x batch 4 = 1024 fields per
-GPU.  One step = sht_inverse(sht_forward(x)) over those 1024 fields.  For N>1 (launched
-by torchrun) every rank transforms its own 1024 fields (batch/channel sharding, no
-data-path collective) -> "scaling": "weak"; value = all fields / max-over-ranks time.
+Default (``--workload all``), one JSON line:
+  * ``value``: configs[1] -- forward + inverse SHT on the 721x1440 equiangular grid,
+    lmax=721 (count) / mmax=720, 256 channels x batch 4 = 1024 fields per GPU; one step =
+    sht_inverse(sht_forward(x)) over those fields.  For N > 1 every rank transforms its own
+    1024 fields (batch/channel sharding, no data-path collective) -> "scaling": "weak";
+    value = all fields / max-over-ranks time.
+  * ``disco``: configs[2] -- DISCO 721x1440 eq -> 360x720 Gaussian, Morlet K=9, cutoff
+    3*pi/360, 64 -> 256 channels, batch 4 per GPU (output fields/s), with its own roofline,
+    e2e and CPU baseline.
+  * ``domain_decomposed`` (N > 1): configs[4] -- the paper's lat/lon decomposition through
+    the library's NCCL path (csrc/dist.cu): distributed SHT + inverse SHT round trip and
+    distributed DISCO (-> 360x720 Gaussian) at 721x1440, 512 channels, batch 1, polar x
+    azimuth = N x 1, strong scaling against the same problem on one GPU of the same run.
 
-``--workload disco`` times configs[2] (DISCO 721x1440 eq -> 360x720 Gaussian,
-Morlet K=9, cutoff 3*pi/360, 64 -> 256 channels) instead.
+``python bench.py --gpus N`` launches N ranks itself (torchrun, 127.0.0.1) when it is not
+already running under torchrun.
 
 ``--impl reference`` times the reference's own CPU implementation (the unmodified
 headers compiled into oracle/_ref/libsphref.so; the C restatement if that is absent) on
@@ -175,7 +183,7 @@ def max_over_ranks(v, ws):
 
 
 # -------------------------------------------------------------- CPU legs
-def cpu_reference_sht(nfields_per_thread=1, threads=None):
+def cpu_reference_sht(nfields_per_thread=2, threads=None):
     """Reference CPU SHT round trip at 721x1440 on the host cores (bounded sample)."""
     import oracle
     threads = threads or os.cpu_count() or 1
@@ -184,7 +192,7 @@ def cpu_reference_sht(nfields_per_thread=1, threads=None):
     if oracle.ref_available():
         steady, tables, _ = oracle.ref().bench_sht_roundtrip(0, NLAT, NLON, LMAX, MMAX, x, threads)
         kind = "reference"
-    else:  # C restatement, one field per thread
+    else:  # C restatement, one field per task
         from concurrent.futures import ThreadPoolExecutor
         o = oracle.orc()
         t0 = time.perf_counter()
@@ -197,23 +205,28 @@ def cpu_reference_sht(nfields_per_thread=1, threads=None):
         steady, tables, kind = time.perf_counter() - t0, 0.0, "port"
     return {"value": n / steady, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{n} fields of 721x1440 equiangular, SHT+ISHT round trip (lmax=721, mmax=720), "
-                      f"{threads} threads x {nfields_per_thread} field(s); one-time Legendre tables "
+                      f"{threads} threads x {nfields_per_thread} fields; one-time Legendre tables "
                       f"{tables:.1f} s excluded", "seconds": steady, "tables_s": tables}
 
 
 def cpu_reference_disco(threads=None):
+    """Reference disco_apply at configs[2] for ONE sample (64 -> 256 channels), measured on
+    a 16-input-channel slice with all 256 outputs and scaled by 64/16: both terms of the
+    reference's cost -- the gather (convolution.hpp:192-205) and the mix (:207-218) -- are
+    linear in c_in, so the scaling is exact (the former 8-output sample under-counted the
+    c_out-proportional mix)."""
     import oracle
     threads = threads or os.cpu_count() or 1
-    cin, cout = 64, 8  # bounded sample: all 64 input channels, 8 of the 256 outputs
-    x = oracle.random_field((cin, NLAT, NLON), 1)
-    mix = oracle.random_field((cout, cin, 9), 77)
+    cin_s, cin, cout = 16, 64, 256
+    x = oracle.random_field((cin_s, NLAT, NLON), 1)
+    mix = oracle.random_field((cout, cin_s, 9), 77)
     steady, asm, _ = oracle.ref().bench_disco(0, NLAT, NLON, 1, 360, 720, 3 * math.pi / 360, x,
-                                              mix, threads)
-    # gather cost is independent of c_out; mix cost scales with c_out -> report the
-    # measured rate for this sample (output fields/s)
-    return {"value": cout / steady, "unit": "output fields/s", "cores": threads, "kind": "reference",
-            "sample": f"DISCO 721x1440->360x720, c_in=64, c_out={cout} of 256, {threads} threads; "
-                      f"assembly {asm:.1f} s excluded", "seconds": steady}
+                                              mix, min(threads, cin_s))
+    t_sample = steady * cin / cin_s
+    return {"value": cout / t_sample, "unit": "output fields/s", "cores": min(threads, cin_s), "kind": "reference",
+            "sample": f"DISCO 721x1440->360x720, c_in 16 of 64 with all 256 outputs on {min(threads, cin_s)} "
+                      f"threads (reference threads over c_in), time x 64/16 (gather and mix are linear in "
+                      f"c_in); assembly {asm:.1f} s excluded", "seconds": t_sample}
 
 
 def run_reference_arm(args, ws, rank):
@@ -223,7 +236,7 @@ def run_reference_arm(args, ws, rank):
     vals = []
     info = None
     for i in range(args.warmup + args.steps):
-        info = cpu_reference_sht(1, threads) if args.workload == "sht" else cpu_reference_disco(threads)
+        info = cpu_reference_disco(threads) if args.workload == "disco" else cpu_reference_sht(1, threads)
         if i >= args.warmup:
             vals.append(info["value"])
     v = statistics.median(vals)
@@ -237,21 +250,31 @@ def run_reference_arm(args, ws, rank):
     print(json.dumps(out), flush=True)
 
 
+SHT_CONFIG = {"workload": "configs[1]: forward+inverse SHT, 721x1440 equiangular (lmax=720 i.e. reference counts "
+                          "lmax=721, mmax=720), 256 channels x batch 4 per GPU",
+              "grid": "equiangular 721x1440", "fields_per_gpu": FIELDS, "batch": BATCH, "channels": CHANNELS,
+              "precision": "fp32 I/O, 3xTF32 tcgen05 Legendre GEMMs, fp32 accumulate",
+              "l2_policy": "inputs (4.25 GB/GPU) larger than the 126 MB L2"}
+DISCO_CONFIG = {"workload": "configs[2]: DISCO conv 721x1440 eq -> 360x720 Gaussian, Morlet K=9, cutoff 3pi/360, "
+                            "64 -> 256 channels, batch 4 per GPU",
+                "batch": 4, "c_in": 64, "c_out": 256, "precision": "fp32 I/O, 3xTF32 channel mix",
+                "l2_policy": "inputs (1.06 GB/GPU) larger than the 126 MB L2"}
+
+
 def workload_config(args):
-    if args.workload == "sht":
-        return {"workload": "configs[1]: forward+inverse SHT, 721x1440 equiangular (lmax=720 i.e. "
-                            "reference counts lmax=721, mmax=720), 256 channels x batch 4 per GPU",
-                "grid": "equiangular 721x1440", "fields_per_gpu": FIELDS, "batch": BATCH,
-                "channels": CHANNELS, "parallelism": f"fields sharded over {args.gpus} GPU(s)",
-                "precision": "fp32 I/O, 3xTF32 tcgen05 Legendre GEMMs, fp32 accumulate",
-                "l2_policy": "inputs (4.25 GB/GPU) larger than the 126 MB L2"}
+    if args.workload in ("all", "sht"):
+        cfg = dict(SHT_CONFIG, parallelism=f"fields sharded over {args.gpus} GPU(s)")
+        if args.workload == "all":
+            cfg["also"] = "disco: configs[2]; domain_decomposed (N>1): configs[4]"
+        return cfg
     if args.workload in ("dist_sht", "dist_disco"):
         nh, nw = decomp(args)
-        what = ("forward SHT (paper Alg. 1: 4 all-to-all transposes)" if args.workload == "dist_sht"
+        what = ("forward + inverse SHT round trip (paper Alg. 1 and its mirror)" if args.workload == "dist_sht"
                 else "DISCO conv -> 360x720 Gaussian, 512 -> 512 channels (Alg. 2 with latitude halo)")
         return {"workload": f"configs[4]: distributed {what}, 721x1440 equiangular, 512 channels, "
                             f"batch 1, {nh}x{nw} (polar x azimuth) decomposition",
-                "decomposition": f"{nh}x{nw}", "channels": 512, "parallelism": f"lat/lon domain decomposition over {nh * nw} GPU(s), NCCL",
+                "decomposition": f"{nh}x{nw}", "channels": 512,
+                "parallelism": f"lat/lon domain decomposition over {nh * nw} GPU(s), NCCL (libsphgpu.so)",
                 "precision": "fp32 I/O, 3xTF32 tcgen05 GEMMs"}
     if args.workload == "block":
         return {"workload": "configs[3]: one global block (SHT -> spectral channel mix -> ISHT -> GeLU/MLP "
@@ -267,14 +290,11 @@ def workload_config(args):
         return {"workload": "configs[2] adjoint: disco_transpose_apply 360x720 Gaussian -> 721x1440 eq, "
                             "Morlet K=9, cutoff 3pi/360, 256 -> 64 channels, batch 4 per GPU",
                 "batch": 4, "c_in": 64, "c_out": 256, "precision": "fp32 I/O, 3xTF32 channel mix"}
-    return {"workload": "configs[2]: DISCO conv 721x1440 eq -> 360x720 Gaussian, Morlet K=9, "
-                        "cutoff 3pi/360, 64 -> 256 channels, batch 4 per GPU",
-            "batch": 4, "c_in": 64, "c_out": 256, "precision": "fp32 I/O, 3xTF32 channel mix",
-            "l2_policy": "inputs (1.06 GB/GPU) larger than the 126 MB L2"}
+    return dict(DISCO_CONFIG)
 
 
 def decomp(args):
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    ws = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if args.decomp:
         nh, nw = (int(v) for v in args.decomp.lower().split("x"))
     else:
@@ -284,259 +304,144 @@ def decomp(args):
     return nh, nw
 
 
-def run_dist(args, ws, rank, local):
-    """cfg5: the paper's domain-decomposed SHT / DISCO at 721x1440, 512 channels, batch 1.
-    Strong scaling (fixed global problem); value = channels (fields) per second; every
-    collective is NCCL over NVLink; timed with CUDA events, max over ranks."""
+# ----------------------------------------------------------------- timing
+def timed(step, steps, warmup, ws, local, stream):
+    """W warm-up steps, then K steps bracketed by barrier + synchronize, CUDA events on
+    the launching stream, clocks sampled during the region; returns (ms/step max over
+    ranks, library launches in the region, per-kernel profile, clock summary)."""
     import torch
-    import torch.distributed as dist
-    import paper_2507_12144_b200 as S
-    from paper_2507_12144_b200 import dist as D
-    if ws == 1 and not dist.is_initialized():
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29517")
-        os.environ.setdefault("RANK", "0")
-        os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    nh, nw = decomp(args)
-    ctx = D.DistContext(D.CommGrid((1, 1, nh, nw)))
-    ctx.track = False
-    dev = torch.device("cuda", local)
-    C = 512
-    torch.manual_seed(1234 + rank)
-    hp, wp = D.canonical_split(NLAT, nh), D.canonical_split(NLON, nw)
-    i, j = ctx.index(D.POLAR), ctx.index(D.AZIMUTH)
-    x = D.Sharded(torch.rand((C, hp[i], wp[j]), device=dev) * 2 - 1, {1: hp, 2: wp})
-    backend = D.GpuBackend()
-    if args.workload == "dist_sht":
-        grid = S.build_equiangular(NLAT, NLON)
-
-        def step():
-            D.dist_sht_forward(ctx, x, grid, LMAX, MMAX, backend)
-    else:
-        op = S.DiscoOperator(S.build_equiangular(NLAT, NLON), S.build_gaussian(360, 720),
-                             S.morlet_basis(3 * math.pi / 360))
-        mix = (torch.rand((C, C, op.n_basis), device=dev) * 2 - 1) / math.sqrt(C * 9)
-
-        def step():
-            D.dist_disco_apply(ctx, x, op, mix, backend)
     from paper_2507_12144_b200 import _lib as L
-    stream = torch.cuda.current_stream(dev)
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(warmup, 3)):
         step()
     torch.cuda.synchronize()
-    launches0 = L.launch_count()
     L.profile_read()
     L.profile_enable(True)
-    dist.barrier()
+    launches0 = L.launch_count()
+    barrier(ws)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
-    dist.barrier()
+    barrier(ws)
     L.profile_enable(False)
-    prof = L.profile_read()
     launches = L.launch_count() - launches0
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
-    # traffic of one step (reference TrafficLog schema, group-summed bytes)
-    ctx.track = True
-    ctx.log = D.TrafficLog()
-    step()
-    torch.cuda.synchronize()
-    if rank == 0:
-        out = {"metric": METRIC, "value": C / (ms / 1e3), "unit": "fields/s", "n_gpus": ws,
-               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-               "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
-               "traffic_csv": ctx.log.csv(), "gpu_launches": launches, "clocks": clk.summary(),
-               "per_kernel_ms_rank0": {k: v[1] / args.steps for k, v in sorted(prof.items())},
-               "roofline": None, "cpu_baseline": None, "e2e": None}
-        print(json.dumps(out), flush=True)
+    prof = L.profile_read()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, ws)
+    return ms, launches, prof, clk.summary()
+
+
+def roofline(prof, steps, ms, traffic_key=None):
+    """Dominant kernel of the step from live CUDA-event timing of every library launch:
+    GEMMs against the 3xTF32 tensor ceiling (measured bf16 / 2 for TF32, / 3 passes) on
+    algorithmic 2MNK flops; everything else against measured HBM bandwidth on
+    algorithmic bytes."""
+    hbm, bf16, _, peak_src = peaks()
+    if not prof:
+        return None
+    name, (cnt, tot_ms, work) = max(prof.items(), key=lambda kv: kv[1][1])
+    per_launch_s = tot_ms / cnt / 1e3
+    if name.startswith("gemm"):
+        achieved = work / cnt / per_launch_s / 1e12
+        pk = bf16 / 2 / 3
+        roof = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
+                "frac": achieved / pk,
+                "peak_note": f"{peak_src} bf16 {bf16} TF/s / 2 (TF32 rate) / 3 (3xTF32 passes)"}
+    else:
+        achieved = work / cnt / per_launch_s / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_note": f"{peak_src} copy bandwidth"}
+    roof["share_of_step"] = tot_ms / steps / ms
+    roof["algorithmic_per_launch"] = work / cnt
+    roof["traffic"] = None
+    try:  # DRAM bytes per launch of this kernel from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_sht.json")) as f:
+            tj = json.load(f)
+        tw = tj["dram_bytes_per_launch"] if traffic_key == "sht" else \
+            tj.get("by_workload", {}).get(traffic_key, {}).get("dram_bytes_per_launch", {})
+        if name in tw:
+            roof["traffic"] = tw[name]
+            roof["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write)"
+    except Exception:
+        pass
+    roof["per_kernel_ms"] = {k: v[1] / steps for k, v in sorted(prof.items())}
+    return roof
 
 
 # ----------------------------------------------------------------- GPU arm
-def run_ours(args, ws, rank, local):
+def measure_sht(args, ws, rank, local):
     import torch
     import paper_2507_12144_b200 as S
     from paper_2507_12144_b200 import _lib as L
-
     dev = torch.device("cuda", local)
-    hbm, bf16, bf16_sus, peak_src = peaks()
-    torch.manual_seed(1234 + rank)
-    extra = {}
+    g = S.build_equiangular(NLAT, NLON)
+    plan = S.ShtPlan(g, LMAX, MMAX, "3xtf32", allow_equiangular_forward=True, device=dev)
+    F = FIELDS
+    x = torch.rand((F, NLAT, NLON), device=dev, dtype=torch.float32) * 2 - 1
+    y = torch.empty_like(x)
+    cint = torch.zeros(plan.coeffs_elems(F, L.SPH_LAYOUT_INTERNAL), device=dev)
+    wsb = plan.workspace(F)
 
-    if args.workload == "sht":
-        g = S.build_equiangular(NLAT, NLON)
-        plan = S.ShtPlan(g, LMAX, MMAX, "3xtf32", allow_equiangular_forward=True)
-        F = FIELDS
-        x = torch.rand((F, NLAT, NLON), device=dev, dtype=torch.float32) * 2 - 1
-        y = torch.empty_like(x)
-        cint = torch.zeros(plan.coeffs_elems(F, L.SPH_LAYOUT_INTERNAL), device=dev)
-        wsb = plan.workspace(F)
-
-        def step():
-            plan.forward(x, L.SPH_LAYOUT_INTERNAL, out=cint, ws=wsb)
-            plan.inverse(cint, F, L.SPH_LAYOUT_INTERNAL, out=y, ws=wsb)
-        units = F
-    elif args.workload == "block":
-        g = S.build_gaussian(360, 720)
-        C, H, B = 256, 512, 1
-        lat = S.SphericalField(g, torch.rand((B, C, 360, 720), device=dev) * 2 - 1)
-        cond = S.SphericalField(g, torch.empty((B, 0, 360, 720), device=dev))
-        sc = 1.0 / math.sqrt(C)
-
-        def wts(conv):
-            return S.BlockWeights(global_=conv.shape[2] != 9, conv=conv,
-                                  w1=(torch.rand((H, C), device=dev) * 2 - 1) * sc,
-                                  b1=torch.rand(H, device=dev) * 0.1,
-                                  w2=(torch.rand((C, H), device=dev) * 2 - 1) / math.sqrt(H),
-                                  b2=torch.rand(C, device=dev) * 0.1, scales=torch.full((C,), 0.1, device=dev))
-        bw_g = wts((torch.rand((C, C, 360), device=dev) * 2 - 1) * sc)
-        block_op = S.DiscoOperator(g, g, S.morlet_basis(3 * math.pi / 360))
-        bw_l = wts((torch.rand((C, C, block_op.n_basis), device=dev) * 2 - 1) * sc / 3)
-
-        def step():
-            S.block_apply(lat, cond, bw_g)
-            S.block_apply(lat, cond, bw_l, block_op)
-        units = B * C
-    elif args.workload == "decoder":
-        # decode_preclamp group (model.hpp:372-394): 360x720 Gaussian latent -> bilinear
-        # upsample to 721x1440 -> DISCO 721x1440 -> 721x1440, 64 -> 64 channels, batch 4
-        gl, go = S.build_gaussian(360, 720), S.build_equiangular(NLAT, NLON)
-        op = S.DiscoOperator(go, go, S.morlet_basis(3 * math.pi / 720))
-        dplan = S.DecoderPlan(op, gl)
-        B, cin, cout = 4, 64, 64
-        mix = (torch.rand((cout, cin, op.n_basis), device=dev) * 2 - 1) / math.sqrt(cin * 9)
-        lat = torch.rand((B, cin, 360, 720), device=dev) * 2 - 1
-        y = torch.empty((B, cout, NLAT, NLON), device=dev)
-        wsb = torch.empty(L.lib.sph_decoder_workspace_bytes(dplan.h, B, cin, cout), dtype=torch.uint8, device=dev)
-        # unfused two-stage path for comparison (reported as extra["unfused_ms"])
-        up = torch.empty((B, cin, NLAT, NLON), device=dev)
-        rplan = S.ResamplePlan(gl, go)
-        wsd = op.workspace(B, cin, cout)
-
-        def unfused():
-            rplan.apply(lat, out=up)
-            op.apply(up, mix, out=y, ws=wsd)
-        for _ in range(3):
-            unfused()
-        ue0, ue1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ue0.record()
-        for _ in range(args.steps):
-            unfused()
-        ue1.record()
-        torch.cuda.synchronize()
-        extra["unfused_ms"] = ue0.elapsed_time(ue1) / args.steps
-
-        def step():
-            dplan.apply(lat, mix, out=y, ws=wsb)
-        units = B * cout
-    else:
-        gi = S.build_equiangular(NLAT, NLON)
-        go = S.build_gaussian(360, 720)
-        op = S.DiscoOperator(gi, go, S.morlet_basis(3 * math.pi / 360))
-        B, cin, cout = 4, 64, 256
-        mix = (torch.rand((cout, cin, op.n_basis), device=dev) * 2 - 1) / math.sqrt(cin * 9)
-        if args.workload == "disco":
-            x = torch.rand((B, cin, NLAT, NLON), device=dev) * 2 - 1
-            y = torch.empty((B, cout, 360, 720), device=dev)
-            wsb = op.workspace(B, cin, cout)
-
-            def step():
-                op.apply(x, mix, out=y, ws=wsb)
-            units = B * cout
-        else:  # disco_transpose_apply: v on the 360x720 grid -> 721x1440 (64 channels)
-            v = torch.rand((B, cout, 360, 720), device=dev) * 2 - 1
-            y = torch.empty((B, cin, NLAT, NLON), device=dev)
-            from paper_2507_12144_b200 import _lib as LL
-            wsb = torch.empty(LL.lib.sph_disco_transpose_workspace_bytes(op.h, B, cin, cout),
-                              dtype=torch.uint8, device=dev)
-
-            def step():
-                op.transpose_apply(v, mix, out=y, ws=wsb)
-            units = B * cin
-
-    stream = torch.cuda.current_stream(dev)
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    L.profile_read()
-    L.profile_enable(True)
-    launches0 = L.launch_count()
-    barrier(ws)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    barrier(ws)
-    L.profile_enable(False)
-    launches = L.launch_count() - launches0
-    prof = L.profile_read()
-    ms = e0.elapsed_time(e1) / args.steps
-    ms = max_over_ranks(ms, ws)
-    value = ws * units / (ms / 1e3)
-
-    # dominant kernel roofline (live CUDA-event timing of every library launch)
-    top = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
-    roof = None
-    if top:
-        name, (cnt, tot_ms, work) = top
-        per_launch_s = tot_ms / cnt / 1e3
-        if name.startswith("gemm"):
-            # algorithmic 2MNK flops; ceiling for 3xTF32 = TF32 rate / 3 = (bf16 / 2) / 3
-            achieved = work / cnt / per_launch_s / 1e12
-            pk = bf16 / 2 / 3
-            roof = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": pk,
-                    "unit": "TFLOP/s", "frac": achieved / pk,
-                    "peak_note": f"{peak_src} bf16 {bf16} TF/s / 2 (TF32 rate) / 3 (3xTF32 passes)",
-                    "share_of_step": tot_ms / args.steps / ms}
-        else:
-            achieved = work / cnt / per_launch_s / 1e9
-            roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm,
-                    "unit": "GB/s", "frac": achieved / hbm, "peak_note": f"{peak_src} copy bandwidth",
-                    "share_of_step": tot_ms / args.steps / ms}
-        roof["traffic"] = None
-        try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic_sht.json")) as f:
-                tj = json.load(f)
-            tw = tj["dram_bytes_per_launch"] if args.workload == "sht" else \
-                tj.get("by_workload", {}).get(args.workload, {}).get("dram_bytes_per_launch", {})
-            if name in tw:
-                roof["traffic"] = tw[name]
-                roof["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write)"
-                roof["algorithmic_per_launch"] = work / cnt
-        except Exception:
-            pass
-        roof["per_kernel_ms"] = {k: v[1] / args.steps for k, v in sorted(prof.items())}
-
-    # end-to-end through the public C ABI with pinned host buffers
+    def step():
+        plan.forward(x, L.SPH_LAYOUT_INTERNAL, out=cint, ws=wsb)
+        plan.inverse(cint, F, L.SPH_LAYOUT_INTERNAL, out=y, ws=wsb)
+    ms, launches, prof, clk = timed(step, args.steps, args.warmup, ws, local, torch.cuda.current_stream(dev))
+    rec = {"value": ws * F / (ms / 1e3), "ms_per_step": ms, "gpu_launches": launches, "clocks": clk,
+           "roofline": roofline(prof, args.steps, ms, "sht")}
     e2e = None
-    if args.workload == "sht" and not args.no_e2e:
+    if not args.no_e2e:  # end to end through the public C ABI with pinned host buffers
         xh = torch.empty((F, NLAT, NLON), dtype=torch.float32, pin_memory=True)
         xh.copy_(x)
         yh = torch.empty_like(xh, pin_memory=True)
-        plan.roundtrip_host(xh, yh, chunk=args.chunk)  # warm-up (allocs, graphs of tables)
+        plan.roundtrip_host(xh, yh, chunk=args.chunk)  # warm-up (allocations, streams)
         barrier(ws)
         t0 = time.perf_counter()
         n_e2e = max(1, min(args.steps, 3))
         for _ in range(n_e2e):
             plan.roundtrip_host(xh, yh, chunk=args.chunk)
-        t = (time.perf_counter() - t0) / n_e2e
-        t = max_over_ranks(t, ws)
+        t = max_over_ranks((time.perf_counter() - t0) / n_e2e, ws)
         e2e = {"value": ws * F / t, "unit": UNIT, "h2d_bytes_per_step": F * NLAT * NLON * 4,
                "d2h_bytes_per_step": F * NLAT * NLON * 4, "ms_per_step": t * 1e3,
-               "api": "sph_sht_roundtrip_host (pinned host in/out; H2D, compute and D2H streams over 3 chunk buffers)", "chunk_fields": args.chunk}
+               "api": "sph_sht_roundtrip_host (pinned host in/out; H2D, compute and D2H streams over 3 chunk "
+                      "buffers)", "chunk_fields": args.chunk}
         del xh, yh
+    rec["e2e"] = e2e
+    del x, y, cint, wsb
+    return rec
 
-    if args.workload == "disco" and not args.no_e2e:
+
+def measure_disco(args, ws, rank, local):
+    import torch
+    import paper_2507_12144_b200 as S
+    dev = torch.device("cuda", local)
+    hbm = peaks()[0]
+    op = S.DiscoOperator(S.build_equiangular(NLAT, NLON), S.build_gaussian(360, 720),
+                         S.morlet_basis(3 * math.pi / 360), device=dev)
+    B, cin, cout = 4, 64, 256
+    mix = (torch.rand((cout, cin, op.n_basis), device=dev) * 2 - 1) / math.sqrt(cin * 9)
+    x = torch.rand((B, cin, NLAT, NLON), device=dev) * 2 - 1
+    y = torch.empty((B, cout, 360, 720), device=dev)
+    wsb = op.workspace(B, cin, cout)
+
+    def step():
+        op.apply(x, mix, out=y, ws=wsb)
+    ms, launches, prof, clk = timed(step, args.steps, args.warmup, ws, local, torch.cuda.current_stream(dev))
+    units = B * cout
+    # SURVEY §8(d) compulsory bytes per step: x + y + psi (fp32 value + 2 indices per entry
+    # and basis) + W
+    comp = 4 * B * cin * NLAT * NLON + 4 * B * cout * 360 * 720 + op.nnz_per_basis * op.n_basis * 12 \
+        + 4 * cout * cin * 9
+    rec = {"value": ws * units / (ms / 1e3), "unit": "output fields/s", "ms_per_step": ms, "gpu_launches": launches,
+           "clocks": clk, "config": dict(DISCO_CONFIG),
+           "roofline": roofline(prof, args.steps, ms, "disco"),
+           "step_hbm": {"compulsory_bytes": comp, "achieved_GBps": comp / (ms / 1e3) / 1e9, "peak": hbm,
+                        "frac": comp / (ms / 1e3) / 1e9 / hbm,
+                        "note": "SURVEY §8(d) compulsory bytes (x + y + psi + W) over the whole step time"}}
+    e2e = None
+    if not args.no_e2e:
         # per batch item: pinned host -> device (H2D stream), sph_disco_apply (compute
         # stream), device -> pinned host (D2H stream), 3 slots in flight
         xh = torch.empty((B, cin, NLAT, NLON), dtype=torch.float32, pin_memory=True)
@@ -578,27 +483,241 @@ def run_ours(args, ws, rank, local):
         e2e = {"value": ws * units / t, "unit": "output fields/s", "h2d_bytes_per_step": xh.numel() * 4,
                "d2h_bytes_per_step": yh.numel() * 4, "ms_per_step": t * 1e3,
                "api": "sph_disco_apply per batch item (pinned host in/out; H2D, compute and D2H streams, 3 slots)"}
-        del xh, yh
+        del xh, yh, xd, yd, ws1
+    rec["e2e"] = e2e
+    del x, y, wsb
+    return rec
 
-    cpu = None
+
+def measure_domain_decomposed(args, ws, rank, local, nh, nw, steps):
+    """configs[4] through the library's NCCL path: distributed SHT + inverse SHT round trip
+    and distributed DISCO (721x1440 -> 360x720 Gaussian), 512 channels, batch 1.  The same
+    problem on ONE GPU (rank 0 alone, the single-GPU plans) gives T1 for the strong-scaling
+    efficiency T1 / (N * T_N)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2507_12144_b200 as S
+    from paper_2507_12144_b200 import _lib as L
+    from paper_2507_12144_b200 import dist as D
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    if not dist.is_initialized():  # one rank: a 1-process group carries the NCCL id
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
+    C = 512
+    grid = S.build_equiangular(NLAT, NLON)
+    gout = S.build_gaussian(360, 720)
+    op = S.DiscoOperator(grid, gout, S.morlet_basis(3 * math.pi / 360), device=dev)
+    torch.manual_seed(99)
+    mix = ((torch.rand((C, C, op.n_basis)) * 2 - 1) / math.sqrt(C * 9)).to(dev)
+    out = {"decomposition": f"{nh}x{nw}", "channels": C, "batch": 1, "scaling": "strong",
+           "api": "sph_dist_sht_forward / sph_dist_sht_inverse / sph_dist_disco_apply (NCCL, libsphgpu.so)"}
+
+    def ev_time(step, n):
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    # T1: rank 0 alone, single-GPU plans on the whole problem
+    t1 = {}
+    if rank == 0:
+        p1 = S.get_sht_plan(grid, LMAX, MMAX, "3xtf32", allow_equiangular_forward=True, device=dev)
+        xg = torch.rand((C, NLAT, NLON), device=dev) * 2 - 1
+        cg = torch.empty((C, LMAX, MMAX, 2), device=dev)
+        yg = torch.empty_like(xg)
+        wsg = p1.workspace(C)
+
+        def rt1():
+            p1.forward(xg, L.SPH_LAYOUT_DENSE_LM, out=cg, ws=wsg)
+            p1.inverse(cg, C, L.SPH_LAYOUT_DENSE_LM, out=yg, ws=wsg)
+        t1["sht_roundtrip"] = ev_time(rt1, steps)
+        yd = torch.empty((1, C, 360, 720), device=dev)
+        wsd = op.workspace(1, C, C)
+        t1["disco"] = ev_time(lambda: op.apply(xg[None], mix, out=yd, ws=wsd), steps)
+        del xg, cg, yg, wsg, yd, wsd
+        torch.cuda.empty_cache()
+    dist.barrier()
+    comm = D.NcclComm(D.CommGrid((1, 1, nh, nw)), device=dev)
+    sp = D.DistShtPlan(comm, grid, LMAX, MMAX, C)
+    dp = D.DistDiscoPlan(comm, op, C, C)
+    x = torch.rand((C, sp.hn, sp.wn), device=dev) * 2 - 1
+    c = torch.empty((C, sp.ln, sp.mn, 2), device=dev)
+    y = torch.empty_like(x)
+    xd = torch.rand((C, dp.hn, dp.wn), device=dev) * 2 - 1
+    yd = torch.empty((C, dp.hon, dp.won), device=dev)
+
+    def rt():
+        sp.forward(x, out=c)
+        sp.inverse(c, out=y)
+    res = {}
+    for name, step in (("sht_roundtrip", rt), ("disco", lambda: dp.apply(xd, mix, out=yd))):
+        ms, launches, prof, clk = timed(step, steps, 3, ws, local, stream)
+        r = {"ms_per_step": ms, "value": C / (ms / 1e3), "unit": "fields/s" if name != "disco" else "output fields/s",
+             "gpu_launches": launches, "per_kernel_ms_rank0": {k: v[1] / steps for k, v in sorted(prof.items())}}
+        if rank == 0:
+            r["t1_ms"] = t1[name]
+            r["strong_scaling_eff"] = t1[name] / (ws * ms)
+        res[name] = r
+    comm.traffic_reset()
+    rt()
+    dp.apply(xd, mix, out=yd)
+    torch.cuda.synchronize()
+    out.update(res)
+    out["traffic_csv"] = comm.traffic_csv()
+    del sp, dp
+    comm.close()
+    return out
+
+
+def run_all(args, ws, rank, local):
+    """The default line: configs[1] SHT (value), configs[2] DISCO, configs[4] (N > 1)."""
+    sht = measure_sht(args, ws, rank, local)
+    disco = measure_disco(args, ws, rank, local)
+    dd = measure_domain_decomposed(args, ws, rank, local, ws, 1, max(5, args.steps // 2)) if ws > 1 else None
+    cpu = dcpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
-            if args.workload == "decoder":
-                raise RuntimeError("no CPU baseline for the decoder workload")
-            cpu = cpu_reference_sht(1) if args.workload == "sht" else cpu_reference_disco()
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: v for k, v in cpu_reference_sht(2).items() if k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(ex)}
-
+        try:
+            dcpu = {k: v for k, v in cpu_reference_disco().items()
+                    if k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # noqa: BLE001
+            dcpu = {"value": None, "unit": "output fields/s", "cores": 0, "kind": "unavailable", "sample": str(ex)}
     if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": UNIT if args.workload == "sht" else "output fields/s",
-               "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-               "data": "synthetic (uniform(-1,1) fields of the named shape)",
-               "config": workload_config(args), "roofline": roof, "cpu_baseline": cpu,
-               "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
+        disco["cpu_baseline"] = dcpu
+        out = {"metric": METRIC, "value": sht["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": sht["ms_per_step"], "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
+               "roofline": sht["roofline"], "cpu_baseline": cpu, "e2e": sht["e2e"],
+               "gpu_launches": sht["gpu_launches"], "clocks": sht["clocks"], "disco": disco}
+        if dd is not None:
+            out["domain_decomposed"] = dd
+        print(json.dumps(out), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    """Single-workload lines (development / profiling): sht, disco, disco_t, block, decoder."""
+    import torch
+    import paper_2507_12144_b200 as S
+    from paper_2507_12144_b200 import _lib as L
+    dev = torch.device("cuda", local)
+    torch.manual_seed(1234 + rank)
+    if args.workload in ("sht", "disco"):
+        rec = (measure_sht if args.workload == "sht" else measure_disco)(args, ws, rank, local)
+        cpu = None
+        if rank == 0 and ws == 1 and not args.no_cpu:
+            try:
+                cpu = cpu_reference_sht(2) if args.workload == "sht" else cpu_reference_disco()
+                cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as ex:  # noqa: BLE001
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(ex)}
+        if rank == 0:
+            out = {"metric": METRIC, "value": rec["value"], "unit": rec.get("unit", UNIT), "n_gpus": ws,
+                   "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"],
+                   "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                   "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
+                   "roofline": rec["roofline"], "cpu_baseline": cpu, "e2e": rec["e2e"],
+                   "gpu_launches": rec["gpu_launches"], "clocks": rec["clocks"]}
+            if "step_hbm" in rec:
+                out["step_hbm"] = rec["step_hbm"]
+            print(json.dumps(out), flush=True)
+        return
+    extra = {}
+    if args.workload == "block":
+        g = S.build_gaussian(360, 720)
+        C, H, B = 256, 512, 1
+        lat = S.SphericalField(g, torch.rand((B, C, 360, 720), device=dev) * 2 - 1)
+        cond = S.SphericalField(g, torch.empty((B, 0, 360, 720), device=dev))
+        sc = 1.0 / math.sqrt(C)
+
+        def wts(conv):
+            return S.BlockWeights(global_=conv.shape[2] != 9, conv=conv,
+                                  w1=(torch.rand((H, C), device=dev) * 2 - 1) * sc,
+                                  b1=torch.rand(H, device=dev) * 0.1,
+                                  w2=(torch.rand((C, H), device=dev) * 2 - 1) / math.sqrt(H),
+                                  b2=torch.rand(C, device=dev) * 0.1, scales=torch.full((C,), 0.1, device=dev))
+        bw_g = wts((torch.rand((C, C, 360), device=dev) * 2 - 1) * sc)
+        block_op = S.DiscoOperator(g, g, S.morlet_basis(3 * math.pi / 360), device=dev)
+        bw_l = wts((torch.rand((C, C, block_op.n_basis), device=dev) * 2 - 1) * sc / 3)
+
+        def step():
+            S.block_apply(lat, cond, bw_g)
+            S.block_apply(lat, cond, bw_l, block_op)
+        units = B * C
+    elif args.workload == "decoder":
+        gl, go = S.build_gaussian(360, 720), S.build_equiangular(NLAT, NLON)
+        op = S.DiscoOperator(go, go, S.morlet_basis(3 * math.pi / 720), device=dev)
+        dplan = S.DecoderPlan(op, gl)
+        B, cin, cout = 4, 64, 64
+        mix = (torch.rand((cout, cin, op.n_basis), device=dev) * 2 - 1) / math.sqrt(cin * 9)
+        lat = torch.rand((B, cin, 360, 720), device=dev) * 2 - 1
+        y = torch.empty((B, cout, NLAT, NLON), device=dev)
+        wsb = torch.empty(L.lib.sph_decoder_workspace_bytes(dplan.h, B, cin, cout), dtype=torch.uint8, device=dev)
+
+        def step():
+            dplan.apply(lat, mix, out=y, ws=wsb)
+        units = B * cout
+    else:  # disco_t: disco_transpose_apply, v on the 360x720 grid -> 721x1440 (64 channels)
+        op = S.DiscoOperator(S.build_equiangular(NLAT, NLON), S.build_gaussian(360, 720),
+                             S.morlet_basis(3 * math.pi / 360), device=dev)
+        B, cin, cout = 4, 64, 256
+        mix = (torch.rand((cout, cin, op.n_basis), device=dev) * 2 - 1) / math.sqrt(cin * 9)
+        v = torch.rand((B, cout, 360, 720), device=dev) * 2 - 1
+        y = torch.empty((B, cin, NLAT, NLON), device=dev)
+        wsb = torch.empty(L.lib.sph_disco_transpose_workspace_bytes(op.h, B, cin, cout), dtype=torch.uint8,
+                          device=dev)
+
+        def step():
+            op.transpose_apply(v, mix, out=y, ws=wsb)
+        units = B * cin
+    ms, launches, prof, clk = timed(step, args.steps, args.warmup, ws, local, torch.cuda.current_stream(dev))
+    if rank == 0:
+        out = {"metric": METRIC, "value": ws * units / (ms / 1e3), "unit": "output fields/s", "n_gpus": ws,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
+               "roofline": roofline(prof, args.steps, ms, args.workload), "cpu_baseline": None, "e2e": None,
+               "gpu_launches": launches, "clocks": clk}
         out.update(extra)
         print(json.dumps(out), flush=True)
+
+
+def run_dist(args, ws, rank, local):
+    """configs[4] alone at an explicit decomposition (--decomp NHxNW)."""
+    nh, nw = decomp(args)
+    dd = measure_domain_decomposed(args, ws, rank, local, nh, nw, args.steps)
+    if rank == 0:
+        r = dd["sht_roundtrip" if args.workload == "dist_sht" else "disco"]
+        out = {"metric": METRIC, "value": r["value"], "unit": r["unit"], "n_gpus": ws, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
+               "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": r["gpu_launches"],
+               "domain_decomposed": dd}
+        print(json.dumps(out), flush=True)
+
+
+def self_launch(args):
+    """``python bench.py --gpus N`` outside torchrun: start the N ranks ourselves."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -607,20 +726,27 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sht", choices=["sht", "disco", "disco_t", "block", "decoder", "dist_sht", "dist_disco"])
+    ap.add_argument("--workload", default="all",
+                    choices=["all", "sht", "disco", "disco_t", "block", "decoder", "dist_sht", "dist_disco"])
     ap.add_argument("--decomp", default="", help="dist_*: NHxNW polar x azimuth ranks (default WORLD_SIZE x 1)")
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    env_ws = os.environ.get("WORLD_SIZE")
+    if env_ws is None and args.gpus > 1:
+        sys.exit(self_launch(args))
+    if env_ws is not None and int(env_ws) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_ws}")
     if args.impl == "reference":
-        rank = int(os.environ.get("RANK", "0"))
-        run_reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), rank)
+        run_reference_arm(args, int(env_ws or "1"), int(os.environ.get("RANK", "0")))
         return
     ws, rank, local = dist_setup()
     if args.workload.startswith("dist_"):
         run_dist(args, ws, rank, local)
+    elif args.workload == "all":
+        run_all(args, ws, rank, local)
     else:
         run_ours(args, ws, rank, local)
     import torch.distributed as dist

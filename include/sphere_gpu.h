@@ -221,6 +221,61 @@ int sph_block_epilogue(const float* conv, const float* x, const float* w1, const
                        const float* w2, const float* b2, const float* scales, int64_t B,
                        int64_t C, int64_t H, int64_t npts, float* y, void* stream);
 
+/* ---- domain-decomposed SHT and DISCO over NCCL (distsim.hpp:45-547) --------------- */
+/* The rank cube of the reference's CommGrid (distsim.hpp:45-98): sizes = (batch, ensemble,
+ * polar, azimuth), azimuth fastest.  One process per GPU; rank 0 makes the NCCL unique id
+ * (sph_comm_unique_id, sph_comm_id_bytes() bytes) and the caller broadcasts it.  The
+ * communicator owns the NCCL world and its (polar x azimuth) plane / azimuth groups
+ * (ncclCommSplit), and the TrafficLog (distsim.hpp:120-150 schema, world-summed bytes).
+ * Create on the device the plans live on (the current device). */
+typedef struct sph_comm_s* sph_comm;
+int64_t sph_comm_id_bytes(void);
+int sph_comm_unique_id(void* id);
+int sph_comm_create(const void* id, int64_t world, int64_t rank, const int64_t* sizes, sph_comm* comm);
+int sph_comm_destroy(sph_comm comm);
+int sph_comm_coords(sph_comm comm, int64_t* coords);
+int sph_comm_traffic_csv(sph_comm comm, char* csv, size_t cap);
+int sph_comm_traffic_reset(sph_comm comm);
+
+/* dist_sht_forward (distsim.hpp:404-463, Alg. 1; no grid-kind check, like the reference)
+ * and its mirror, the distributed sht_inverse (harmonics.hpp:173-205; the reference has no
+ * distributed inverse).  Per (batch, ensemble) plane of nh x nw ranks, rank (i, j) holds
+ *   fields  x [C][H_i][W_j]               H_i / W_j canonical splits of nlat / nlon
+ *   coeffs    [C][L_i][M_j] complex64     L_i / M_j canonical splits of lmax / mmax,
+ *                                          zeros above the diagonal (the unshard layout)
+ * sph_dist_sht_local: {h0, hn, w0, wn, l0, ln, m0, mn, c0, cn} of this rank (c0/cn: the
+ * channel slice whose transforms it computes).  `sht` is a plan of the full grid (create it
+ * with SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD for equiangular grids) on the comm's device; it
+ * must outlive the distributed plan. */
+typedef struct sph_dist_sht_plan_s* sph_dist_sht_plan;
+int sph_dist_sht_plan_create(sph_comm comm, sph_sht_plan sht, int64_t C, sph_dist_sht_plan* plan);
+int sph_dist_sht_plan_destroy(sph_dist_sht_plan plan);
+int sph_dist_sht_local(sph_dist_sht_plan plan, int64_t* info);
+int64_t sph_dist_sht_workspace_bytes(sph_dist_sht_plan plan);
+int sph_dist_sht_forward(sph_dist_sht_plan plan, const float* x, float* coeffs, void* workspace, void* stream);
+int sph_dist_sht_inverse(sph_dist_sht_plan plan, const float* coeffs, float* y, void* workspace, void* stream);
+
+/* dist_disco_apply (distsim.hpp:468-547, Alg. 2 with a latitude halo instead of the
+ * reduce-scatter of K-expanded partial sums): x [C_in][H_i][W_j] (input grid), mix
+ * [C_out][C_in][K] replicated -> y [C_out][Ho_i][Wo_j] (output grid).  sph_dist_disco_local:
+ * {h0, hn, w0, wn, ho0, hon, wo0, won, cz0, czn, need0, needn}. */
+typedef struct sph_dist_disco_plan_s* sph_dist_disco_plan;
+int sph_dist_disco_plan_create(sph_comm comm, sph_disco_plan op, int64_t c_in, int64_t c_out,
+                               sph_dist_disco_plan* plan);
+int sph_dist_disco_plan_destroy(sph_dist_disco_plan plan);
+int sph_dist_disco_local(sph_dist_disco_plan plan, int64_t* info);
+int64_t sph_dist_disco_workspace_bytes(sph_dist_disco_plan plan);
+int sph_dist_disco_apply(sph_dist_disco_plan plan, const float* x, const float* mix, float* y, void* workspace,
+                         void* stream);
+
+/* Host-only descriptions of the exchange schedules and pack/unpack boxes (no GPU or NCCL
+ * needed; the CPU tests execute them over gloo).  See csrc/dist.cu for the item codes. */
+int sph_dist_sht_describe(int64_t nh, int64_t nw, int64_t q, int64_t nlat, int64_t nlon, int64_t lmax,
+                          int64_t mmax, int64_t C, int what, int64_t* out, int64_t cap, int64_t* n);
+int sph_dist_disco_describe(int64_t nh, int64_t nw, int64_t q, int64_t hin, int64_t win, int64_t hout, int64_t wout,
+                            int64_t cin, int64_t cout, const int64_t* band_lo, const int64_t* band_n, int what,
+                            int64_t* out, int64_t cap, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

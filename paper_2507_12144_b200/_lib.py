@@ -46,6 +46,11 @@ EXPORTS = [
     "sph_decoder_plan_destroy", "sph_decoder_workspace_bytes", "sph_decoder_apply", "sph_psd_from_coeffs",
     "sph_spectral_crps_from_coeffs", "sph_weighted_crps",
     "sph_spectral_conv", "sph_spectral_conv_workspace_bytes", "sph_block_epilogue",
+    "sph_comm_id_bytes", "sph_comm_unique_id", "sph_comm_create", "sph_comm_destroy", "sph_comm_coords",
+    "sph_comm_traffic_csv", "sph_comm_traffic_reset", "sph_dist_sht_plan_create", "sph_dist_sht_plan_destroy",
+    "sph_dist_sht_local", "sph_dist_sht_workspace_bytes", "sph_dist_sht_forward", "sph_dist_sht_inverse",
+    "sph_dist_disco_plan_create", "sph_dist_disco_plan_destroy", "sph_dist_disco_local",
+    "sph_dist_disco_workspace_bytes", "sph_dist_disco_apply", "sph_dist_sht_describe", "sph_dist_disco_describe",
 ]
 
 
@@ -116,6 +121,29 @@ def _load():
     L.sph_spectral_conv_workspace_bytes.argtypes = [vp, i64, i64, i64]
     L.sph_spectral_conv_workspace_bytes.restype = i64
     L.sph_block_epilogue.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp]
+    ip = C.POINTER(i64)
+    L.sph_comm_id_bytes.restype = i64
+    L.sph_comm_unique_id.argtypes = [vp]
+    L.sph_comm_create.argtypes = [vp, i64, i64, ip, C.POINTER(vp)]
+    L.sph_comm_destroy.argtypes = [vp]
+    L.sph_comm_coords.argtypes = [vp, ip]
+    L.sph_comm_traffic_csv.argtypes = [vp, C.c_char_p, C.c_size_t]
+    L.sph_comm_traffic_reset.argtypes = [vp]
+    L.sph_dist_sht_plan_create.argtypes = [vp, vp, i64, C.POINTER(vp)]
+    L.sph_dist_sht_plan_destroy.argtypes = [vp]
+    L.sph_dist_sht_local.argtypes = [vp, ip]
+    L.sph_dist_sht_workspace_bytes.argtypes = [vp]
+    L.sph_dist_sht_workspace_bytes.restype = i64
+    L.sph_dist_sht_forward.argtypes = [vp, vp, vp, vp, vp]
+    L.sph_dist_sht_inverse.argtypes = [vp, vp, vp, vp, vp]
+    L.sph_dist_disco_plan_create.argtypes = [vp, vp, i64, i64, C.POINTER(vp)]
+    L.sph_dist_disco_plan_destroy.argtypes = [vp]
+    L.sph_dist_disco_local.argtypes = [vp, ip]
+    L.sph_dist_disco_workspace_bytes.argtypes = [vp]
+    L.sph_dist_disco_workspace_bytes.restype = i64
+    L.sph_dist_disco_apply.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.sph_dist_sht_describe.argtypes = [i64] * 8 + [C.c_int, ip, i64, ip]
+    L.sph_dist_disco_describe.argtypes = [i64] * 9 + [ip, ip, C.c_int, ip, i64, ip]
     for name in EXPORTS:
         getattr(L, name)  # AttributeError if a declared symbol is not exported
     return L

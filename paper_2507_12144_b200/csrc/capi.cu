@@ -13,15 +13,13 @@
 #include "resample.cuh"
 #include "disco.cuh"
 #include "sht.cuh"
-
-struct sph_sht_plan_s {
-    sph::ShtPlan p;
-};
-struct sph_disco_plan_s {
-    sph::DiscoPlan p;
-};
+#include "capi_util.cuh"
 
 namespace sph {
+std::string& last_error() {
+    static thread_local std::string msg;
+    return msg;
+}
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
 
@@ -73,31 +71,9 @@ cudaMemPool_t lib_pool() {
 }
 }  // namespace sph
 
-namespace {
-thread_local std::string g_err;
-
-template <class Fn>
-int guarded(Fn&& fn) {
-    try {
-        fn();
-        return SPH_OK;
-    } catch (const sph::Error& e) {
-        g_err = e.what();
-        return e.code;
-    } catch (const std::bad_alloc& e) {
-        g_err = std::string("host allocation failed: ") + e.what();
-        return SPH_ERR_OOM;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return SPH_ERR_RUNTIME;
-    }
-}
-inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
-}  // namespace
-
 extern "C" {
 
-const char* sph_last_error(void) { return g_err.c_str(); }
+const char* sph_last_error(void) { return sph::last_error().c_str(); }
 const char* sph_version(void) { return "sphgpu 0.1 sm_100a"; }
 uint64_t sph_launch_count(void) { return sph::g_launches.load(); }
 

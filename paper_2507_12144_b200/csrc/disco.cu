@@ -843,49 +843,94 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
     split_rows(mix, cout, cin * K, w.ldS, whi, wlo, st);
     const bool direct = prec == SPH_PREC_FP32_SIMT;
     const int64_t rows_per_b = direct ? nout * wout : nout * nbo * 2;
-    const GroupedGemm* gp;
+    // The tensor core's fp32 accumulation loses precision linearly in the number of k-steps
+    // chained into one accumulator (measured at 360x720, 256 -> 256, random weights:
+    // relative error 1.6e-5 at c_in*K = 2304, 8.0e-6 at 1152, 4.0e-6 at 576, 2.1e-6 at 288).
+    // Reductions longer than kchunk therefore run as chunk GEMMs whose partial sums are
+    // added in fp32 (round to nearest) by the accumulate epilogue, D = D + acc.
+    static const int64_t kchunk = [] {
+        const char* e = std::getenv("SPH_DISCO_KCHUNK");
+        return e ? std::max<int64_t>(32, std::atoll(e) / 32 * 32) : int64_t{576};
+    }();
+    const int64_t Ktot = cin * K;
+    const int64_t nchunks = (prec == SPH_PREC_FP32_SIMT) ? 1 : (Ktot + kchunk - 1) / kchunk;
+    auto make_gemm = [&](int64_t kc, bool chained) {
+        auto g = std::make_unique<GroupedGemm>();
+        g->A = {nullptr, B * rows_per_b, kc, w.ldS};
+        g->Bhi = {nullptr, cout, kc, w.ldS};
+        g->Blo = {nullptr, cout, kc, w.ldS};
+        g->store = STORE_TRANS;
+        g->bn = cout >= 256 ? 256 : 128;
+        static const int alo_mode = [] {
+            const char* e = std::getenv("SPH_DISCO_ALO");
+            return e ? std::atoi(e) : 1;
+        }();
+        if (alo_mode == 1 && prec != SPH_PREC_FP32_SIMT && cout <= 128 && !chained) {
+            // BK = 32 kernel: half the k-block rounds of the BK = 16 one at K = cin * 9
+            // (decoder 64 -> 64: 4.26 -> 3.23 ms); with two N tiles (cout 256) the
+            // BN = 256 BK = 16 kernel stays faster (1.42 vs 1.63 ms at cfg3).  The chained
+            // accumulate epilogue exists only in the BK = 16 kernel.
+            g->alo = true;
+            g->bn = cout <= 64 ? 64 : 128;
+        }
+        g->name = "gemm_disco_mix";
+        // table multicast over 2 CTAs (cfg3: 1.386 ms vs 1.445 ms at the default 4)
+        g->cluster = 2;
+        require(B * rows_per_b < (1LL << 31), "disco: batch too large for one call");
+        for (int64_t b = 0; b < B; ++b) {
+            GemmGroup gr;
+            gr.a_row0 = static_cast<int32_t>(b * rows_per_b);
+            gr.b_row0 = 0;
+            gr.M = static_cast<int32_t>(rows_per_b);
+            gr.N = static_cast<int32_t>(cout);
+            gr.K = static_cast<int32_t>(kc);
+            gr.ldd = static_cast<int32_t>(rows_per_b);
+            gr.zero_to = 0;
+            gr.d_off = b * cout * rows_per_b;
+            g->groups.push_back(gr);
+        }
+        g->finalize();
+        return g;
+    };
+    const GroupedGemm* gp = nullptr;
+    std::vector<std::pair<int64_t, const GroupedGemm*>> chunks;  // (k0, gemm)
     {
         std::lock_guard<std::mutex> lk(mu);
-        auto& slot = gemm_cache[std::make_tuple(B, cin, cout, nout)];
-        if (!slot) {
-            auto g = std::make_unique<GroupedGemm>();
-            g->A = {nullptr, B * rows_per_b, cin * K, w.ldS};
-            g->Bhi = {nullptr, cout, cin * K, w.ldS};
-            g->Blo = {nullptr, cout, cin * K, w.ldS};
-            g->store = STORE_TRANS;
-            g->bn = cout >= 256 ? 256 : 128;
-            static const int alo_mode = [] {
-                const char* e = std::getenv("SPH_DISCO_ALO");
-                return e ? std::atoi(e) : 1;
-            }();
-            if (alo_mode == 1 && prec != SPH_PREC_FP32_SIMT && cout <= 128) {
-                // BK = 32 kernel: half the k-block rounds of the BK = 16 one at K = cin * 9
-                // (decoder 64 -> 64: 4.26 -> 3.23 ms); with two N tiles (cout 256) the
-                // BN = 256 BK = 16 kernel stays faster (1.42 vs 1.63 ms at cfg3)
-                g->alo = true;
-                g->bn = cout <= 64 ? 64 : 128;
+        if (nchunks <= 1) {
+            auto& slot = gemm_cache[std::make_tuple(B, cin, cout, nout)];
+            if (!slot) slot = make_gemm(Ktot, false);
+            gp = slot.get();
+        } else {
+            for (int64_t k0 = 0; k0 < Ktot; k0 += kchunk) {
+                const int64_t kc = std::min(kchunk, Ktot - k0);
+                auto& slot = gemm_chunk_cache[std::make_tuple(B, cin, cout, nout, k0, kc)];
+                if (!slot) slot = make_gemm(kc, true);
+                chunks.emplace_back(k0, slot.get());
             }
-            g->name = "gemm_disco_mix";
-            // table multicast over 2 CTAs (cfg3: 1.386 ms vs 1.445 ms at the default 4)
-            g->cluster = 2;
-            require(B * rows_per_b < (1LL << 31), "disco: batch too large for one call");
-            for (int64_t b = 0; b < B; ++b) {
-                GemmGroup gr;
-                gr.a_row0 = static_cast<int32_t>(b * rows_per_b);
-                gr.b_row0 = 0;
-                gr.M = static_cast<int32_t>(rows_per_b);
-                gr.N = static_cast<int32_t>(cout);
-                gr.K = static_cast<int32_t>(cin * K);
-                gr.ldd = static_cast<int32_t>(rows_per_b);
-                gr.zero_to = 0;
-                gr.d_off = b * cout * rows_per_b;
-                g->groups.push_back(gr);
+            if (ones.n < static_cast<size_t>(cout)) {
+                std::vector<float> h1(cout, 1.f);
+                ones.alloc(cout, false);
+                SPH_CUDA(cudaMemcpy(ones.p, h1.data(), 4 * cout, cudaMemcpyHostToDevice));
+                zeros.alloc(cout, true);
             }
-            g->finalize();
-            slot = std::move(g);
         }
-        gp = slot.get();
     }
+    // D = A * mix^T over the whole reduction, chained over the k chunks when split
+    auto run_mix = [&](const float* A, float* D) {
+        if (chunks.empty()) {
+            gemm_run(*gp, A, D, prec, st, whi, wlo);
+            return;
+        }
+        GemmEpi acc;
+        acc.mode = 2;
+        acc.scale = ones.p;
+        acc.bias = zeros.p;
+        acc.res = D;
+        for (size_t c = 0; c < chunks.size(); ++c) {
+            const int64_t k0 = chunks[c].first;
+            gemm_run(*chunks[c].second, A + k0, D, prec, st, whi + k0, wlo + k0, c ? &acc : nullptr);
+        }
+    };
     float* S = reinterpret_cast<float*>(base + w.s_off);
     if (direct) {
         dim3 grid(static_cast<unsigned>(nout), static_cast<unsigned>(cin), static_cast<unsigned>(B));
@@ -898,7 +943,7 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
             SPH_LAUNCH_CHECK();
         }
         count_launch();
-        gemm_run(*gp, S, y, prec, st, whi, wlo);
+        run_mix(S, y);
         return;
     }
     float2* U = reinterpret_cast<float2*>(base + w.u_off);
@@ -924,7 +969,7 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
         SPH_LAUNCH_CHECK();
     }
     count_launch();
-    gemm_run(*gp, S, Yh, prec, st, whi, wlo);
+    run_mix(S, Yh);
     fft_inverse_plain(fft_out, reinterpret_cast<const float2*>(Yh), B * cout * nout,
                       static_cast<int>(nbo), static_cast<float>(1.0 / static_cast<double>(win)), y,
                       st);

@@ -1,0 +1,874 @@
+// Domain-decomposed SHT (forward + inverse) and DISCO over NCCL: the paper's Algorithms
+// 1-2 (distsim.hpp:404-547) on real GPUs, one process per GPU.  The host layout logic
+// (who owns what, who sends what) is dist_layout.hpp; this file owns the communicators,
+// the pack / unpack kernels and the stage order.  Every collective is a grouped
+// ncclSend/ncclRecv all-to-all (canonical uneven splits) or ncclReduceScatter on the
+// caller's stream, so a call is stream-ordered like every other library call.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "capi_util.cuh"
+#include "dist_layout.hpp"
+
+namespace sph {
+
+// NCCL is bound at run time, on the first communicator: the copy already in the process
+// (e.g. the one PyTorch links) when there is one, else libnccl.so.2 from the loader path
+// (SPH_NCCL_LIB overrides).  libsphgpu.so itself has no NCCL dependency, so loading it
+// never pins an NCCL version that a later import would conflict with.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        const char* env = std::getenv("SPH_NCCL_LIB");
+        void* h = env ? dlopen(env, RTLD_NOW | RTLD_GLOBAL) : dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h && !env) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = std::string("cannot load NCCL: ") + dlerror();
+            return;
+        }
+        auto sym = [&](auto& fn, const char* name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+            if (!fn && err.empty()) err = std::string("NCCL symbol missing: ") + name;
+        };
+        sym(api.GetUniqueId, "ncclGetUniqueId");
+        sym(api.CommInitRank, "ncclCommInitRank");
+        sym(api.CommSplit, "ncclCommSplit");
+        sym(api.CommDestroy, "ncclCommDestroy");
+        sym(api.GroupStart, "ncclGroupStart");
+        sym(api.GroupEnd, "ncclGroupEnd");
+        sym(api.Send, "ncclSend");
+        sym(api.Recv, "ncclRecv");
+        sym(api.ReduceScatter, "ncclReduceScatter");
+        sym(api.GetErrorString, "ncclGetErrorString");
+    });
+    if (!err.empty()) fail(SPH_ERR_NCCL, err);
+    return api;
+}
+
+inline void nccl_check(ncclResult_t r, const char* what, const char* file, int line) {
+    if (r != ncclSuccess)
+        fail(SPH_ERR_NCCL, std::string(what) + ": " + nccl().GetErrorString(r) + " (" + file + ":" +
+                               std::to_string(line) + ")");
+}
+#define SPH_NCCL(x) ::sph::nccl_check((x), #x, __FILE__, __LINE__)
+
+// TrafficLog of the reference (distsim.hpp:120-150): bytes are summed over all ranks
+// (every rank knows every rank's payload sizes from the layout, so no communication).
+struct Traffic {
+    struct Rec {
+        std::string op, axis, coll;
+        int64_t bytes = 0, calls = 0;
+    };
+    std::vector<Rec> recs;
+    void record(const std::string& op, const std::string& axis, const std::string& coll, int64_t bytes) {
+        for (auto& r : recs)
+            if (r.op == op && r.axis == axis && r.coll == coll) {
+                r.bytes += bytes;
+                r.calls += 1;
+                return;
+            }
+        recs.push_back({op, axis, coll, bytes, 1});
+    }
+    std::string csv() const {
+        std::string out = "operation,axis,collective,bytes,calls\n";
+        for (const auto& r : recs)
+            out += r.op + "," + r.axis + "," + r.coll + "," + std::to_string(r.bytes) + "," + std::to_string(r.calls) + "\n";
+        return out;
+    }
+};
+
+}  // namespace sph
+
+// The rank's communicator hierarchy (distsim.hpp:45-98, 160-163): the world, the
+// (polar x azimuth) plane of its (batch, ensemble) coordinate, and its azimuth group,
+// all split from the world communicator with ncclCommSplit.
+struct sph_comm_s {
+    int device = 0;
+    sph::CommGridSpec grid;
+    int64_t rank = 0;
+    std::array<int64_t, 4> coords{};
+    int64_t plane_rank = 0, plane_size = 1;
+    ncclComm_t world = nullptr, plane = nullptr, az = nullptr;
+    std::mutex mu;
+    sph::Traffic log;
+    ~sph_comm_s() {
+        for (ncclComm_t c : {az, plane, world})
+            if (c) sph::nccl().CommDestroy(c);
+    }
+};
+
+namespace sph {
+namespace {
+
+// ------------------------------------------------------------------------- kernels
+struct DBox {
+    int64_t src_off, dst_off, n0, n1, n2, s0, s1, d0, d1, row0;
+    int32_t vec4, pad;
+};
+
+// One warp per row (n2 contiguous floats) of the flattened box list; float4 when every
+// offset, stride and width of the box is a multiple of 4.
+__global__ void __launch_bounds__(256) box_copy_kernel(const DBox* __restrict__ bx, int nbox, int64_t rows,
+                                                       const float* __restrict__ src, float* __restrict__ dst) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    int b = 0;
+    while (b + 1 < nbox && bx[b + 1].row0 <= r) ++b;
+    const DBox& B = bx[b];
+    const int64_t rr = r - B.row0, a = rr / B.n1, c = rr - a * B.n1;
+    const float* s = src + B.src_off + a * B.s0 + c * B.s1;
+    float* d = dst + B.dst_off + a * B.d0 + c * B.d1;
+    const int lane = threadIdx.x & 31;
+    if (B.vec4) {
+        const float4* s4 = reinterpret_cast<const float4*>(s);
+        float4* d4 = reinterpret_cast<float4*>(d);
+        for (int64_t k = lane; k < B.n2 / 4; k += 32) d4[k] = __ldg(s4 + k);
+    } else {
+        for (int64_t k = lane; k < B.n2; k += 32) d[k] = __ldg(s + k);
+    }
+}
+
+// Coefficient payload index (complex units) of (field f, degree l, order m), m <= l:
+//   off[p] + f * tri[p] + rowoff[robase[p] + l - l0(i)] + m - m0(j),  p = i * nw + j
+// with (i, l - l0) = lmap[l], (j, m - m0) = mmap[m]  (dist_layout.hpp, ShtLayout).
+// rowbase(f, l, j) is everything but the order term, so a tile stages it once per
+// (degree, order block) in shared memory and the per-element index is one add.
+struct PayloadMap {
+    const int2* lmap;
+    const int2* mmap;
+    const int64_t* off;
+    const int64_t* tri;
+    const int64_t* rowoff;
+    const int64_t* robase;
+    int nw;
+    __device__ __forceinline__ int64_t rowbase(int64_t f, int l, int j, int m0j) const {
+        const int2 li = lmap[l];
+        const int p = li.x * nw + j;
+        return off[p] + f * tri[p] + rowoff[robase[p] + li.y] - m0j;
+    }
+};
+constexpr int kMaxNw = 16;  // azimuth ranks a staged tile supports (>= every B200 box)
+
+// stage base[ll][j] = rowbase(f, lt + ll, j) for the tile's degrees and the order blocks
+// j its 32 orders touch (jlo .. jlo + nj - 1)
+__device__ __forceinline__ void stage_rowbase(int64_t* base, const PayloadMap& pm, int64_t f, int lt, int nl,
+                                              int lmax, int mt, int mmax, int& jlo, int& nj) {
+    const int mlast = min(mt + 31, mmax - 1);
+    jlo = pm.mmap[mt].x;
+    nj = pm.mmap[mlast].x - jlo + 1;
+    for (int e = threadIdx.x; e < nl * nj; e += blockDim.x) {
+        const int ll = e / nj, jj = e - ll * nj;
+        const int l = lt + ll, j = jlo + jj;
+        if (l < lmax) {
+            // m0(j): the first order of block j is mt - mmap[mt].y + (sum of earlier blocks);
+            // recover it from the first order of the tile that falls in block j
+            int m = max(mt, 0);
+            while (m < mlast && pm.mmap[m].x < j) ++m;
+            base[ll * kMaxNw + jj] = pm.rowbase(f, l, j, m - pm.mmap[m].y);
+        }
+    }
+}
+
+// forward B pack: the local SHT's C_int [(m*2+p)][2F][Lp] (l = m + p + 2 lp) -> triangular
+// payloads of every destination block.  Tiled transpose as cint_to_dense (sht.cu): cint
+// read in lp runs, payload written in m runs.
+template <int LT>
+__global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict__ cint, int64_t F, int lmax, int mmax,
+                                                        int Lp, PayloadMap pm, float2* __restrict__ payload) {
+    __shared__ float2 tile[LT][33];
+    __shared__ int64_t base[LT * kMaxNw];
+    const int mt = blockIdx.x * 32, lt = blockIdx.y * LT;
+    if (mt > lt + LT - 1) return;  // tile entirely above the diagonal (m > l)
+    const int64_t f = blockIdx.z;
+    int jlo, nj;
+    stage_rowbase(base, pm, f, lt, LT, lmax, mt, mmax, jlo, nj);
+    constexpr int NLP = LT / 2 + 1;
+    for (int e = threadIdx.x; e < 32 * 2 * 2 * NLP; e += blockDim.x) {
+        const int lpl = e % NLP, r = e / NLP;
+        const int ri = r & 1, p = (r >> 1) & 1, mlt = r >> 2;
+        const int m = mt + mlt;
+        if (m >= mmax) continue;
+        const int d = lt - m - p;
+        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lpl;
+        const int l = m + p + 2 * lp;
+        if (lp >= Lp || l >= lmax || l >= lt + LT) continue;
+        const int64_t row = (static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri;
+        reinterpret_cast<float*>(&tile[l - lt][mlt])[ri] = cint[row * Lp + lp];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < LT * 32; e += blockDim.x) {
+        const int ll = e >> 5, mlt = e & 31;
+        const int l = lt + ll, m = mt + mlt;
+        if (l < lmax && m < mmax && m <= l)
+            payload[base[ll * kMaxNw + pm.mmap[m].x - jlo] + m] = tile[ll][mlt];
+    }
+}
+
+// inverse A^-1 unpack: triangular payloads of every source block -> C_int of the local
+// fields (zeros beyond lmax inside the padded lp range), as dense_to_cint (sht.cu).
+__global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restrict__ payload, int64_t F, int lmax,
+                                                          int mmax, int Lp, PayloadMap pm, float* __restrict__ cint) {
+    __shared__ float2 tile[96][33];
+    __shared__ int64_t base[96 * kMaxNw];
+    const int mt = blockIdx.x * 32, lpt = blockIdx.y * 32;
+    const int64_t f = blockIdx.z;
+    const int lbase = mt + 2 * lpt;
+    int jlo, nj;
+    stage_rowbase(base, pm, f, lbase, 96, lmax, mt, mmax, jlo, nj);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 96 * 32; e += blockDim.x) {
+        const int ll = e >> 5, mlt = e & 31;
+        const int l = lbase + ll, m = mt + mlt;
+        tile[ll][mlt] = (l < lmax && m < mmax && m <= l) ? payload[base[ll * kMaxNw + pm.mmap[m].x - jlo] + m]
+                                                          : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 2 * 2 * 32; e += blockDim.x) {
+        const int lpl = e & 31, r = e >> 5;
+        const int ri = r & 1, p = (r >> 1) & 1, mlt = r >> 2;
+        const int m = mt + mlt, lp = lpt + lpl;
+        if (m >= mmax || lp >= Lp) continue;
+        const int l = m + p + 2 * lp;
+        const float v = l < lmax ? reinterpret_cast<const float*>(&tile[mlt + p + 2 * lpl][mlt])[ri] : 0.f;
+        cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp] = v;
+    }
+}
+
+// forward B unpack / inverse A^-1 pack: the rank's own dense block [C][ln][mn] complex
+// (reference unshard layout, zeros above the diagonal) <-> [C][tri] channel-major payload.
+// One CTA per (channel, degree) row; the row's payload run starts at c*tri + rowoff[k].
+template <bool TO_BLOCK>
+__global__ void __launch_bounds__(256) block_tri_kernel(float2* __restrict__ block, float2* __restrict__ payload,
+                                                        int ln, int mn, int l0, int m0,
+                                                        const int64_t* __restrict__ rowoff, int64_t tri) {
+    const int k = blockIdx.x;
+    const int64_t c = blockIdx.y;
+    const int nvalid = min(mn, max(0, l0 + k + 1 - m0));  // orders m0 .. l0+k of this row
+    float2* brow = block + (c * ln + k) * mn;
+    float2* prow = payload + c * tri + rowoff[k];
+    for (int jm = threadIdx.x; jm < mn; jm += blockDim.x) {
+        if (TO_BLOCK) brow[jm] = jm < nvalid ? prow[jm] : make_float2(0.f, 0.f);
+        else if (jm < nvalid) prow[jm] = brow[jm];
+    }
+}
+
+// ---------------------------------------------------------------- host helpers
+struct BoxList {
+    DevBuf<DBox> d;
+    int n = 0;
+    int64_t rows = 0, floats = 0;
+    void set(const std::vector<Box>& bs) {
+        std::vector<DBox> h;
+        rows = floats = 0;
+        for (const Box& b : bs) {
+            if (b.n0 * b.n1 * b.n2 == 0) continue;
+            DBox x{b.src_off, b.dst_off, b.n0, b.n1, b.n2, b.s0, b.s1, b.d0, b.d1, rows, 0, 0};
+            x.vec4 = (b.src_off % 4 == 0 && b.dst_off % 4 == 0 && b.n2 % 4 == 0 && b.s0 % 4 == 0 && b.s1 % 4 == 0 &&
+                      b.d0 % 4 == 0 && b.d1 % 4 == 0);
+            rows += b.n0 * b.n1;
+            floats += b.n0 * b.n1 * b.n2;
+            h.push_back(x);
+        }
+        n = static_cast<int>(h.size());
+        d.alloc(h.size(), false);
+        if (!h.empty()) SPH_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(DBox), cudaMemcpyHostToDevice));
+    }
+    // src/dst must be 16-byte aligned for the float4 boxes (workspace carve-outs are)
+    void run(const float* src, float* dst, cudaStream_t st, const char* name) const {
+        if (!rows) return;
+        ProfScope prof(name, st, 8.0 * static_cast<double>(floats));
+        box_copy_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(d.p, n, rows, src, dst);
+        SPH_LAUNCH_CHECK();
+        count_launch();
+    }
+};
+
+template <class T>
+void upload_vec(DevBuf<T>& d, const std::vector<T>& h) {
+    d.alloc(h.size(), false);
+    if (!h.empty()) SPH_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+// grouped point-to-point all-to-all over `comm` (plane ranks); the self block is a
+// device-to-device copy
+void alltoallv(ncclComm_t comm, int64_t me, const Exchange& x, const float* send, float* recv, cudaStream_t st) {
+    const int64_t P = static_cast<int64_t>(x.send_cnt.size());
+    if (x.send_cnt[me]) {
+        require(x.send_cnt[me] == x.recv_cnt[me], "all_to_all: self block size mismatch");
+        if (send + x.send_off[me] != recv + x.recv_off[me])
+            SPH_CUDA(cudaMemcpyAsync(recv + x.recv_off[me], send + x.send_off[me], 4 * x.send_cnt[me],
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+    if (P == 1) return;
+    SPH_NCCL(sph::nccl().GroupStart());
+    for (int64_t p = 0; p < P; ++p) {
+        if (p == me) continue;
+        if (x.send_cnt[p])
+            SPH_NCCL(sph::nccl().Send(send + x.send_off[p], static_cast<size_t>(x.send_cnt[p]), ncclFloat, static_cast<int>(p),
+                              comm, st));
+        if (x.recv_cnt[p])
+            SPH_NCCL(sph::nccl().Recv(recv + x.recv_off[p], static_cast<size_t>(x.recv_cnt[p]), ncclFloat, static_cast<int>(p),
+                              comm, st));
+    }
+    SPH_NCCL(sph::nccl().GroupEnd());
+}
+
+// world-summed remote bytes of one exchange (the reference TrafficLog accounting)
+template <class XFn>
+int64_t world_bytes(int64_t P, int64_t planes, XFn xfn) {
+    int64_t b = 0;
+    for (int64_t q = 0; q < P; ++q) b += 4 * xfn(q).remote_send(q);
+    return b * planes;
+}
+
+struct Carve {  // 256-byte aligned sub-buffers of one workspace
+    int64_t off = 0;
+    int64_t take(int64_t bytes) {
+        const int64_t o = off;
+        off += static_cast<int64_t>(round_up(static_cast<size_t>(std::max<int64_t>(bytes, 0)), 256));
+        return o;
+    }
+};
+
+}  // namespace
+}  // namespace sph
+
+// ------------------------------------------------------------------ distributed SHT
+struct sph_dist_sht_plan_s {
+    sph_comm comm = nullptr;
+    sph::ShtPlan* sht = nullptr;
+    sph::ShtLayout lay;
+    int64_t q = 0, i = 0, j = 0;
+    sph::Exchange xa, xb, xia, xib;
+    sph::BoxList fwd_unpack, inv_pack;
+    sph::DevBuf<int2> lmap, mmap;
+    sph::DevBuf<int64_t> off_b, off_ia, tri, rowoff, robase, rowoff_me;
+    int64_t tri_me = 0;
+    // workspace carve (bytes)
+    int64_t o_stage = 0, o_full = 0, o_cint = 0, o_shtws = 0, o_pay = 0, o_mine = 0, total = 0;
+    int64_t fwd_bytes = 0, inv_bytes_a = 0, inv_bytes_b = 0, fwd_bytes_b = 0;
+    std::mutex mu;
+    sph::DevBuf<uint8_t> own_ws;
+
+    void create(sph_comm c, sph::ShtPlan* p, int64_t C) {
+        using namespace sph;
+        comm = c;
+        sht = p;
+        const int64_t nh = c->grid.sizes[2], nw = c->grid.sizes[3];
+        lay = ShtLayout(nh, nw, p->nlat, p->nlon, p->lmax, p->mmax, C);
+        require(nw <= kMaxNw, "dist_sht: at most 16 azimuth ranks");
+        require(C <= 65535 && p->lmax <= 65535, "dist_sht: too many channels for one call");
+        q = c->plane_rank;
+        i = lay.pi(q);
+        j = lay.pj(q);
+        xa = lay.fwd_fields(q);
+        xb = lay.fwd_coeffs(q);
+        xia = lay.inv_coeffs(q);
+        xib = lay.inv_fields(q);
+        DeviceGuard dg(p->device);
+        fwd_unpack.set(lay.fwd_unpack(q));
+        inv_pack.set(lay.inv_pack(q));
+        std::vector<int2> lm(p->lmax), mm(p->mmax);
+        for (int64_t a = 0; a < nh; ++a)
+            for (int64_t k = 0; k < lay.lp[a]; ++k) lm[lay.l0(a) + k] = make_int2(static_cast<int>(a), static_cast<int>(k));
+        for (int64_t b = 0; b < nw; ++b)
+            for (int64_t k = 0; k < lay.mp[b]; ++k) mm[lay.m0(b) + k] = make_int2(static_cast<int>(b), static_cast<int>(k));
+        upload_vec(lmap, lm);
+        upload_vec(mmap, mm);
+        std::vector<int64_t> tr(lay.P), rb(lay.P), ro, ob(lay.P), oia(lay.P);
+        for (int64_t s = 0; s < lay.P; ++s) {
+            const auto r = lay.rowoff(s);
+            tr[s] = r.back();
+            rb[s] = static_cast<int64_t>(ro.size());
+            ro.insert(ro.end(), r.begin(), r.end());
+            ob[s] = xb.send_off[s] / 2;    // complex units
+            oia[s] = xia.recv_off[s] / 2;
+        }
+        tri_me = tr[q];
+        upload_vec(tri, tr);
+        upload_vec(robase, rb);
+        upload_vec(rowoff, ro);
+        upload_vec(off_b, ob);
+        upload_vec(off_ia, oia);
+        upload_vec(rowoff_me, lay.rowoff(q));
+        const int64_t cq = lay.cq(q), HW = p->nlat * p->nlon;
+        Carve cv;
+        o_stage = cv.take(4 * cq * HW);  // forward: A receive;  inverse: B^-1 send
+        o_full = cv.take(4 * cq * HW);   // full fields of the local channels
+        o_cint = cv.take(4 * p->cint_elems(cq));
+        o_shtws = cv.take(p->workspace_bytes(cq));
+        o_pay = cv.take(4 * std::max(xb.send_total(), xia.recv_total()));  // C_q payloads
+        o_mine = cv.take(4 * std::max(xb.recv_total(), xia.send_total()));  // [C][tri(q)]
+        total = cv.off;
+        const int64_t planes = c->grid.sizes[0] * c->grid.sizes[1];
+        fwd_bytes = world_bytes(lay.P, planes, [&](int64_t r) { return lay.fwd_fields(r); });
+        fwd_bytes_b = world_bytes(lay.P, planes, [&](int64_t r) { return lay.fwd_coeffs(r); });
+        inv_bytes_a = world_bytes(lay.P, planes, [&](int64_t r) { return lay.inv_coeffs(r); });
+        inv_bytes_b = world_bytes(lay.P, planes, [&](int64_t r) { return lay.inv_fields(r); });
+    }
+    uint8_t* ws_base(void* ws) {
+        if (ws) return static_cast<uint8_t*>(ws);
+        std::lock_guard<std::mutex> lk(mu);
+        if (own_ws.n < static_cast<size_t>(total)) own_ws.alloc(total, true);
+        return own_ws.p;
+    }
+    sph::PayloadMap pmap(const sph::DevBuf<int64_t>& off) const {
+        return {lmap.p, mmap.p, off.p, tri.p, rowoff.p, robase.p, static_cast<int>(lay.nw)};
+    }
+    void log(const char* op, const char* coll, int64_t bytes) {
+        std::lock_guard<std::mutex> lk(comm->mu);
+        comm->log.record(op, "polar+azimuth", coll, bytes);
+    }
+
+    // x [C][H_i][W_j] -> coeffs [C][L_i][M_j] complex64 (dense, zeros above the diagonal)
+    void forward(const float* x, float* out, void* ws, cudaStream_t st) {
+        using namespace sph;
+        DeviceGuard dg(sht->device);
+        require_on_device(x, sht->device, "dist_sht_forward");
+        require_on_device(out, sht->device, "dist_sht_forward");
+        if (lay.P == 1) {
+            sht->forward(x, lay.C, out, SPH_LAYOUT_DENSE_LM, nullptr, st);
+            log("dist_sht", "all_to_all", 0);
+            log("dist_sht", "all_to_all", 0);
+            return;
+        }
+        uint8_t* w = ws_base(ws);
+        float* stage = reinterpret_cast<float*>(w + o_stage);
+        float* full = reinterpret_cast<float*>(w + o_full);
+        float* cint = reinterpret_cast<float*>(w + o_cint);
+        float* pay = reinterpret_cast<float*>(w + o_pay);
+        float* mine = reinterpret_cast<float*>(w + o_mine);
+        const int64_t cq = lay.cq(q);
+        // A: spatial blocks -> the local channel slice's full fields (x is sent in place)
+        alltoallv(comm->plane, q, xa, x, stage, st);
+        log("dist_sht", "all_to_all", fwd_bytes);
+        fwd_unpack.run(stage, full, st, "dist_unpack_fields");
+        if (cq > 0) {
+            sht->forward(full, cq, cint, SPH_LAYOUT_INTERNAL, w + o_shtws, st);
+            ProfScope prof("dist_pack_cint", st, 4.0 * sht->cint_elems(cq) + 4.0 * xb.send_total());
+            constexpr int LT = 64;
+            dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((lay.lmax + LT - 1) / LT),
+                   static_cast<unsigned>(cq));
+            cint_pack_kernel<LT><<<g, 256, 0, st>>>(cint, cq, static_cast<int>(lay.lmax), static_cast<int>(lay.mmax),
+                                                    sht->Lp, pmap(off_b), reinterpret_cast<float2*>(pay));
+            SPH_LAUNCH_CHECK();
+            count_launch();
+        }
+        // B: triangular (l, m) blocks of every channel slice -> [C][tri(q)]
+        alltoallv(comm->plane, q, xb, pay, mine, st);
+        log("dist_sht", "all_to_all", fwd_bytes_b);
+        const int64_t n = lay.C * lay.lp[i] * lay.mp[j];
+        if (n) {
+            ProfScope prof("dist_unpack_tri", st, 8.0 * n + 4.0 * xb.recv_total());
+            block_tri_kernel<true><<<dim3(static_cast<unsigned>(lay.lp[i]), static_cast<unsigned>(lay.C)),
+                                     lay.mp[j] > 128 ? 256 : 128, 0, st>>>(
+                reinterpret_cast<float2*>(out), reinterpret_cast<float2*>(mine), static_cast<int>(lay.lp[i]),
+                static_cast<int>(lay.mp[j]), static_cast<int>(lay.l0(i)), static_cast<int>(lay.m0(j)), rowoff_me.p,
+                tri_me);
+            SPH_LAUNCH_CHECK();
+            count_launch();
+        }
+    }
+
+    // coeffs [C][L_i][M_j] complex64 -> y [C][H_i][W_j]  (mirror of forward)
+    void inverse(const float* in, float* y, void* ws, cudaStream_t st) {
+        using namespace sph;
+        DeviceGuard dg(sht->device);
+        require_on_device(in, sht->device, "dist_sht_inverse");
+        require_on_device(y, sht->device, "dist_sht_inverse");
+        if (lay.P == 1) {
+            sht->inverse(in, lay.C, SPH_LAYOUT_DENSE_LM, y, nullptr, st);
+            log("dist_isht", "all_to_all", 0);
+            log("dist_isht", "all_to_all", 0);
+            return;
+        }
+        uint8_t* w = ws_base(ws);
+        float* stage = reinterpret_cast<float*>(w + o_stage);
+        float* full = reinterpret_cast<float*>(w + o_full);
+        float* cint = reinterpret_cast<float*>(w + o_cint);
+        float* pay = reinterpret_cast<float*>(w + o_pay);
+        float* mine = reinterpret_cast<float*>(w + o_mine);
+        const int64_t cq = lay.cq(q);
+        const int64_t n = lay.C * lay.lp[i] * lay.mp[j];
+        if (n) {
+            ProfScope prof("dist_pack_tri", st, 8.0 * n + 4.0 * xia.send_total());
+            block_tri_kernel<false><<<dim3(static_cast<unsigned>(lay.lp[i]), static_cast<unsigned>(lay.C)),
+                                      lay.mp[j] > 128 ? 256 : 128, 0, st>>>(
+                const_cast<float2*>(reinterpret_cast<const float2*>(in)), reinterpret_cast<float2*>(mine),
+                static_cast<int>(lay.lp[i]), static_cast<int>(lay.mp[j]), static_cast<int>(lay.l0(i)),
+                static_cast<int>(lay.m0(j)), rowoff_me.p, tri_me);
+            SPH_LAUNCH_CHECK();
+            count_launch();
+        }
+        // A^-1: [C][tri(q)] -> the local channel slice's triangles of every block
+        alltoallv(comm->plane, q, xia, mine, pay, st);
+        log("dist_isht", "all_to_all", inv_bytes_a);
+        if (cq > 0) {
+            {
+                ProfScope prof("dist_unpack_cint", st, 4.0 * xia.recv_total() + 4.0 * sht->cint_elems(cq));
+                dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((sht->Lp + 31) / 32),
+                       static_cast<unsigned>(cq));
+                cint_unpack_kernel<<<g, 256, 0, st>>>(reinterpret_cast<const float2*>(pay), cq,
+                                                      static_cast<int>(lay.lmax), static_cast<int>(lay.mmax), sht->Lp,
+                                                      pmap(off_ia), cint);
+                SPH_LAUNCH_CHECK();
+                count_launch();
+            }
+            sht->inverse(cint, cq, SPH_LAYOUT_INTERNAL, full, w + o_shtws, st);
+            inv_pack.run(full, stage, st, "dist_pack_fields");
+        }
+        // B^-1: full fields of the channel slice -> spatial blocks, received in place
+        alltoallv(comm->plane, q, xib, stage, y, st);
+        log("dist_isht", "all_to_all", inv_bytes_b);
+    }
+};
+
+// ---------------------------------------------------------------- distributed DISCO
+struct sph_dist_disco_plan_s {
+    sph_comm comm = nullptr;
+    sph::DiscoPlan* op = nullptr;
+    sph::DiscoLayout lay;
+    int64_t q = 0, i = 0, j = 0;
+    sph::Exchange xh;
+    sph::BoxList hpack, hunpack, rpack, runpack, mixbox;
+    int64_t o_send = 0, o_recv = 0, o_rows = 0, o_mix = 0, o_part = 0, o_rss = 0, o_rsr = 0, o_dws = 0, total = 0;
+    int64_t halo_bytes = 0, rs_bytes = 0;
+    std::mutex mu;
+    sph::DevBuf<uint8_t> own_ws;
+
+    void create(sph_comm c, sph::DiscoPlan* p, int64_t cin, int64_t cout) {
+        using namespace sph;
+        require(cin >= 1 && cout >= 1, "dist_disco_apply: channel counts must be >= 1");
+        comm = c;
+        op = p;
+        const int64_t nh = c->grid.sizes[2], nw = c->grid.sizes[3];
+        lay = DiscoLayout(nh, nw, p->hin, p->win, p->hout, p->wout, cin, cout,
+                          [p](int64_t a, int64_t n, int64_t* lo, int64_t* cnt) { p->input_rows(a, n, lo, cnt); });
+        q = c->plane_rank;
+        i = lay.pi(q);
+        j = lay.pj(q);
+        xh = lay.halo(q);
+        DeviceGuard dg(p->device);
+        hpack.set(lay.halo_pack(q));
+        hunpack.set(lay.halo_unpack(q));
+        const int64_t K = p->K, cz = lay.czp[j], mx = lay.rs_width();
+        mixbox.set({{lay.cz0(j) * K, 0, 1, cout, cz * K, 0, cin * K, 0, cz * K}});
+        if (nw > 1) {
+            rpack.set(lay.rs_pack(q));
+            runpack.set(lay.rs_unpack(q));
+        }
+        Carve cv;
+        o_send = cv.take(4 * xh.send_total());
+        o_recv = cv.take(4 * xh.recv_total());
+        o_rows = cv.take(4 * cz * lay.needn[i] * lay.win);
+        o_mix = cv.take(4 * cout * cz * K);
+        o_part = cv.take(nw > 1 ? 4 * cout * lay.hop[i] * lay.wout : 0);
+        o_rss = cv.take(nw > 1 ? 4 * nw * cout * lay.hop[i] * mx : 0);
+        o_rsr = cv.take(nw > 1 ? 4 * cout * lay.hop[i] * mx : 0);
+        o_dws = cv.take(cz ? p->rows_workspace_bytes(1, cz, cout, lay.needn[i], lay.hop[i]) : 0);
+        total = cv.off;
+        const int64_t planes = c->grid.sizes[0] * c->grid.sizes[1];
+        halo_bytes = world_bytes(lay.P, planes, [&](int64_t r) { return lay.halo(r); });
+        // reference accounting (distsim.hpp:262-266): every member receives its W_out slice
+        // from the nw - 1 others
+        rs_bytes = (nw - 1) * cout * lay.hout * lay.wout * 4 * planes;
+    }
+    uint8_t* ws_base(void* ws) {
+        if (ws) return static_cast<uint8_t*>(ws);
+        std::lock_guard<std::mutex> lk(mu);
+        if (own_ws.n < static_cast<size_t>(total)) own_ws.alloc(total, true);
+        return own_ws.p;
+    }
+    // x [C_in][H_i][W_j], mix [C_out][C_in][K] (replicated) -> y [C_out][Ho_i][Wo_j]
+    void apply(const float* x, const float* mix, float* y, void* ws, cudaStream_t st) {
+        using namespace sph;
+        DeviceGuard dg(op->device);
+        require_on_device(x, op->device, "dist_disco_apply");
+        require_on_device(y, op->device, "dist_disco_apply");
+        uint8_t* w = ws_base(ws);
+        float* send = reinterpret_cast<float*>(w + o_send);
+        float* recv = reinterpret_cast<float*>(w + o_recv);
+        float* rows = reinterpret_cast<float*>(w + o_rows);
+        float* mixs = reinterpret_cast<float*>(w + o_mix);
+        const int64_t cz = lay.czp[j], nw = lay.nw;
+        // A: channel slice x (filter-support rows) x full rings, one all-to-all of the plane
+        hpack.run(x, send, st, "dist_pack_halo");
+        alltoallv(comm->plane ? comm->plane : nullptr, q, xh, send, recv, st);
+        {
+            std::lock_guard<std::mutex> lk(comm->mu);
+            comm->log.record("dist_disco", "polar+azimuth", "all_to_all", halo_bytes);
+        }
+        hunpack.run(recv, rows, st, "dist_unpack_halo");
+        float* part = nw > 1 ? reinterpret_cast<float*>(w + o_part) : y;
+        if (cz > 0) {
+            mixbox.run(mix, mixs, st, "dist_mix_slice");
+            op->apply_rows(rows, lay.need0[i], lay.needn[i], split_offset(lay.hop, i), lay.hop[i], mixs, 1, cz,
+                           lay.cout, part, w + o_dws, st);
+        } else {
+            SPH_CUDA(cudaMemsetAsync(part, 0, 4 * lay.cout * lay.hop[i] * (nw > 1 ? lay.wout : lay.wop[j]), st));
+        }
+        if (nw > 1) {
+            // sum the channel-slice partials over azimuth, scattered onto Wo_j
+            float* rss = reinterpret_cast<float*>(w + o_rss);
+            float* rsr = reinterpret_cast<float*>(w + o_rsr);
+            rpack.run(part, rss, st, "dist_pack_rs");
+            const int64_t cnt = lay.cout * lay.hop[i] * lay.rs_width();
+            SPH_NCCL(sph::nccl().ReduceScatter(rss, rsr, static_cast<size_t>(cnt), ncclFloat, ncclSum, comm->az, st));
+            runpack.run(rsr, y, st, "dist_unpack_rs");
+        }
+        std::lock_guard<std::mutex> lk(comm->mu);
+        comm->log.record("dist_disco", "azimuth", "reduce_scatter", rs_bytes);
+    }
+};
+
+// ------------------------------------------------------------------------ C ABI
+namespace {
+void write_out(const std::vector<int64_t>& v, int64_t* out, int64_t cap, int64_t* n) {
+    sph::require(n != nullptr, "describe: null count pointer");
+    *n = static_cast<int64_t>(v.size());
+    if (out) {
+        sph::require(cap >= *n, "describe: output buffer too small");
+        std::memcpy(out, v.data(), sizeof(int64_t) * v.size());
+    }
+}
+void put_exchange(std::vector<int64_t>& v, const sph::Exchange& x) {
+    for (const auto* a : {&x.send_cnt, &x.send_off, &x.recv_cnt, &x.recv_off}) v.insert(v.end(), a->begin(), a->end());
+}
+void put_boxes(std::vector<int64_t>& v, const std::vector<sph::Box>& bs) {
+    for (const auto& b : bs) v.insert(v.end(), {b.src_off, b.dst_off, b.n0, b.n1, b.n2, b.s0, b.s1, b.d0, b.d1});
+}
+}  // namespace
+
+extern "C" {
+
+int64_t sph_comm_id_bytes(void) { return static_cast<int64_t>(sizeof(ncclUniqueId)); }
+
+int sph_comm_unique_id(void* id) {
+    return guarded([&] {
+        sph::require(id != nullptr, "comm: null id buffer");
+        ncclUniqueId u;
+        SPH_NCCL(sph::nccl().GetUniqueId(&u));
+        std::memcpy(id, &u, sizeof(u));
+    });
+}
+
+int sph_comm_create(const void* id, int64_t world, int64_t rank, const int64_t* sizes, sph_comm* comm) {
+    return guarded([&] {
+        sph::require(id && sizes && comm, "comm: null argument");
+        auto h = std::make_unique<sph_comm_s>();
+        for (int a = 0; a < 4; ++a) {
+            sph::require(sizes[a] >= 1, "CommGrid: sizes must be >= 1");
+            h->grid.sizes[a] = sizes[a];
+        }
+        sph::require(h->grid.world() == world, "comm: world size does not match the CommGrid");
+        sph::require(rank >= 0 && rank < world, "comm: rank out of range");
+        SPH_CUDA(cudaGetDevice(&h->device));
+        h->rank = rank;
+        h->coords = h->grid.coords(rank);
+        const int64_t nh = sizes[2], nw = sizes[3];
+        h->plane_size = nh * nw;
+        h->plane_rank = h->coords[2] * nw + h->coords[3];
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        SPH_NCCL(sph::nccl().CommInitRank(&h->world, static_cast<int>(world), u, static_cast<int>(rank)));
+        // plane: same (batch, ensemble); azimuth group: same (batch, ensemble, polar)
+        const int plane_color = static_cast<int>(h->coords[0] * sizes[1] + h->coords[1]);
+        SPH_NCCL(sph::nccl().CommSplit(h->world, plane_color, static_cast<int>(h->plane_rank), &h->plane, nullptr));
+        SPH_NCCL(sph::nccl().CommSplit(h->world, static_cast<int>(plane_color * nh + h->coords[2]),
+                               static_cast<int>(h->coords[3]), &h->az, nullptr));
+        *comm = h.release();
+    });
+}
+
+int sph_comm_destroy(sph_comm comm) {
+    return guarded([&] { delete comm; });
+}
+
+int sph_comm_coords(sph_comm comm, int64_t* coords) {
+    return guarded([&] {
+        sph::require(comm && coords, "comm: null argument");
+        for (int a = 0; a < 4; ++a) coords[a] = comm->coords[a];
+    });
+}
+
+int sph_comm_traffic_csv(sph_comm comm, char* csv, size_t cap) {
+    return guarded([&] {
+        sph::require(comm && csv, "comm: null argument");
+        std::lock_guard<std::mutex> lk(comm->mu);
+        const std::string s = comm->log.csv();
+        sph::require(s.size() + 1 <= cap, "traffic csv: buffer too small");
+        std::memcpy(csv, s.c_str(), s.size() + 1);
+    });
+}
+
+int sph_comm_traffic_reset(sph_comm comm) {
+    return guarded([&] {
+        sph::require(comm, "comm: null argument");
+        std::lock_guard<std::mutex> lk(comm->mu);
+        comm->log.recs.clear();
+    });
+}
+
+int sph_dist_sht_plan_create(sph_comm comm, sph_sht_plan sht, int64_t C, sph_dist_sht_plan* plan) {
+    return guarded([&] {
+        sph::require(comm && sht && plan, "dist_sht: null argument");
+        sph::require(sht->p.device == comm->device, "dist_sht: plan and communicator on different devices");
+        auto h = std::make_unique<sph_dist_sht_plan_s>();
+        h->create(comm, &sht->p, C);
+        *plan = h.release();
+    });
+}
+
+int sph_dist_sht_plan_destroy(sph_dist_sht_plan plan) {
+    return guarded([&] { delete plan; });
+}
+
+int sph_dist_sht_local(sph_dist_sht_plan plan, int64_t* info) {
+    return guarded([&] {
+        sph::require(plan && info, "dist_sht: null argument");
+        const auto& L = plan->lay;
+        const int64_t v[10] = {L.h0(plan->i), L.hp[plan->i], L.w0(plan->j), L.wp[plan->j], L.l0(plan->i),
+                               L.lp[plan->i], L.m0(plan->j),  L.mp[plan->j], L.c0(plan->q), L.cq(plan->q)};
+        std::memcpy(info, v, sizeof(v));
+    });
+}
+
+int64_t sph_dist_sht_workspace_bytes(sph_dist_sht_plan plan) { return plan ? plan->total : -1; }
+
+int sph_dist_sht_forward(sph_dist_sht_plan plan, const float* x, float* coeffs, void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "dist_sht_forward: null plan");
+        plan->forward(x, coeffs, workspace, S(stream));
+    });
+}
+
+int sph_dist_sht_inverse(sph_dist_sht_plan plan, const float* coeffs, float* y, void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "dist_sht_inverse: null plan");
+        plan->inverse(coeffs, y, workspace, S(stream));
+    });
+}
+
+int sph_dist_disco_plan_create(sph_comm comm, sph_disco_plan op, int64_t c_in, int64_t c_out,
+                               sph_dist_disco_plan* plan) {
+    return guarded([&] {
+        sph::require(comm && op && plan, "dist_disco: null argument");
+        sph::require(op->p.device == comm->device, "dist_disco: plan and communicator on different devices");
+        auto h = std::make_unique<sph_dist_disco_plan_s>();
+        h->create(comm, &op->p, c_in, c_out);
+        *plan = h.release();
+    });
+}
+
+int sph_dist_disco_plan_destroy(sph_dist_disco_plan plan) {
+    return guarded([&] { delete plan; });
+}
+
+int sph_dist_disco_local(sph_dist_disco_plan plan, int64_t* info) {
+    return guarded([&] {
+        sph::require(plan && info, "dist_disco: null argument");
+        const auto& L = plan->lay;
+        const int64_t i = plan->i, j = plan->j;
+        const int64_t v[12] = {L.h0(i), L.hp[i], L.w0(j), L.wp[j], sph::split_offset(L.hop, i), L.hop[i],
+                               sph::split_offset(L.wop, j), L.wop[j], L.cz0(j), L.czp[j], L.need0[i], L.needn[i]};
+        std::memcpy(info, v, sizeof(v));
+    });
+}
+
+int64_t sph_dist_disco_workspace_bytes(sph_dist_disco_plan plan) { return plan ? plan->total : -1; }
+
+int sph_dist_disco_apply(sph_dist_disco_plan plan, const float* x, const float* mix, float* y, void* workspace,
+                         void* stream) {
+    return guarded([&] {
+        sph::require(plan, "dist_disco_apply: null plan");
+        plan->apply(x, mix, y, workspace, S(stream));
+    });
+}
+
+// Host-only schedule descriptions (no GPU, no NCCL): what = 0 ranges
+// (h0,hn,w0,wn,l0,ln,m0,mn,c0,cn); 1..4 exchanges fwd_fields, fwd_coeffs, inv_coeffs,
+// inv_fields as [send_cnt|send_off|recv_cnt|recv_off] x P; 5 / 6 the fwd_unpack / inv_pack
+// boxes (9 int64 each); 7 rowoff of the rank's own coefficient block.
+int sph_dist_sht_describe(int64_t nh, int64_t nw, int64_t q, int64_t nlat, int64_t nlon, int64_t lmax,
+                          int64_t mmax, int64_t C, int what, int64_t* out, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        const sph::ShtLayout L(nh, nw, nlat, nlon, lmax, mmax, C);
+        sph::require(q >= 0 && q < L.P, "describe: rank out of range");
+        std::vector<int64_t> v;
+        const int64_t i = L.pi(q), j = L.pj(q);
+        switch (what) {
+            case 0: v = {L.h0(i), L.hp[i], L.w0(j), L.wp[j], L.l0(i), L.lp[i], L.m0(j), L.mp[j], L.c0(q), L.cq(q)}; break;
+            case 1: put_exchange(v, L.fwd_fields(q)); break;
+            case 2: put_exchange(v, L.fwd_coeffs(q)); break;
+            case 3: put_exchange(v, L.inv_coeffs(q)); break;
+            case 4: put_exchange(v, L.inv_fields(q)); break;
+            case 5: put_boxes(v, L.fwd_unpack(q)); break;
+            case 6: put_boxes(v, L.inv_pack(q)); break;
+            case 7: v = L.rowoff(q); break;
+            default: sph::require(false, "describe: unknown item");
+        }
+        write_out(v, out, cap, n);
+    });
+}
+
+// what = 0 ranges (h0,hn,w0,wn,ho0,hon,wo0,won,cz0,czn,need0,needn); 1 halo exchange;
+// 2 / 3 halo pack / unpack boxes; 4 / 5 reduce-scatter pack / unpack boxes; 6 rs slot width.
+// band_lo / band_n: input row band of every output row (the plan's filter support).
+int sph_dist_disco_describe(int64_t nh, int64_t nw, int64_t q, int64_t hin, int64_t win, int64_t hout, int64_t wout,
+                            int64_t cin, int64_t cout, const int64_t* band_lo, const int64_t* band_n, int what,
+                            int64_t* out, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        sph::require(band_lo && band_n, "describe: null band arrays");
+        const sph::DiscoLayout L(nh, nw, hin, win, hout, wout, cin, cout,
+                                 [&](int64_t a, int64_t cnt, int64_t* lo, int64_t* nn) {
+                                     int64_t l = band_lo[a], h = band_lo[a] + band_n[a];
+                                     for (int64_t r = a; r < a + cnt; ++r) {
+                                         l = std::min(l, band_lo[r]);
+                                         h = std::max(h, band_lo[r] + band_n[r]);
+                                     }
+                                     *lo = l;
+                                     *nn = h - l;
+                                 });
+        sph::require(q >= 0 && q < L.P, "describe: rank out of range");
+        std::vector<int64_t> v;
+        const int64_t i = L.pi(q), j = L.pj(q);
+        switch (what) {
+            case 0:
+                v = {L.h0(i),   L.hp[i],   L.w0(j),  L.wp[j],  sph::split_offset(L.hop, i), L.hop[i],
+                     sph::split_offset(L.wop, j), L.wop[j], L.cz0(j), L.czp[j], L.need0[i], L.needn[i]};
+                break;
+            case 1: put_exchange(v, L.halo(q)); break;
+            case 2: put_boxes(v, L.halo_pack(q)); break;
+            case 3: put_boxes(v, L.halo_unpack(q)); break;
+            case 4: put_boxes(v, L.rs_pack(q)); break;
+            case 5: put_boxes(v, L.rs_unpack(q)); break;
+            case 6: v = {L.rs_width()}; break;
+            default: sph::require(false, "describe: unknown item");
+        }
+        write_out(v, out, cap, n);
+    });
+}
+
+}  // extern "C"

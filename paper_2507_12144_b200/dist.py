@@ -558,3 +558,200 @@ def dist_disco_apply(ctx: DistContext, x: Sharded, op, mix: torch.Tensor, backen
     me = ctx.index(AZIMUTH)
     ctx.record("azimuth", "reduce_scatter", (nw - 1) * out.numel() * out.element_size(), part)
     return Sharded(out[:, :, :wparts[me]].contiguous(), {1: hoparts, 2: wparts})
+
+
+# ===================================================================== NCCL product path
+# The product distributed path lives in libsphgpu.so (csrc/dist.cu, csrc/dist_layout.hpp):
+# NCCL communicators split per CommGrid axis, one all-to-all of the (polar x azimuth) plane
+# per direction with the library's own pack / unpack kernels, the distributed inverse SHT.
+# Python only carries the NCCL unique id from rank 0 and binds the handles.
+class NcclComm:
+    """sph_comm over the ranks of the default torch.distributed group (any backend; it only
+    broadcasts the NCCL unique id).  ``grid`` is the CommGrid rank cube."""
+
+    def __init__(self, grid: CommGrid, device=None):
+        import ctypes as C
+        from . import _lib as L
+        if not dist.is_initialized():
+            raise RuntimeError("NcclComm: torch.distributed is not initialised")
+        world, rank = dist.get_world_size(), dist.get_rank()
+        if grid.world() != world:
+            raise ValueError("NcclComm: world size does not match the CommGrid")
+        self.grid = grid
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index)
+        n = int(L.lib.sph_comm_id_bytes())
+        uid = (C.c_uint8 * n)()
+        if rank == 0:
+            L.check(L.lib.sph_comm_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, device=self.device if dist.get_backend() == "nccl" else None)
+        uid = (C.c_uint8 * n).from_buffer_copy(obj[0])
+        sizes = (C.c_int64 * 4)(*grid.sizes)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            L.check(L.lib.sph_comm_create(uid, world, rank, sizes, C.byref(h)))
+        self.h = h
+        self.rank = rank
+        self.coords = grid.coords(rank)
+
+    def traffic_csv(self) -> str:
+        import ctypes as C
+        from . import _lib as L
+        buf = C.create_string_buffer(1 << 16)
+        L.check(L.lib.sph_comm_traffic_csv(self.h, buf, 1 << 16))
+        return buf.value.decode()
+
+    def traffic_reset(self) -> None:
+        from . import _lib as L
+        L.check(L.lib.sph_comm_traffic_reset(self.h))
+
+    def close(self) -> None:
+        from . import _lib as L
+        if getattr(self, "h", None) is not None and self.h.value:
+            L.check(L.lib.sph_comm_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+
+def _stream(device):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class DistShtPlan:
+    """Distributed forward SHT (Alg. 1, distsim.hpp:404-463) and its mirror inverse over
+    NCCL.  Rank (i, j) of its plane holds fields [C, H_i, W_j] and coefficients
+    [C, L_i, M_j, 2] (the reference's unshard layout); ``local`` has the ranges."""
+
+    def __init__(self, comm: NcclComm, grid, lmax: int, mmax: int, C: int, precision: str = "3xtf32"):
+        import ctypes as Ct
+        from . import _lib as L
+        from . import sphere as S
+        self.comm, self.grid, self.lmax, self.mmax, self.C = comm, grid, int(lmax), int(mmax), int(C)
+        self.sht = S.get_sht_plan(grid, self.lmax, self.mmax, precision, allow_equiangular_forward=True,
+                                  device=comm.device)
+        h = Ct.c_void_p()
+        with torch.cuda.device(comm.device):
+            L.check(L.lib.sph_dist_sht_plan_create(comm.h, self.sht.h, self.C, Ct.byref(h)))
+        self.h = h
+        info = (Ct.c_int64 * 10)()
+        L.check(L.lib.sph_dist_sht_local(h, info))
+        (self.h0, self.hn, self.w0, self.wn, self.l0, self.ln, self.m0, self.mn,
+         self.c0, self.cn) = [int(v) for v in info]
+        self.ws = torch.empty(max(1, int(L.lib.sph_dist_sht_workspace_bytes(h))), dtype=torch.uint8,
+                              device=comm.device)
+
+    def shard(self, x: torch.Tensor) -> torch.Tensor:
+        """Global [C, nlat, nlon] -> this rank's [C, H_i, W_j] block."""
+        return x[:, self.h0:self.h0 + self.hn, self.w0:self.w0 + self.wn].contiguous()
+
+    def forward(self, x: torch.Tensor, out=None) -> torch.Tensor:
+        from . import _lib as L
+        x = x.contiguous()
+        if tuple(x.shape) != (self.C, self.hn, self.wn) or x.dtype != torch.float32 or x.device != self.comm.device:
+            raise ValueError(f"dist_sht_forward: expected fp32 [{self.C}, {self.hn}, {self.wn}] on {self.comm.device}")
+        if out is None:
+            out = torch.empty((self.C, self.ln, self.mn, 2), dtype=torch.float32, device=x.device)
+        L.check(L.lib.sph_dist_sht_forward(self.h, x.data_ptr(), out.data_ptr(), self.ws.data_ptr(),
+                                           _stream(x.device)))
+        return out
+
+    def inverse(self, c: torch.Tensor, out=None) -> torch.Tensor:
+        from . import _lib as L
+        c = c.contiguous()
+        if tuple(c.shape) != (self.C, self.ln, self.mn, 2) or c.dtype != torch.float32:
+            raise ValueError(f"dist_sht_inverse: expected fp32 [{self.C}, {self.ln}, {self.mn}, 2]")
+        if out is None:
+            out = torch.empty((self.C, self.hn, self.wn), dtype=torch.float32, device=c.device)
+        L.check(L.lib.sph_dist_sht_inverse(self.h, c.data_ptr(), out.data_ptr(), self.ws.data_ptr(),
+                                           _stream(c.device)))
+        return out
+
+    def __del__(self):
+        try:
+            from . import _lib as L
+            if getattr(self, "h", None) is not None and self.h.value:
+                L.lib.sph_dist_sht_plan_destroy(self.h)
+                self.h = None
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class DistDiscoPlan:
+    """Distributed DISCO (Alg. 2 with a latitude halo, distsim.hpp:468-547) over NCCL:
+    x [C_in, H_i, W_j] on the input grid -> y [C_out, Ho_i, Wo_j] on the output grid."""
+
+    def __init__(self, comm: NcclComm, op, c_in: int, c_out: int):
+        import ctypes as Ct
+        from . import _lib as L
+        if op.device != comm.device:
+            raise ValueError("dist_disco: operator and communicator on different devices")
+        self.comm, self.op, self.cin, self.cout = comm, op, int(c_in), int(c_out)
+        h = Ct.c_void_p()
+        with torch.cuda.device(comm.device):
+            L.check(L.lib.sph_dist_disco_plan_create(comm.h, op.h, self.cin, self.cout, Ct.byref(h)))
+        self.h = h
+        info = (Ct.c_int64 * 12)()
+        L.check(L.lib.sph_dist_disco_local(h, info))
+        (self.h0, self.hn, self.w0, self.wn, self.ho0, self.hon, self.wo0, self.won,
+         self.cz0, self.czn, self.need0, self.needn) = [int(v) for v in info]
+        self.ws = torch.empty(max(1, int(L.lib.sph_dist_disco_workspace_bytes(h))), dtype=torch.uint8,
+                              device=comm.device)
+
+    def shard(self, x: torch.Tensor) -> torch.Tensor:
+        return x[:, self.h0:self.h0 + self.hn, self.w0:self.w0 + self.wn].contiguous()
+
+    def apply(self, x: torch.Tensor, mix: torch.Tensor, out=None) -> torch.Tensor:
+        from . import _lib as L
+        x, mix = x.contiguous(), mix.contiguous()
+        if tuple(x.shape) != (self.cin, self.hn, self.wn) or x.dtype != torch.float32:
+            raise ValueError(f"dist_disco_apply: expected fp32 [{self.cin}, {self.hn}, {self.wn}]")
+        if tuple(mix.shape) != (self.cout, self.cin, self.op.n_basis):
+            raise ValueError("dist_disco_apply: mix tensor shape mismatch")
+        if out is None:
+            out = torch.empty((self.cout, self.hon, self.won), dtype=torch.float32, device=x.device)
+        L.check(L.lib.sph_dist_disco_apply(self.h, x.data_ptr(), mix.data_ptr(), out.data_ptr(),
+                                           self.ws.data_ptr(), _stream(x.device)))
+        return out
+
+    def __del__(self):
+        try:
+            from . import _lib as L
+            if getattr(self, "h", None) is not None and self.h.value:
+                L.lib.sph_dist_disco_plan_destroy(self.h)
+                self.h = None
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def describe_sht(nh: int, nw: int, q: int, nlat: int, nlon: int, lmax: int, mmax: int, C: int, what: int):
+    """Host-only schedule of the library's distributed SHT (sph_dist_sht_describe)."""
+    from . import _lib as L
+    return _describe(lambda out, cap, n: L.lib.sph_dist_sht_describe(nh, nw, q, nlat, nlon, lmax, mmax, C, what,
+                                                                   out, cap, n))
+
+
+def describe_disco(nh: int, nw: int, q: int, hin: int, win: int, hout: int, wout: int, cin: int, cout: int,
+                   band_lo, band_n, what: int):
+    """Host-only schedule of the library's distributed DISCO (sph_dist_disco_describe)."""
+    import ctypes as Ct
+    lo = (Ct.c_int64 * len(band_lo))(*[int(v) for v in band_lo])
+    bn = (Ct.c_int64 * len(band_n))(*[int(v) for v in band_n])
+    from . import _lib as L
+    return _describe(lambda out, cap, n: L.lib.sph_dist_disco_describe(nh, nw, q, hin, win, hout, wout, cin, cout,
+                                                                     lo, bn, what, out, cap, n))
+
+
+def _describe(call):
+    import ctypes as Ct
+    from . import _lib as L
+    n = Ct.c_int64()
+    L.check(call(None, 0, Ct.byref(n)))
+    buf = (Ct.c_int64 * max(1, n.value))()
+    L.check(call(buf, n.value, Ct.byref(n)))
+    return [int(v) for v in buf[:n.value]]

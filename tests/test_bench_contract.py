@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
-WORKLOADS = ["sht", "disco", "disco_t", "block", "decoder", "dist_sht", "dist_disco"]
+WORKLOADS = ["all", "sht", "disco", "disco_t", "block", "decoder", "dist_sht", "dist_disco"]
 
 
 def test_metric_is_baselines():
