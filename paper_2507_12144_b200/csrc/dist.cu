@@ -110,6 +110,7 @@ struct sph_comm_s {
     int64_t rank = 0;
     std::array<int64_t, 4> coords{};
     int64_t plane_rank = 0, plane_size = 1;
+    int nccl_ctas = 16;  // maxCTAs of the plane communicator (SPH_NCCL_MAX_CTAS)
     ncclComm_t world = nullptr, plane = nullptr, az = nullptr;
     std::mutex mu;
     sph::Traffic log;
@@ -356,21 +357,66 @@ struct Carve {  // 256-byte aligned sub-buffers of one workspace
 }  // namespace sph
 
 // ------------------------------------------------------------------ distributed SHT
+namespace sph {
+namespace {
+// One channel chunk of the distributed SHT: an independent Alg. 1 problem on channels
+// [c_begin, c_begin + C_k) (its own canonical channel slices, exchanges and boxes).
+struct ShtChunk {
+    ShtLayout lay;
+    int64_t c_begin = 0;
+    Exchange xa, xb, xia, xib;
+    BoxList fwd_unpack, inv_pack;
+    DevBuf<int64_t> off_b, off_ia;  // payload offsets per block (complex units)
+    int64_t bytes_fa = 0, bytes_fb = 0, bytes_ia = 0, bytes_ib = 0;
+};
+
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t make() {
+        cudaEvent_t e;
+        SPH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev.push_back(e);
+        return e;
+    }
+    ~Events() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+};
+}  // namespace
+}  // namespace sph
+
+// Channel chunks are software-pipelined over two streams: the caller's stream runs the
+// compute (unpack, fused SHT, pack) and an internal stream issues every NCCL exchange, so
+// chunk k+1's inbound all-to-all and chunk k-1's outbound one run while chunk k computes.
+// During the overlapped region the persistent GEMM leaves SPH_NCCL_MAX_CTAS SMs to the
+// NCCL kernels (GemmSmCap; the plane communicator is split with that maxCTAs).  Buffers
+// that cross streams are double-buffered (set k % 2) and guarded by events.
 struct sph_dist_sht_plan_s {
     sph_comm comm = nullptr;
     sph::ShtPlan* sht = nullptr;
-    sph::ShtLayout lay;
+    sph::ShtLayout lay;  // the whole problem (ranges reported to the caller)
     int64_t q = 0, i = 0, j = 0;
-    sph::Exchange xa, xb, xia, xib;
-    sph::BoxList fwd_unpack, inv_pack;
+    std::vector<std::unique_ptr<sph::ShtChunk>> chunks;
     sph::DevBuf<int2> lmap, mmap;
-    sph::DevBuf<int64_t> off_b, off_ia, tri, rowoff, robase, rowoff_me;
+    sph::DevBuf<int64_t> tri, rowoff, robase, rowoff_me;
     int64_t tri_me = 0;
-    // workspace carve (bytes)
-    int64_t o_stage = 0, o_full = 0, o_cint = 0, o_shtws = 0, o_pay = 0, o_mine = 0, total = 0;
-    int64_t fwd_bytes = 0, inv_bytes_a = 0, inv_bytes_b = 0, fwd_bytes_b = 0;
-    std::mutex mu;
+    // workspace carve (bytes): stage / pay / mine are double-buffered
+    int64_t o_stage[2] = {0, 0}, o_pay[2] = {0, 0}, o_mine[2] = {0, 0};
+    int64_t o_full = 0, o_cint = 0, o_shtws = 0, total = 0;
+    cudaStream_t cs = nullptr;
+    sph::Events evs;
+    cudaEvent_t e_start = nullptr, e_end = nullptr;
+    cudaEvent_t eA[2], eUA[2], eP[2], eB[2], eP1[2], eA1[2], eUC[2], eP2[2], eB2[2];
+    int sm_cap = 0;
+    std::mutex mu, call_mu;
     sph::DevBuf<uint8_t> own_ws;
+
+    ~sph_dist_sht_plan_s() {
+        if (cs) {
+            cudaStreamSynchronize(cs);
+            cudaStreamDestroy(cs);
+        }
+    }
 
     void create(sph_comm c, sph::ShtPlan* p, int64_t C) {
         using namespace sph;
@@ -383,13 +429,48 @@ struct sph_dist_sht_plan_s {
         q = c->plane_rank;
         i = lay.pi(q);
         j = lay.pj(q);
-        xa = lay.fwd_fields(q);
-        xb = lay.fwd_coeffs(q);
-        xia = lay.inv_coeffs(q);
-        xib = lay.inv_fields(q);
         DeviceGuard dg(p->device);
-        fwd_unpack.set(lay.fwd_unpack(q));
-        inv_pack.set(lay.inv_pack(q));
+        // channel chunks: >= one channel per rank and chunk, SPH_DIST_CHUNKS (default 4)
+        static const int64_t want = [] {
+            const char* e = std::getenv("SPH_DIST_CHUNKS");
+            return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{4};
+        }();
+        const int64_t nchunk = lay.P == 1 ? 1 : std::max<int64_t>(1, std::min(want, C / lay.P));
+        const std::vector<int64_t> csplit = canonical_split(C, nchunk);
+        const int64_t planes = c->grid.sizes[0] * c->grid.sizes[1];
+        const int64_t HW = p->nlat * p->nlon;
+        int64_t m_stage = 0, m_full = 0, m_cint = 0, m_ws = 0, m_pay = 0, m_mine = 0;
+        for (int64_t k = 0; k < nchunk; ++k) {
+            auto ch = std::make_unique<ShtChunk>();
+            ch->lay = ShtLayout(nh, nw, p->nlat, p->nlon, p->lmax, p->mmax, csplit[k]);
+            ch->c_begin = split_offset(csplit, k);
+            const ShtLayout& L = ch->lay;
+            ch->xa = L.fwd_fields(q);
+            ch->xb = L.fwd_coeffs(q);
+            ch->xia = L.inv_coeffs(q);
+            ch->xib = L.inv_fields(q);
+            ch->fwd_unpack.set(L.fwd_unpack(q));
+            ch->inv_pack.set(L.inv_pack(q));
+            std::vector<int64_t> ob(L.P), oia(L.P);
+            for (int64_t s2 = 0; s2 < L.P; ++s2) {
+                ob[s2] = ch->xb.send_off[s2] / 2;
+                oia[s2] = ch->xia.recv_off[s2] / 2;
+            }
+            upload_vec(ch->off_b, ob);
+            upload_vec(ch->off_ia, oia);
+            ch->bytes_fa = world_bytes(L.P, planes, [&](int64_t r) { return L.fwd_fields(r); });
+            ch->bytes_fb = world_bytes(L.P, planes, [&](int64_t r) { return L.fwd_coeffs(r); });
+            ch->bytes_ia = world_bytes(L.P, planes, [&](int64_t r) { return L.inv_coeffs(r); });
+            ch->bytes_ib = world_bytes(L.P, planes, [&](int64_t r) { return L.inv_fields(r); });
+            const int64_t cq = L.cq(q);
+            m_stage = std::max({m_stage, ch->xa.recv_total(), ch->xib.send_total()});
+            m_full = std::max(m_full, cq * HW);
+            m_cint = std::max(m_cint, p->cint_elems(cq));
+            m_ws = std::max(m_ws, p->workspace_bytes(cq));
+            m_pay = std::max({m_pay, ch->xb.send_total(), ch->xia.recv_total()});
+            m_mine = std::max({m_mine, ch->xb.recv_total(), ch->xia.send_total()});
+            chunks.push_back(std::move(ch));
+        }
         std::vector<int2> lm(p->lmax), mm(p->mmax);
         for (int64_t a = 0; a < nh; ++a)
             for (int64_t k = 0; k < lay.lp[a]; ++k) lm[lay.l0(a) + k] = make_int2(static_cast<int>(a), static_cast<int>(k));
@@ -397,36 +478,45 @@ struct sph_dist_sht_plan_s {
             for (int64_t k = 0; k < lay.mp[b]; ++k) mm[lay.m0(b) + k] = make_int2(static_cast<int>(b), static_cast<int>(k));
         upload_vec(lmap, lm);
         upload_vec(mmap, mm);
-        std::vector<int64_t> tr(lay.P), rb(lay.P), ro, ob(lay.P), oia(lay.P);
-        for (int64_t s = 0; s < lay.P; ++s) {
-            const auto r = lay.rowoff(s);
-            tr[s] = r.back();
-            rb[s] = static_cast<int64_t>(ro.size());
+        std::vector<int64_t> tr(lay.P), rb(lay.P), ro;
+        for (int64_t s2 = 0; s2 < lay.P; ++s2) {
+            const auto r = lay.rowoff(s2);
+            tr[s2] = r.back();
+            rb[s2] = static_cast<int64_t>(ro.size());
             ro.insert(ro.end(), r.begin(), r.end());
-            ob[s] = xb.send_off[s] / 2;    // complex units
-            oia[s] = xia.recv_off[s] / 2;
         }
         tri_me = tr[q];
         upload_vec(tri, tr);
         upload_vec(robase, rb);
         upload_vec(rowoff, ro);
-        upload_vec(off_b, ob);
-        upload_vec(off_ia, oia);
         upload_vec(rowoff_me, lay.rowoff(q));
-        const int64_t cq = lay.cq(q), HW = p->nlat * p->nlon;
         Carve cv;
-        o_stage = cv.take(4 * cq * HW);  // forward: A receive;  inverse: B^-1 send
-        o_full = cv.take(4 * cq * HW);   // full fields of the local channels
-        o_cint = cv.take(4 * p->cint_elems(cq));
-        o_shtws = cv.take(p->workspace_bytes(cq));
-        o_pay = cv.take(4 * std::max(xb.send_total(), xia.recv_total()));  // C_q payloads
-        o_mine = cv.take(4 * std::max(xb.recv_total(), xia.send_total()));  // [C][tri(q)]
+        for (int b = 0; b < 2; ++b) o_stage[b] = cv.take(4 * m_stage);
+        o_full = cv.take(4 * m_full);
+        o_cint = cv.take(4 * m_cint);
+        o_shtws = cv.take(m_ws);
+        for (int b = 0; b < 2; ++b) o_pay[b] = cv.take(4 * m_pay);
+        for (int b = 0; b < 2; ++b) o_mine[b] = cv.take(4 * m_mine);
         total = cv.off;
-        const int64_t planes = c->grid.sizes[0] * c->grid.sizes[1];
-        fwd_bytes = world_bytes(lay.P, planes, [&](int64_t r) { return lay.fwd_fields(r); });
-        fwd_bytes_b = world_bytes(lay.P, planes, [&](int64_t r) { return lay.fwd_coeffs(r); });
-        inv_bytes_a = world_bytes(lay.P, planes, [&](int64_t r) { return lay.inv_coeffs(r); });
-        inv_bytes_b = world_bytes(lay.P, planes, [&](int64_t r) { return lay.inv_fields(r); });
+        if (lay.P > 1) {
+            int lo = 0, hi = 0;
+            SPH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            SPH_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, hi));
+            e_start = evs.make();
+            e_end = evs.make();
+            for (int b = 0; b < 2; ++b) {
+                eA[b] = evs.make();
+                eUA[b] = evs.make();
+                eP[b] = evs.make();
+                eB[b] = evs.make();
+                eP1[b] = evs.make();
+                eA1[b] = evs.make();
+                eUC[b] = evs.make();
+                eP2[b] = evs.make();
+                eB2[b] = evs.make();
+            }
+            if (chunks.size() > 1) sm_cap = std::max(16, num_sms() - c->nccl_ctas);
+        }
     }
     uint8_t* ws_base(void* ws) {
         if (ws) return static_cast<uint8_t*>(ws);
@@ -437,10 +527,16 @@ struct sph_dist_sht_plan_s {
     sph::PayloadMap pmap(const sph::DevBuf<int64_t>& off) const {
         return {lmap.p, mmap.p, off.p, tri.p, rowoff.p, robase.p, static_cast<int>(lay.nw)};
     }
-    void log(const char* op, const char* coll, int64_t bytes) {
+    void log(const char* op, int64_t bytes) {
         std::lock_guard<std::mutex> lk(comm->mu);
-        comm->log.record(op, "polar+azimuth", coll, bytes);
+        comm->log.record(op, "polar+azimuth", "all_to_all", bytes);
     }
+    template <class T>
+    static T* at(uint8_t* w, int64_t off) {
+        return reinterpret_cast<T*>(w + off);
+    }
+    void wait(cudaStream_t s, cudaEvent_t e) { SPH_CUDA(cudaStreamWaitEvent(s, e, 0)); }
+    void rec(cudaEvent_t e, cudaStream_t s) { SPH_CUDA(cudaEventRecord(e, s)); }
 
     // x [C][H_i][W_j] -> coeffs [C][L_i][M_j] complex64 (dense, zeros above the diagonal)
     void forward(const float* x, float* out, void* ws, cudaStream_t st) {
@@ -450,46 +546,78 @@ struct sph_dist_sht_plan_s {
         require_on_device(out, sht->device, "dist_sht_forward");
         if (lay.P == 1) {
             sht->forward(x, lay.C, out, SPH_LAYOUT_DENSE_LM, nullptr, st);
-            log("dist_sht", "all_to_all", 0);
-            log("dist_sht", "all_to_all", 0);
+            log("dist_sht", 0);
+            log("dist_sht", 0);
             return;
         }
+        std::lock_guard<std::mutex> call(call_mu);  // the plan's streams / events serve one call at a time
         uint8_t* w = ws_base(ws);
-        float* stage = reinterpret_cast<float*>(w + o_stage);
-        float* full = reinterpret_cast<float*>(w + o_full);
-        float* cint = reinterpret_cast<float*>(w + o_cint);
-        float* pay = reinterpret_cast<float*>(w + o_pay);
-        float* mine = reinterpret_cast<float*>(w + o_mine);
-        const int64_t cq = lay.cq(q);
-        // A: spatial blocks -> the local channel slice's full fields (x is sent in place)
-        alltoallv(comm->plane, q, xa, x, stage, st);
-        log("dist_sht", "all_to_all", fwd_bytes);
-        fwd_unpack.run(stage, full, st, "dist_unpack_fields");
-        if (cq > 0) {
-            sht->forward(full, cq, cint, SPH_LAYOUT_INTERNAL, w + o_shtws, st);
-            ProfScope prof("dist_pack_cint", st, 4.0 * sht->cint_elems(cq) + 4.0 * xb.send_total());
-            constexpr int LT = 64;
-            dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((lay.lmax + LT - 1) / LT),
-                   static_cast<unsigned>(cq));
-            cint_pack_kernel<LT><<<g, 256, 0, st>>>(cint, cq, static_cast<int>(lay.lmax), static_cast<int>(lay.mmax),
-                                                    sht->Lp, pmap(off_b), reinterpret_cast<float2*>(pay));
-            SPH_LAUNCH_CHECK();
-            count_launch();
+        GemmSmCap cap(sm_cap);
+        const int64_t n = static_cast<int64_t>(chunks.size());
+        const int64_t fblk = lay.field_block(q), cblk = 2 * lay.lp[i] * lay.mp[j];
+        rec(e_start, st);
+        wait(cs, e_start);
+        int64_t bytes_a = 0, bytes_b = 0;  // one TrafficLog record per exchange of the call
+        auto issue_a = [&](int64_t k) {  // inbound exchange of chunk k on the comm stream
+            const ShtChunk& ch = *chunks[k];
+            const int b = k & 1;
+            if (k >= 2) wait(cs, eUA[b]);  // stage[b] consumed by chunk k-2's unpack
+            alltoallv(comm->plane, q, ch.xa, x + ch.c_begin * fblk, at<float>(w, o_stage[b]), cs);
+            rec(eA[b], cs);
+            bytes_a += ch.bytes_fa;
+        };
+        auto unpack_b = [&](int64_t k) {  // chunk k's received triangles -> its output rows
+            const ShtChunk& ch = *chunks[k];
+            const int b = k & 1;
+            wait(st, eB[b]);
+            const int64_t C = ch.lay.C;
+            if (C * lay.lp[i] * lay.mp[j]) {
+                ProfScope prof("dist_unpack_tri", st, 8.0 * C * lay.lp[i] * lay.mp[j] + 4.0 * ch.xb.recv_total());
+                block_tri_kernel<true><<<dim3(static_cast<unsigned>(lay.lp[i]), static_cast<unsigned>(C)),
+                                         lay.mp[j] > 128 ? 256 : 128, 0, st>>>(
+                    reinterpret_cast<float2*>(out + ch.c_begin * cblk), at<float2>(w, o_mine[b]),
+                    static_cast<int>(lay.lp[i]), static_cast<int>(lay.mp[j]), static_cast<int>(lay.l0(i)),
+                    static_cast<int>(lay.m0(j)), rowoff_me.p, tri_me);
+                SPH_LAUNCH_CHECK();
+                count_launch();
+            }
+        };
+        issue_a(0);
+        for (int64_t k = 0; k < n; ++k) {
+            const ShtChunk& ch = *chunks[k];
+            const int b = k & 1;
+            const int64_t cq = ch.lay.cq(q);
+            if (k + 1 < n) issue_a(k + 1);
+            // compute of chunk k on the caller's stream
+            wait(st, eA[b]);
+            ch.fwd_unpack.run(at<float>(w, o_stage[b]), at<float>(w, o_full), st, "dist_unpack_fields");
+            rec(eUA[b], st);
+            if (cq > 0) {
+                sht->forward(at<float>(w, o_full), cq, at<float>(w, o_cint), SPH_LAYOUT_INTERNAL, w + o_shtws, st);
+                ProfScope prof("dist_pack_cint", st, 4.0 * sht->cint_elems(cq) + 4.0 * ch.xb.send_total());
+                constexpr int LT = 64;
+                dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((lay.lmax + LT - 1) / LT),
+                       static_cast<unsigned>(cq));
+                cint_pack_kernel<LT><<<g, 256, 0, st>>>(at<float>(w, o_cint), cq, static_cast<int>(lay.lmax),
+                                                        static_cast<int>(lay.mmax), sht->Lp, pmap(ch.off_b),
+                                                        at<float2>(w, o_pay[b]));
+                SPH_LAUNCH_CHECK();
+                count_launch();
+            }
+            rec(eP[b], st);
+            if (k >= 1) unpack_b(k - 1);  // the previous chunk's outbound exchange has had chunk k's compute to land
+            // outbound exchange of chunk k (mine[b] was last read by chunk k-2's unpack, which
+            // the caller's stream ran before eP[b])
+            wait(cs, eP[b]);
+            alltoallv(comm->plane, q, ch.xb, at<float>(w, o_pay[b]), at<float>(w, o_mine[b]), cs);
+            rec(eB[b], cs);
+            bytes_b += ch.bytes_fb;
         }
-        // B: triangular (l, m) blocks of every channel slice -> [C][tri(q)]
-        alltoallv(comm->plane, q, xb, pay, mine, st);
-        log("dist_sht", "all_to_all", fwd_bytes_b);
-        const int64_t n = lay.C * lay.lp[i] * lay.mp[j];
-        if (n) {
-            ProfScope prof("dist_unpack_tri", st, 8.0 * n + 4.0 * xb.recv_total());
-            block_tri_kernel<true><<<dim3(static_cast<unsigned>(lay.lp[i]), static_cast<unsigned>(lay.C)),
-                                     lay.mp[j] > 128 ? 256 : 128, 0, st>>>(
-                reinterpret_cast<float2*>(out), reinterpret_cast<float2*>(mine), static_cast<int>(lay.lp[i]),
-                static_cast<int>(lay.mp[j]), static_cast<int>(lay.l0(i)), static_cast<int>(lay.m0(j)), rowoff_me.p,
-                tri_me);
-            SPH_LAUNCH_CHECK();
-            count_launch();
-        }
+        unpack_b(n - 1);
+        rec(e_end, cs);
+        wait(st, e_end);
+        log("dist_sht", bytes_a);
+        log("dist_sht", bytes_b);
     }
 
     // coeffs [C][L_i][M_j] complex64 -> y [C][H_i][W_j]  (mirror of forward)
@@ -500,48 +628,84 @@ struct sph_dist_sht_plan_s {
         require_on_device(y, sht->device, "dist_sht_inverse");
         if (lay.P == 1) {
             sht->inverse(in, lay.C, SPH_LAYOUT_DENSE_LM, y, nullptr, st);
-            log("dist_isht", "all_to_all", 0);
-            log("dist_isht", "all_to_all", 0);
+            log("dist_isht", 0);
+            log("dist_isht", 0);
             return;
         }
+        std::lock_guard<std::mutex> call(call_mu);
         uint8_t* w = ws_base(ws);
-        float* stage = reinterpret_cast<float*>(w + o_stage);
-        float* full = reinterpret_cast<float*>(w + o_full);
-        float* cint = reinterpret_cast<float*>(w + o_cint);
-        float* pay = reinterpret_cast<float*>(w + o_pay);
-        float* mine = reinterpret_cast<float*>(w + o_mine);
-        const int64_t cq = lay.cq(q);
-        const int64_t n = lay.C * lay.lp[i] * lay.mp[j];
-        if (n) {
-            ProfScope prof("dist_pack_tri", st, 8.0 * n + 4.0 * xia.send_total());
-            block_tri_kernel<false><<<dim3(static_cast<unsigned>(lay.lp[i]), static_cast<unsigned>(lay.C)),
-                                      lay.mp[j] > 128 ? 256 : 128, 0, st>>>(
-                const_cast<float2*>(reinterpret_cast<const float2*>(in)), reinterpret_cast<float2*>(mine),
-                static_cast<int>(lay.lp[i]), static_cast<int>(lay.mp[j]), static_cast<int>(lay.l0(i)),
-                static_cast<int>(lay.m0(j)), rowoff_me.p, tri_me);
-            SPH_LAUNCH_CHECK();
-            count_launch();
-        }
-        // A^-1: [C][tri(q)] -> the local channel slice's triangles of every block
-        alltoallv(comm->plane, q, xia, mine, pay, st);
-        log("dist_isht", "all_to_all", inv_bytes_a);
-        if (cq > 0) {
-            {
-                ProfScope prof("dist_unpack_cint", st, 4.0 * xia.recv_total() + 4.0 * sht->cint_elems(cq));
-                dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((sht->Lp + 31) / 32),
-                       static_cast<unsigned>(cq));
-                cint_unpack_kernel<<<g, 256, 0, st>>>(reinterpret_cast<const float2*>(pay), cq,
-                                                      static_cast<int>(lay.lmax), static_cast<int>(lay.mmax), sht->Lp,
-                                                      pmap(off_ia), cint);
+        GemmSmCap cap(sm_cap);
+        const int64_t n = static_cast<int64_t>(chunks.size());
+        const int64_t fblk = lay.field_block(q), cblk = 2 * lay.lp[i] * lay.mp[j];
+        rec(e_start, st);
+        wait(cs, e_start);
+        int64_t bytes_a = 0, bytes_b = 0;
+        auto pack_tri = [&](int64_t k) {  // chunk k's rows of the own block -> [C_k][tri] (caller's stream)
+            const ShtChunk& ch = *chunks[k];
+            const int b = k & 1;
+            const int64_t C = ch.lay.C;
+            if (C * lay.lp[i] * lay.mp[j]) {
+                ProfScope prof("dist_pack_tri", st, 8.0 * C * lay.lp[i] * lay.mp[j] + 4.0 * ch.xia.send_total());
+                block_tri_kernel<false><<<dim3(static_cast<unsigned>(lay.lp[i]), static_cast<unsigned>(C)),
+                                          lay.mp[j] > 128 ? 256 : 128, 0, st>>>(
+                    const_cast<float2*>(reinterpret_cast<const float2*>(in + ch.c_begin * cblk)),
+                    at<float2>(w, o_mine[b]), static_cast<int>(lay.lp[i]), static_cast<int>(lay.mp[j]),
+                    static_cast<int>(lay.l0(i)), static_cast<int>(lay.m0(j)), rowoff_me.p, tri_me);
                 SPH_LAUNCH_CHECK();
                 count_launch();
             }
-            sht->inverse(cint, cq, SPH_LAYOUT_INTERNAL, full, w + o_shtws, st);
-            inv_pack.run(full, stage, st, "dist_pack_fields");
+            rec(eP1[b], st);
+        };
+        auto issue_a = [&](int64_t k) {
+            const ShtChunk& ch = *chunks[k];
+            const int b = k & 1;
+            wait(cs, eP1[b]);
+            if (k >= 2) wait(cs, eUC[b]);  // pay[b] consumed by chunk k-2's unpack
+            alltoallv(comm->plane, q, ch.xia, at<float>(w, o_mine[b]), at<float>(w, o_pay[b]), cs);
+            rec(eA1[b], cs);
+            bytes_a += ch.bytes_ia;
+        };
+        pack_tri(0);
+        issue_a(0);
+        for (int64_t k = 0; k < n; ++k) {
+            const ShtChunk& ch = *chunks[k];
+            const int b = k & 1;
+            const int64_t cq = ch.lay.cq(q);
+            if (k + 1 < n) {
+                // mine[(k+1)&1] was sent by chunk k-1's inbound exchange, which the caller's
+                // stream waited for (eA1) before chunk k-1's unpack
+                pack_tri(k + 1);
+                issue_a(k + 1);
+            }
+            wait(st, eA1[b]);
+            if (cq > 0) {
+                {
+                    ProfScope prof("dist_unpack_cint", st, 4.0 * ch.xia.recv_total() + 4.0 * sht->cint_elems(cq));
+                    dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((sht->Lp + 31) / 32),
+                           static_cast<unsigned>(cq));
+                    cint_unpack_kernel<<<g, 256, 0, st>>>(at<const float2>(w, o_pay[b]), cq,
+                                                          static_cast<int>(lay.lmax), static_cast<int>(lay.mmax),
+                                                          sht->Lp, pmap(ch.off_ia), at<float>(w, o_cint));
+                    SPH_LAUNCH_CHECK();
+                    count_launch();
+                }
+                rec(eUC[b], st);
+                sht->inverse(at<float>(w, o_cint), cq, SPH_LAYOUT_INTERNAL, at<float>(w, o_full), w + o_shtws, st);
+                if (k >= 2) wait(st, eB2[b]);  // stage[b] sent by chunk k-2's outbound exchange
+                ch.inv_pack.run(at<float>(w, o_full), at<float>(w, o_stage[b]), st, "dist_pack_fields");
+            } else {
+                rec(eUC[b], st);
+            }
+            rec(eP2[b], st);
+            wait(cs, eP2[b]);
+            alltoallv(comm->plane, q, ch.xib, at<float>(w, o_stage[b]), y + ch.c_begin * fblk, cs);
+            rec(eB2[b], cs);
+            bytes_b += ch.bytes_ib;
         }
-        // B^-1: full fields of the channel slice -> spatial blocks, received in place
-        alltoallv(comm->plane, q, xib, stage, y, st);
-        log("dist_isht", "all_to_all", inv_bytes_b);
+        rec(e_end, cs);
+        wait(st, e_end);
+        log("dist_isht", bytes_a);
+        log("dist_isht", bytes_b);
     }
 };
 
@@ -695,7 +859,12 @@ int sph_comm_create(const void* id, int64_t world, int64_t rank, const int64_t* 
         SPH_NCCL(sph::nccl().CommInitRank(&h->world, static_cast<int>(world), u, static_cast<int>(rank)));
         // plane: same (batch, ensemble); azimuth group: same (batch, ensemble, polar)
         const int plane_color = static_cast<int>(h->coords[0] * sizes[1] + h->coords[1]);
-        SPH_NCCL(sph::nccl().CommSplit(h->world, plane_color, static_cast<int>(h->plane_rank), &h->plane, nullptr));
+        // the plane's all-to-alls run beside compute kernels: bound their CTAs so the
+        // distributed plans can leave exactly that many SMs free (GemmSmCap)
+        if (const char* e = std::getenv("SPH_NCCL_MAX_CTAS")) h->nccl_ctas = std::max(1, std::atoi(e));
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.maxCTAs = h->nccl_ctas;
+        SPH_NCCL(sph::nccl().CommSplit(h->world, plane_color, static_cast<int>(h->plane_rank), &h->plane, &cfg));
         SPH_NCCL(sph::nccl().CommSplit(h->world, static_cast<int>(plane_color * nh + h->coords[2]),
                                static_cast<int>(h->coords[3]), &h->az, nullptr));
         *comm = h.release();

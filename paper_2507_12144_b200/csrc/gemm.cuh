@@ -119,6 +119,19 @@ struct GemmEpi {
 void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStream_t stream,
               const float* Bhi = nullptr, const float* Blo = nullptr, const GemmEpi* epi = nullptr);
 
+// SMs the persistent tcgen05 GEMM may occupy for launches from this thread (0 = all).
+// A scope that runs compute while NCCL kernels progress on another stream caps it, so the
+// communication kernels find SMs: a persistent CTA that waits for an SM would stall its
+// whole static tile stream.
+struct GemmSmCap {
+    int prev;
+    explicit GemmSmCap(int sms);
+    ~GemmSmCap();
+    GemmSmCap(const GemmSmCap&) = delete;
+    GemmSmCap& operator=(const GemmSmCap&) = delete;
+};
+int gemm_sm_cap();
+
 // Host helpers: split fp32 table values into tf32 hi (round-to-nearest) and lo.
 void tf32_split_host(const float* x, size_t n, float* hi, float* lo);
 

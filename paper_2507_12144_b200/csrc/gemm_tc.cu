@@ -1066,6 +1066,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     }
     const GemmTileList& tl = g.tiles_for(CL);
     int gsz = static_cast<int>(std::min<int64_t>(tl.n * CL, grid));
+    if (gemm_sm_cap() > 0) gsz = std::min(gsz, gemm_sm_cap());
     gsz = std::max(CL, gsz / CL * CL);
     ProfScope prof(g.name, st, g.flops);
     cudaLaunchConfig_t cfg{};
@@ -1122,6 +1123,13 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
 }
 
 }  // namespace tc
+
+namespace {
+thread_local int t_sm_cap = 0;
+}
+GemmSmCap::GemmSmCap(int sms) : prev(t_sm_cap) { t_sm_cap = sms; }
+GemmSmCap::~GemmSmCap() { t_sm_cap = prev; }
+int gemm_sm_cap() { return t_sm_cap; }
 
 void gemm_run_simt(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
                    float* D, cudaStream_t st, const GemmEpi& epi);
