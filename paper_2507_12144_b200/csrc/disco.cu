@@ -759,6 +759,23 @@ struct DiscoWs {
     int64_t ldS, u_off, s_off, y_off, whi_off, wlo_off, total;
 };
 // workspace for B samples, input rows nin, output rows nout
+// The tensor core's fp32 accumulation loses precision linearly in the number of k-steps
+// chained into one accumulator (measured at 360x720, 256 -> 256, random weights:
+// relative error 1.6e-5 at c_in*K = 2304, 8.0e-6 at 1152, 4.0e-6 at 576, 2.1e-6 at 288,
+// profiles/disco_ksplit_probe.py).  Mix reductions longer than kchunk run as chunk GEMMs
+// over column slices of S and of the mix table, each writing its own partial spectrum;
+// the C2R adds the partials in fp32 (round to nearest) while it loads them.
+int64_t disco_kchunk() {
+    static const int64_t kc = [] {
+        const char* e = std::getenv("SPH_DISCO_KCHUNK");
+        return e ? std::max<int64_t>(32, std::atoll(e) / 32 * 32) : int64_t{576};
+    }();
+    return kc;
+}
+int64_t disco_nchunks(const DiscoPlan& p, int64_t cin) {
+    return p.prec == SPH_PREC_FP32_SIMT ? 1 : (cin * p.K + disco_kchunk() - 1) / disco_kchunk();
+}
+
 DiscoWs disco_ws(const DiscoPlan& p, int64_t B, int64_t cin, int64_t cout, int64_t nin, int64_t nout) {
     DiscoWs w;
     w.ldS = static_cast<int64_t>(round_up(cin * p.K, 4));
@@ -777,8 +794,8 @@ DiscoWs disco_ws(const DiscoPlan& p, int64_t B, int64_t cin, int64_t cout, int64
         o += round_up(B * nin * p.nbi * cin * 8, 256);
         w.s_off = o;
         o += round_up(B * nout * p.nbo * 2 * w.ldS * 4, 256);
-        w.y_off = o;
-        o += round_up(B * cout * nout * p.nbo * 2 * 4, 256);
+        w.y_off = o;  // one partial spectrum per k chunk
+        o += disco_nchunks(p, cin) * round_up(B * cout * nout * p.nbo * 2 * 4, 256);
     }
     w.total = o + 256;
     return w;
@@ -843,18 +860,10 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
     split_rows(mix, cout, cin * K, w.ldS, whi, wlo, st);
     const bool direct = prec == SPH_PREC_FP32_SIMT;
     const int64_t rows_per_b = direct ? nout * wout : nout * nbo * 2;
-    // The tensor core's fp32 accumulation loses precision linearly in the number of k-steps
-    // chained into one accumulator (measured at 360x720, 256 -> 256, random weights:
-    // relative error 1.6e-5 at c_in*K = 2304, 8.0e-6 at 1152, 4.0e-6 at 576, 2.1e-6 at 288).
-    // Reductions longer than kchunk therefore run as chunk GEMMs whose partial sums are
-    // added in fp32 (round to nearest) by the accumulate epilogue, D = D + acc.
-    static const int64_t kchunk = [] {
-        const char* e = std::getenv("SPH_DISCO_KCHUNK");
-        return e ? std::max<int64_t>(32, std::atoll(e) / 32 * 32) : int64_t{576};
-    }();
+    const int64_t kchunk = disco_kchunk();
     const int64_t Ktot = cin * K;
-    const int64_t nchunks = (prec == SPH_PREC_FP32_SIMT) ? 1 : (Ktot + kchunk - 1) / kchunk;
-    auto make_gemm = [&](int64_t kc, bool chained) {
+    const int64_t nchunks = direct ? 1 : disco_nchunks(*this, cin);
+    auto make_gemm = [&](int64_t kc) {
         auto g = std::make_unique<GroupedGemm>();
         g->A = {nullptr, B * rows_per_b, kc, w.ldS};
         g->Bhi = {nullptr, cout, kc, w.ldS};
@@ -865,11 +874,10 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
             const char* e = std::getenv("SPH_DISCO_ALO");
             return e ? std::atoi(e) : 1;
         }();
-        if (alo_mode == 1 && prec != SPH_PREC_FP32_SIMT && cout <= 128 && !chained) {
+        if (alo_mode == 1 && prec != SPH_PREC_FP32_SIMT && cout <= 128) {
             // BK = 32 kernel: half the k-block rounds of the BK = 16 one at K = cin * 9
             // (decoder 64 -> 64: 4.26 -> 3.23 ms); with two N tiles (cout 256) the
-            // BN = 256 BK = 16 kernel stays faster (1.42 vs 1.63 ms at cfg3).  The chained
-            // accumulate epilogue exists only in the BK = 16 kernel.
+            // BN = 256 BK = 16 kernel stays faster (1.42 vs 1.63 ms at cfg3)
             g->alo = true;
             g->bn = cout <= 64 ? 64 : 128;
         }
@@ -898,37 +906,27 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
         std::lock_guard<std::mutex> lk(mu);
         if (nchunks <= 1) {
             auto& slot = gemm_cache[std::make_tuple(B, cin, cout, nout)];
-            if (!slot) slot = make_gemm(Ktot, false);
+            if (!slot) slot = make_gemm(Ktot);
             gp = slot.get();
         } else {
             for (int64_t k0 = 0; k0 < Ktot; k0 += kchunk) {
                 const int64_t kc = std::min(kchunk, Ktot - k0);
                 auto& slot = gemm_chunk_cache[std::make_tuple(B, cin, cout, nout, k0, kc)];
-                if (!slot) slot = make_gemm(kc, true);
+                if (!slot) slot = make_gemm(kc);
                 chunks.emplace_back(k0, slot.get());
-            }
-            if (ones.n < static_cast<size_t>(cout)) {
-                std::vector<float> h1(cout, 1.f);
-                ones.alloc(cout, false);
-                SPH_CUDA(cudaMemcpy(ones.p, h1.data(), 4 * cout, cudaMemcpyHostToDevice));
-                zeros.alloc(cout, true);
             }
         }
     }
-    // D = A * mix^T over the whole reduction, chained over the k chunks when split
+    // D = A * mix^T; with a k split, chunk c writes partial spectrum c at D + c * dpart
+    const int64_t dpart = static_cast<int64_t>(round_up(B * cout * nout * nbo * 2 * 4, 256)) / 4;
     auto run_mix = [&](const float* A, float* D) {
         if (chunks.empty()) {
             gemm_run(*gp, A, D, prec, st, whi, wlo);
             return;
         }
-        GemmEpi acc;
-        acc.mode = 2;
-        acc.scale = ones.p;
-        acc.bias = zeros.p;
-        acc.res = D;
         for (size_t c = 0; c < chunks.size(); ++c) {
             const int64_t k0 = chunks[c].first;
-            gemm_run(*chunks[c].second, A + k0, D, prec, st, whi + k0, wlo + k0, c ? &acc : nullptr);
+            gemm_run(*chunks[c].second, A + k0, D + c * dpart, prec, st, whi + k0, wlo + k0);
         }
     };
     float* S = reinterpret_cast<float*>(base + w.s_off);
@@ -972,7 +970,7 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
     run_mix(S, Yh);
     fft_inverse_plain(fft_out, reinterpret_cast<const float2*>(Yh), B * cout * nout,
                       static_cast<int>(nbo), static_cast<float>(1.0 / static_cast<double>(win)), y,
-                      st);
+                      st, static_cast<int>(std::max<int64_t>(1, static_cast<int64_t>(chunks.size()))), dpart / 2);
 }
 
 // ------------------------------------------------------------ transpose

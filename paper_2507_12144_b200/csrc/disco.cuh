@@ -61,11 +61,9 @@ struct DiscoPlan {
     std::mutex mu;
     std::map<std::tuple<int64_t, int64_t, int64_t, int64_t>, std::unique_ptr<GroupedGemm>> gemm_cache;
     // k-split of the 3xTF32 mix reduction (c_in * K > kchunk): chunk GEMMs keyed by
-    // (B, cin, cout, nout, k0, kc), chained through the accumulate epilogue; ones / zeros
-    // are its scale / bias vectors
+    // (B, cin, cout, nout, k0, kc), each writing its own partial spectrum
     std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t, int64_t>, std::unique_ptr<GroupedGemm>>
         gemm_chunk_cache;
-    DevBuf<float> ones, zeros;
     std::map<std::tuple<int64_t, int64_t, int64_t>, std::unique_ptr<GroupedGemm>> gemm_t_cache;
     DevBuf<uint8_t> own_ws;
 

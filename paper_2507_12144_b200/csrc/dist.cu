@@ -110,7 +110,7 @@ struct sph_comm_s {
     int64_t rank = 0;
     std::array<int64_t, 4> coords{};
     int64_t plane_rank = 0, plane_size = 1;
-    int nccl_ctas = 16;  // maxCTAs of the plane communicator (SPH_NCCL_MAX_CTAS)
+    int nccl_ctas = 32;  // maxCTAs of the plane communicator (SPH_NCCL_MAX_CTAS)
     ncclComm_t world = nullptr, plane = nullptr, az = nullptr;
     std::mutex mu;
     sph::Traffic log;
@@ -433,7 +433,7 @@ struct sph_dist_sht_plan_s {
         // channel chunks: >= one channel per rank and chunk, SPH_DIST_CHUNKS (default 4)
         static const int64_t want = [] {
             const char* e = std::getenv("SPH_DIST_CHUNKS");
-            return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{4};
+            return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{2};
         }();
         const int64_t nchunk = lay.P == 1 ? 1 : std::max<int64_t>(1, std::min(want, C / lay.P));
         const std::vector<int64_t> csplit = canonical_split(C, nchunk);

@@ -497,6 +497,8 @@ struct PlainInvIO {
     float scale;
     float* rings;
     int dbg = 0;
+    int nparts = 1;            // partial spectra summed on load (DISCO k split)
+    int64_t part_stride = 0;   // float2 between partials
     template <int N1, int N2>
     __device__ __forceinline__ void store_b(int P, int n, int p, int k1, const float2 (&b)[N2]) const {
         const int64_t ra = 2 * (static_cast<int64_t>(blockIdx.x) * P + p), rb = ra + 1;
@@ -523,6 +525,11 @@ struct PlainInvIO {
                 if (k < nbins) {
                     if (ra < nrings) ha = __ldg(bins + ra * nbins + k);
                     if (rb < nrings) hb = __ldg(bins + rb * nbins + k);
+                    for (int q = 1; q < nparts; ++q) {  // k-split partial spectra, fp32 sum
+                        const float2* bq = bins + q * part_stride;
+                        if (ra < nrings) ha = cadd(ha, __ldg(bq + ra * nbins + k));
+                        if (rb < nrings) hb = cadd(hb, __ldg(bq + rb * nbins + k));
+                    }
                 }
             });
     }
@@ -1011,15 +1018,17 @@ void fft_forward_plain(const FftPlan& fp, const float* rings, int64_t nrings, in
 }
 
 void fft_inverse_plain(const FftPlan& fp, const float2* bins, int64_t nrings, int nbins,
-                       float scale, float* rings, cudaStream_t st) {
+                       float scale, float* rings, cudaStream_t st, int nparts, int64_t part_stride) {
     if (nrings == 0) return;
     const int P = rpb_of(fp);
     const int64_t nc = (nrings + 1) / 2;
     const int64_t nblk = (nc + P - 1) / P;
     require(nblk < (1LL << 31), "fft: too many rings");
     PlainInvIO io{bins, nrings, nbins, scale, rings};
+    io.nparts = std::max(1, nparts);
+    io.part_stride = part_stride;
     run_transform<true>(fp, io, dim3(static_cast<unsigned>(nblk)), st, "fft_inv_plain",
-                        4.0 * nrings * (fp.n + 2.0 * nbins));
+                        4.0 * nrings * (fp.n + 2.0 * io.nparts * nbins));
 }
 
 void fft_forward_cminor(const FftPlan& fp, const float* x, int64_t B, int64_t C, int64_t H,

@@ -56,9 +56,11 @@ void fft_forward_plain(const FftPlan& fp, const float* rings, int64_t nrings, in
                        float scale, float2* bins, cudaStream_t st);
 
 // Plain C2R: bins [nrings][nbins] complex half spectra (bins >= nbins are zero,
-// Im of DC / Nyquist ignored) -> rings [nrings][n] real, times `scale`.
+// Im of DC / Nyquist ignored) -> rings [nrings][n] real, times `scale`.  nparts > 1: the
+// spectrum is the fp32 sum of nparts partial spectra part_stride float2 apart (the DISCO
+// mix's k-split partials), added while loading.
 void fft_inverse_plain(const FftPlan& fp, const float2* bins, int64_t nrings, int nbins,
-                       float scale, float* rings, cudaStream_t st);
+                       float scale, float* rings, cudaStream_t st, int nparts = 1, int64_t part_stride = 0);
 
 // Channel-minor forward transform for DISCO: x [B][C][H][n] ->
 // U [B][H][nbins][C] complex (bins m < nbins, unscaled).  planar = 1: real planes
