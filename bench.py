@@ -265,7 +265,8 @@ def workload_config(args):
     if args.workload in ("all", "sht"):
         cfg = dict(SHT_CONFIG, parallelism=f"fields sharded over {args.gpus} GPU(s)")
         if args.workload == "all":
-            cfg["also"] = "disco: configs[2]; domain_decomposed (N>1): configs[4]"
+            cfg["also"] = ("cfg1: configs[0] (CUDA graph); disco: configs[2]; block: configs[3]; "
+                           "domain_decomposed (N>1): configs[4]")
         return cfg
     if args.workload in ("dist_sht", "dist_disco"):
         nh, nw = decomp(args)
@@ -489,6 +490,71 @@ def measure_disco(args, ws, rank, local):
     return rec
 
 
+def measure_cfg1(args, ws, rank, local):
+    """configs[0]: SHT -> ISHT round trip, 91x180 equiangular (lmax 91 / mmax 90), 32
+    fields -- latency-bound, so it runs as ONE CUDA-graph launch (the library's calls are
+    stream-ordered and capture); the eager time is reported beside it."""
+    import torch
+    import paper_2507_12144_b200 as S
+    from paper_2507_12144_b200 import _lib as L
+    dev = torch.device("cuda", local)
+    p = S.ShtPlan(S.build_equiangular(91, 180), 91, 90, "3xtf32", allow_equiangular_forward=True, device=dev)
+    F = 32
+    x = torch.rand((F, 91, 180), device=dev) * 2 - 1
+    c = torch.zeros(p.coeffs_elems(F, L.SPH_LAYOUT_INTERNAL), device=dev)
+    y = torch.empty_like(x)
+    wsb = p.workspace(F)
+    s = torch.cuda.Stream(dev)
+
+    def step():
+        p.forward(x, L.SPH_LAYOUT_INTERNAL, out=c, ws=wsb)
+        p.inverse(c, F, L.SPH_LAYOUT_INTERNAL, out=y, ws=wsb)
+    with torch.cuda.stream(s):
+        eager_ms, _, _, _ = timed(step, 50, 5, ws, local, s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            step()
+        graph_ms, launches, _, clk = timed(g.replay, 50, 5, ws, local, s)
+    return {"workload": "configs[0]: SHT->ISHT round trip, 91x180 equiangular (lmax=91, mmax=90), 32 fields",
+            "value": ws * F / (graph_ms / 1e3), "unit": "fields/s", "ms_per_step": graph_ms,
+            "eager_ms_per_step": eager_ms, "launch": "one CUDA graph replay per step (4 library kernels)",
+            "clocks": clk}
+
+
+def measure_block(args, ws, rank, local):
+    """configs[3]: one global block (SHT -> spectral channel mix -> ISHT -> GeLU/MLP
+    epilogue) + one local block (DISCO 360x720 -> 360x720 -> MLP epilogue), 256 channels,
+    MLP hidden 512, batch 1."""
+    import torch
+    import paper_2507_12144_b200 as S
+    dev = torch.device("cuda", local)
+    g = S.build_gaussian(360, 720)
+    C, H, B = 256, 512, 1
+    lat = S.SphericalField(g, torch.rand((B, C, 360, 720), device=dev) * 2 - 1)
+    cond = S.SphericalField(g, torch.empty((B, 0, 360, 720), device=dev))
+    sc = 1.0 / math.sqrt(C)
+
+    def wts(conv):
+        return S.BlockWeights(global_=conv.shape[2] != 9, conv=conv,
+                              w1=(torch.rand((H, C), device=dev) * 2 - 1) * sc,
+                              b1=torch.rand(H, device=dev) * 0.1,
+                              w2=(torch.rand((C, H), device=dev) * 2 - 1) / math.sqrt(H),
+                              b2=torch.rand(C, device=dev) * 0.1, scales=torch.full((C,), 0.1, device=dev))
+    bw_g = wts((torch.rand((C, C, 360), device=dev) * 2 - 1) * sc)
+    block_op = S.DiscoOperator(g, g, S.morlet_basis(3 * math.pi / 360), device=dev)
+    bw_l = wts((torch.rand((C, C, block_op.n_basis), device=dev) * 2 - 1) * sc / 3)
+
+    def step():
+        S.block_apply(lat, cond, bw_g)
+        S.block_apply(lat, cond, bw_l, block_op)
+    ms, launches, prof, clk = timed(step, max(5, args.steps // 2), args.warmup, ws, local,
+                                    torch.cuda.current_stream(dev))
+    return {"workload": "configs[3]: global + local block pair at 360x720 Gaussian, 256 channels, MLP hidden 512, "
+                        "batch 1", "value": ws * B * C / (ms / 1e3), "unit": "fields/s (block-pair outputs)",
+            "ms_per_step": ms, "gpu_launches": launches, "clocks": clk,
+            "per_kernel_ms": {k: v[1] / max(5, args.steps // 2) for k, v in sorted(prof.items())}}
+
+
 def measure_domain_decomposed(args, ws, rank, local, nh, nw, steps):
     """configs[4] through the library's NCCL path: distributed SHT + inverse SHT round trip
     and distributed DISCO (721x1440 -> 360x720 Gaussian), 512 channels, batch 1.  The same
@@ -581,6 +647,8 @@ def run_all(args, ws, rank, local):
     """The default line: configs[1] SHT (value), configs[2] DISCO, configs[4] (N > 1)."""
     sht = measure_sht(args, ws, rank, local)
     disco = measure_disco(args, ws, rank, local)
+    cfg1 = measure_cfg1(args, ws, rank, local)
+    block = measure_block(args, ws, rank, local)
     dd = measure_domain_decomposed(args, ws, rank, local, ws, 1, max(5, args.steps // 2)) if ws > 1 else None
     cpu = dcpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -600,7 +668,8 @@ def run_all(args, ws, rank, local):
                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
                "roofline": sht["roofline"], "cpu_baseline": cpu, "e2e": sht["e2e"],
-               "gpu_launches": sht["gpu_launches"], "clocks": sht["clocks"], "disco": disco}
+               "gpu_launches": sht["gpu_launches"], "clocks": sht["clocks"], "disco": disco,
+               "cfg1": cfg1, "block": block}
         if dd is not None:
             out["domain_decomposed"] = dd
         print(json.dumps(out), flush=True)
