@@ -46,6 +46,15 @@ class OracleBackend:
                 out[c, h, :, 0], out[c, h, :, 1] = b.real, b.imag
         return torch.from_numpy(out)
 
+    def sht_full(self, grid, lmax, mmax, x):
+        """The fused order's per-rank transform (dist.py: _dist_sht_fused): all latitudes
+        and longitudes of the rank's channel slice -> [C, lmax, mmax, 2], the reference's
+        Alg. 1 arithmetic on one rank (dist_sht_forward 1x1 == the C restatement)."""
+        xn = x.numpy()
+        c = oracle.orc().sht_forward(grid.kind, grid.nlat, grid.nlon, lmax, mmax, xn) if xn.shape[0] else \
+            np.zeros((0, lmax, mmax), complex)
+        return torch.from_numpy(np.stack([c.real, c.imag], -1))
+
     def legendre_stage(self, grid, lmax, mmax, bins, m0):
         o = oracle.orc()
         colat, w = o.grid(grid.kind, grid.nlat, grid.nlon)
@@ -186,7 +195,7 @@ def main():
     else:
         grid, backend = _Grid(1, 16, 32), OracleBackend()
     x = torch.tensor(oracle.random_field((3, 16, 32), 30), dtype=dt, device=dev)
-    out = D.dist_sht_forward(ctx, D.shard_field(ctx, x), grid, 16, 16, backend)
+    out = D.dist_sht_forward(ctx, D.shard_field(ctx, x), grid, 16, 16, backend, order="reference")
     glob = D.unshard(ctx, out).cpu().numpy()
     got = glob[..., 0] + 1j * glob[..., 1]
     key = f"dist_sht_{args.nh}x{args.nw}"
@@ -197,14 +206,14 @@ def main():
     if key + "_csv" in G.files:
         rep["ref_sht_csv"] = str(G[key + "_csv"])
 
-    # ---- fused order pipelined over 3 channel chunks (GPU backend only)
-    if cuda:
-        x = torch.tensor(oracle.random_field((7, 16, 32), 36), dtype=dt, device=dev)
-        out = D.dist_sht_forward(ctx, D.shard_field(ctx, x), grid, 16, 16, backend, chunks=3)
-        glob = D.unshard(ctx, out).cpu().numpy()
-        got = glob[..., 0] + 1j * glob[..., 1]
-        want = oracle.orc().sht_forward(1, 16, 32, 16, 16, x.cpu().numpy())
-        rep["sht_chunked_err"] = float(np.abs(got - want).max() / np.abs(want).max())
+    # ---- fused order (T1, T3', per-rank SHT, T4', T2'), pipelined over 3 channel chunks,
+    # on both backends: the oracle's sht_full makes the order testable over gloo
+    x = torch.tensor(oracle.random_field((7, 16, 32), 36), dtype=dt, device=dev)
+    out = D.dist_sht_forward(ctx, D.shard_field(ctx, x), grid, 16, 16, backend, chunks=3)
+    glob = D.unshard(ctx, out).cpu().numpy()
+    got = glob[..., 0] + 1j * glob[..., 1]
+    want = oracle.orc().sht_forward(1, 16, 32, 16, 16, x.cpu().numpy())
+    rep["sht_chunked_err"] = float(np.abs(got - want).max() / np.abs(want).max())
 
     # ---- equiangular 91x180 (cfg1 grid) dist SHT vs the oracle (reference equiangular path)
     if cuda:
