@@ -369,6 +369,24 @@ def roofline(prof, steps, ms, traffic_key=None):
     except Exception:
         pass
     roof["per_kernel_ms"] = {k: v[1] / steps for k, v in sorted(prof.items())}
+    # every kernel of the step against its own bound (north_star: tensor-pipe fraction for
+    # the GEMMs, HBM fraction for the FFT / DISCO kernels), from the same live timings
+    per = {}
+    for k, (n, t_ms, w) in sorted(prof.items()):
+        if n == 0 or t_ms <= 0 or w <= 0:
+            continue
+        if k.startswith("gemm"):
+            a = w / (t_ms / 1e3) / 1e12
+            per[k] = {"bound": "tensor", "achieved_TFLOPs": a, "frac": a / (bf16 / 2 / 3)}
+        else:
+            a = w / (t_ms / 1e3) / 1e9
+            per[k] = {"bound": "hbm", "achieved_GBps": a, "frac": a / hbm}
+    roof["per_kernel"] = per
+    try:  # ncu counters of the same kernels (committed capture, profiles/capture_r2.sh)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_sht.json")) as f:
+            roof["ncu_tensor_pipe_active_pct"] = json.load(f).get("tensor_pipe_active_pct")
+    except Exception:
+        pass
     return roof
 
 
@@ -410,7 +428,22 @@ def measure_sht(args, ws, rank, local):
                       "buffers)", "chunk_fields": args.chunk}
         del xh, yh
     rec["e2e"] = e2e
-    del x, y, cint, wsb
+    # the same round trip through the REFERENCE coefficient layout ([F][lmax][mmax]
+    # complex64, zeros above the diagonal) -- what a drop-in caller of sht_forward /
+    # sht_inverse pays: the GEMM-native layout's conversions included
+    del cint
+    dense = torch.empty((F, LMAX, MMAX, 2), device=dev)
+
+    def step_dense():
+        plan.forward(x, L.SPH_LAYOUT_DENSE_LM, out=dense, ws=wsb)
+        plan.inverse(dense, F, L.SPH_LAYOUT_DENSE_LM, out=y, ws=wsb)
+    ms_d, launches_d, prof_d, _ = timed(step_dense, max(5, args.steps // 2), args.warmup, ws, local,
+                                        torch.cuda.current_stream(dev))
+    rec["reference_layout"] = {"value": ws * F / (ms_d / 1e3), "unit": UNIT, "ms_per_step": ms_d,
+                               "gpu_launches": launches_d,
+                               "per_kernel_ms": {k: v[1] / max(5, args.steps // 2) for k, v in sorted(prof_d.items())},
+                               "api": "sph_sht_forward / sph_sht_inverse with SPH_LAYOUT_DENSE_LM"}
+    del x, y, dense, wsb
     return rec
 
 
@@ -668,7 +701,8 @@ def run_all(args, ws, rank, local):
                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
                "roofline": sht["roofline"], "cpu_baseline": cpu, "e2e": sht["e2e"],
-               "gpu_launches": sht["gpu_launches"], "clocks": sht["clocks"], "disco": disco,
+               "gpu_launches": sht["gpu_launches"], "clocks": sht["clocks"],
+               "reference_layout": sht["reference_layout"], "disco": disco,
                "cfg1": cfg1, "block": block}
         if dd is not None:
             out["domain_decomposed"] = dd

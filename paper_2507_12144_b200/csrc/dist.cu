@@ -192,67 +192,84 @@ __device__ __forceinline__ void stage_rowbase(int64_t* base, const PayloadMap& p
     }
 }
 
+// Degree rows of a tile are stored split by parity (srow = (dl & 1) * DL/2 + dl / 2) so a
+// warp walking one C_int row (every other degree) hits consecutive shared-memory rows --
+// the layout of sht.cu's cint_to_dense / dense_to_cint.
+template <int DL>
+__device__ __forceinline__ int srow_of(int dl) {
+    return (dl & 1) * (DL / 2) + (dl >> 1);
+}
+
 // forward B pack: the local SHT's C_int [(m*2+p)][2F][Lp] (l = m + p + 2 lp) -> triangular
-// payloads of every destination block.  Tiled transpose as cint_to_dense (sht.cu): cint
-// read in lp runs, payload written in m runs.
-template <int LT>
+// payloads of every destination block.  CTA (32 orders, 64 degrees, field f): C_int rows
+// read as 32-lane lp runs, payload written in order runs.
+template <int DL>
 __global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict__ cint, int64_t F, int lmax, int mmax,
                                                         int Lp, PayloadMap pm, float2* __restrict__ payload) {
-    __shared__ float2 tile[LT][33];
-    __shared__ int64_t base[LT * kMaxNw];
-    const int mt = blockIdx.x * 32, lt = blockIdx.y * LT;
-    if (mt > lt + LT - 1) return;  // tile entirely above the diagonal (m > l)
+    __shared__ float tre[DL][33], tim[DL][33];
+    __shared__ int64_t base[DL * kMaxNw];
+    const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;
+    if (mt > lt + DL - 1) return;  // tile entirely above the diagonal (m > l)
     const int64_t f = blockIdx.z;
     int jlo, nj;
-    stage_rowbase(base, pm, f, lt, LT, lmax, mt, mmax, jlo, nj);
-    constexpr int NLP = LT / 2 + 1;
-    for (int e = threadIdx.x; e < 32 * 2 * 2 * NLP; e += blockDim.x) {
-        const int lpl = e % NLP, r = e / NLP;
-        const int ri = r & 1, p = (r >> 1) & 1, mlt = r >> 2;
+    stage_rowbase(base, pm, f, lt, DL, lmax, mt, mmax, jlo, nj);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < 128; r += 8) {
+        const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
         const int m = mt + mlt;
         if (m >= mmax) continue;
         const int d = lt - m - p;
-        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lpl;
+        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
         const int l = m + p + 2 * lp;
-        if (lp >= Lp || l >= lmax || l >= lt + LT) continue;
-        const int64_t row = (static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri;
-        reinterpret_cast<float*>(&tile[l - lt][mlt])[ri] = cint[row * Lp + lp];
+        if (lp >= Lp || l >= lmax || l >= lt + DL) continue;
+        const float v = cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp];
+        const int sr = srow_of<DL>(l - lt);
+        if (ri) tim[sr][mlt] = v;
+        else tre[sr][mlt] = v;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < LT * 32; e += blockDim.x) {
-        const int ll = e >> 5, mlt = e & 31;
-        const int l = lt + ll, m = mt + mlt;
+    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
+        const int dl = e >> 5, mlt = e & 31;
+        const int l = lt + dl, m = mt + mlt;
+        const int sr = srow_of<DL>(dl);
         if (l < lmax && m < mmax && m <= l)
-            payload[base[ll * kMaxNw + pm.mmap[m].x - jlo] + m] = tile[ll][mlt];
+            payload[base[dl * kMaxNw + pm.mmap[m].x - jlo] + m] = make_float2(tre[sr][mlt], tim[sr][mlt]);
     }
 }
 
 // inverse A^-1 unpack: triangular payloads of every source block -> C_int of the local
-// fields (zeros beyond lmax inside the padded lp range), as dense_to_cint (sht.cu).
+// fields (zeros beyond lmax inside the padded lp range: the inverse GEMM's K tail
+// multiplies them).  CTA (32 orders, 32 lp, field f): the 96 degrees of the tile loaded
+// in order runs, C_int rows written as 32-lane lp runs.
 __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restrict__ payload, int64_t F, int lmax,
                                                           int mmax, int Lp, PayloadMap pm, float* __restrict__ cint) {
-    __shared__ float2 tile[96][33];
-    __shared__ int64_t base[96 * kMaxNw];
+    constexpr int DL = 96;
+    __shared__ float tre[DL][33], tim[DL][33];
+    __shared__ int64_t base[DL * kMaxNw];
     const int mt = blockIdx.x * 32, lpt = blockIdx.y * 32;
     const int64_t f = blockIdx.z;
     const int lbase = mt + 2 * lpt;
     int jlo, nj;
-    stage_rowbase(base, pm, f, lbase, 96, lmax, mt, mmax, jlo, nj);
+    stage_rowbase(base, pm, f, lbase, DL, lmax, mt, mmax, jlo, nj);
     __syncthreads();
-    for (int e = threadIdx.x; e < 96 * 32; e += blockDim.x) {
-        const int ll = e >> 5, mlt = e & 31;
-        const int l = lbase + ll, m = mt + mlt;
-        tile[ll][mlt] = (l < lmax && m < mmax && m <= l) ? payload[base[ll * kMaxNw + pm.mmap[m].x - jlo] + m]
+    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
+        const int dl = e >> 5, mlt = e & 31;
+        const int l = lbase + dl, m = mt + mlt;
+        const float2 v = (l < lmax && m < mmax && m <= l) ? payload[base[dl * kMaxNw + pm.mmap[m].x - jlo] + m]
                                                           : make_float2(0.f, 0.f);
+        const int sr = srow_of<DL>(dl);
+        tre[sr][mlt] = v.x;
+        tim[sr][mlt] = v.y;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < 32 * 2 * 2 * 32; e += blockDim.x) {
-        const int lpl = e & 31, r = e >> 5;
-        const int ri = r & 1, p = (r >> 1) & 1, mlt = r >> 2;
-        const int m = mt + mlt, lp = lpt + lpl;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < 128; r += 8) {
+        const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
+        const int m = mt + mlt, lp = lpt + lane;
         if (m >= mmax || lp >= Lp) continue;
         const int l = m + p + 2 * lp;
-        const float v = l < lmax ? reinterpret_cast<const float*>(&tile[mlt + p + 2 * lpl][mlt])[ri] : 0.f;
+        const int sr = srow_of<DL>(mlt + p + 2 * lane);
+        const float v = l < lmax ? (ri ? tim[sr][mlt] : tre[sr][mlt]) : 0.f;
         cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp] = v;
     }
 }

@@ -121,65 +121,87 @@ void upload(DevBuf<T>& d, const std::vector<T>& h) {
 // ---------------------------------------------------------------- kernels
 // Internal coefficient layout cint[(ml*2 + p)][2F (f, re/im)][Lp] (l = m + p + 2 lp,
 // lp contiguous) <-> dense [F][lmax][mcols] complex (m contiguous): tiled transposes
-// through shared memory so both sides are read / written in contiguous runs (the
-// element-wise form read cint with a stride of 2F*Lp floats: 3 ms at 512 x 721 x 720).
-// CTA (32 orders, 64 degrees, field f): the (m, p, re/im) rows are read as 33-lane runs
-// of lp covering the tile's degrees, the dense rows written as 32-order runs.
-template <int LT>
-__global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int64_t lmax,
-                                                            int64_t m0, int64_t mcount, int64_t out_mcount, int Lp,
+// through shared memory, both global sides in contiguous runs.  A (order, parity, re/im)
+// row of cint covers every OTHER degree, so the tile stores degree rows split by parity
+// (srow = (dl & 1) * half + dl / 2): a warp walking one cint row then touches consecutive
+// smem rows (stride 33 words -> conflict-free), and a dense row is one smem row.
+// (Round 1 interleaved the degrees: rows two apart put a warp's stores on 8 banks.)
+template <int DL>
+__device__ __forceinline__ int srow_of(int dl) {
+    return (dl & 1) * (DL / 2) + (dl >> 1);
+}
+
+// CTA (32 orders, 64 degrees, field f): 128 cint rows (order, parity, re/im) read as
+// 32-lane runs of lp (each run is the tile's 32 degrees of that parity class), dense rows
+// written as 32-order float2 runs (zeros above the diagonal).
+__global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int lmax,
+                                                            int m0, int mcount, int out_mcount, int Lp,
                                                             float2* __restrict__ dense, int64_t f0) {
-    __shared__ float2 tile[LT][33];
-    const int mt = blockIdx.x * 32, lt = blockIdx.y * LT;
+    constexpr int DL = 64;
+    __shared__ float tre[DL][33], tim[DL][33];
+    const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;
     const int64_t f = f0 + blockIdx.z;
-    for (int e = threadIdx.x; e < LT * 32; e += blockDim.x) tile[e >> 5][e & 31] = make_float2(0.f, 0.f);
-    __syncthreads();
-    constexpr int NLP = LT / 2 + 1;
-    for (int e = threadIdx.x; e < 32 * 2 * 2 * NLP; e += blockDim.x) {
-        const int lpl = e % NLP, r = e / NLP;
-        const int ri = r & 1, p = (r >> 1) & 1, mlt = r >> 2;
-        const int ml = mt + mlt;
-        if (ml >= mcount) continue;
-        const int m = static_cast<int>(m0) + ml;
-        const int d = lt - m - p;
-        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lpl;
-        const int l = m + p + 2 * lp;
-        if (lp >= Lp || l >= lmax || l >= lt + LT) continue;
-        const int64_t row = (static_cast<int64_t>(ml) * 2 + p) * 2 * F + 2 * f + ri;
-        reinterpret_cast<float*>(&tile[l - lt][mlt])[ri] = cint[row * Lp + lp];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
+        tre[e >> 5][e & 31] = 0.f;
+        tim[e >> 5][e & 31] = 0.f;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < LT * 32; e += blockDim.x) {
-        const int ll = e >> 5, mlt = e & 31;
-        const int64_t l = lt + ll;
+    if (m0 + mt <= lt + DL - 1) {  // else the whole tile is above the diagonal (m > l)
+        for (int r = warp; r < 128; r += 8) {
+            const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
+            const int ml = mt + mlt;
+            if (ml >= mcount) continue;
+            const int m = m0 + ml;
+            const int d = lt - m - p;
+            const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
+            const int l = m + p + 2 * lp;
+            if (lp >= Lp || l >= lmax || l >= lt + DL) continue;
+            const float v = cint[((static_cast<int64_t>(ml) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp];
+            const int sr = srow_of<DL>(l - lt);
+            if (ri) tim[sr][mlt] = v;
+            else tre[sr][mlt] = v;
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
+        const int dl = e >> 5, mlt = e & 31;
+        const int64_t l = lt + dl;
         const int oc = mt + mlt;
-        if (l < lmax && oc < out_mcount) dense[(f * lmax + l) * out_mcount + oc] = tile[ll][mlt];
+        const int sr = srow_of<DL>(dl);
+        if (l < lmax && oc < out_mcount) dense[(f * lmax + l) * out_mcount + oc] = make_float2(tre[sr][mlt], tim[sr][mlt]);
     }
 }
 
 // CTA (32 orders, 32 lp, field f): the degrees l = m + p + 2 lp of the tile span 96 dense
-// rows, loaded as 32-order runs; the cint rows are written as 32-lp runs.
+// rows, loaded as 32-order runs; the cint rows are written as 32-lp runs (zeros beyond
+// lmax inside the padded lp range: the inverse GEMM's K tail multiplies them).
 __global__ void __launch_bounds__(256) dense_to_cint_kernel(const float2* __restrict__ dense, int64_t F, int64_t lmax,
                                                             int64_t mmax, int Lp, float* __restrict__ cint,
                                                             int64_t f0) {
-    __shared__ float2 tile[96][33];
+    constexpr int DL = 96;
+    __shared__ float tre[DL][33], tim[DL][33];
     const int mt = blockIdx.x * 32, lpt = blockIdx.y * 32;
     const int64_t f = f0 + blockIdx.z;
     const int lbase = mt + 2 * lpt;
-    for (int e = threadIdx.x; e < 96 * 32; e += blockDim.x) {
-        const int ll = e >> 5, mlt = e & 31;
-        const int64_t l = lbase + ll;
+    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
+        const int dl = e >> 5, mlt = e & 31;
+        const int64_t l = lbase + dl;
         const int m = mt + mlt;
-        tile[ll][mlt] = (l < lmax && m < mmax) ? dense[(f * lmax + l) * mmax + m] : make_float2(0.f, 0.f);
+        const float2 v = (l < lmax && m < mmax) ? dense[(f * lmax + l) * mmax + m] : make_float2(0.f, 0.f);
+        const int sr = srow_of<DL>(dl);
+        tre[sr][mlt] = v.x;
+        tim[sr][mlt] = v.y;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < 32 * 2 * 2 * 32; e += blockDim.x) {
-        const int lpl = e & 31, r = e >> 5;
-        const int ri = r & 1, p = (r >> 1) & 1, mlt = r >> 2;
-        const int m = mt + mlt, lp = lpt + lpl;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < 128; r += 8) {
+        const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
+        const int m = mt + mlt, lp = lpt + lane;
         if (m >= mmax || lp >= Lp) continue;
         const int l = m + p + 2 * lp;
-        const float v = l < lmax ? reinterpret_cast<const float*>(&tile[mlt + p + 2 * lpl][mlt])[ri] : 0.f;
+        const int sr = srow_of<DL>(mlt + p + 2 * lane);
+        const float v = l < lmax ? (ri ? tim[sr][mlt] : tre[sr][mlt]) : 0.f;
         cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp] = v;
     }
 }
@@ -214,13 +236,15 @@ __global__ void fold_bins_kernel(const float2* __restrict__ bins, const int2* __
 void cint_to_dense(const ShtPlan& p, const float* cint, int64_t F, int64_t m0, int64_t mcount,
                    int64_t out_mcount, float* dense, cudaStream_t st) {
     if (F * p.lmax * out_mcount == 0) return;
-    ProfScope prof("sht_to_dense", st, 16.0 * F * p.lmax * out_mcount);
+    double pairs = 0;  // stored (l, m) entries read from cint
+    for (int64_t ml = 0; ml < mcount; ++ml) pairs += static_cast<double>(std::max<int64_t>(0, p.lmax - (m0 + ml)));
+    ProfScope prof("sht_to_dense", st, 8.0 * F * p.lmax * out_mcount + 8.0 * F * pairs);
     for (int64_t f0 = 0; f0 < F; f0 += 65535) {
-        constexpr int LT = 128;
-        dim3 grid(static_cast<unsigned>((out_mcount + 31) / 32), static_cast<unsigned>((p.lmax + LT - 1) / LT),
+        dim3 grid(static_cast<unsigned>((out_mcount + 31) / 32), static_cast<unsigned>((p.lmax + 63) / 64),
                   static_cast<unsigned>(std::min<int64_t>(65535, F - f0)));
-        cint_to_dense_kernel<LT><<<grid, 256, 0, st>>>(cint, F, p.lmax, m0, mcount, out_mcount, p.Lp,
-                                                       reinterpret_cast<float2*>(dense), f0);
+        cint_to_dense_kernel<<<grid, 256, 0, st>>>(cint, F, static_cast<int>(p.lmax), static_cast<int>(m0),
+                                                   static_cast<int>(mcount), static_cast<int>(out_mcount), p.Lp,
+                                                   reinterpret_cast<float2*>(dense), f0);
         SPH_LAUNCH_CHECK();
         count_launch();
     }
