@@ -228,34 +228,38 @@ __global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict_
         else tre[sr][mlt] = v;
     }
     __syncthreads();
+    const int mme = mt + (threadIdx.x & 31);  // this thread's order (blockDim % 32 == 0)
+    const int jme = mme < mmax ? pm.mmap[mme].x - jlo : 0;
     for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
         const int dl = e >> 5, mlt = e & 31;
         const int l = lt + dl, m = mt + mlt;
         const int sr = srow_of<DL>(dl);
         if (l < lmax && m < mmax && m <= l)
-            payload[base[dl * kMaxNw + pm.mmap[m].x - jlo] + m] = make_float2(tre[sr][mlt], tim[sr][mlt]);
+            payload[base[dl * kMaxNw + jme] + m] = make_float2(tre[sr][mlt], tim[sr][mlt]);
     }
 }
 
 // inverse A^-1 unpack: triangular payloads of every source block -> C_int of the local
-// fields (zeros beyond lmax inside the padded lp range: the inverse GEMM's K tail
-// multiplies them).  CTA (32 orders, 32 lp, field f): the 96 degrees of the tile loaded
-// in order runs, C_int rows written as 32-lane lp runs.
+// fields.  CTA (32 orders, 64 degrees, field f): the tile's payload entries loaded once in
+// order runs, each (order, parity, re/im) C_int row's 32 lp of the tile written as one
+// run; degree tiles run to lmax + 63 so every lp the inverse GEMM reads (L(m, p) rounded
+// to its 32-wide k-block) is written, zeros beyond lmax.
 __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restrict__ payload, int64_t F, int lmax,
                                                           int mmax, int Lp, PayloadMap pm, float* __restrict__ cint) {
-    constexpr int DL = 96;
+    constexpr int DL = 64;
     __shared__ float tre[DL][33], tim[DL][33];
     __shared__ int64_t base[DL * kMaxNw];
-    const int mt = blockIdx.x * 32, lpt = blockIdx.y * 32;
+    const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;
     const int64_t f = blockIdx.z;
-    const int lbase = mt + 2 * lpt;
     int jlo, nj;
-    stage_rowbase(base, pm, f, lbase, DL, lmax, mt, mmax, jlo, nj);
+    stage_rowbase(base, pm, f, lt, DL, lmax, mt, mmax, jlo, nj);
     __syncthreads();
+    const int mme = mt + (threadIdx.x & 31);  // this thread's order (blockDim % 32 == 0)
+    const int jme = mme < mmax ? pm.mmap[mme].x - jlo : 0;
     for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
         const int dl = e >> 5, mlt = e & 31;
-        const int l = lbase + dl, m = mt + mlt;
-        const float2 v = (l < lmax && m < mmax && m <= l) ? payload[base[dl * kMaxNw + pm.mmap[m].x - jlo] + m]
+        const int l = lt + dl, m = mt + mlt;
+        const float2 v = (l < lmax && m < mmax && m <= l) ? payload[base[dl * kMaxNw + jme] + m]
                                                           : make_float2(0.f, 0.f);
         const int sr = srow_of<DL>(dl);
         tre[sr][mlt] = v.x;
@@ -265,10 +269,15 @@ __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restri
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int r = warp; r < 128; r += 8) {
         const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
-        const int m = mt + mlt, lp = lpt + lane;
-        if (m >= mmax || lp >= Lp) continue;
+        const int m = mt + mlt;
+        if (m >= mmax) continue;
+        const int d = lt - m - p;
+        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
         const int l = m + p + 2 * lp;
-        const int sr = srow_of<DL>(mlt + p + 2 * lane);
+        const int n = lmax - m;
+        const int Lmp = n <= 0 ? 0 : (p == 0 ? (n + 1) / 2 : n / 2);
+        if (l >= lt + DL || lp >= Lp || lp >= ((Lmp + 31) & ~31)) continue;
+        const int sr = srow_of<DL>(l - lt);
         const float v = l < lmax ? (ri ? tim[sr][mlt] : tre[sr][mlt]) : 0.f;
         cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp] = v;
     }
@@ -698,7 +707,7 @@ struct sph_dist_sht_plan_s {
             if (cq > 0) {
                 {
                     ProfScope prof("dist_unpack_cint", st, 4.0 * ch.xia.recv_total() + 4.0 * sht->cint_elems(cq));
-                    dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((sht->Lp + 31) / 32),
+                    dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((lay.lmax + 63 + 63) / 64),
                            static_cast<unsigned>(cq));
                     cint_unpack_kernel<<<g, 256, 0, st>>>(at<const float2>(w, o_pay[b]), cq,
                                                           static_cast<int>(lay.lmax), static_cast<int>(lay.mmax),
