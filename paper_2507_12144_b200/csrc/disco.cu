@@ -614,6 +614,116 @@ __global__ void __launch_bounds__(256) disco_band_t2_kernel(
     }
 }
 
+// Even channel counts: disco_band_t2_kernel with a channel PAIR per thread accumulated in
+// packed fp32x2 registers (FFMA2 with the staged psi value as the broadcast scalar): per
+// (output row, input row) 9 broadcast LDS.64 feed 18 FFMA2 for two channels instead of
+// 9 LDS + 36 FFMA for one.  The pair's 2 x 9 S values per re/im row are one contiguous
+// 72-byte run, loaded as 9 LDG.64.  threads = 4 orders x 32 lanes, 64 channels per pass.
+__global__ void __launch_bounds__(128) disco_band_t3_kernel(
+    const float* __restrict__ S, const float2* __restrict__ psi_t, const int32_t* __restrict__ band0,
+    const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, const int32_t* __restrict__ tt_ptr,
+    const int32_t* __restrict__ tt_h, int64_t Hin, int64_t nbi, int64_t Hout, int64_t nbo, int wout, int K,
+    int64_t C, int64_t ldS, float2* __restrict__ Ut, int64_t B) {
+    extern __shared__ float2 psm[];
+    __shared__ int s_q0[TB_MAXH + 1], s_lo[TB_MAXH], s_hi[TB_MAXH];
+    const int mi = threadIdx.x / 32, cl = threadIdx.x % 32;
+    const int64_t mbase = static_cast<int64_t>(blockIdx.x) * 4;
+    const int64_t m = mbase + mi;
+    const int r0 = blockIdx.y * TB_RT;
+    const int nr = min(TB_RT, static_cast<int>(Hin) - r0);
+    const int t0 = tt_ptr[blockIdx.y], nt = tt_ptr[blockIdx.y + 1] - t0;
+    if (threadIdx.x == 0) {
+        int q = 0;
+        for (int t = 0; t < nt; ++t) {
+            const int h = tt_h[t0 + t];
+            const int lo = max(band0[h], r0), hi = min(band0[h] + bandc[h], r0 + nr);
+            s_q0[t] = q;
+            s_lo[t] = lo;
+            s_hi[t] = hi;
+            q += max(0, hi - lo);
+        }
+        s_q0[nt] = q;
+    }
+    __syncthreads();
+    const int nm = static_cast<int>(nbi - mbase < 4 ? nbi - mbase : 4);
+    for (int t = 0; t < nt; ++t) {
+        const int h = tt_h[t0 + t];
+        const int lo = s_lo[t], n = s_hi[t] - lo;
+        if (n <= 0) continue;
+        const float2* src = psi_t + (psi_off[h] + (lo - band0[h])) * nbi * K + mbase * K;
+        for (int e = threadIdx.x; e < n * 4 * K; e += blockDim.x) {
+            const int rr = e / (4 * K), rem = e - rr * 4 * K;
+            const int mm = rem / K, k = rem - mm * K;
+            psm[((s_q0[t] + rr) * 4 + mm) * 9 + k] =
+                mm < nm ? __ldg(src + static_cast<int64_t>(rr) * nbi * K + rem) : make_float2(0.f, 0.f);
+        }
+    }
+    __syncthreads();
+    if (m >= nbi) return;
+    const int half = wout / 2;
+    const int mo = static_cast<int>(m % wout);
+    const bool cj = mo > half;
+    const int mp = cj ? wout - mo : mo;
+    const float sg = cj ? -1.f : 1.f;
+    for (int64_t b = 0; b < B; ++b) {
+        const float* Sb = S + b * Hout * nbo * 2 * ldS;
+        for (int64_t c0 = 0; c0 < C; c0 += 64) {
+            const int64_t c = c0 + 2 * cl;
+            if (c >= C) break;
+            // acc[i] = (re c, re c+1), acc[TB_RT + i] = (im c, im c+1) of input row r0 + i
+            float2 are[TB_RT], aim[TB_RT];
+#pragma unroll
+            for (int i = 0; i < TB_RT; ++i) are[i] = aim[i] = make_float2(0.f, 0.f);
+            for (int t = 0; t < nt; ++t) {
+                const int h = tt_h[t0 + t];
+                const int lo = s_lo[t], hi = s_hi[t];
+                if (hi <= lo) continue;
+                const float2* sr = reinterpret_cast<const float2*>(Sb + (static_cast<int64_t>(h) * nbo + mp) * 2 * ldS + c * 9);
+                const float2* si = reinterpret_cast<const float2*>(reinterpret_cast<const float*>(sr) + ldS);
+                float vr[18], vi[18];
+#pragma unroll
+                for (int j = 0; j < 9; ++j) {
+                    const float2 a = __ldg(sr + j), bq = __ldg(si + j);
+                    vr[2 * j] = a.x;
+                    vr[2 * j + 1] = a.y;
+                    vi[2 * j] = sg * bq.x;
+                    vi[2 * j + 1] = sg * bq.y;
+                }
+                float2 xr[9], xi[9];  // (channel c, channel c+1) per basis function
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    xr[k] = make_float2(vr[k], vr[9 + k]);
+                    xi[k] = make_float2(vi[k], vi[9 + k]);
+                }
+                const float2* pq = psm + (s_q0[t] - lo + r0) * 36 + mi * 9;
+#pragma unroll
+                for (int i = 0; i < TB_RT; ++i) {
+                    const int r = r0 + i;
+                    if (r < lo || r >= hi) continue;
+                    const float2* pk = pq + i * 36;
+                    float2 ar = are[i], ai = aim[i];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        const float2 p = pk[k];
+                        // re += p.x xr - p.y xi,  im += p.x xi + p.y xr
+                        ar = __ffma2_rn(make_float2(p.x, p.x), xr[k], ar);
+                        ar = __ffma2_rn(make_float2(-p.y, -p.y), xi[k], ar);
+                        ai = __ffma2_rn(make_float2(p.x, p.x), xi[k], ai);
+                        ai = __ffma2_rn(make_float2(p.y, p.y), xr[k], ai);
+                    }
+                    are[i] = ar;
+                    aim[i] = ai;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < TB_RT; ++i)
+                if (i < nr)
+                    *reinterpret_cast<float4*>(Ut + ((b * Hin + r0 + i) * nbi + m) * C + c) =
+                        make_float4(are[i].x, aim[i].x, are[i].y, aim[i].y);
+        }
+    }
+}
+
 }  // namespace
 
 void split_rows(const float* src, int64_t rows, int64_t cols, int64_t ld, float* hi, float* lo,
@@ -1140,9 +1250,22 @@ void DiscoPlan::transpose_apply(const float* v, const float* mix, int64_t B, int
                 SPH_CUDA(cudaFuncSetAttribute(disco_band_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               200 * 1024));
             });
-            disco_band_t2_kernel<<<grid, 256, psm_bytes, st>>>(S, d_psi_t.p, d_band0.p, d_bandc.p, d_psi_off.p,
-                                                               d_tb_ptr.p, d_tb_h.p, hin, nbi, hout, nbo,
-                                                               static_cast<int>(wout), K, cin, w.ldS, Ut, B);
+            static const bool t3 = !std::getenv("SPH_DISCO_T2");
+            if (t3 && K == 9 && cin % 2 == 0 && w.ldS % 2 == 0) {
+                // channel pairs + FFMA2 (the K = 9 Morlet basis; S rows of 2 x 9 floats per pair)
+                static std::once_flag once3;
+                std::call_once(once3, [] {
+                    SPH_CUDA(cudaFuncSetAttribute(disco_band_t3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  200 * 1024));
+                });
+                disco_band_t3_kernel<<<grid, 128, psm_bytes, st>>>(S, d_psi_t.p, d_band0.p, d_bandc.p,
+                                                                   d_psi_off.p, d_tb_ptr.p, d_tb_h.p, hin, nbi, hout,
+                                                                   nbo, static_cast<int>(wout), K, cin, w.ldS, Ut, B);
+            } else {
+                disco_band_t2_kernel<<<grid, 256, psm_bytes, st>>>(S, d_psi_t.p, d_band0.p, d_bandc.p, d_psi_off.p,
+                                                                   d_tb_ptr.p, d_tb_h.p, hin, nbi, hout, nbo,
+                                                                   static_cast<int>(wout), K, cin, w.ldS, Ut, B);
+            }
         } else {
             disco_band_t_kernel<<<grid, 256, 0, st>>>(S, d_psi_t.p, d_band0.p, d_bandc.p, d_psi_off.p, d_tb_ptr.p,
                                                       d_tb_h.p, hin, nbi, hout, nbo, static_cast<int>(wout), K, cin,

@@ -111,6 +111,24 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar & 0xFEFFFFFFu)
         : "memory");
 }
+// L2 cache-policy variants (SPH_GEMM_L2HINT): evict-first for the streamed output, evict-
+// last for the table tiles every M-run of a group re-reads
+__device__ __forceinline__ uint64_t l2_policy(bool evict_last) {
+    uint64_t pol;
+    if (evict_last)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                                      uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar & 0xFEFFFFFFu), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void tc_commit_pair_mc(uint32_t bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
@@ -160,6 +178,22 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t sr
                      reinterpret_cast<uint64_t>(map)),
                  "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                  : "memory");
+}
+__device__ __forceinline__ void tma_store_4d_hint(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2,
+                                                  int c3, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d_hint(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2,
+                                                  uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(src), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
 }
 // TMA tensor store of a [1][32][32] box from SMEM (bulk async-group of this thread)
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
@@ -359,7 +393,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
                    int tma_store, int a_quad,  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B
-                   int d_mode, int d_t, int d_g2, int pf, GemmEpi epi) {
+                   int d_mode, int d_t, int d_g2, int pf, GemmEpi epi, int l2hint) {
     // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
     // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads
     // (a whole-tile cp.async.bulk.prefetch.L2 one tile ahead was measured slower: cfg2
@@ -398,6 +432,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    const uint64_t pol_first = l2hint ? l2_policy(false) : 0, pol_last = l2hint ? l2_policy(true) : 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -527,6 +562,13 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                         const int brow = w.b_row + crank * pair_half(w);
                         for (int a = 0; a < na; ++a) {
                             const int kx = (kb * KS + a) * KB;
+                            if (l2hint & 2) {
+                                tma_load_2d_pair_hint(b_hi(s) + a * L::B_ATOM, &map_bhi, kx, brow, full_bar(s), pol_last);
+                                if (three_pass)
+                                    tma_load_2d_pair_hint(b_lo(s) + a * L::B_ATOM, &map_blo, kx, brow, full_bar(s),
+                                                          pol_last);
+                                continue;
+                            }
                             tma_load_2d_pair(b_hi(s) + a * L::B_ATOM, &map_bhi, kx, brow, full_bar(s));
                             if (three_pass)
                                 tma_load_2d_pair(b_lo(s) + a * L::B_ATOM, &map_blo, kx, brow, full_bar(s));
@@ -793,7 +835,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) {
-                        if (store_mode == STORE_ROW)
+                        if (l2hint & 1) {  // streamed output: evict-first
+                            if (store_mode == STORE_ROW)
+                                tma_store_3d_hint(&map_d, smem_u32(ob), w.n0 + c, row0, w.dg, pol_first);
+                            else if (d_mode == 1)
+                                tma_store_4d_hint(&map_d, smem_u32(ob), 0, w.dg, row0 / 32, w.n0 + c, pol_first);
+                            else
+                                tma_store_3d_hint(&map_d, smem_u32(ob), row0, w.n0 + c, w.dg, pol_first);
+                        } else if (store_mode == STORE_ROW)
                             tma_store_3d(&map_d, smem_u32(ob), w.n0 + c, row0, w.dg);
                         else if (d_mode == 1)  // box {32 rows, group, row tile, 32 n}
                             tma_store_4d(&map_d, smem_u32(ob), 0, w.dg, row0 / 32, w.n0 + c);
@@ -1087,6 +1136,8 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     // data-tile L2 prefetch distance: off by default (cfg2 Legendre fwd 2.46 ms at 0 vs
     // 2.52 / 2.52 / 2.57 ms at 2 / 4 / 8 k-blocks ahead, profiles/gemm_pf.sh)
     const int pf_dist = pf_env >= 0 ? pf_env : 0;
+    // L2 cache hints (experiment knob): 1 evict-first output stores, 2 evict-last table loads
+    static const int l2hint = std::getenv("SPH_GEMM_L2HINT") ? std::atoi(std::getenv("SPH_GEMM_L2HINT")) : 0;
     long long* trace = nullptr;
     if (trace_dir) {
         SPH_CUDA(cudaMalloc(&trace, (6 * 512 + 4096) * sizeof(long long)));
@@ -1096,7 +1147,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
                                 static_cast<int>(tl.n), D,
                                 g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0,
                                 quad ? (g.a_rows_g % 32 == 0 ? 2 : 1) : 0, g.d_mode, static_cast<int>(g.d_t),
-                                static_cast<int>(g.d_g2), pf_dist, epi));
+                                static_cast<int>(g.d_g2), pf_dist, epi, l2hint));
     count_launch();
     if (trace) {
         std::vector<long long> h(6 * 512 + 4096);
