@@ -214,6 +214,12 @@ int sph_spectral_conv(sph_sht_plan plan, const float* x, const float* kernel, in
                       void* stream);
 int64_t sph_spectral_conv_workspace_bytes(sph_sht_plan plan, int64_t B, int64_t c_in,
                                           int64_t c_out);
+/* The channel mix of spectral_conv alone (convolution.hpp:295-302) on reference-layout
+ * coefficients: out(b,o,l,m) = sum_i coeffs(b,i,l,m) kernel(o,i,l) for the plan's (lmax,
+ * mmax); coeffs [B][c_in][lmax][mmax] complex64 -> out [B][c_out][lmax][mmax]; kernel
+ * [c_out][c_in][klmax], klmax >= lmax; any grid kind.  Workspace as sph_spectral_conv. */
+int sph_spectral_mix(sph_sht_plan plan, const float* coeffs, const float* kernel, int64_t B, int64_t c_in,
+                     int64_t c_out, int64_t klmax, float* out, void* workspace, void* stream);
 /* block_apply epilogue (model.hpp:355-368): per point
  *   y = x + scales .* (W2 gelu(W1 gelu(conv) + b1) + b2),  gelu exact-erfc (model.hpp:42)
  * conv, x, y: [B][C][npts]; w1 [H][C], b1 [H], w2 [C][H], b2 [C], scales [C]. */

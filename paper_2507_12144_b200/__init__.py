@@ -14,4 +14,5 @@ from .sphere import (  # noqa: F401
     isotropic_basis, morlet_basis, require_same_sampling, sht_forward, sht_inverse,
     sht_forward_adjoint, sht_inverse_adjoint,
     spectral_conv,
+    spectral_mix,
 )

@@ -45,7 +45,7 @@ EXPORTS = [
     "sph_resample_workspace_bytes", "sph_bilinear_resample", "sph_decoder_plan_create",
     "sph_decoder_plan_destroy", "sph_decoder_workspace_bytes", "sph_decoder_apply", "sph_psd_from_coeffs",
     "sph_spectral_crps_from_coeffs", "sph_weighted_crps",
-    "sph_spectral_conv", "sph_spectral_conv_workspace_bytes", "sph_block_epilogue",
+    "sph_spectral_conv", "sph_spectral_conv_workspace_bytes", "sph_spectral_mix", "sph_block_epilogue",
     "sph_comm_id_bytes", "sph_comm_unique_id", "sph_comm_create", "sph_comm_destroy", "sph_comm_coords",
     "sph_comm_traffic_csv", "sph_comm_traffic_reset", "sph_dist_sht_plan_create", "sph_dist_sht_plan_destroy",
     "sph_dist_sht_local", "sph_dist_sht_workspace_bytes", "sph_dist_sht_forward", "sph_dist_sht_inverse",
@@ -118,6 +118,7 @@ def _load():
     L.sph_spectral_crps_from_coeffs.argtypes = [vp, vp, i64, i64, i64, i64, i64, C.c_int, vp, vp]
     L.sph_weighted_crps.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int, vp, vp]
     L.sph_spectral_conv.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp, vp, vp]
+    L.sph_spectral_mix.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp, vp, vp]
     L.sph_spectral_conv_workspace_bytes.argtypes = [vp, i64, i64, i64]
     L.sph_spectral_conv_workspace_bytes.restype = i64
     L.sph_block_epilogue.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp]

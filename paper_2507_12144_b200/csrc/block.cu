@@ -211,7 +211,9 @@ struct SpecProblem {
 };
 
 std::mutex g_mu;
-std::map<std::tuple<const void*, int64_t, int64_t, int64_t>, std::unique_ptr<SpecProblem>> g_spec;
+// keyed by the plan's address AND its truncation: a plan created later at a freed plan's
+// address must not inherit its per-degree tile list
+std::map<std::tuple<const void*, int64_t, int64_t, int64_t, int64_t, int64_t>, std::unique_ptr<SpecProblem>> g_spec;
 std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int>, std::unique_ptr<GroupedGemm>> g_mlp;
 
 struct SpecWs {
@@ -241,35 +243,22 @@ int64_t spectral_conv_ws_bytes(const ShtPlan& p, int64_t B, int64_t cin, int64_t
     return spec_ws(p, B, cin, cout).total;
 }
 
-void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, int64_t cin,
-                   int64_t cout, int64_t klmax, float* y, void* ws, cudaStream_t st) {
-    require(p.kind == SPH_GAUSSIAN, "spectral_conv: requires a gaussian grid");  // :287-288
-    require(cin >= 1 && cout >= 1 && klmax >= 1, "spectral_conv: kernel channel mismatch");
-    const int64_t lmax = std::min<int64_t>(klmax, p.nlat);
-    const int64_t mmax = std::min<int64_t>(lmax, p.nlon / 2);
-    require(p.lmax == lmax && p.mmax == mmax,
-            "spectral_conv: plan truncation must be lmax=min(klmax,nlat), mmax=min(lmax,nlon/2)");
-    if (B == 0) return;
-    DeviceGuard dguard(p.device);
-    const SpecWs w = spec_ws(p, B, cin, cout);
-    uint8_t* base = static_cast<uint8_t*>(ws);
-    DevBuf<uint8_t> tmp;
-    if (!base) {
-        tmp.alloc(w.total, false);
-        base = tmp.p;
-    }
-    float* cin_i = reinterpret_cast<float*>(base + w.cin_off);
-    float* cout_i = reinterpret_cast<float*>(base + w.cout_off);
+namespace {
+// y(o,l,m) = sum_i c(i,l,m) k(o,i,l)  (convolution.hpp:295-302) on the GEMM-native C_int
+// layout of the plan: gather per degree l into [(m, re/im, b)][c_in] rows, one grouped
+// tcgen05 GEMM over l with the kernel transposed to [l][c_out][c_in], scatter back.
+void spectral_mix_cint(ShtPlan& p, const float* cin_i, const float* kernel, int64_t B, int64_t cin,
+                       int64_t cout, int64_t klmax, float* cout_i, uint8_t* base, const SpecWs& w,
+                       cudaStream_t st) {
+    const int64_t lmax = p.lmax, mmax = p.mmax;
     float* Xg = reinterpret_cast<float*>(base + w.x_off);
     float* Yg = reinterpret_cast<float*>(base + w.y_off);
     float* khi = reinterpret_cast<float*>(base + w.khi_off);
     float* klo = reinterpret_cast<float*>(base + w.klo_off);
-    void* sws = base + w.sht_off;
-
     SpecProblem* sp;
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        auto& slot = g_spec[std::make_tuple(static_cast<const void*>(&p), B, cin, cout)];
+        auto& slot = g_spec[std::make_tuple(static_cast<const void*>(&p), B, cin, cout, p.lmax, p.mmax)];
         if (!slot) {
             auto s = std::make_unique<SpecProblem>();
             s->row_off.assign(lmax + 1, 0);
@@ -308,38 +297,83 @@ void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, i
         }
         sp = slot.get();
     }
+    dim3 grid(static_cast<unsigned>((w.ldx + 31) / 32), static_cast<unsigned>((lmax + 31) / 32),
+              static_cast<unsigned>(cout));
+    {
+        ProfScope prof("spectral_kernel_split", st);
+        kernel_transpose_split<<<grid, dim3(32, 8), 0, st>>>(kernel, cout, cin, klmax, lmax, w.ldx, khi, klo);
+        SPH_LAUNCH_CHECK();
+    }
+    {
+        ProfScope prof("spectral_gather", st);
+        require(mmax * 4 * B <= 65535, "spectral_conv: too many orders x batches for the gather grid");
+        dim3 tg(static_cast<unsigned>((w.ldx + 31) / 32), static_cast<unsigned>((p.Lp + 31) / 32),
+                static_cast<unsigned>(mmax * 4 * B));
+        spec_gather_kernel<<<tg, dim3(32, 8), 0, st>>>(cin_i, sp->d_row_off.p, lmax, B, cin, p.Lp, w.ldx, Xg);
+        SPH_LAUNCH_CHECK();
+    }
+    count_launch(2);
+    gemm_run(sp->gemm, Xg, Yg, p.prec, st, khi, klo);
+    {
+        ProfScope prof("spectral_scatter", st);
+        dim3 ts(static_cast<unsigned>((cout + 31) / 32), static_cast<unsigned>((p.Lp + 31) / 32),
+                static_cast<unsigned>(mmax * 4 * B));
+        spec_scatter_kernel<<<ts, dim3(32, 8), 0, st>>>(Yg, sp->d_row_off.p, lmax, B, cout, p.Lp, w.ldy, cout_i);
+        SPH_LAUNCH_CHECK();
+    }
+    count_launch();
+}
+}  // namespace
+
+void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, int64_t cin,
+                   int64_t cout, int64_t klmax, float* y, void* ws, cudaStream_t st) {
+    require(p.kind == SPH_GAUSSIAN, "spectral_conv: requires a gaussian grid");  // :287-288
+    require(cin >= 1 && cout >= 1 && klmax >= 1, "spectral_conv: kernel channel mismatch");
+    const int64_t lmax = std::min<int64_t>(klmax, p.nlat);
+    const int64_t mmax = std::min<int64_t>(lmax, p.nlon / 2);
+    require(p.lmax == lmax && p.mmax == mmax,
+            "spectral_conv: plan truncation must be lmax=min(klmax,nlat), mmax=min(lmax,nlon/2)");
+    if (B == 0) return;
+    DeviceGuard dguard(p.device);
+    const SpecWs w = spec_ws(p, B, cin, cout);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    DevBuf<uint8_t> tmp;
+    if (!base) {
+        tmp.alloc(w.total, false);
+        base = tmp.p;
+    }
+    float* cin_i = reinterpret_cast<float*>(base + w.cin_off);
+    float* cout_i = reinterpret_cast<float*>(base + w.cout_off);
+    void* sws = base + w.sht_off;
     // 1. forward SHT of the B*cin input fields (convolution.hpp:294)
     p.forward(x, B * cin, cin_i, SPH_LAYOUT_INTERNAL, sws, st);
-    // 2. y(o,l,m) = sum_i c(i,l,m) k(o,i,l)  (convolution.hpp:295-302) as per-l GEMMs
-    {
-        dim3 grid(static_cast<unsigned>((w.ldx + 31) / 32), static_cast<unsigned>((lmax + 31) / 32),
-                  static_cast<unsigned>(cout));
-        {
-            ProfScope prof("spectral_kernel_split", st);
-            kernel_transpose_split<<<grid, dim3(32, 8), 0, st>>>(kernel, cout, cin, klmax, lmax, w.ldx, khi, klo);
-            SPH_LAUNCH_CHECK();
-        }
-        {
-            ProfScope prof("spectral_gather", st);
-            require(mmax * 4 * B <= 65535, "spectral_conv: too many orders x batches for the gather grid");
-            dim3 tg(static_cast<unsigned>((w.ldx + 31) / 32), static_cast<unsigned>((p.Lp + 31) / 32),
-                    static_cast<unsigned>(mmax * 4 * B));
-            spec_gather_kernel<<<tg, dim3(32, 8), 0, st>>>(cin_i, sp->d_row_off.p, lmax, B, cin, p.Lp, w.ldx, Xg);
-            SPH_LAUNCH_CHECK();
-        }
-        count_launch(2);
-        gemm_run(sp->gemm, Xg, Yg, p.prec, st, khi, klo);
-        {
-            ProfScope prof("spectral_scatter", st);
-            dim3 ts(static_cast<unsigned>((cout + 31) / 32), static_cast<unsigned>((p.Lp + 31) / 32),
-                    static_cast<unsigned>(mmax * 4 * B));
-            spec_scatter_kernel<<<ts, dim3(32, 8), 0, st>>>(Yg, sp->d_row_off.p, lmax, B, cout, p.Lp, w.ldy, cout_i);
-            SPH_LAUNCH_CHECK();
-        }
-        count_launch();
-    }
+    // 2. the per-degree channel mix (convolution.hpp:295-302)
+    spectral_mix_cint(p, cin_i, kernel, B, cin, cout, klmax, cout_i, base, w, st);
     // 3. inverse SHT (convolution.hpp:303)
     p.inverse(cout_i, B * cout, SPH_LAYOUT_INTERNAL, y, sws, st);
+    if (tmp.p) SPH_CUDA(cudaStreamSynchronize(st));
+}
+
+void spectral_mix(ShtPlan& p, const float* coeffs, const float* kernel, int64_t B, int64_t cin, int64_t cout,
+                  int64_t klmax, float* out, void* ws, cudaStream_t st) {
+    require(cin >= 1 && cout >= 1, "spectral_mix: kernel channel mismatch");
+    require(klmax >= p.lmax, "spectral_mix: kernel must cover every degree of the coefficients");
+    if (B == 0) return;
+    DeviceGuard dguard(p.device);
+    require_on_device(coeffs, p.device, "spectral_mix");
+    require_on_device(out, p.device, "spectral_mix");
+    const SpecWs w = spec_ws(p, B, cin, cout);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    DevBuf<uint8_t> tmp;
+    if (!base) {
+        tmp.alloc(w.total, false);
+        base = tmp.p;
+    }
+    float* cin_i = reinterpret_cast<float*>(base + w.cin_off);
+    float* cout_i = reinterpret_cast<float*>(base + w.cout_off);
+    dense_to_cint(p, coeffs, B * cin, cin_i, st);
+    spectral_mix_cint(p, cin_i, kernel, B, cin, cout, klmax, cout_i, base, w, st);
+    cint_to_dense(p, cout_i, B * cout, 0, p.mmax, p.mmax, out, st);
     if (tmp.p) SPH_CUDA(cudaStreamSynchronize(st));
 }
 

@@ -365,6 +365,14 @@ int sph_spectral_conv(sph_sht_plan plan, const float* x, const float* kernel, in
     });
 }
 
+int sph_spectral_mix(sph_sht_plan plan, const float* coeffs, const float* kernel, int64_t B, int64_t c_in,
+                     int64_t c_out, int64_t klmax, float* out, void* workspace, void* stream) {
+    return guarded([&] {
+        sph::require(plan, "spectral_mix: null plan");
+        sph::spectral_mix(plan->p, coeffs, kernel, B, c_in, c_out, klmax, out, workspace, S(stream));
+    });
+}
+
 int64_t sph_spectral_conv_workspace_bytes(sph_sht_plan plan, int64_t B, int64_t c_in,
                                           int64_t c_out) {
     return plan ? sph::spectral_conv_ws_bytes(plan->p, B, c_in, c_out) : -1;

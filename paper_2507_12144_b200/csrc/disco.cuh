@@ -91,6 +91,10 @@ struct DiscoPlan {
 void spectral_conv(ShtPlan& p, const float* x, const float* kernel, int64_t B, int64_t cin,
                    int64_t cout, int64_t klmax, float* y, void* ws, cudaStream_t st);
 int64_t spectral_conv_ws_bytes(const ShtPlan& p, int64_t B, int64_t cin, int64_t cout);
+// the mix stage alone on reference-layout coefficients [B][cin][lmax][mmax] complex64 ->
+// [B][cout][lmax][mmax] (same workspace size as spectral_conv)
+void spectral_mix(ShtPlan& p, const float* coeffs, const float* kernel, int64_t B, int64_t cin, int64_t cout,
+                  int64_t klmax, float* out, void* ws, cudaStream_t st);
 
 void block_epilogue(const float* conv, const float* x, const float* w1, const float* b1,
                     const float* w2, const float* b2, const float* scales, int64_t B, int64_t C,

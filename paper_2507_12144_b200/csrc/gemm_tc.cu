@@ -1136,8 +1136,9 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     // data-tile L2 prefetch distance: off by default (cfg2 Legendre fwd 2.46 ms at 0 vs
     // 2.52 / 2.52 / 2.57 ms at 2 / 4 / 8 k-blocks ahead, profiles/gemm_pf.sh)
     const int pf_dist = pf_env >= 0 ? pf_env : 0;
-    // L2 cache hints (experiment knob): 1 evict-first output stores, 2 evict-last table loads
-    static const int l2hint = std::getenv("SPH_GEMM_L2HINT") ? std::atoi(std::getenv("SPH_GEMM_L2HINT")) : 0;
+    // L2 cache hints: 1 evict-first output stores, 2 evict-last table loads (pair kernel).
+    // cfg2 round trip 9.33 -> 9.23 ms with both (profiles/r2/gemm_l2hint_sweep.log)
+    static const int l2hint = std::getenv("SPH_GEMM_L2HINT") ? std::atoi(std::getenv("SPH_GEMM_L2HINT")) : 3;
     long long* trace = nullptr;
     if (trace_dir) {
         SPH_CUDA(cudaMalloc(&trace, (6 * 512 + 4096) * sizeof(long long)));

@@ -693,6 +693,34 @@ def spectral_conv(field: SphericalField, kernel: torch.Tensor,
     return SphericalField(g, y.reshape(*lead, cout, g.nlat, g.nlon))
 
 
+def spectral_mix(coeffs: SpectralCoeffs, kernel: torch.Tensor, precision: str = "3xtf32",
+                 grid: Optional[GridSpec] = None) -> SpectralCoeffs:
+    """The channel mix of spectral_conv alone (convolution.hpp:295-302):
+    out(.., o, l, m) = sum_i coeffs(.., i, l, m) kernel(o, i, l); coeffs [B][c_in][lmax][mmax]
+    complex, kernel [c_out][c_in][klmax] with klmax >= lmax.  ``grid`` only selects the
+    plan the mix runs on (any grid with nlat >= lmax, nlon >= 2 mmax)."""
+    c = coeffs.coeffs
+    if c.dtype != torch.complex64:
+        c = c.to(torch.complex64)
+    cout, cin, klmax = kernel.shape
+    if c.shape[-3] != cin:
+        raise L.SphInvalidArgument(1, "spectral_mix: kernel channel mismatch")
+    lead = tuple(c.shape[:-3])
+    B = int(np.prod(lead)) if lead else 1
+    g = grid or build_gaussian(coeffs.lmax, max(2 * coeffs.mmax, 2))
+    plan = get_sht_plan(g, coeffs.lmax, coeffs.mmax, precision, device=c.device)
+    cr = torch.view_as_real(c.contiguous())
+    k = _dev_f32(kernel, "spectral_mix")
+    out = torch.empty((B, cout, coeffs.lmax, coeffs.mmax, 2), dtype=torch.float32, device=c.device)
+    n = int(L.lib.sph_spectral_conv_workspace_bytes(plan.h, B, cin, cout))
+    ws = torch.empty(n, dtype=torch.uint8, device=c.device)
+    with torch.cuda.device(c.device):
+        check(L.lib.sph_spectral_mix(plan.h, _ptr(cr), _ptr(k), B, cin, cout, klmax, _ptr(out), _ptr(ws),
+                                     _stream(c.device)))
+    return SpectralCoeffs(coeffs.lmax, coeffs.mmax,
+                          torch.view_as_complex(out).reshape(*lead, cout, coeffs.lmax, coeffs.mmax))
+
+
 # ------------------------------------------------------------------- block
 @dataclass
 class BlockWeights:

@@ -99,3 +99,22 @@ def test_block_epilogue_vs_oracle_cfg4_width():
     y = N(S.block_epilogue(T(conv), T(x), bw))
     ref = oracle.orc().block_epilogue(conv.reshape(C, P), x.reshape(C, P), w1, b1, w2, b2, sc)
     assert rel_l2(y.reshape(C, P) - x.reshape(C, P), ref - x.reshape(C, P)) <= TOL
+
+
+def test_spectral_mix_alone_vs_numpy():
+    """sph_spectral_mix: the per-degree channel mix of spectral_conv (convolution.hpp:295-302)
+    on reference-layout coefficients, against the same contraction in fp64 numpy; any grid
+    kind (coefficients of an equiangular field), batch 2, c_in 5 -> c_out 3."""
+    rng = np.random.default_rng(7)
+    lmax = mmax = 16
+    B, cin, cout = 2, 5, 3
+    c = rng.uniform(-1, 1, (B, cin, lmax, mmax)) + 1j * rng.uniform(-1, 1, (B, cin, lmax, mmax))
+    c[..., 0] = c[..., 0].real
+    c *= np.tril(np.ones((lmax, mmax)))  # zeros above the diagonal (m > l), the reference layout
+    k = rng.uniform(-1, 1, (cout, cin, 20))
+    out = S.spectral_mix(S.SpectralCoeffs(lmax, mmax, torch.tensor(c, dtype=torch.complex64, device=DEV)),
+                         T(k), grid=S.build_equiangular(17, 32)).coeffs
+    ref = np.einsum("bilm,oil->bolm", c, k[:, :, :lmax])
+    got = out.cpu().numpy().astype(np.complex128)
+    assert rel_l2(got, ref) <= TOL
+    assert np.all(got[..., np.triu_indices(lmax, 1, mmax)[0], np.triu_indices(lmax, 1, mmax)[1]] == 0)
