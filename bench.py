@@ -520,6 +520,19 @@ def measure_disco(args, ws, rank, local):
         del xh, yh, xd, yd, ws1
     rec["e2e"] = e2e
     del x, y, wsb
+    # the adjoint on the same operator (disco_transpose_apply, convolution.hpp:226-266; the
+    # DISCO backward pass w.r.t. its input): 256 -> 64 channels back onto 721x1440
+    from paper_2507_12144_b200 import _lib as L
+    v = torch.rand((B, cout, 360, 720), device=dev) * 2 - 1
+    yt = torch.empty((B, cin, NLAT, NLON), device=dev)
+    wst = torch.empty(L.lib.sph_disco_transpose_workspace_bytes(op.h, B, cin, cout), dtype=torch.uint8, device=dev)
+    ms_t, launches_t, prof_t, _ = timed(lambda: op.transpose_apply(v, mix, out=yt, ws=wst), max(5, args.steps // 2),
+                                        args.warmup, ws, local, torch.cuda.current_stream(dev))
+    rec["transpose"] = {"workload": "disco_transpose_apply 360x720 -> 721x1440, 256 -> 64 channels, batch 4",
+                        "value": ws * B * cin / (ms_t / 1e3), "unit": "output fields/s", "ms_per_step": ms_t,
+                        "gpu_launches": launches_t,
+                        "per_kernel_ms": {k: w[1] / max(5, args.steps // 2) for k, w in sorted(prof_t.items())}}
+    del v, yt, wst
     return rec
 
 
