@@ -402,149 +402,6 @@ __global__ void __launch_bounds__(128) disco_band2_kernel(
     }
 }
 
-// disco_band2_kernel with TWO batch items per thread: the staged psi value of a slot is
-// the same for every batch item, so one broadcast LDS.128 now feeds 8 FFMA2 (4 per batch
-// item) and the per-slot bookkeeping (offset LDS, loop control) is amortised over twice
-// the FMAs -- band2 ran ~40 % FFMA2 of its issued instructions.  Batch pairs (b, b+1);
-// an odd last item runs with the second half masked.
-__global__ void __launch_bounds__(128, 3) disco_band3_kernel(
-    const float4* __restrict__ U, const float2* __restrict__ psi_hat, const int32_t* __restrict__ band0,
-    const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, int64_t Hin, int64_t nbi,
-    int64_t Hout, int64_t nbo, int win, int wout, int s, int K, int64_t C, int64_t ldS,
-    float* __restrict__ S, int64_t h_in0, int64_t ho0, int64_t B) {
-    constexpr int LANES = 32, CP = 64;
-    __shared__ float4 ps[BAND2_SLOTS][4][9];
-    __shared__ int32_t uo[BAND2_SLOTS][4];
-    __shared__ __align__(16) float so[4][2][CP * 9];
-    const int mi = threadIdx.x / LANES, cl = threadIdx.x % LANES;
-    const int64_t mp0 = static_cast<int64_t>(blockIdx.x) * 4;
-    const int64_t mp = mp0 + mi;
-    const int64_t h = blockIdx.y;
-    const int64_t hg = ho0 + h;
-    const int h0 = band0[hg] - static_cast<int>(h_in0), nb = bandc[hg];
-    const int64_t po = psi_off[hg];
-    const int half = win / 2;
-    const int nslot = nb * s;
-    const int64_t C2 = C / 2;  // float4 per U bin row
-    const int nt = static_cast<int>(nbo - mp0 < 4 ? nbo - mp0 : 4);
-    for (int slot0 = 0; slot0 < nslot; slot0 += BAND2_SLOTS) {
-        const int ns = min(BAND2_SLOTS, nslot - slot0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < ns * 4; i += blockDim.x) {
-            const int sl = i >> 2, t = i & 3;
-            const int slot = slot0 + sl;
-            const int bi = slot / s, q = slot - bi * s;
-            const int64_t m = mp0 + t;
-            const int kq = static_cast<int>(m) + wout * q;
-            const bool fold = kq > half;
-            const int idx = fold ? win - kq : kq;
-            const float sg = fold ? -1.f : 1.f;
-            const float2* src = psi_hat + ((po + bi) * nbi + idx) * K;
-#pragma unroll
-            for (int kk = 0; kk < 9; ++kk) {
-                float2 v = make_float2(0.f, 0.f);
-                if (m < nbo && kk < K) v = __ldg(src + kk);
-                ps[sl][t][kk] = make_float4(v.x, v.y, sg * v.x, -sg * v.y);
-            }
-            uo[sl][t] = bi * static_cast<int>(nbi) + (m < nbo ? idx : 0);
-        }
-        __syncthreads();
-        const bool mact = mp < nbo;
-        for (int64_t b = 0; b < B; b += 2) {
-            const bool two = b + 1 < B;
-            for (int64_t c0 = 0; c0 < C; c0 += CP) {
-                const int64_t c = c0 + 2 * cl;
-                const int cn = static_cast<int>(C - c0 < CP ? C - c0 : CP);
-                float2 re0[9], im0[9], re1[9], im1[9];
-#pragma unroll
-                for (int k = 0; k < 9; ++k) re0[k] = im0[k] = re1[k] = im1[k] = make_float2(0.f, 0.f);
-                if (mact && c < C) {
-                    const float4* Ub0 = U + ((b * Hin + h0) * nbi * C + c) / 2;
-                    const float4* Ub1 = Ub0 + (two ? Hin * nbi * C2 : 0);
-                    constexpr int CH = 2;
-                    float4 ua0[CH], ua1[CH], ub0[CH], ub1[CH];
-                    auto load = [&](int sl0, float4 (&u0)[CH], float4 (&u1)[CH]) {
-#pragma unroll
-                        for (int j = 0; j < CH; ++j) {
-                            const int sl = sl0 + j;
-                            const int64_t o = sl < ns ? static_cast<int64_t>(uo[sl][mi]) * C2 : 0;
-                            u0[j] = sl < ns ? __ldg(Ub0 + o) : make_float4(0.f, 0.f, 0.f, 0.f);
-                            u1[j] = (sl < ns && two) ? __ldg(Ub1 + o) : make_float4(0.f, 0.f, 0.f, 0.f);
-                        }
-                    };
-                    auto consume = [&](int sl0, const float4 (&u0)[CH], const float4 (&u1)[CH]) {
-#pragma unroll
-                        for (int j = 0; j < CH; ++j) {
-                            if (sl0 + j >= ns) break;
-                            const float4* pp = &ps[sl0 + j][mi][0];
-                            const float2 X0 = make_float2(u0[j].x, u0[j].y), Y0 = make_float2(u0[j].z, u0[j].w);
-                            const float2 X1 = make_float2(u1[j].x, u1[j].y), Y1 = make_float2(u1[j].z, u1[j].w);
-#pragma unroll
-                            for (int k = 0; k < 9; ++k) {
-                                const float4 qv = pp[k];
-                                ffma2(re0[k], qv.y, Y0);
-                                ffma2(re0[k], qv.x, X0);
-                                ffma2(im0[k], qv.z, Y0);
-                                ffma2(im0[k], qv.w, X0);
-                                ffma2(re1[k], qv.y, Y1);
-                                ffma2(re1[k], qv.x, X1);
-                                ffma2(im1[k], qv.z, Y1);
-                                ffma2(im1[k], qv.w, X1);
-                            }
-                        }
-                    };
-                    load(0, ua0, ua1);
-                    for (int sl0 = 0; sl0 < ns; sl0 += 2 * CH) {
-                        if (sl0 + CH < ns) load(sl0 + CH, ub0, ub1);
-                        consume(sl0, ua0, ua1);
-                        if (sl0 + CH >= ns) break;
-                        if (sl0 + 2 * CH < ns) load(sl0 + 2 * CH, ua0, ua1);
-                        consume(sl0 + CH, ub0, ub1);
-                    }
-                }
-                // each batch item's tile through the staging buffer, stored as contiguous
-                // rows of cn * K floats per (order, re/im) (as disco_band2_kernel)
-                const int rowlen = cn * K;
-                const bool vec = (rowlen & 3) == 0 && (ldS & 3) == 0 && ((c0 * K) & 3) == 0;
-                const int q4 = vec ? rowlen >> 2 : rowlen;
-                for (int bb = 0; bb < (two ? 2 : 1); ++bb) {
-                    __syncthreads();
-#pragma unroll
-                    for (int k = 0; k < 9; ++k)
-                        if (k < K) {
-                            const float2 rv = bb ? re1[k] : re0[k], iv = bb ? im1[k] : im0[k];
-                            so[mi][0][(2 * cl) * K + k] = rv.x;
-                            so[mi][0][(2 * cl + 1) * K + k] = rv.y;
-                            so[mi][1][(2 * cl) * K + k] = iv.x;
-                            so[mi][1][(2 * cl + 1) * K + k] = iv.y;
-                        }
-                    __syncthreads();
-                    float* sbase = S + ((((b + bb) * Hout + h) * nbo + mp0) * 2) * ldS + c0 * K;
-                    for (int i = threadIdx.x; i < nt * 2 * q4; i += blockDim.x) {
-                        const int r = i / q4, j = i - r * q4;
-                        float* drow = sbase + static_cast<int64_t>(r) * ldS;
-                        const float* srow = &so[r >> 1][r & 1][0];
-                        if (vec) {
-                            float4 v = reinterpret_cast<const float4*>(srow)[j];
-                            float4* dst = reinterpret_cast<float4*>(drow) + j;
-                            if (slot0 != 0) {
-                                const float4 o = *dst;
-                                v.x += o.x;
-                                v.y += o.y;
-                                v.z += o.z;
-                                v.w += o.w;
-                            }
-                            *dst = v;
-                        } else {
-                            drow[j] = slot0 != 0 ? drow[j] + srow[j] : srow[j];
-                        }
-                    }
-                }
-            }
-        }
-    }
-}
-
 // Direct gather in the reference order (convolution.hpp:192-205), fp32:
 // T[(b*Hout + h)*Wout + w][c*K + k] = sum_e vals[e][k] u[b][c][h_in][(w_rel + s w) % Win]
 __global__ void __launch_bounds__(256) disco_gather_kernel(
@@ -1208,13 +1065,7 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
     {
         // algorithmic bytes: U read once, S written once
         ProfScope prof("disco_band", st, 8.0 * B * nin * nbi * cin + 4.0 * B * nout * nbo * 2 * cin * K);
-        static const int band_v = std::getenv("SPH_DISCO_BAND") ? std::atoi(std::getenv("SPH_DISCO_BAND")) : 3;
-        if (pair_layout(cin) && band_v == 3 && B >= 2)
-            disco_band3_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const float4*>(U), d_psi_hat.p, d_band0.p,
-                                                     d_bandc.p, d_psi_off.p, nin, nbi, nout, nbo,
-                                                     static_cast<int>(win), static_cast<int>(wout),
-                                                     static_cast<int>(stride), K, cin, w.ldS, S, h_in0, ho0, B);
-        else if (pair_layout(cin))
+        if (pair_layout(cin))
             disco_band2_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const float4*>(U), d_psi_hat.p, d_band0.p,
                                                      d_bandc.p, d_psi_off.p, nin, nbi, nout, nbo,
                                                      static_cast<int>(win), static_cast<int>(wout),
