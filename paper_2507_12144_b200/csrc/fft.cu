@@ -14,6 +14,7 @@
 #include <set>
 
 #include "fft.cuh"
+#include "gemm.cuh"  // EOI_TILE: the inverse GEMM's EOi field tiles
 #include "fft4.cuh"
 
 namespace sph {
@@ -327,7 +328,7 @@ struct UnfoldIO {
     int R, nlat, msynth, lmax;
     int64_t F, twoF;
     float* y;
-    int64_t T;  // 32-row field tiles
+    int64_t T;  // EOI_TILE-row field tiles (gemm.cuh)
     template <int N1, int N2>
     __device__ __forceinline__ void store_b(int P, int N, int p, int k1, const float2 (&b)[N2]) const {
         const int64_t f = static_cast<int64_t>(blockIdx.x) * P + p;
@@ -367,9 +368,9 @@ struct UnfoldIO {
         const bool pair = rows[r].y >= 0;
         const int64_t row = 2 * (f0 + j);  // re row of field f0 + j
         const float2* e = reinterpret_cast<const float2*>(
-            eoi + ((static_cast<int64_t>(r) * T + row / 32) * 2 * msynth) * 32 + (row & 31));
-        const int64_t so = 16;  // parity stride in float2 (next g)
-        const int64_t sm = 32;  // order stride in float2 (g += 2)
+            eoi + ((static_cast<int64_t>(r) * T + row / EOI_TILE) * 2 * msynth) * EOI_TILE + (row % EOI_TILE));
+        const int64_t so = EOI_TILE / 2;  // parity stride in float2 (next g)
+        const int64_t sm = EOI_TILE;      // order stride in float2 (g += 2)
         // batches of UB orders: all 2*UB loads issued before any use (memory-level
         // parallelism for the latency-bound load phase)
         constexpr int UB = 8;
@@ -993,7 +994,7 @@ void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi,
     const int P = rpb_of(fp);
     (void)ld_eo;  // EOi is [m][parity][R][2F] (transposed GEMM store)
     static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
-    UnfoldIO io{fft_dbg, eoi, fr.d_rows.p, fr.R, nlat, msynth, lmax, F, 2 * F, y, (2 * F + 31) / 32};
+    UnfoldIO io{fft_dbg, eoi, fr.d_rows.p, fr.R, nlat, msynth, lmax, F, 2 * F, y, (2 * F + EOI_TILE - 1) / EOI_TILE};
     require(fr.R <= 65535, "fft: too many latitude rows");
     dim3 grid(static_cast<unsigned>((F + P - 1) / P), static_cast<unsigned>(fr.R));
     const double bytes = 4.0 * F * (static_cast<double>(nlat) * fp.n + 4.0 * msynth * fr.R);

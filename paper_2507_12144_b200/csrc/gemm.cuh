@@ -15,6 +15,12 @@
 
 namespace sph {
 
+// Rows per field tile of the inverse SHT's EOi layout (GroupedGemm::d_mode 1):
+// EOi[r][t][g][EOI_TILE], r ring pair, t = row / EOI_TILE, g = 2 m + parity.  128 rows: a
+// CTA's 4 epilogue warps write each (r, t, g) run of 512 B together (32 rows measured
+// 128-byte pieces 11.8 MB apart at cfg2: the inverse GEMM's epilogue cost 0.77 of 2.27 ms).
+constexpr int EOI_TILE = 128;
+
 struct GemmGroup {
     int32_t a_row0;  // first row of this group in the 2D A tensor
     int32_t b_row0;  // first row of this group in the 2D B tensor
@@ -83,8 +89,8 @@ struct GroupedGemm {
     bool a_quad = false;
     int64_t a_rows_g = 0, a_groups = 0, a_kq = 0;
     // d_mode 1 (STORE_TRANS only): D element (group dg, n, m) at
-    // ((n * d_t + m / 32) * d_g2 + dg) * 32 + m % 32, dg = d_off / (N * ldd): the inverse
-    // SHT's field-tile-major EOi, so each unfold CTA reads one contiguous chunk (fft.cu)
+    // ((n * d_t + m / EOI_TILE) * d_g2 + dg) * EOI_TILE + m % EOI_TILE, dg = d_off / (N * ldd):
+    // the inverse SHT's field-tile-major EOi, so each unfold CTA reads contiguous runs (fft.cu)
     int d_mode = 0;
     int64_t d_t = 0, d_g2 = 0;
     int64_t d_rows = 0, d_groups3 = 0, d_ldd = 0;

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
                         dbase[static_cast<int64_t>(m) * g.ldd + z] = 0.f;
             }
             else if (d_mode == 1)
-                D[((static_cast<int64_t>(n) * d_t + m / 32) * d_g2 + g.d_off / d_gsz) * 32 + (m & 31)] = acc[i][j];
+                D[((static_cast<int64_t>(n) * d_t + m / EOI_TILE) * d_g2 + g.d_off / d_gsz) * EOI_TILE + (m % EOI_TILE)] =
+                    acc[i][j];
             else if (epi.mode == 2) {
                 const int64_t e = g.d_off + static_cast<int64_t>(n) * g.ldd + m;
                 D[e] = epi.res[e] + epi.scale[n] * (acc[i][j] + epi.bias[n]);

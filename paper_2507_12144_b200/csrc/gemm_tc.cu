@@ -839,13 +839,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                             if (store_mode == STORE_ROW)
                                 tma_store_3d_hint(&map_d, smem_u32(ob), w.n0 + c, row0, w.dg, pol_first);
                             else if (d_mode == 1)
-                                tma_store_4d_hint(&map_d, smem_u32(ob), 0, w.dg, row0 / 32, w.n0 + c, pol_first);
+                                tma_store_4d_hint(&map_d, smem_u32(ob), row0 % EOI_TILE, w.dg, row0 / EOI_TILE, w.n0 + c,
+                                                  pol_first);
                             else
                                 tma_store_3d_hint(&map_d, smem_u32(ob), row0, w.n0 + c, w.dg, pol_first);
                         } else if (store_mode == STORE_ROW)
                             tma_store_3d(&map_d, smem_u32(ob), w.n0 + c, row0, w.dg);
-                        else if (d_mode == 1)  // box {32 rows, group, row tile, 32 n}
-                            tma_store_4d(&map_d, smem_u32(ob), 0, w.dg, row0 / 32, w.n0 + c);
+                        else if (d_mode == 1)  // box {32 rows of the field tile, group, tile, 32 n}
+                            tma_store_4d(&map_d, smem_u32(ob), row0 % EOI_TILE, w.dg, row0 / EOI_TILE, w.n0 + c);
                         else
                             tma_store_3d(&map_d, smem_u32(ob), row0, w.n0 + c, w.dg);
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -912,8 +913,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                 } else {
                     const int m = row0 + lane;
                     if (m < w.M && d_mode == 1) {
-                        float* dp = D + ((static_cast<int64_t>(w.n0 + c) * d_t + m / 32) * d_g2 + w.dg) * 32 + (m & 31);
-                        const int64_t nstride = static_cast<int64_t>(d_t) * d_g2 * 32;
+                        float* dp = D + ((static_cast<int64_t>(w.n0 + c) * d_t + m / EOI_TILE) * d_g2 + w.dg) * EOI_TILE +
+                                    (m % EOI_TILE);
+                        const int64_t nstride = static_cast<int64_t>(d_t) * d_g2 * EOI_TILE;
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj)
                             if (c + jj < nrem) dp[jj * nstride] = __uint_as_float(va[jj]);
@@ -1086,12 +1088,13 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     std::memset(&md, 0, sizeof(md));
     const bool tstore = g.tma_store && (ALO || g.store == STORE_ROW);
     if (tstore && g.d_mode == 1) {
-        // [n][row tile of 32][group][32]: box {32, 1, 1, 32} = 128-byte pieces (16-row tiles
+        // [n][field tile][group][EOI_TILE]: box {32, 1, 1, 32} = a warp's 128-byte quarter of
+        // a 512-byte run, the CTA's 4 lane-quarter warps fill the run together (16-row tiles
         // with 64-byte pieces measured 3.5 vs 2.1 ms on the cfg2 inverse GEMM)
-        cuuint64_t dims[4] = {32, static_cast<cuuint64_t>(g.d_g2), static_cast<cuuint64_t>(g.d_t),
+        cuuint64_t dims[4] = {EOI_TILE, static_cast<cuuint64_t>(g.d_g2), static_cast<cuuint64_t>(g.d_t),
                               static_cast<cuuint64_t>(g.d_rows)};
-        cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(g.d_g2 * 128),
-                                 static_cast<cuuint64_t>(g.d_t * g.d_g2 * 128)};
+        cuuint64_t strides[3] = {4 * EOI_TILE, static_cast<cuuint64_t>(g.d_g2 * 4 * EOI_TILE),
+                                 static_cast<cuuint64_t>(g.d_t * g.d_g2 * 4 * EOI_TILE)};
         cuuint32_t box[4] = {32, 1, 1, 32};
         cuuint32_t estr[4] = {1, 1, 1, 1};
         require((reinterpret_cast<uintptr_t>(D) & 15) == 0, "gemm: output must be 16B aligned");
@@ -1256,6 +1259,18 @@ static void build_tiles(const GroupedGemm& g, int cl, GemmTileList& out) {
         gorder.push_back(gi);
     }
     std::stable_sort(gorder.begin(), gorder.end(), [&](size_t a, size_t b) { return gcost[a] > gcost[b]; });
+    // SPH_GEMM_ORDER=1: alternate the longest and the shortest remaining groups, so a CTA's
+    // short-K (epilogue-bound) tiles sit between long ones whose MMAs hide their epilogues
+    static const int order = std::getenv("SPH_GEMM_ORDER") ? std::atoi(std::getenv("SPH_GEMM_ORDER")) : 0;
+    if (order == 1 && gorder.size() > 2) {
+        std::vector<size_t> alt;
+        alt.reserve(gorder.size());
+        for (size_t lo = 0, hi = gorder.size(); lo < hi;) {
+            alt.push_back(gorder[lo++]);
+            if (lo < hi) alt.push_back(gorder[--hi]);
+        }
+        gorder.swap(alt);
+    }
     std::vector<GemmWork> ts;
     for (size_t gi : gorder) {
         const GemmGroup& gr = g.groups[gi];

@@ -415,7 +415,7 @@ const GroupedGemm& ShtPlan::inv_gemm(int64_t F) {
         g->Blo = {pi_lo.p, mmax * 2 * R, Lmax_p, Lp};
         g->store = STORE_TRANS;  // EOi[r][2F/32][m, parity][32] (fft.cu UnfoldIO)
         g->d_mode = 1;
-        g->d_t = (2 * F + 31) / 32;
+        g->d_t = (2 * F + EOI_TILE - 1) / EOI_TILE;
         g->d_g2 = 2 * msynth;
         g->bn = 192;  // TMEM-resident A operand variant
         g->name = "gemm_legendre_inv";

@@ -47,7 +47,7 @@ struct ShtPlan {
         return n <= 0 ? 0 : (p == 0 ? (n + 1) / 2 : n / 2);
     }
     // E/O (forward, quad-interleaved) and EOi (inverse, field tiles of 32 rows) share it
-    int64_t eo_elems(int64_t F) const { return mmax * 2 * ((2 * F + 31) / 32 * 32) * Rp; }
+    int64_t eo_elems(int64_t F) const { return mmax * 2 * ((2 * F + EOI_TILE - 1) / EOI_TILE * EOI_TILE) * Rp; }
     int64_t cint_elems(int64_t F) const { return mmax * 2 * 2 * F * Lp; }
     int64_t dense_elems(int64_t F) const { return F * lmax * mmax * 2; }
     int64_t workspace_bytes(int64_t F) const { return 4 * (eo_elems(F) + cint_elems(F)) + 256; }
