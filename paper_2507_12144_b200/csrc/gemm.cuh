@@ -79,6 +79,10 @@ struct GroupedGemm {
     bool alo = false;              // bn 64 / 128: the BK = 32 A_lo-in-TMEM kernel (bn 192 always is)
     int ks = 1;                    // 32-wide atoms per pipeline stage (1 or 2; A_lo-in-TMEM kernels)
     bool row_tma = false;          // non-ALO STORE_ROW: TMA-store epilogue (uniform D groups)
+    // blo_conv (3xTF32, bn = 192): Bhi is the RAW fp32 table and no lo table is loaded; the
+    // converter warps split the SMEM tile in place (hi = rna_tf32(B), lo = B - hi, the host
+    // split's values) next to A_lo: half the table's TMA bytes
+    bool blo_conv = false;
     bool pair = false;             // cta_group::2 CTA-pair MMA (set by finalize)
     // TMA-store epilogue (ALO kernel): D is a uniform 3D [d_groups3][d_rows][ldd] view
     // (every group has the same ldd and row count, d_off a multiple of d_rows * ldd)

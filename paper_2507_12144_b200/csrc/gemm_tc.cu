@@ -393,7 +393,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
                    int tma_store, int a_quad,  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B
-                   int d_mode, int d_t, int d_g2, int pf, GemmEpi epi, int l2hint) {
+                   int d_mode, int d_t, int d_g2, int pf, GemmEpi epi, int l2hint, int blo_conv) {
     // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
     // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads
     // (a whole-tile cp.async.bulk.prefetch.L2 one tile ahead was measured slower: cfg2
@@ -554,6 +554,18 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                         if (++s == STAGES) { s = 0; ph ^= 1; }
                         continue;
                     }
+                    if (PAIR && three_pass && blo_conv) {
+                        // converter-split table: each CTA's converter must see ITS table half
+                        // land, so both halves signal their own CTA's full barrier (plain TMA);
+                        // the leader's MMA still waits for both through the conv barrier
+                        mbar_expect_tx(full_bar(s), na * (L::A_ATOM + L::B_ATOM));
+                        load_a(s, w, kb, na);
+                        const int brow = w.b_row + crank * pair_half(w);
+                        for (int a = 0; a < na; ++a)
+                            tma_load_2d(b_hi(s) + a * L::B_ATOM, &map_bhi, (kb * KS + a) * KB, brow, full_bar(s));
+                        if (++s == STAGES) { s = 0; ph ^= 1; }
+                        continue;
+                    }
                     if constexpr (PAIR) {
                         // leader's full barrier: own A + both CTAs' table halves; peer's: A
                         const int nb = (three_pass ? 2 : 1) * na * L::B_ATOM;
@@ -576,19 +588,19 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                         if (++s == STAGES) { s = 0; ph ^= 1; }
                         continue;
                     }
-                    mbar_expect_tx(full_bar(s), na * (L::A_ATOM + (three_pass ? 2 : 1) * L::B_ATOM));
+                    mbar_expect_tx(full_bar(s), na * (L::A_ATOM + (three_pass && !blo_conv ? 2 : 1) * L::B_ATOM));
                     load_a(s, w, kb, na);
                     for (int a = 0; a < na; ++a) {
                         const int kx = (kb * KS + a) * KB;
                         if (CL == 1) {
                             tma_load_2d(b_hi(s) + a * L::B_ATOM, &map_bhi, kx, w.b_row, full_bar(s));
-                            if (three_pass)
+                            if (three_pass && !blo_conv)
                                 tma_load_2d(b_lo(s) + a * L::B_ATOM, &map_blo, kx, w.b_row, full_bar(s));
                         } else {
                             const uint32_t off = a * L::B_ATOM + crank * B_ROWS * KB * 4;
                             tma_load_2d_mc(b_hi(s) + off, &map_bhi, kx, w.b_row + crank * B_ROWS, full_bar(s),
                                            cmask);
-                            if (three_pass)
+                            if (three_pass && !blo_conv)
                                 tma_load_2d_mc(b_lo(s) + off, &map_blo, kx, w.b_row + crank * B_ROWS,
                                                full_bar(s), cmask);
                         }
@@ -696,6 +708,32 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                             }
                             tmem_st16(tmem_alo(s) + at * KB + 16 * h + (static_cast<uint32_t>(32 * q) << 16), lo);
                         }
+                        }
+                        if (blo_conv) {
+                            // the raw fp32 table tile split in place, element-wise at the same
+                            // (swizzled) SMEM positions, exactly as the host split of the
+                            // forward tables: hi = rna_tf32(B), lo = B - hi.  Runs while the
+                            // TMEM stores drain; the async proxy (the MMA's descriptor reads)
+                            // sees the generic stores after the proxy fence
+                            float4* bh = reinterpret_cast<float4*>(smem + (b_hi(s) - sbase));
+                            float4* bl = reinterpret_cast<float4*>(smem + (b_lo(s) - sbase));
+                            const int nb4 = na * L::B_ATOM / 16;
+                            for (int i = ct; i < nb4; i += 128) {
+                                const float4 v = bh[i];
+                                float4 h, o;
+                                uint32_t u;
+                                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v.x)); h.x = __uint_as_float(u);
+                                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v.y)); h.y = __uint_as_float(u);
+                                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v.z)); h.z = __uint_as_float(u);
+                                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v.w)); h.w = __uint_as_float(u);
+                                o.x = v.x - h.x;
+                                o.y = v.y - h.y;
+                                o.z = v.z - h.z;
+                                o.w = v.w - h.w;
+                                bh[i] = h;
+                                bl[i] = o;
+                            }
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         }
                         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                         tc_fence_before();
@@ -1151,7 +1189,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
                                 static_cast<int>(tl.n), D,
                                 g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0,
                                 quad ? (g.a_rows_g % 32 == 0 ? 2 : 1) : 0, g.d_mode, static_cast<int>(g.d_t),
-                                static_cast<int>(g.d_g2), pf_dist, epi, l2hint));
+                                static_cast<int>(g.d_g2), pf_dist, epi, l2hint, (three && g.blo_conv) ? 1 : 0));
     count_launch();
     if (trace) {
         std::vector<long long> h(6 * 512 + 4096);
@@ -1201,7 +1239,9 @@ void gemm_run(const GroupedGemm& g, const float* A, float* D, int prec, cudaStre
         return;
     }
     const bool three = prec == SPH_PREC_3XTF32;
-    require(!three || Blo, "gemm: 3xTF32 needs the lo table");
+    require(!three || Blo || g.blo_conv, "gemm: 3xTF32 needs the lo table");
+    require(!g.blo_conv || g.bn == 192, "gemm: converter-formed B_lo only in the A_lo-in-TMEM bn=192 kernel");
+    if (!Blo) Blo = Bhi;  // unused by the kernel when the converter forms B_lo
     const int cl = g.cluster;
     if (g.bn == 192 && g.pair && g.ks == 2)
         tc::launch<192, 2, 2, true, true, 2>(g, A, Bhi, Blo, D, three, st, epi);

@@ -11,6 +11,7 @@
 // with G_b = 0.  Each (m, parity) block is one group of the grouped GEMM.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <thread>
 
 #include "sht.cuh"
@@ -66,6 +67,11 @@ void build_grid(int kind, int64_t nlat, int64_t nlon, std::vector<double>& colat
 }
 
 namespace {
+
+bool inv_blo_conv() {
+    static const bool on = !std::getenv("SPH_GEMM_BLO_CONV") || std::atoi(std::getenv("SPH_GEMM_BLO_CONV")) != 0;
+    return on;
+}
 
 // Phat_l^m(x) for l in [m, lmax) by the reference recurrence (harmonics.hpp:68-100),
 // fp64.  fl[l] = sqrt((4l^2-1)/(l^2-m^2)) precomputed per m.
@@ -360,7 +366,12 @@ void ShtPlan::create(int kind_, int64_t nlat_, int64_t nlon_, int64_t lmax_, int
         upload(pf_hi, hi);
         upload(pf_lo, lo);
     }
-    {
+    // the inverse table raw: the inverse GEMM's converter warps split it in SMEM
+    // (GroupedGemm::blo_conv: half its table TMA bytes); the SIMT anchor reads it exactly.
+    // SPH_GEMM_BLO_CONV=0: host-split hi / lo tables instead
+    if (inv_blo_conv()) {
+        upload(pi_hi, pit);
+    } else {
         std::vector<float> hi(pit.size()), lo(pit.size());
         tf32_split_host(pit.data(), pit.size(), hi.data(), lo.data());
         upload(pi_hi, hi);
@@ -413,6 +424,7 @@ const GroupedGemm& ShtPlan::inv_gemm(int64_t F) {
         g->A = {nullptr, mmax * 2 * 2 * F, Lmax_p, Lp};
         g->Bhi = {pi_hi.p, mmax * 2 * R, Lmax_p, Lp};
         g->Blo = {pi_lo.p, mmax * 2 * R, Lmax_p, Lp};
+        g->blo_conv = pi_lo.p == nullptr;
         g->store = STORE_TRANS;  // EOi[r][2F/32][m, parity][32] (fft.cu UnfoldIO)
         g->d_mode = 1;
         g->d_t = (2 * F + EOI_TILE - 1) / EOI_TILE;
