@@ -68,6 +68,10 @@ void build_grid(int kind, int64_t nlat, int64_t nlon, std::vector<double>& colat
 
 namespace {
 
+bool fwd_blo_conv() {
+    static const bool on = std::getenv("SPH_GEMM_BLO_CONV_FWD") && std::atoi(std::getenv("SPH_GEMM_BLO_CONV_FWD")) != 0;
+    return on;
+}
 bool inv_blo_conv() {
     static const bool on = !std::getenv("SPH_GEMM_BLO_CONV") || std::atoi(std::getenv("SPH_GEMM_BLO_CONV")) != 0;
     return on;
@@ -360,7 +364,9 @@ void ShtPlan::create(int kind_, int64_t nlat_, int64_t nlon_, int64_t lmax_, int
             }
         }
     });
-    {
+    if (fwd_blo_conv()) {  // experiment knob SPH_GEMM_BLO_CONV_FWD=1: as the inverse below
+        upload(pf_hi, pf);
+    } else {
         std::vector<float> hi(pf.size()), lo(pf.size());
         tf32_split_host(pf.data(), pf.size(), hi.data(), lo.data());
         upload(pf_hi, hi);
@@ -391,6 +397,7 @@ const GroupedGemm& ShtPlan::fwd_gemm(int64_t F) {
         g->a_kq = Rp / 4;
         g->Bhi = {pf_hi.p, pf_rows, R, Rp};
         g->Blo = {pf_lo.p, pf_rows, R, Rp};
+        g->blo_conv = pf_lo.p == nullptr;
         g->store = STORE_ROW;
         g->bn = 192;  // TMEM-resident A operand variant
         g->name = "gemm_legendre_fwd";
@@ -465,6 +472,7 @@ const GroupedGemm& ShtPlan::stage_gemm(int64_t F, int64_t m0, int64_t mcount) {
         g->a_kq = Rp / 4;
         g->Bhi = {pf_hi.p, pf_rows, R, Rp};
         g->Blo = {pf_lo.p, pf_rows, R, Rp};
+        g->blo_conv = pf_lo.p == nullptr;
         g->store = STORE_ROW;
         g->bn = 192;  // TMEM-resident A operand variant
         for (int64_t ml = 0; ml < mcount; ++ml)
