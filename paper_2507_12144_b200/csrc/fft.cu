@@ -715,11 +715,11 @@ __global__ void __launch_bounds__(fft4::THREADS, 2) fft4_kernel(IO io, const flo
 constexpr int FOLD_THREADS = 256;
 // Generic over IO (FoldIO: ring pairs of the SHT; CminorIO: channel pairs of a DISCO
 // input row): IO::rings(P, n, p, pa, pb, sb) gives the two real rings of slot p.
-template <int N1, class IO>
-__global__ void __launch_bounds__(FOLD_THREADS, 2) fft4_fold_kernel(IO io, const float2* __restrict__ twT) {
+template <int N1, class IO, int T = FOLD_THREADS>
+__global__ void __launch_bounds__(T, 512 / T) fft4_fold_kernel(IO io, const float2* __restrict__ twT) {
     extern __shared__ float2 smf[];
-    constexpr int N2 = 45, N = N1 * N2, P = FOLD_THREADS / N1, LD = N + 2;
-    for (int it = threadIdx.x; it < P * N2; it += FOLD_THREADS) {
+    constexpr int N2 = 45, N = N1 * N2, P = T / N1, LD = N + 2;
+    for (int it = threadIdx.x; it < P * N2; it += T) {
         const int p = it / N2, n2 = it - p * N2;
         float2 a[N1];
         const float *pa, *pb;
@@ -763,14 +763,14 @@ __global__ void __launch_bounds__(FOLD_THREADS, 2) fft4_fold_kernel(IO io, const
 // Generic over IO (UnfoldIO, PlainInvIO, CminorInvIO): IO::load builds the spectra in
 // shared memory, IO::store_b(P, N1, p, k1, b) writes thread (p, k1)'s N2 outputs
 // X[k1 + N1 k2] of ring slot p straight from registers (coalesced over k1).
-template <int N1, class IO>
-__global__ void __launch_bounds__(fft4::THREADS, 2) fft4_unfold_kernel(IO io, const float2* __restrict__ twT) {
+template <int N1, class IO, int T = fft4::THREADS>
+__global__ void __launch_bounds__(T, 512 / T) fft4_unfold_kernel(IO io, const float2* __restrict__ twT) {
     extern __shared__ float2 smu[];
-    constexpr int N2 = 45, N = N1 * N2, P = fft4::THREADS / N1, LD = N + 2;
+    constexpr int N2 = 45, N = N1 * N2, P = T / N1, LD = N + 2;
     io.load(smu, std::integral_constant<int, P>{}, std::integral_constant<int, N>{}, LD);
     __syncthreads();
     if (io.dbg & 32) return;
-    for (int it = threadIdx.x; it < P * N2; it += fft4::THREADS) {
+    for (int it = threadIdx.x; it < P * N2; it += T) {
         const int p = it / N2, n2 = it - p * N2;
         float2 a[N1];
         const float2* r = smu + p * LD + n2;
@@ -856,19 +856,39 @@ void launch4(const FftPlan& fp, const IO& io, dim3 grid, cudaStream_t st) {
     fft4_kernel<N1, INV, IO><<<grid, fft4::THREADS, sm, st>>>(io, fp.twT.p);
 }
 
+// CTA size of the fused SHT ring transforms (SPH_FFT_FOLD_THREADS / SPH_FFT_UNFOLD_THREADS,
+// 128 or 256)
+int fold_threads() {
+    static const int t = std::getenv("SPH_FFT_FOLD_THREADS") ? std::atoi(std::getenv("SPH_FFT_FOLD_THREADS")) : FOLD_THREADS;
+    return t == 128 ? 128 : 256;
+}
+int unfold_threads() {
+    static const int t = std::getenv("SPH_FFT_UNFOLD_THREADS") ? std::atoi(std::getenv("SPH_FFT_UNFOLD_THREADS")) : fft4::THREADS;
+    return t == 128 ? 128 : 256;
+}
+
 template <bool FWD>
 void launch_fused(const FftPlan& fp, const FoldIO& fio, const UnfoldIO& uio, dim3 grid, cudaStream_t st) {
+    const int T = FWD ? fold_threads() : unfold_threads();
     auto go = [&](auto n1c) {
         constexpr int N1 = decltype(n1c)::value;
-        const size_t sm = static_cast<size_t>(fft4::THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
-        if (FWD) {
-            const size_t smf = static_cast<size_t>(FOLD_THREADS / N1) * (N1 * 45 + 2) * sizeof(float2);
-            set_smem_once(fft4_fold_kernel<N1, FoldIO>, smf);
-            fft4_fold_kernel<N1, FoldIO><<<grid, FOLD_THREADS, smf, st>>>(fio, fp.twT.p);
-        } else {
-            set_smem_once(fft4_unfold_kernel<N1, UnfoldIO>, sm);
-            fft4_unfold_kernel<N1, UnfoldIO><<<grid, fft4::THREADS, sm, st>>>(uio, fp.twT.p);
-        }
+        const size_t sm = static_cast<size_t>(T / N1) * (N1 * 45 + 2) * sizeof(float2);
+        auto run = [&](auto tc) {
+            constexpr int TT = decltype(tc)::value;
+            if constexpr (TT / N1 >= 4) {  // FoldIO's quad path needs 4 ring pairs per CTA
+                if (FWD) {
+                    set_smem_once(fft4_fold_kernel<N1, FoldIO, TT>, sm);
+                    fft4_fold_kernel<N1, FoldIO, TT><<<grid, TT, sm, st>>>(fio, fp.twT.p);
+                } else {
+                    set_smem_once(fft4_unfold_kernel<N1, UnfoldIO, TT>, sm);
+                    fft4_unfold_kernel<N1, UnfoldIO, TT><<<grid, TT, sm, st>>>(uio, fp.twT.p);
+                }
+            } else {
+                fail(SPH_ERR_RUNTIME, "fft4: CTA too small for the ring split");
+            }
+        };
+        if (T == 128) run(std::integral_constant<int, 128>{});
+        else run(std::integral_constant<int, 256>{});
     };
     switch (fp.fft4_n1) {
         case 4: go(std::integral_constant<int, 4>{}); break;
@@ -957,7 +977,7 @@ void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int
                       int mmax, float* eo, int64_t ld_eo, cudaStream_t st) {
     if (F == 0) return;
     require(F <= 65535, "fft: at most 65535 fields per call");
-    const int P = fp.fft4_n1 ? FOLD_THREADS / fp.fft4_n1 : rpb_of(fp);
+    const int P = fp.fft4_n1 ? fold_threads() / fp.fft4_n1 : rpb_of(fp);
     static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
     require(ld_eo % 4 == 0, "fft: E/O ring-pair padding must be a multiple of 4");
     FoldIO io{fft_dbg, x, fr.d_rows.p, fr.R, nlat, mmax, eo, ld_eo / 4, 2 * F};
@@ -991,7 +1011,7 @@ void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi,
     (void)mmax;
     if (F == 0) return;
     require(F <= 65535, "fft: at most 65535 fields per call");
-    const int P = rpb_of(fp);
+    const int P = fp.fft4_n1 ? unfold_threads() / fp.fft4_n1 : rpb_of(fp);
     (void)ld_eo;  // EOi is [m][parity][R][2F] (transposed GEMM store)
     static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
     UnfoldIO io{fft_dbg, eoi, fr.d_rows.p, fr.R, nlat, msynth, lmax, F, 2 * F, y, (2 * F + EOI_TILE - 1) / EOI_TILE};
