@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsphgpu.so")
+# SPH_LIBSPHGPU: load another build of the library (same-box A/B runs, profiles/lib_ab.sh)
+LIB_PATH = os.environ.get("SPH_LIBSPHGPU") or os.path.join(_HERE, "libsphgpu.so")
 
 SPH_OK = 0
 SPH_ERR_INVALID_ARGUMENT = 1

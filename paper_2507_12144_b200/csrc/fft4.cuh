@@ -71,19 +71,8 @@ __device__ __forceinline__ void static_for(F&& f) {
     }
 }
 
-// Complex arithmetic on Blackwell's packed fp32x2 pipe (FADD2 / FMUL2 / FFMA2, one
-// instruction per complex add or half a complex multiply).  The ring FFTs are FP-issue
-// bound: 73 % of the fold kernel's instructions were scalar FADD / FFMA / FMUL (round-2
-// ncu source counters), one per real component.  Results are identical per component to
-// the scalar forms up to the contraction choice of the complex multiply (<= 1 ulp).
-__device__ __forceinline__ float2 add(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 sub(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
-// s * a for a real scalar s
-__device__ __forceinline__ float2 scl(float s, float2 a) { return __fmul2_rn(make_float2(s, s), a); }
-// a * (wr + i wi)
-__device__ __forceinline__ float2 cmul(float2 a, float wr, float wi) {
-    return __ffma2_rn(make_float2(a.y, a.y), make_float2(-wi, wr), __fmul2_rn(make_float2(a.x, a.x), make_float2(wr, wi)));
-}
+__device__ __forceinline__ float2 add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 
 // a * exp(-+2 pi i Q / N): exact quadrant rotations, constant twiddle otherwise
 template <int Q, int N, bool INV>
@@ -99,7 +88,7 @@ __device__ __forceinline__ float2 rot(float2 a) {
     } else {
         constexpr cxf w = twiddle(q, N);
         constexpr float wy = INV ? -w.y : w.y;
-        return cmul(a, w.x, wy);
+        return make_float2(a.x * w.x - a.y * wy, a.x * wy + a.y * w.x);
     }
 }
 
@@ -127,33 +116,31 @@ __device__ __forceinline__ void dft(float2 (&v)[M]) {
     } else if constexpr (N == 3) {
         const float2 x0 = v[OFF], x1 = v[OFF + S], x2 = v[OFF + 2 * S];
         const float2 t = add(x1, x2), d = sub(x1, x2);
-        const float2 m = __ffma2_rn(t, make_float2(-0.5f, -0.5f), x0);
+        const float2 m = make_float2(x0.x - 0.5f * t.x, x0.y - 0.5f * t.y);
         const float k = 0.86602540378443864676f;
-        // forward: X1 = m - i k d, X2 = m + i k d:  -i k d = k (d.y, -d.x)
-        const float2 dsw = make_float2(d.y, d.x);
-        const float2 kk = INV ? make_float2(-k, k) : make_float2(k, -k);
+        // forward: X1 = m - i k d, X2 = m + i k d
+        const float2 ikd = INV ? make_float2(-k * d.y, k * d.x) : make_float2(k * d.y, -k * d.x);
         v[OFF] = add(x0, t);
-        v[OFF + S] = __ffma2_rn(dsw, kk, m);
-        v[OFF + 2 * S] = __ffma2_rn(dsw, make_float2(-kk.x, -kk.y), m);
+        v[OFF + S] = add(m, ikd);
+        v[OFF + 2 * S] = sub(m, ikd);
     } else if constexpr (N == 5) {
         const float c1 = 0.30901699437494742410f, c2 = -0.80901699437494742410f;
         const float s1 = 0.95105651629515357212f, s2 = 0.58778525229247312917f;
         const float2 x0 = v[OFF];
         const float2 a1 = add(v[OFF + S], v[OFF + 4 * S]), b1 = sub(v[OFF + S], v[OFF + 4 * S]);
         const float2 a2 = add(v[OFF + 2 * S], v[OFF + 3 * S]), b2 = sub(v[OFF + 2 * S], v[OFF + 3 * S]);
-        const float2 p1 = __ffma2_rn(make_float2(c2, c2), a2, __ffma2_rn(make_float2(c1, c1), a1, x0));
-        const float2 p2 = __ffma2_rn(make_float2(c1, c1), a2, __ffma2_rn(make_float2(c2, c2), a1, x0));
-        const float2 u1 = __ffma2_rn(make_float2(s2, s2), b2, scl(s1, b1));
-        const float2 u2 = __ffma2_rn(make_float2(-s1, -s1), b2, scl(s2, b1));
-        // forward: X1 = p1 - i u1, X4 = p1 + i u1, X2 = p2 - i u2, X3 = p2 + i u2;
-        // -i u = (u.y, -u.x)
-        const float2 sg = INV ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f);
-        const float2 w1 = make_float2(u1.y, u1.x), w2 = make_float2(u2.y, u2.x);
-        v[OFF] = add(add(x0, a1), a2);
-        v[OFF + S] = __ffma2_rn(w1, sg, p1);
-        v[OFF + 4 * S] = __ffma2_rn(w1, make_float2(-sg.x, -sg.y), p1);
-        v[OFF + 2 * S] = __ffma2_rn(w2, sg, p2);
-        v[OFF + 3 * S] = __ffma2_rn(w2, make_float2(-sg.x, -sg.y), p2);
+        const float2 p1 = make_float2(x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y);
+        const float2 p2 = make_float2(x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y);
+        const float2 u1 = make_float2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y);
+        const float2 u2 = make_float2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y);
+        // forward: X1 = p1 - i u1, X4 = p1 + i u1, X2 = p2 - i u2, X3 = p2 + i u2
+        const float2 q1 = INV ? make_float2(-u1.y, u1.x) : make_float2(u1.y, -u1.x);
+        const float2 q2 = INV ? make_float2(-u2.y, u2.x) : make_float2(u2.y, -u2.x);
+        v[OFF] = make_float2(x0.x + a1.x + a2.x, x0.y + a1.y + a2.y);
+        v[OFF + S] = add(p1, q1);
+        v[OFF + 4 * S] = sub(p1, q1);
+        v[OFF + 2 * S] = add(p2, q2);
+        v[OFF + 3 * S] = sub(p2, q2);
     } else {
         constexpr int A = first_factor(N), B = N / A;
         static_assert(A < N, "unsupported prime factor in register DFT");
@@ -200,8 +187,9 @@ __device__ __forceinline__ void transform(float2* buf, const float2* __restrict_
         dft<N1, N1, 0, 1, INV>(a);
 #pragma unroll
         for (int k1 = 1; k1 < N1; ++k1) {
-            const float2 w = __ldg(twT + k1 * N2 + n2);
-            a[k1] = cmul(a[k1], w.x, INV ? -w.y : w.y);
+            float2 w = __ldg(twT + k1 * N2 + n2);
+            if (INV) w.y = -w.y;
+            a[k1] = make_float2(a[k1].x * w.x - a[k1].y * w.y, a[k1].x * w.y + a[k1].y * w.x);
         }
 #pragma unroll
         for (int k1 = 0; k1 < N1; ++k1) r[N2 * k1] = a[k1];
@@ -229,8 +217,9 @@ __device__ __forceinline__ void phase_a_store(float2 (&a)[N1], float2* buf, int 
     dft<N1, N1, 0, 1, INV>(a);
 #pragma unroll
     for (int k1 = 1; k1 < N1; ++k1) {
-        const float2 w = __ldg(twT + k1 * N2 + n2);
-        a[k1] = cmul(a[k1], w.x, INV ? -w.y : w.y);
+        float2 w = __ldg(twT + k1 * N2 + n2);
+        if (INV) w.y = -w.y;
+        a[k1] = make_float2(a[k1].x * w.x - a[k1].y * w.y, a[k1].x * w.y + a[k1].y * w.x);
     }
     float2* r = buf + p * LD + n2;
 #pragma unroll
