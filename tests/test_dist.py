@@ -141,13 +141,14 @@ def test_dist_sht_disco_nccl_product_gpu(tmp_path):
         assert rep["sht_calls"] == {"dist_sht": 4, "dist_isht": 4}, rep["traffic_csv"]
 
 
-@pytest.mark.parametrize("nh,nw", [(2, 1), (1, 2), (2, 2), (4, 1)])
+@pytest.mark.parametrize("nh,nw", [(2, 1), (1, 2), (2, 2), (4, 1), (8, 1), (4, 2)])
 def test_library_dist_schedule_gloo(nh, nw, tmp_path):
     """The C++ layout of the product distributed path (sph_dist_*_describe: ranges,
     all-to-all counts / offsets, pack / unpack boxes) executed over gloo with the fp64
     oracle as the local transform: forward SHT, mirrored inverse SHT and latitude-halo
     DISCO equal the serial oracle to 1e-12 at every decomposition, including uneven
-    channel slices and a rank with no channels (3 channels over 4 ranks)."""
+    channel slices and a rank with no channels (3 channels over 4 ranks).  8 x 1 is the
+    decomposition `bench.py --gpus 8` runs (the 8-GPU case gpurun cannot reach)."""
     out = tmp_path / f"sched_{nh}x{nw}.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nh * nw}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
