@@ -745,8 +745,9 @@ def run_ours(args, ws, rank, local):
                    "data": "synthetic (uniform(-1,1) fields of the named shape)", "config": workload_config(args),
                    "roofline": rec["roofline"], "cpu_baseline": cpu, "e2e": rec["e2e"],
                    "gpu_launches": rec["gpu_launches"], "clocks": rec["clocks"]}
-            if "step_hbm" in rec:
-                out["step_hbm"] = rec["step_hbm"]
+            for k in ("step_hbm", "reference_layout"):
+                if k in rec:
+                    out[k] = rec[k]
             print(json.dumps(out), flush=True)
         return
     extra = {}
