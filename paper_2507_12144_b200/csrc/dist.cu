@@ -154,21 +154,15 @@ __global__ void __launch_bounds__(256) box_copy_kernel(const DBox* __restrict__ 
 // Coefficient payload index (complex units) of (field f, degree l, order m), m <= l:
 //   off[p] + f * tri[p] + rowoff[robase[p] + l - l0(i)] + m - m0(j),  p = i * nw + j
 // with (i, l - l0) = lmap[l], (j, m - m0) = mmap[m]  (dist_layout.hpp, ShtLayout).
-// rowbase(f, l, j) is everything but the order term, so a tile stages it once per
-// (degree, order block) in shared memory and the per-element index is one add.
+// The host flattens everything but the field term into per-(degree, order block) tables,
+//   b0[l * nw + j] = off[p] + rowoff[robase[p] + l - l0(i)] - m0(j),  tr[l * nw + j] = tri[p]
+// so a tile stages rowbase(f, l, j) = b0 + f * tr with two independent loads (the chained
+// lmap -> off / tri / robase -> rowoff lookups were a 4-deep dependent-load chain per CTA).
 struct PayloadMap {
-    const int2* lmap;
     const int2* mmap;
-    const int64_t* off;
-    const int64_t* tri;
-    const int64_t* rowoff;
-    const int64_t* robase;
+    const int64_t* b0;
+    const int64_t* tr;
     int nw;
-    __device__ __forceinline__ int64_t rowbase(int64_t f, int l, int j, int m0j) const {
-        const int2 li = lmap[l];
-        const int p = li.x * nw + j;
-        return off[p] + f * tri[p] + rowoff[robase[p] + li.y] - m0j;
-    }
 };
 constexpr int kMaxNw = 16;  // azimuth ranks a staged tile supports (>= every B200 box)
 
@@ -181,13 +175,10 @@ __device__ __forceinline__ void stage_rowbase(int64_t* base, const PayloadMap& p
     nj = pm.mmap[mlast].x - jlo + 1;
     for (int e = threadIdx.x; e < nl * nj; e += blockDim.x) {
         const int ll = e / nj, jj = e - ll * nj;
-        const int l = lt + ll, j = jlo + jj;
+        const int l = lt + ll;
         if (l < lmax) {
-            // m0(j): the first order of block j is mt - mmap[mt].y + (sum of earlier blocks);
-            // recover it from the first order of the tile that falls in block j
-            int m = max(mt, 0);
-            while (m < mlast && pm.mmap[m].x < j) ++m;
-            base[ll * kMaxNw + jj] = pm.rowbase(f, l, j, m - pm.mmap[m].y);
+            const int64_t t = static_cast<int64_t>(l) * pm.nw + jlo + jj;
+            base[ll * kMaxNw + jj] = __ldg(pm.b0 + t) + f * __ldg(pm.tr + t);
         }
     }
 }
@@ -214,18 +205,32 @@ __global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict_
     int jlo, nj;
     stage_rowbase(base, pm, f, lt, DL, lmax, mt, mmax, jlo, nj);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = warp; r < 128; r += 8) {
-        const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
-        const int m = mt + mlt;
-        if (m >= mmax) continue;
-        const int d = lt - m - p;
-        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
-        const int l = m + p + 2 * lp;
-        if (lp >= Lp || l >= lmax || l >= lt + DL) continue;
-        const float v = cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp];
-        const int sr = srow_of<DL>(l - lt);
-        if (ri) tim[sr][mlt] = v;
-        else tre[sr][mlt] = v;
+    {  // a warp's 16 rows: all loads issued before any shared-memory store
+        constexpr int RPW = 128 / 8;
+        float v[RPW];
+        int sr[RPW];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int r = warp + 8 * i;
+            const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
+            const int m = mt + mlt;
+            const int d = lt - m - p;
+            const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
+            const int l = m + p + 2 * lp;
+            sr[i] = -1;
+            v[i] = 0.f;
+            if (m < mmax && lp < Lp && l < lmax && l < lt + DL) {
+                v[i] = __ldg(cint + ((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp);
+                sr[i] = srow_of<DL>(l - lt);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            if (sr[i] < 0) continue;
+            const int r = warp + 8 * i;
+            if (r & 1) tim[sr[i]][r >> 2] = v[i];
+            else tre[sr[i]][r >> 2] = v[i];
+        }
     }
     __syncthreads();
     const int mme = mt + (threadIdx.x & 31);  // this thread's order (blockDim % 32 == 0)
@@ -256,14 +261,23 @@ __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restri
     __syncthreads();
     const int mme = mt + (threadIdx.x & 31);  // this thread's order (blockDim % 32 == 0)
     const int jme = mme < mmax ? pm.mmap[mme].x - jlo : 0;
-    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
-        const int dl = e >> 5, mlt = e & 31;
-        const int l = lt + dl, m = mt + mlt;
-        const float2 v = (l < lmax && m < mmax && m <= l) ? payload[base[dl * kMaxNw + jme] + m]
-                                                          : make_float2(0.f, 0.f);
-        const int sr = srow_of<DL>(dl);
-        tre[sr][mlt] = v.x;
-        tim[sr][mlt] = v.y;
+    {  // the tile's 8 loads per thread issued before any shared-memory store
+        constexpr int EPT = DL * 32 / 256;
+        float2 v[EPT];
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            const int e = threadIdx.x + 256 * i;
+            const int dl = e >> 5, m = mt + (e & 31), l = lt + dl;
+            v[i] = (l < lmax && m < mmax && m <= l) ? __ldg(payload + base[dl * kMaxNw + jme] + m)
+                                                    : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            const int e = threadIdx.x + 256 * i;
+            const int sr = srow_of<DL>(e >> 5);
+            tre[sr][e & 31] = v[i].x;
+            tim[sr][e & 31] = v[i].y;
+        }
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -392,7 +406,8 @@ struct ShtChunk {
     int64_t c_begin = 0;
     Exchange xa, xb, xia, xib;
     BoxList fwd_unpack, inv_pack;
-    DevBuf<int64_t> off_b, off_ia;  // payload offsets per block (complex units)
+    DevBuf<int64_t> b0_b, b0_ia;  // flattened payload row bases per (degree, order block) (PayloadMap)
+    std::vector<int64_t> off_b_h, off_ia_h;  // payload offsets per block (complex units)
     int64_t bytes_fa = 0, bytes_fb = 0, bytes_ia = 0, bytes_ib = 0;
 };
 
@@ -423,8 +438,8 @@ struct sph_dist_sht_plan_s {
     sph::ShtLayout lay;  // the whole problem (ranges reported to the caller)
     int64_t q = 0, i = 0, j = 0;
     std::vector<std::unique_ptr<sph::ShtChunk>> chunks;
-    sph::DevBuf<int2> lmap, mmap;
-    sph::DevBuf<int64_t> tri, rowoff, robase, rowoff_me;
+    sph::DevBuf<int2> mmap;
+    sph::DevBuf<int64_t> tr, rowoff_me;
     int64_t tri_me = 0;
     // workspace carve (bytes): stage / pay / mine are double-buffered
     int64_t o_stage[2] = {0, 0}, o_pay[2] = {0, 0}, o_mine[2] = {0, 0};
@@ -482,8 +497,8 @@ struct sph_dist_sht_plan_s {
                 ob[s2] = ch->xb.send_off[s2] / 2;
                 oia[s2] = ch->xia.recv_off[s2] / 2;
             }
-            upload_vec(ch->off_b, ob);
-            upload_vec(ch->off_ia, oia);
+            ch->off_b_h = ob;
+            ch->off_ia_h = oia;
             ch->bytes_fa = world_bytes(L.P, planes, [&](int64_t r) { return L.fwd_fields(r); });
             ch->bytes_fb = world_bytes(L.P, planes, [&](int64_t r) { return L.fwd_coeffs(r); });
             ch->bytes_ia = world_bytes(L.P, planes, [&](int64_t r) { return L.inv_coeffs(r); });
@@ -497,25 +512,36 @@ struct sph_dist_sht_plan_s {
             m_mine = std::max({m_mine, ch->xb.recv_total(), ch->xia.send_total()});
             chunks.push_back(std::move(ch));
         }
-        std::vector<int2> lm(p->lmax), mm(p->mmax);
-        for (int64_t a = 0; a < nh; ++a)
-            for (int64_t k = 0; k < lay.lp[a]; ++k) lm[lay.l0(a) + k] = make_int2(static_cast<int>(a), static_cast<int>(k));
+        std::vector<int2> mm(p->mmax);
         for (int64_t b = 0; b < nw; ++b)
             for (int64_t k = 0; k < lay.mp[b]; ++k) mm[lay.m0(b) + k] = make_int2(static_cast<int>(b), static_cast<int>(k));
-        upload_vec(lmap, lm);
         upload_vec(mmap, mm);
-        std::vector<int64_t> tr(lay.P), rb(lay.P), ro;
-        for (int64_t s2 = 0; s2 < lay.P; ++s2) {
-            const auto r = lay.rowoff(s2);
-            tr[s2] = r.back();
-            rb[s2] = static_cast<int64_t>(ro.size());
-            ro.insert(ro.end(), r.begin(), r.end());
+        // PayloadMap tables: tr[l][j] = tri of block (i(l), j); the chunk's b0[l][j] adds its
+        // block offsets (rowoff of block p at degree l, minus the block's first order)
+        std::vector<std::vector<int64_t>> rof(lay.P);
+        for (int64_t s2 = 0; s2 < lay.P; ++s2) rof[s2] = lay.rowoff(s2);
+        tri_me = rof[q].back();
+        std::vector<int64_t> trt(p->lmax * nw), rel(p->lmax * nw);
+        std::vector<int64_t> pof(p->lmax * nw);
+        for (int64_t a = 0; a < nh; ++a)
+            for (int64_t k = 0; k < lay.lp[a]; ++k)
+                for (int64_t b = 0; b < nw; ++b) {
+                    const int64_t t = (lay.l0(a) + k) * nw + b, s2 = a * nw + b;
+                    trt[t] = rof[s2].back();
+                    rel[t] = rof[s2][k] - lay.m0(b);
+                    pof[t] = s2;
+                }
+        upload_vec(tr, trt);
+        for (auto& chp : chunks) {
+            std::vector<int64_t> bb(trt.size()), bi(trt.size());
+            for (size_t t = 0; t < trt.size(); ++t) {
+                bb[t] = chp->off_b_h[pof[t]] + rel[t];
+                bi[t] = chp->off_ia_h[pof[t]] + rel[t];
+            }
+            upload_vec(chp->b0_b, bb);
+            upload_vec(chp->b0_ia, bi);
         }
-        tri_me = tr[q];
-        upload_vec(tri, tr);
-        upload_vec(robase, rb);
-        upload_vec(rowoff, ro);
-        upload_vec(rowoff_me, lay.rowoff(q));
+        upload_vec(rowoff_me, rof[q]);
         Carve cv;
         for (int b = 0; b < 2; ++b) o_stage[b] = cv.take(4 * m_stage);
         o_full = cv.take(4 * m_full);
@@ -550,8 +576,8 @@ struct sph_dist_sht_plan_s {
         if (own_ws.n < static_cast<size_t>(total)) own_ws.alloc(total, true);
         return own_ws.p;
     }
-    sph::PayloadMap pmap(const sph::DevBuf<int64_t>& off) const {
-        return {lmap.p, mmap.p, off.p, tri.p, rowoff.p, robase.p, static_cast<int>(lay.nw)};
+    sph::PayloadMap pmap(const sph::DevBuf<int64_t>& b0) const {
+        return {mmap.p, b0.p, tr.p, static_cast<int>(lay.nw)};
     }
     void log(const char* op, int64_t bytes) {
         std::lock_guard<std::mutex> lk(comm->mu);
@@ -625,7 +651,7 @@ struct sph_dist_sht_plan_s {
                 dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((lay.lmax + LT - 1) / LT),
                        static_cast<unsigned>(cq));
                 cint_pack_kernel<LT><<<g, 256, 0, st>>>(at<float>(w, o_cint), cq, static_cast<int>(lay.lmax),
-                                                        static_cast<int>(lay.mmax), sht->Lp, pmap(ch.off_b),
+                                                        static_cast<int>(lay.mmax), sht->Lp, pmap(ch.b0_b),
                                                         at<float2>(w, o_pay[b]));
                 SPH_LAUNCH_CHECK();
                 count_launch();
@@ -711,7 +737,7 @@ struct sph_dist_sht_plan_s {
                            static_cast<unsigned>(cq));
                     cint_unpack_kernel<<<g, 256, 0, st>>>(at<const float2>(w, o_pay[b]), cq,
                                                           static_cast<int>(lay.lmax), static_cast<int>(lay.mmax),
-                                                          sht->Lp, pmap(ch.off_ia), at<float>(w, o_cint));
+                                                          sht->Lp, pmap(ch.b0_ia), at<float>(w, o_cint));
                     SPH_LAUNCH_CHECK();
                     count_launch();
                 }
