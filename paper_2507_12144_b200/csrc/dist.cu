@@ -406,6 +406,13 @@ struct ShtChunk {
     int64_t c_begin = 0;
     Exchange xa, xb, xia, xib;
     BoxList fwd_unpack, inv_pack;
+    // nw == 1: every stage block holds whole rings, so the ring transforms address the
+    // stage buffers in place through per-latitude tables (fft.cuh RingRows: roff, then
+    // fstr, nlat each) and the unpack / pack box copies are skipped
+    bool direct = false;
+    DevBuf<int64_t> rows_a, rows_b;
+    RingRows ring_a() const { return {rows_a.p, rows_a.p ? rows_a.p + rows_a.n / 2 : nullptr}; }
+    RingRows ring_b() const { return {rows_b.p, rows_b.p ? rows_b.p + rows_b.n / 2 : nullptr}; }
     DevBuf<int64_t> b0_b, b0_ia;  // flattened payload row bases per (degree, order block) (PayloadMap)
     std::vector<int64_t> off_b_h, off_ia_h;  // payload offsets per block (complex units)
     int64_t bytes_fa = 0, bytes_fb = 0, bytes_ia = 0, bytes_ib = 0;
@@ -492,6 +499,31 @@ struct sph_dist_sht_plan_s {
             ch->xib = L.inv_fields(q);
             ch->fwd_unpack.set(L.fwd_unpack(q));
             ch->inv_pack.set(L.inv_pack(q));
+            ch->direct = nw == 1 && L.cq(q) > 0 && !std::getenv("SPH_DIST_BOXCOPY");
+            if (ch->direct) {
+                // ring rows of the stage blocks: fields side offset h * nlon, stage side
+                // (block offset + c * row stride), per-field stride of the block
+                const int64_t nlat = p->nlat, nlon = p->nlon;
+                auto tables = [&](const std::vector<Box>& bs, bool fields_is_dst) {
+                    std::vector<int64_t> t(2 * nlat, -1);
+                    for (const Box& b : bs) {
+                        const int64_t foff = fields_is_dst ? b.dst_off : b.src_off;
+                        const int64_t soff = fields_is_dst ? b.src_off : b.dst_off;
+                        const int64_t fs0 = fields_is_dst ? b.d0 : b.s0, fs1 = fields_is_dst ? b.d1 : b.s1;
+                        const int64_t ss0 = fields_is_dst ? b.s0 : b.d0, ss1 = fields_is_dst ? b.s1 : b.d1;
+                        require(b.n2 == nlon && foff % nlon == 0 && fs0 == nlat * nlon && fs1 == nlon,
+                                "dist_sht: stage block is not whole rings");
+                        for (int64_t c = 0; c < b.n1; ++c) {
+                            t[foff / nlon + c] = soff + c * ss1;
+                            t[nlat + foff / nlon + c] = ss0;
+                        }
+                    }
+                    for (int64_t h = 0; h < nlat; ++h) require(t[h] >= 0, "dist_sht: stage rows do not cover the grid");
+                    return t;
+                };
+                upload_vec(ch->rows_a, tables(L.fwd_unpack(q), true));
+                upload_vec(ch->rows_b, tables(L.inv_pack(q), false));
+            }
             std::vector<int64_t> ob(L.P), oia(L.P);
             for (int64_t s2 = 0; s2 < L.P; ++s2) {
                 ob[s2] = ch->xb.send_off[s2] / 2;
@@ -642,10 +674,18 @@ struct sph_dist_sht_plan_s {
             if (k + 1 < n) issue_a(k + 1);
             // compute of chunk k on the caller's stream
             wait(st, eA[b]);
-            ch.fwd_unpack.run(at<float>(w, o_stage[b]), at<float>(w, o_full), st, "dist_unpack_fields");
-            rec(eUA[b], st);
+            if (!ch.direct) {
+                ch.fwd_unpack.run(at<float>(w, o_stage[b]), at<float>(w, o_full), st, "dist_unpack_fields");
+                rec(eUA[b], st);
+            }
             if (cq > 0) {
-                sht->forward(at<float>(w, o_full), cq, at<float>(w, o_cint), SPH_LAYOUT_INTERNAL, w + o_shtws, st);
+                if (ch.direct) {  // the fold reads the received blocks in place
+                    sht->forward(at<float>(w, o_stage[b]), cq, at<float>(w, o_cint), SPH_LAYOUT_INTERNAL, w + o_shtws,
+                                 st, ch.ring_a());
+                    rec(eUA[b], st);
+                } else {
+                    sht->forward(at<float>(w, o_full), cq, at<float>(w, o_cint), SPH_LAYOUT_INTERNAL, w + o_shtws, st);
+                }
                 ProfScope prof("dist_pack_cint", st, 4.0 * sht->cint_elems(cq) + 4.0 * ch.xb.send_total());
                 constexpr int LT = 64;
                 dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((lay.lmax + LT - 1) / LT),
@@ -742,9 +782,15 @@ struct sph_dist_sht_plan_s {
                     count_launch();
                 }
                 rec(eUC[b], st);
-                sht->inverse(at<float>(w, o_cint), cq, SPH_LAYOUT_INTERNAL, at<float>(w, o_full), w + o_shtws, st);
-                if (k >= 2) wait(st, eB2[b]);  // stage[b] sent by chunk k-2's outbound exchange
-                ch.inv_pack.run(at<float>(w, o_full), at<float>(w, o_stage[b]), st, "dist_pack_fields");
+                if (ch.direct) {  // the unfold writes the outbound blocks in place
+                    if (k >= 2) wait(st, eB2[b]);  // stage[b] sent by chunk k-2's outbound exchange
+                    sht->inverse(at<float>(w, o_cint), cq, SPH_LAYOUT_INTERNAL, at<float>(w, o_stage[b]), w + o_shtws,
+                                 st, ch.ring_b());
+                } else {
+                    sht->inverse(at<float>(w, o_cint), cq, SPH_LAYOUT_INTERNAL, at<float>(w, o_full), w + o_shtws, st);
+                    if (k >= 2) wait(st, eB2[b]);  // stage[b] sent by chunk k-2's outbound exchange
+                    ch.inv_pack.run(at<float>(w, o_full), at<float>(w, o_stage[b]), st, "dist_pack_fields");
+                }
             } else {
                 rec(eUC[b], st);
             }

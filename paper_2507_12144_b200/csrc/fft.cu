@@ -181,6 +181,11 @@ struct FoldIO {
     float* eo;
     int64_t Rq, twoF;
     int fy_fast = 0;  // grid (field group, ring quad): concurrent CTAs fill adjacent E/O runs
+    RingRows rrows{};  // optional per-latitude ring addressing (fft.cuh)
+    // ring (field f, latitude row) of x
+    __device__ __forceinline__ const float* ring(int64_t f, int row, int n) const {
+        return rrows.roff ? x + f * rrows.fstr[row] + rrows.roff[row] : x + (f * nlat + row) * static_cast<int64_t>(n);
+    }
     __device__ __forceinline__ int qx_of() const { return fy_fast ? blockIdx.y : blockIdx.x; }
     __device__ __forceinline__ int fy_of() const { return fy_fast ? blockIdx.x : blockIdx.y; }
     // slot p of a CTA -> (ring pair, field); false if outside [0, R) x [0, F).
@@ -204,10 +209,9 @@ struct FoldIO {
                                           float& sb) const {
         int rr, f;
         if (!slot(P, p, rr, f)) return false;
-        const float* xf = x + static_cast<int64_t>(f) * nlat * n;
         const int2 rw = rows[rr];
-        pa = xf + static_cast<int64_t>(rw.x) * n;
-        pb = xf + static_cast<int64_t>(rw.y < 0 ? rw.x : rw.y) * n;
+        pa = ring(f, rw.x, n);
+        pb = ring(f, rw.y < 0 ? rw.x : rw.y, n);
         sb = rw.y < 0 ? 0.f : 1.f;
         return true;
     }
@@ -220,10 +224,9 @@ struct FoldIO {
                 float4* d = reinterpret_cast<float4*>(buf + j * ld);
                 int rr, f;
                 if (slot(P, j, rr, f)) {
-                    const float* xf = x + static_cast<int64_t>(f) * nlat * n;
                     const int2 rw = rows[rr];
-                    const float4* pa = reinterpret_cast<const float4*>(xf + static_cast<int64_t>(rw.x) * n);
-                    const float4* pb = reinterpret_cast<const float4*>(xf + static_cast<int64_t>(rw.y < 0 ? rw.x : rw.y) * n);
+                    const float4* pa = reinterpret_cast<const float4*>(ring(f, rw.x, n));
+                    const float4* pb = reinterpret_cast<const float4*>(ring(f, rw.y < 0 ? rw.x : rw.y, n));
                     const bool hb = rw.y >= 0;
                     for (int k4 = lane; k4 < n4; k4 += 32) {
                         const float4 va = __ldg(pa + k4);
@@ -244,12 +247,13 @@ struct FoldIO {
                 int rr, f;
                 const bool ok = slot(P, j, rr, f);
                 const int2 rw = ok ? rows[rr] : make_int2(0, -1);
-                const float* xf = x + static_cast<int64_t>(ok ? f : 0) * nlat * n;
+                const float* xa = ok ? ring(f, rw.x, n) : x;
+                const float* xb = ok && rw.y >= 0 ? ring(f, rw.y, n) : x;
                 for (int k = lane; k < n; k += 32) {
                     float2 v = make_float2(0.f, 0.f);
                     if (ok) {
-                        v.x = xf[static_cast<int64_t>(rw.x) * n + k];
-                        if (rw.y >= 0) v.y = xf[static_cast<int64_t>(rw.y) * n + k];
+                        v.x = xa[k];
+                        if (rw.y >= 0) v.y = xb[k];
                     }
                     buf[j * ld + k] = v;
                 }
@@ -329,6 +333,10 @@ struct UnfoldIO {
     int64_t F, twoF;
     float* y;
     int64_t T;  // EOI_TILE-row field tiles (gemm.cuh)
+    RingRows rrows{};  // optional per-latitude ring addressing (fft.cuh)
+    __device__ __forceinline__ float* ring(int64_t f, int row, int n) const {
+        return rrows.roff ? y + f * rrows.fstr[row] + rrows.roff[row] : y + (f * nlat + row) * static_cast<int64_t>(n);
+    }
     template <int N1, int N2>
     __device__ __forceinline__ void store_b(int P, int N, int p, int k1, const float2 (&b)[N2]) const {
         const int64_t f = static_cast<int64_t>(blockIdx.x) * P + p;
@@ -338,12 +346,11 @@ struct UnfoldIO {
         }
         if (f >= F) return;
         const int2 rw = rows[blockIdx.y];
-        float* yf = y + f * nlat * N;
-        float* pa = yf + static_cast<int64_t>(rw.x) * N + k1;
+        float* pa = ring(f, rw.x, N) + k1;
 #pragma unroll
         for (int k2 = 0; k2 < N2; ++k2) pa[N1 * k2] = b[k2].x;
         if (rw.y >= 0) {
-            float* pb = yf + static_cast<int64_t>(rw.y) * N + k1;
+            float* pb = ring(f, rw.y, N) + k1;
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) pb[N1 * k2] = b[k2].y;
         }
@@ -408,9 +415,8 @@ struct UnfoldIO {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
         for (int j = warp; j < nf; j += nw) {
             const float2* zr = buf + j * ld;
-            float* yf = y + (f0 + j) * nlat * n;
-            float* pa = yf + static_cast<int64_t>(rw.x) * n;
-            float* pb = yf + static_cast<int64_t>(rw.y) * n;
+            float* pa = ring(f0 + j, rw.x, n);
+            float* pb = rw.y >= 0 ? ring(f0 + j, rw.y, n) : pa;
             for (int k = lane; k < n; k += 32) {
                 pa[k] = zr[k].x;
                 if (rw.y >= 0) pb[k] = zr[k].y;
@@ -974,13 +980,14 @@ void FftPlan::build(int n_) {
 }
 
 void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int64_t F, int nlat,
-                      int mmax, float* eo, int64_t ld_eo, cudaStream_t st) {
+                      int mmax, float* eo, int64_t ld_eo, cudaStream_t st, RingRows rr) {
     if (F == 0) return;
     require(F <= 65535, "fft: at most 65535 fields per call");
     const int P = fp.fft4_n1 ? fold_threads() / fp.fft4_n1 : rpb_of(fp);
     static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
     require(ld_eo % 4 == 0, "fft: E/O ring-pair padding must be a multiple of 4");
     FoldIO io{fft_dbg, x, fr.d_rows.p, fr.R, nlat, mmax, eo, ld_eo / 4, 2 * F};
+    io.rrows = rr;
     // field groups fastest (measured at cfg2: 2.21 -> 2.11 ms): concurrently running CTAs
     // write adjacent 64-byte runs of the same (m, parity, quad) E/O row instead of runs
     // 32 KB apart; SPH_FFT_FY_FAST=0 restores quad-fastest
@@ -1007,7 +1014,7 @@ void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int
 
 void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi, int64_t F,
                         int nlat, int mmax, int msynth, int lmax, int64_t ld_eo, float* y,
-                        cudaStream_t st) {
+                        cudaStream_t st, RingRows rr) {
     (void)mmax;
     if (F == 0) return;
     require(F <= 65535, "fft: at most 65535 fields per call");
@@ -1015,6 +1022,7 @@ void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi,
     (void)ld_eo;  // EOi is [m][parity][R][2F] (transposed GEMM store)
     static const int fft_dbg = std::getenv("SPH_FFT_DEBUG") ? std::atoi(std::getenv("SPH_FFT_DEBUG")) : 0;
     UnfoldIO io{fft_dbg, eoi, fr.d_rows.p, fr.R, nlat, msynth, lmax, F, 2 * F, y, (2 * F + EOI_TILE - 1) / EOI_TILE};
+    io.rrows = rr;
     require(fr.R <= 65535, "fft: too many latitude rows");
     dim3 grid(static_cast<unsigned>((F + P - 1) / P), static_cast<unsigned>(fr.R));
     const double bytes = 4.0 * F * (static_cast<double>(nlat) * fp.n + 4.0 * msynth * fr.R);

@@ -37,10 +37,19 @@ struct FoldRows {
     DevBuf<int2> d_rows;
 };
 
+// Optional ring addressing for the SHT ring transforms: ring (field f, latitude row h) at
+// base + f * fstr[h] + roff[h] (device arrays over latitude rows) instead of the dense
+// [F][nlat][nlon] layout -- the distributed SHT reads / writes its all-to-all stage buffers
+// in place (csrc/dist.cu).  Null pointers: the dense layout.
+struct RingRows {
+    const int64_t* roff = nullptr;
+    const int64_t* fstr = nullptr;
+};
+
 // Forward: x [F][nlat][nlon] -> EO[(m*2+p)*2F + 2f+reim][r] (row stride ld_eo),
 // m < mmax.  (E for p = 0, O for p = 1; raw DFT sums, no 2pi/nlon scale.)
 void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int64_t F,
-                      int nlat, int mmax, float* eo, int64_t ld_eo, cudaStream_t st);
+                      int nlat, int mmax, float* eo, int64_t ld_eo, cudaStream_t st, RingRows rr = {});
 
 // Inverse: EOi[(m*2+p)][r][2f+reim] (Ev/Od per folded row, the inverse GEMM's
 // transposed store; ld_eo unused) -> y [F][nlat][nlon].
@@ -48,7 +57,7 @@ void fft_forward_fold(const FftPlan& fp, const FoldRows& fr, const float* x, int
 // treated as zero: L_mp = number of l in [m, lmax) with (l - m) % 2 == p.
 void fft_inverse_unfold(const FftPlan& fp, const FoldRows& fr, const float* eoi, int64_t F,
                         int nlat, int mmax, int msynth, int lmax, int64_t ld_eo, float* y,
-                        cudaStream_t st);
+                        cudaStream_t st, RingRows rr = {});
 
 // Plain forward ring transform for the distributed stage (distsim.hpp:413-430):
 // rings [nrings][nlon] -> bins [nrings][nbins] complex64, scaled by `scale`.

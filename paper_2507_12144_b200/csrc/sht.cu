@@ -529,7 +529,8 @@ void* ShtPlan::workspace(void* ws, int64_t bytes) {
     return own_ws.p;
 }
 
-void ShtPlan::forward(const float* x, int64_t F, float* out, int layout, void* ws, cudaStream_t st) {
+void ShtPlan::forward(const float* x, int64_t F, float* out, int layout, void* ws, cudaStream_t st,
+                      RingRows rr) {
     require(kind == SPH_GAUSSIAN || (flags & (SPH_FLAG_ALLOW_EQUIANGULAR_FORWARD | SPH_FLAG_ADJOINT)),
             "sht_forward: requires a gaussian grid");
     require(nlat >= lmax && nlon >= 2 * mmax, "sht_forward: resolution insufficient for lmax/mmax");
@@ -542,14 +543,14 @@ void ShtPlan::forward(const float* x, int64_t F, float* out, int layout, void* w
     uint8_t* w8 = static_cast<uint8_t*>(workspace(ws, workspace_bytes(F)));
     float* eo = reinterpret_cast<float*>(w8);
     float* ctmp = reinterpret_cast<float*>(w8 + round_up(4 * eo_elems(F), 256));
-    fft_forward_fold(fft, fold, x, F, static_cast<int>(nlat), static_cast<int>(mmax), eo, Rp, st);
+    fft_forward_fold(fft, fold, x, F, static_cast<int>(nlat), static_cast<int>(mmax), eo, Rp, st, rr);
     float* target = layout == SPH_LAYOUT_INTERNAL ? out : ctmp;
     gemm_run(fwd_gemm(F), eo, target, prec, st);
     if (layout == SPH_LAYOUT_DENSE_LM) cint_to_dense(*this, target, F, 0, mmax, mmax, out, st);
 }
 
 void ShtPlan::inverse(const float* coeffs, int64_t F, int layout, float* y, void* ws,
-                      cudaStream_t st) {
+                      cudaStream_t st, RingRows rr) {
     require(layout == SPH_LAYOUT_DENSE_LM || layout == SPH_LAYOUT_INTERNAL, "sht_inverse: bad layout");
     require(F >= 0, "sht_inverse: negative field count");
     if (F == 0) return;
@@ -566,7 +567,7 @@ void ShtPlan::inverse(const float* coeffs, int64_t F, int layout, float* y, void
     }
     gemm_run(inv_gemm(F), src, eoi, prec, st);
     fft_inverse_unfold(fft, fold, eoi, F, static_cast<int>(nlat), static_cast<int>(mmax),
-                       static_cast<int>(msynth), static_cast<int>(lmax), Rp, y, st);
+                       static_cast<int>(msynth), static_cast<int>(lmax), Rp, y, st, rr);
 }
 
 void ShtPlan::fft_stage(const float* rings, int64_t F, int64_t h, float* bins, cudaStream_t st) {

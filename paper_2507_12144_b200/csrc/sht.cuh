@@ -58,8 +58,12 @@ struct ShtPlan {
     const GroupedGemm& stage_gemm(int64_t F, int64_t m0, int64_t mcount);
     void* workspace(void* ws, int64_t bytes);
 
-    void forward(const float* x, int64_t F, float* out, int layout, void* ws, cudaStream_t st);
-    void inverse(const float* coeffs, int64_t F, int layout, float* y, void* ws, cudaStream_t st);
+    // rr: optional ring addressing of x / y (fft.cuh RingRows; the distributed SHT's stage
+    // buffers), default the dense [F][nlat][nlon] layout
+    void forward(const float* x, int64_t F, float* out, int layout, void* ws, cudaStream_t st,
+                 RingRows rr = {});
+    void inverse(const float* coeffs, int64_t F, int layout, float* y, void* ws, cudaStream_t st,
+                 RingRows rr = {});
     void fft_stage(const float* rings, int64_t F, int64_t h, float* bins, cudaStream_t st);
     void legendre_stage(const float* bins, int64_t F, int64_t m0, int64_t mcount, float* coeffs,
                         void* ws, cudaStream_t st);
