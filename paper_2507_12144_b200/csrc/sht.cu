@@ -15,6 +15,7 @@
 #include <thread>
 
 #include "sht.cuh"
+#include "tile_rows.cuh"
 
 namespace sph {
 
@@ -129,74 +130,56 @@ void upload(DevBuf<T>& d, const std::vector<T>& h) {
 }
 
 // ---------------------------------------------------------------- kernels
-// Internal coefficient layout cint[(ml*2 + p)][2F (f, re/im)][Lp] (l = m + p + 2 lp,
-// lp contiguous) <-> dense [F][lmax][mcols] complex (m contiguous): tiled transposes
-// through shared memory, both global sides in contiguous runs.  A (order, parity, re/im)
-// row of cint covers every OTHER degree, so the tile stores degree rows split by parity
-// (srow = (dl & 1) * half + dl / 2): a warp walking one cint row then touches consecutive
-// smem rows (stride 33 words -> conflict-free), and a dense row is one smem row.
-// (Round 1 interleaved the degrees: rows two apart put a warp's stores on 8 banks.)
-template <int DL>
-__device__ __forceinline__ int srow_of(int dl) {
-    return (dl & 1) * (DL / 2) + (dl >> 1);
-}
-
+// Internal coefficient layout <-> dense [F][lmax][mcols] complex (m contiguous): tiled
+// transposes through shared memory (tile_rows.cuh), both global sides in contiguous runs.
 // CTA (32 orders, 64 degrees, field f): 128 cint rows (order, parity, re/im) read as
 // 32-lane runs of lp (each run is the tile's 32 degrees of that parity class), dense rows
-// written as 32-order float2 runs (zeros above the diagonal).
+// written as 32-order float2 runs (zeros above the diagonal, decided at the store).
 __global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int lmax,
                                                             int m0, int mcount, int out_mcount, int Lp,
                                                             float2* __restrict__ dense, int64_t f0) {
-    constexpr int DL = 64;
+    constexpr int DL = 64, RPW = 128 / 8;
     __shared__ float tre[DL][33], tim[DL][33];
     // fields slowest: concurrently running CTAs share a field's dense rows (fields fastest,
     // for adjacent C_int rows instead, measured 2.42 vs 2.27 ms at 1024 fields)
     const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;
     const int64_t f = f0 + blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
-        tre[e >> 5][e & 31] = 0.f;
-        tim[e >> 5][e & 31] = 0.f;
-    }
-    __syncthreads();
     if (m0 + mt <= lt + DL - 1) {  // else the whole tile is above the diagonal (m > l)
-        // a warp's 16 rows: all loads issued before any shared-memory store (one load in
-        // flight per warp left the kernel latency-bound)
-        constexpr int RPW = 128 / 8;
+        const int p = (warp >> 1) & 1, ri = warp & 1;
+        float (*T)[33] = ri ? tim : tre;
+        const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
+        const float* row0 = cint + ((static_cast<int64_t>(mt + (warp >> 2)) * 2 + p) * 2 * F + 2 * f + ri) * Lp;
         float v[RPW];
-        int sr[RPW];
+        bool ok[RPW];
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            const int r = warp + 8 * i;
-            const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
-            const int ml = mt + mlt;
-            const int m = m0 + ml;
-            const int d = lt - m - p;
-            const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
-            const int l = m + p + 2 * lp;
-            sr[i] = -1;
-            v[i] = 0.f;
-            if (ml < mcount && lp < Lp && l < lmax && l < lt + DL) {
-                v[i] = __ldg(cint + ((static_cast<int64_t>(ml) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp);
-                sr[i] = srow_of<DL>(l - lt);
-            }
+        for (int i = 0; i < RPW; ++i) {  // all loads before any shared-memory store
+            const int ml = mt + (warp >> 2) + 2 * i;
+            const TileRow tr(lt - (m0 + ml) - p);
+            const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
+            ok[i] = ml < mcount && dl < DL && lp < Lp && lt + dl < lmax;
+            v[i] = ok[i] ? __ldg(row0 + i * gstep + lp) : 0.f;
         }
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-            if (sr[i] < 0) continue;
-            const int r = warp + 8 * i;
-            const int mlt = r >> 2, ri = r & 1;
-            if (ri) tim[sr[i]][mlt] = v[i];
-            else tre[sr[i]][mlt] = v[i];
+            if (!ok[i]) continue;
+            const int ml = mt + (warp >> 2) + 2 * i;
+            const TileRow tr(lt - (m0 + ml) - p);
+            T[tr.s0 + lane][(warp >> 2) + 2 * i] = v[i];
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
-        const int dl = e >> 5, mlt = e & 31;
-        const int64_t l = lt + dl;
-        const int oc = mt + mlt;
-        const int sr = srow_of<DL>(dl);
-        if (l < lmax && oc < out_mcount) dense[(f * lmax + l) * out_mcount + oc] = make_float2(tre[sr][mlt], tim[sr][mlt]);
+    const int oc = mt + lane;
+    const bool mok = oc < out_mcount;
+    const bool have = mt + lane < mcount;  // orders beyond mcount are zero columns
+    float2* dst = dense + (f * lmax + lt + warp) * out_mcount + oc;
+#pragma unroll
+    for (int i = 0; i < DL / 8; ++i) {
+        const int dl = warp + 8 * i, l = lt + dl;
+        if (l >= lmax || !mok) continue;
+        const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
+        const bool val = have && m0 + mt + lane <= l;
+        dst[static_cast<int64_t>(i) * 8 * out_mcount] = val ? make_float2(tre[sr][lane], tim[sr][lane]) : make_float2(0.f, 0.f);
     }
 }
 
@@ -208,44 +191,43 @@ __global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restr
 __global__ void __launch_bounds__(256) dense_to_cint_kernel(const float2* __restrict__ dense, int64_t F, int64_t lmax,
                                                             int64_t mmax, int Lp, float* __restrict__ cint,
                                                             int64_t f0) {
-    constexpr int DL = 64;
+    constexpr int DL = 64, RPW = 128 / 8, EPT = DL * 32 / 256;
     __shared__ float tre[DL][33], tim[DL][33];
     const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;  // fields slowest (3.60 vs 2.90 ms fastest)
     const int64_t f = f0 + blockIdx.z;
-    {  // the tile's 8 loads per thread issued before any shared-memory store
-        constexpr int EPT = DL * 32 / 256;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lmx = static_cast<int>(lmax), mmx = static_cast<int>(mmax);
+    {  // element i: degree lt + warp + 8 i, order mt + lane; all loads before the stores
+        const int m = mt + lane;
+        const float2* src = dense + (f * lmax + lt + warp) * mmax + m;
         float2 v[EPT];
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-            const int e = threadIdx.x + 256 * i;
-            const int dl = e >> 5, mlt = e & 31;
-            const int64_t l = lt + dl;
-            const int m = mt + mlt;
-            v[i] = (l < lmax && m < mmax && m <= l) ? __ldg(dense + (f * lmax + l) * mmax + m) : make_float2(0.f, 0.f);
+            const int l = lt + warp + 8 * i;
+            v[i] = (l < lmx && m < mmx && m <= l) ? __ldg(src + static_cast<int64_t>(i) * 8 * mmax) : make_float2(0.f, 0.f);
         }
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-            const int e = threadIdx.x + 256 * i;
-            const int sr = srow_of<DL>(e >> 5);
-            tre[sr][e & 31] = v[i].x;
-            tim[sr][e & 31] = v[i].y;
+            const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
+            tre[sr][lane] = v[i].x;
+            tim[sr][lane] = v[i].y;
         }
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = warp; r < 128; r += 8) {
-        const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
-        const int m = mt + mlt;
-        if (m >= mmax) continue;
-        const int d = lt - m - p;
-        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
-        const int l = m + p + 2 * lp;
-        const int n = static_cast<int>(lmax) - m;
-        const int Lmp = n <= 0 ? 0 : (p == 0 ? (n + 1) / 2 : n / 2);
-        if (l >= lt + DL || lp >= Lp || lp >= ((Lmp + 31) & ~31)) continue;
-        const int sr = srow_of<DL>(l - lt);
-        const float v = l < lmax ? (ri ? tim[sr][mlt] : tre[sr][mlt]) : 0.f;
-        cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp] = v;
+    const int p = (warp >> 1) & 1, ri = warp & 1;
+    const float (*T)[33] = ri ? tim : tre;
+    const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
+    float* row0 = cint + ((static_cast<int64_t>(mt + (warp >> 2)) * 2 + p) * 2 * F + 2 * f + ri) * Lp;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int mlt = (warp >> 2) + 2 * i, m = mt + mlt;
+        if (m >= mmx) continue;
+        const TileRow tr(lt - m - p);
+        const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
+        const int n = lmx - m;
+        const int Lmp = n <= 0 ? 0 : (n + 1 - p) >> 1;
+        if (dl >= DL || lp >= Lp || lp >= ((Lmp + 31) & ~31)) continue;
+        row0[i * gstep + lp] = lt + dl < lmx ? T[tr.s0 + lane][mlt] : 0.f;
     }
 }
 
