@@ -16,6 +16,7 @@
 
 #include "capi_util.cuh"
 #include "dist_layout.hpp"
+#include "tile_rows.cuh"
 
 namespace sph {
 
@@ -183,20 +184,12 @@ __device__ __forceinline__ void stage_rowbase(int64_t* base, const PayloadMap& p
     }
 }
 
-// Degree rows of a tile are stored split by parity (srow = (dl & 1) * DL/2 + dl / 2) so a
-// warp walking one C_int row (every other degree) hits consecutive shared-memory rows --
-// the layout of sht.cu's cint_to_dense / dense_to_cint.
-template <int DL>
-__device__ __forceinline__ int srow_of(int dl) {
-    return (dl & 1) * (DL / 2) + (dl >> 1);
-}
-
 // forward B pack: the local SHT's C_int [(m*2+p)][2F][Lp] (l = m + p + 2 lp) -> triangular
 // payloads of every destination block.  CTA (32 orders, 64 degrees, field f): C_int rows
-// read as 32-lane lp runs, payload written in order runs.
-template <int DL>
+// read as 32-lane lp runs, payload written in order runs (indexing: tile_rows.cuh).
 __global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict__ cint, int64_t F, int lmax, int mmax,
                                                         int Lp, PayloadMap pm, float2* __restrict__ payload) {
+    constexpr int DL = 64, RPW = 128 / 8;
     __shared__ float tre[DL][33], tim[DL][33];
     __shared__ int64_t base[DL * kMaxNw];
     const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;
@@ -206,41 +199,37 @@ __global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict_
     stage_rowbase(base, pm, f, lt, DL, lmax, mt, mmax, jlo, nj);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     {  // a warp's 16 rows: all loads issued before any shared-memory store
-        constexpr int RPW = 128 / 8;
+        const int p = (warp >> 1) & 1, ri = warp & 1;
+        float (*T)[33] = ri ? tim : tre;
+        const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
+        const float* row0 = cint + ((static_cast<int64_t>(mt + (warp >> 2)) * 2 + p) * 2 * F + 2 * f + ri) * Lp;
         float v[RPW];
-        int sr[RPW];
+        bool ok[RPW];
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-            const int r = warp + 8 * i;
-            const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
-            const int m = mt + mlt;
-            const int d = lt - m - p;
-            const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
-            const int l = m + p + 2 * lp;
-            sr[i] = -1;
-            v[i] = 0.f;
-            if (m < mmax && lp < Lp && l < lmax && l < lt + DL) {
-                v[i] = __ldg(cint + ((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp);
-                sr[i] = srow_of<DL>(l - lt);
-            }
+            const int m = mt + (warp >> 2) + 2 * i;
+            const TileRow tr(lt - m - p);
+            const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
+            ok[i] = m < mmax && dl < DL && lp < Lp && lt + dl < lmax;
+            v[i] = ok[i] ? __ldg(row0 + i * gstep + lp) : 0.f;
         }
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-            if (sr[i] < 0) continue;
-            const int r = warp + 8 * i;
-            if (r & 1) tim[sr[i]][r >> 2] = v[i];
-            else tre[sr[i]][r >> 2] = v[i];
+            if (!ok[i]) continue;
+            const TileRow tr(lt - (mt + (warp >> 2) + 2 * i) - p);
+            T[tr.s0 + lane][(warp >> 2) + 2 * i] = v[i];
         }
     }
     __syncthreads();
-    const int mme = mt + (threadIdx.x & 31);  // this thread's order (blockDim % 32 == 0)
-    const int jme = mme < mmax ? pm.mmap[mme].x - jlo : 0;
-    for (int e = threadIdx.x; e < DL * 32; e += blockDim.x) {
-        const int dl = e >> 5, mlt = e & 31;
-        const int l = lt + dl, m = mt + mlt;
-        const int sr = srow_of<DL>(dl);
-        if (l < lmax && m < mmax && m <= l)
-            payload[base[dl * kMaxNw + jme] + m] = make_float2(tre[sr][mlt], tim[sr][mlt]);
+    const int m = mt + lane;  // this thread's order
+    if (m >= mmax) return;
+    const int jme = pm.mmap[m].x - jlo;
+#pragma unroll
+    for (int i = 0; i < DL / 8; ++i) {
+        const int dl = warp + 8 * i, l = lt + dl;
+        if (l >= lmax || m > l) continue;
+        const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
+        payload[base[dl * kMaxNw + jme] + m] = make_float2(tre[sr][lane], tim[sr][lane]);
     }
 }
 
@@ -251,7 +240,7 @@ __global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict_
 // to its 32-wide k-block) is written, zeros beyond lmax.
 __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restrict__ payload, int64_t F, int lmax,
                                                           int mmax, int Lp, PayloadMap pm, float* __restrict__ cint) {
-    constexpr int DL = 64;
+    constexpr int DL = 64, RPW = 128 / 8, EPT = DL * 32 / 256;
     __shared__ float tre[DL][33], tim[DL][33];
     __shared__ int64_t base[DL * kMaxNw];
     const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;
@@ -259,41 +248,39 @@ __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restri
     int jlo, nj;
     stage_rowbase(base, pm, f, lt, DL, lmax, mt, mmax, jlo, nj);
     __syncthreads();
-    const int mme = mt + (threadIdx.x & 31);  // this thread's order (blockDim % 32 == 0)
-    const int jme = mme < mmax ? pm.mmap[mme].x - jlo : 0;
-    {  // the tile's 8 loads per thread issued before any shared-memory store
-        constexpr int EPT = DL * 32 / 256;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {  // element i: degree lt + warp + 8 i, order mt + lane; all loads before the stores
+        const int m = mt + lane;
+        const int jme = m < mmax ? pm.mmap[m].x - jlo : 0;
         float2 v[EPT];
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-            const int e = threadIdx.x + 256 * i;
-            const int dl = e >> 5, m = mt + (e & 31), l = lt + dl;
+            const int dl = warp + 8 * i, l = lt + dl;
             v[i] = (l < lmax && m < mmax && m <= l) ? __ldg(payload + base[dl * kMaxNw + jme] + m)
                                                     : make_float2(0.f, 0.f);
         }
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-            const int e = threadIdx.x + 256 * i;
-            const int sr = srow_of<DL>(e >> 5);
-            tre[sr][e & 31] = v[i].x;
-            tim[sr][e & 31] = v[i].y;
+            const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
+            tre[sr][lane] = v[i].x;
+            tim[sr][lane] = v[i].y;
         }
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = warp; r < 128; r += 8) {
-        const int mlt = r >> 2, p = (r >> 1) & 1, ri = r & 1;
-        const int m = mt + mlt;
+    const int p = (warp >> 1) & 1, ri = warp & 1;
+    const float (*T)[33] = ri ? tim : tre;
+    const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
+    float* row0 = cint + ((static_cast<int64_t>(mt + (warp >> 2)) * 2 + p) * 2 * F + 2 * f + ri) * Lp;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int mlt = (warp >> 2) + 2 * i, m = mt + mlt;
         if (m >= mmax) continue;
-        const int d = lt - m - p;
-        const int lp = (d > 0 ? (d + 1) >> 1 : 0) + lane;
-        const int l = m + p + 2 * lp;
+        const TileRow tr(lt - m - p);
+        const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
         const int n = lmax - m;
-        const int Lmp = n <= 0 ? 0 : (p == 0 ? (n + 1) / 2 : n / 2);
-        if (l >= lt + DL || lp >= Lp || lp >= ((Lmp + 31) & ~31)) continue;
-        const int sr = srow_of<DL>(l - lt);
-        const float v = l < lmax ? (ri ? tim[sr][mlt] : tre[sr][mlt]) : 0.f;
-        cint[((static_cast<int64_t>(m) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lp] = v;
+        const int Lmp = n <= 0 ? 0 : (n + 1 - p) >> 1;
+        if (dl >= DL || lp >= Lp || lp >= ((Lmp + 31) & ~31)) continue;
+        row0[i * gstep + lp] = lt + dl < lmax ? T[tr.s0 + lane][mlt] : 0.f;
     }
 }
 
@@ -690,7 +677,7 @@ struct sph_dist_sht_plan_s {
                 constexpr int LT = 64;
                 dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((lay.lmax + LT - 1) / LT),
                        static_cast<unsigned>(cq));
-                cint_pack_kernel<LT><<<g, 256, 0, st>>>(at<float>(w, o_cint), cq, static_cast<int>(lay.lmax),
+                cint_pack_kernel<<<g, 256, 0, st>>>(at<float>(w, o_cint), cq, static_cast<int>(lay.lmax),
                                                         static_cast<int>(lay.mmax), sht->Lp, pmap(ch.b0_b),
                                                         at<float2>(w, o_pay[b]));
                 SPH_LAUNCH_CHECK();
