@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(256) disco_band_t2_kernel(
 // (output row, input row) 9 broadcast LDS.64 feed 18 FFMA2 for two channels instead of
 // 9 LDS + 36 FFMA for one.  The pair's 2 x 9 S values per re/im row are one contiguous
 // 72-byte run, loaded as 9 LDG.64.  threads = 4 orders x 32 lanes, 64 channels per pass.
-__global__ void __launch_bounds__(128) disco_band_t3_kernel(
+__global__ void __launch_bounds__(128, 4) disco_band_t3_kernel(
     const float* __restrict__ S, const float2* __restrict__ psi_t, const int32_t* __restrict__ band0,
     const int32_t* __restrict__ bandc, const int64_t* __restrict__ psi_off, const int32_t* __restrict__ tt_ptr,
     const int32_t* __restrict__ tt_h, int64_t Hin, int64_t nbi, int64_t Hout, int64_t nbo, int wout, int K,
