@@ -1218,7 +1218,13 @@ void DiscoPlan::transpose_apply(const float* v, const float* mix, int64_t B, int
             g->Bhi = {nullptr, n, cout, w.ldc};
             g->Blo = {nullptr, n, cout, w.ldc};
             g->store = STORE_ROW;
-            g->bn = n >= 256 ? 256 : 128;
+            // N = c_in * K: 576 at cfg3 is 3 x 192 (the bn = 256 tiling pads it to 768);
+            // SPH_DISCO_MIXT_BN overrides
+            static const int bn_env = std::getenv("SPH_DISCO_MIXT_BN") ? std::atoi(std::getenv("SPH_DISCO_MIXT_BN")) : 0;
+            g->bn = bn_env == 128 || bn_env == 192 || bn_env == 256 ? bn_env
+                    : n % 192 == 0 && n % 256 != 0     ? 192
+                    : n >= 256                         ? 256
+                                                       : 128;
             g->name = "gemm_disco_mix_t";
             require(rows < (1LL << 31), "disco_transpose_apply: batch too large for one call");
             GemmGroup gr;
