@@ -991,6 +991,9 @@ void DiscoPlan::apply_rows(const float* x, int64_t h_in0, int64_t nin, int64_t h
             g->alo = true;
             g->bn = cout <= 64 ? 64 : 128;
         }
+        // SPH_DISCO_MIX_BN=192: the CTA-pair bn = 192 kernel (A/B experiments)
+        static const int mix_bn = std::getenv("SPH_DISCO_MIX_BN") ? std::atoi(std::getenv("SPH_DISCO_MIX_BN")) : 0;
+        if (mix_bn == 192 && prec != SPH_PREC_FP32_SIMT) g->bn = 192;
         g->name = "gemm_disco_mix";
         // table multicast over 2 CTAs (cfg3: 1.386 ms vs 1.445 ms at the default 4)
         g->cluster = 2;
