@@ -392,7 +392,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
                    const GemmWork* __restrict__ works,
                    int ntiles, float* __restrict__ D,
                    int store_mode, int three_pass, long long* __restrict__ trace, int dbg,
-                   int tma_store, int a_quad,  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B
+                   int tma_store, int a_quad,  // a_quad: 0 2D SW128, 1 quad 16 B, 2 quad 512 B, 3 quad 1 KB
                    int d_mode, int d_t, int d_g2, int pf, GemmEpi epi, int l2hint, int blo_conv) {
     // dbg (diagnostic, SPH_GEMM_DEBUG bits; results are wrong when set): 1 epilogue skips
     // TMEM loads + stores, 2 converter skips its work, 4 no MMAs, 8 no table loads
@@ -482,7 +482,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     // atom ka (K offset ka * KB) of the data tile into atom slot a of stage s
     auto load_a1 = [&](int s, int a, const GemmWork& w, int ka) {
         const uint32_t dst = a_hi(s) + a * L::A_ATOM;
-        if (ALO && a_quad == 2)  // wide map: 32-row blocks of 512 B
+        if (ALO && a_quad == 3)  // wider map: 64-row blocks of 1 KB
+            tma_load_4d(dst, &map_a, 0, (w.m0 + crank * BM) / 64, ka * (KB / 4), w.ag, full_bar(s));
+        else if (ALO && a_quad == 2)  // wide map: 32-row blocks of 512 B
             tma_load_4d(dst, &map_a, 0, (w.m0 + crank * BM) / 32, ka * (KB / 4), w.ag, full_bar(s));
         else if (ALO && a_quad)
             tma_load_4d(dst, &map_a, 0, w.m0 + crank * BM, ka * (KB / 4), w.ag, full_bar(s));
@@ -496,7 +498,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a,
     };
     // L2 prefetch of a data tile k-block (same box as load_a)
     auto prefetch_a = [&](const GemmWork& w, int kb) {
-        if (ALO && a_quad == 2)
+        if (ALO && a_quad == 3)
+            tma_prefetch_4d(&map_a, 0, (w.m0 + crank * BM) / 64, kb * (KB / 4), w.ag);
+        else if (ALO && a_quad == 2)
             tma_prefetch_4d(&map_a, 0, (w.m0 + crank * BM) / 32, kb * (KB / 4), w.ag);
         else if (ALO && a_quad)
             tma_prefetch_4d(&map_a, 0, w.m0 + crank * BM, kb * (KB / 4), w.ag);
@@ -1061,6 +1065,17 @@ static CUtensorMap make_map(const Mat2D& m, int box_rows, int kb) {
     return map;
 }
 
+// rows per inner run of the quad-interleaved A map: 64 (1 KB, SPH_GEMM_AQUAD_1K=1),
+// 32 (512 B) or 1 (16-byte core-matrix rows) -- every A tile starts on a multiple of BM
+static int quad_rows(const GroupedGemm& g) {
+    static const bool k1 = [] {
+        const char* e = std::getenv("SPH_GEMM_AQUAD_1K");
+        return e && std::atoi(e) != 0;
+    }();
+    if (k1 && g.a_rows_g % 64 == 0) return 64;
+    return g.a_rows_g % 32 == 0 ? 32 : 1;
+}
+
 template <int BN, int STAGES, int CL, bool ALO = false, bool PAIR = false, int KS = 1>
 static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const float* Blo,
                    float* D, bool three, cudaStream_t st, GemmEpi epi) {
@@ -1101,13 +1116,16 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
         // rows % 32 == 0: dims {32 rows x 4 (512 B contiguous), row blocks, quads, groups},
         // box {128, 4, 8, 1} -> 512-byte TMA requests; otherwise {4, rows, quads, groups}
         // with 16-byte requests (measured 3.1 vs 2.4 ms on the cfg2 forward GEMM)
-        const bool wide = g.a_rows_g % 32 == 0;
-        cuuint64_t dims[4] = {wide ? 128u : 4u,
-                              static_cast<cuuint64_t>(wide ? g.a_rows_g / 32 : g.a_rows_g),
+        // rows % 64 == 0 (and SPH_GEMM_AQUAD_1K=1): 1 KB inner runs (64 rows x 4), the same
+        // SMEM image (profiles/tma_eo_rate.cu: 16-byte inner boxes cap TMA at 3.8 TB/s)
+        const int rb = quad_rows(g);
+        const bool wide = rb > 1;
+        cuuint64_t dims[4] = {wide ? 4u * rb : 4u,
+                              static_cast<cuuint64_t>(wide ? g.a_rows_g / rb : g.a_rows_g),
                               static_cast<cuuint64_t>(g.a_kq), static_cast<cuuint64_t>(g.a_groups)};
-        cuuint64_t strides[3] = {static_cast<cuuint64_t>(wide ? 512 : 16), static_cast<cuuint64_t>(g.a_rows_g * 16),
+        cuuint64_t strides[3] = {static_cast<cuuint64_t>(wide ? 16 * rb : 16), static_cast<cuuint64_t>(g.a_rows_g * 16),
                                  static_cast<cuuint64_t>(g.a_kq * g.a_rows_g * 16)};
-        cuuint32_t box[4] = {wide ? 128u : 4u, wide ? BM / 32u : static_cast<cuuint32_t>(BM),
+        cuuint32_t box[4] = {wide ? 4u * rb : 4u, wide ? static_cast<cuuint32_t>(BM / rb) : static_cast<cuuint32_t>(BM),
                              static_cast<cuuint32_t>(bk_of<ALO>() / 4), 1};
         cuuint32_t estr[4] = {1, 1, 1, 1};
         CUresult r = encode_fn()(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(A), dims, strides,
@@ -1188,7 +1206,7 @@ static void launch(const GroupedGemm& g, const float* A, const float* Bhi, const
     SPH_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, md, static_cast<const GemmWork*>(tl.d.p),
                                 static_cast<int>(tl.n), D,
                                 g.store, three ? 1 : 0, trace, dbg, tstore ? 1 : 0,
-                                quad ? (g.a_rows_g % 32 == 0 ? 2 : 1) : 0, g.d_mode, static_cast<int>(g.d_t),
+                                quad ? (quad_rows(g) == 64 ? 3 : quad_rows(g) == 32 ? 2 : 1) : 0, g.d_mode, static_cast<int>(g.d_t),
                                 static_cast<int>(g.d_g2), pf_dist, epi, l2hint, (three && g.blo_conv) ? 1 : 0));
     count_launch();
     if (trace) {
