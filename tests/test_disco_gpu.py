@@ -2,6 +2,7 @@
 the CPU oracle.  Both device paths: the default longitude-Fourier path (3xTF32 channel
 mix) and the fp32 direct-gather anchor.  Cases follow proj/tests/test_convolution.cpp."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -118,6 +119,17 @@ def test_disco_fourier_vs_direct_anchor_full_size():
     ya, yb = a.apply(x, mix), b.apply(x, mix)
     torch.cuda.synchronize()
     assert float((ya - yb).norm() / yb.norm()) <= TOL
+    # output channels {0, 31} of sample 1 against the unmodified reference / fp64 oracle
+    outs = [0, 31]
+    xs = x[1].cpu().numpy().astype(np.float64)
+    ms = mix.cpu().numpy().astype(np.float64)[outs]
+    if oracle.ref_available():
+        _, _, ref = oracle.ref().bench_disco(EQ, 721, 1440, GA, 360, 720, 3 * PI / 360, xs, ms,
+                                             os.cpu_count() or 1, want_y=True)
+    else:
+        oop = oracle.orc().disco_assemble(EQ, 721, 1440, GA, 360, 720, 3 * PI / 360)
+        ref = oracle.orc().disco_apply(oop, xs, ms)
+    assert rel_l2(ya[1, outs].cpu().numpy().astype(np.float64), ref) <= TOL
 
 
 # ------------------------------------------------ disco_transpose_apply (convolution.hpp:226-266)

@@ -218,6 +218,11 @@ def test_gemm_cluster_multicast_matches_simt(monkeypatch, cluster):
     ya = inv(pa, a, 512)
     yb = inv(plan(0, 91, 180, 91, 90, "fp32"), a, 512)
     assert rel_l2(ya, yb) <= 2e-6
+    # and both ends of the batch against the fp64 oracle (not only the SIMT anchor)
+    sub = [0, 255, 511]
+    ref = oracle.orc().sht_forward(0, 91, 180, 91, 90, x[sub])
+    assert rel_l2(a[sub], ref) <= TOL
+    assert rel_l2(ya[sub], oracle.orc().sht_inverse(0, 91, 180, a[sub])) <= TOL
 
 
 # ------------------------------------------------------------- SHT adjoints

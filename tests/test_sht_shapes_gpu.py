@@ -65,3 +65,10 @@ def test_pair_gemm_matches_simt_anchor():
         outs.append((c.cpu().numpy().astype(np.float64), p.inverse(c, 130, L.SPH_LAYOUT_DENSE_LM).cpu().numpy()))
     assert rel_l2(outs[0][0], outs[1][0]) <= TOL
     assert rel_l2(outs[0][1], outs[1][1]) <= TOL
+    # fields at both ends of the pair tiles against the fp64 oracle
+    sub = [0, 129]
+    xs = x[sub].cpu().numpy().astype(np.float64)
+    ref = oracle.orc().sht_forward(0, 181, 360, 181, 180, xs)
+    got = outs[0][0][sub]
+    assert rel_l2(got[..., 0] + 1j * got[..., 1], ref) <= TOL
+    assert rel_l2(outs[0][1][sub], oracle.orc().sht_inverse(0, 181, 360, ref)) <= TOL
