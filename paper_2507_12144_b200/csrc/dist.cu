@@ -202,23 +202,22 @@ __global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict_
         const int p = (warp >> 1) & 1, ri = warp & 1;
         float (*T)[33] = ri ? tim : tre;
         const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
-        const float* row0 = cint + ((static_cast<int64_t>(mt + (warp >> 2)) * 2 + p) * 2 * F + 2 * f + ri) * Lp;
+        const int mw = mt + (warp >> 2);
+        const float* rp = cint + ((static_cast<int64_t>(mw) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lane;
         float v[RPW];
-        bool ok[RPW];
+        int sr[RPW];
+        int d = lt - mw - p;  // TileRow offset, -2 per row
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            const int m = mt + (warp >> 2) + 2 * i;
-            const TileRow tr(lt - m - p);
+        for (int i = 0; i < RPW; ++i, d -= 2, rp += gstep) {
+            const TileRow tr(d);
             const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
-            ok[i] = m < mmax && dl < DL && lp < Lp && lt + dl < lmax;
-            v[i] = ok[i] ? __ldg(row0 + i * gstep + lp) : 0.f;
+            const bool ok = mw + 2 * i < mmax && dl < DL && lp < Lp && lt + dl < lmax;
+            v[i] = ok ? __ldg(rp + tr.lp0) : 0.f;
+            sr[i] = ok ? tr.s0 + lane : -1;
         }
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            if (!ok[i]) continue;
-            const TileRow tr(lt - (mt + (warp >> 2) + 2 * i) - p);
-            T[tr.s0 + lane][(warp >> 2) + 2 * i] = v[i];
-        }
+        for (int i = 0; i < RPW; ++i)
+            if (sr[i] >= 0) T[sr[i]][(warp >> 2) + 2 * i] = v[i];
     }
     __syncthreads();
     const int m = mt + lane;  // this thread's order
@@ -270,17 +269,17 @@ __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restri
     const int p = (warp >> 1) & 1, ri = warp & 1;
     const float (*T)[33] = ri ? tim : tre;
     const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
-    float* row0 = cint + ((static_cast<int64_t>(mt + (warp >> 2)) * 2 + p) * 2 * F + 2 * f + ri) * Lp;
+    const int mw = mt + (warp >> 2);
+    float* rp = cint + ((static_cast<int64_t>(mw) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lane;
+    int d = lt - mw - p;               // TileRow offset, -2 per row
+    int lmp = (lmax - mw + 1 - p) >> 1;  // L(m, p) while m < lmax (<= 0 after), -1 per row
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-        const int mlt = (warp >> 2) + 2 * i, m = mt + mlt;
-        if (m >= mmax) continue;
-        const TileRow tr(lt - m - p);
+    for (int i = 0; i < RPW; ++i, d -= 2, --lmp, rp += gstep) {
+        if (mw + 2 * i >= mmax) break;
+        const TileRow tr(d);
         const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
-        const int n = lmax - m;
-        const int Lmp = n <= 0 ? 0 : (n + 1 - p) >> 1;
-        if (dl >= DL || lp >= Lp || lp >= ((Lmp + 31) & ~31)) continue;
-        row0[i * gstep + lp] = lt + dl < lmax ? T[tr.s0 + lane][mlt] : 0.f;
+        const int lim = min(Lp, (max(lmp, 0) + 31) & ~31);
+        if (dl < DL && lp < lim) rp[tr.lp0] = lt + dl < lmax ? T[tr.s0 + lane][(warp >> 2) + 2 * i] : 0.f;
     }
 }
 

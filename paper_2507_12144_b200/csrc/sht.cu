@@ -149,37 +149,37 @@ __global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restr
         const int p = (warp >> 1) & 1, ri = warp & 1;
         float (*T)[33] = ri ? tim : tre;
         const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
-        const float* row0 = cint + ((static_cast<int64_t>(mt + (warp >> 2)) * 2 + p) * 2 * F + 2 * f + ri) * Lp;
+        const int ml0 = mt + (warp >> 2);
+        const float* rp = cint + ((static_cast<int64_t>(ml0) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lane;
         float v[RPW];
-        bool ok[RPW];
+        int sr[RPW];
+        int d = lt - (m0 + ml0) - p;  // the row's first tile degree offset (TileRow), -2 per row
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {  // all loads before any shared-memory store
-            const int ml = mt + (warp >> 2) + 2 * i;
-            const TileRow tr(lt - (m0 + ml) - p);
+        for (int i = 0; i < RPW; ++i, d -= 2, rp += gstep) {  // all loads before any shared store
+            const TileRow tr(d);
             const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
-            ok[i] = ml < mcount && dl < DL && lp < Lp && lt + dl < lmax;
-            v[i] = ok[i] ? __ldg(row0 + i * gstep + lp) : 0.f;
+            const bool ok = ml0 + 2 * i < mcount && dl < DL && lp < Lp && lt + dl < lmax;
+            v[i] = ok ? __ldg(rp + tr.lp0) : 0.f;
+            sr[i] = ok ? tr.s0 + lane : -1;
         }
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            if (!ok[i]) continue;
-            const int ml = mt + (warp >> 2) + 2 * i;
-            const TileRow tr(lt - (m0 + ml) - p);
-            T[tr.s0 + lane][(warp >> 2) + 2 * i] = v[i];
-        }
+        for (int i = 0; i < RPW; ++i)
+            if (sr[i] >= 0) T[sr[i]][(warp >> 2) + 2 * i] = v[i];
     }
     __syncthreads();
     const int oc = mt + lane;
     const bool mok = oc < out_mcount;
     const bool have = mt + lane < mcount;  // orders beyond mcount are zero columns
+    if (!mok) return;
     float2* dst = dense + (f * lmax + lt + warp) * out_mcount + oc;
+    const int64_t dstep = 8 * static_cast<int64_t>(out_mcount);
+    const int mabs = have ? m0 + mt + lane : lmax;  // stored entries: l >= mabs
+    const int s0 = (warp & 1) * (DL / 2) + (warp >> 1);
 #pragma unroll
-    for (int i = 0; i < DL / 8; ++i) {
-        const int dl = warp + 8 * i, l = lt + dl;
-        if (l >= lmax || !mok) continue;
-        const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
-        const bool val = have && m0 + mt + lane <= l;
-        dst[static_cast<int64_t>(i) * 8 * out_mcount] = val ? make_float2(tre[sr][lane], tim[sr][lane]) : make_float2(0.f, 0.f);
+    for (int i = 0; i < DL / 8; ++i, dst += dstep) {
+        const int l = lt + warp + 8 * i;
+        if (l >= lmax) break;
+        *dst = mabs <= l ? make_float2(tre[s0 + 4 * i][lane], tim[s0 + 4 * i][lane]) : make_float2(0.f, 0.f);
     }
 }
 
@@ -200,11 +200,13 @@ __global__ void __launch_bounds__(256) dense_to_cint_kernel(const float2* __rest
     {  // element i: degree lt + warp + 8 i, order mt + lane; all loads before the stores
         const int m = mt + lane;
         const float2* src = dense + (f * lmax + lt + warp) * mmax + m;
+        const int64_t sstep = 8 * mmax;
+        const int lmin = m < mmx ? m : lmx;  // stored entries: m <= l < lmax
         float2 v[EPT];
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) {
+        for (int i = 0; i < EPT; ++i, src += sstep) {
             const int l = lt + warp + 8 * i;
-            v[i] = (l < lmx && m < mmx && m <= l) ? __ldg(src + static_cast<int64_t>(i) * 8 * mmax) : make_float2(0.f, 0.f);
+            v[i] = (l < lmx && lmin <= l) ? __ldg(src) : make_float2(0.f, 0.f);
         }
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
@@ -217,17 +219,17 @@ __global__ void __launch_bounds__(256) dense_to_cint_kernel(const float2* __rest
     const int p = (warp >> 1) & 1, ri = warp & 1;
     const float (*T)[33] = ri ? tim : tre;
     const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
-    float* row0 = cint + ((static_cast<int64_t>(mt + (warp >> 2)) * 2 + p) * 2 * F + 2 * f + ri) * Lp;
+    const int mw = mt + (warp >> 2);
+    float* rp = cint + ((static_cast<int64_t>(mw) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lane;
+    int d = lt - mw - p;              // TileRow offset, -2 per row
+    int lmp = (lmx - mw + 1 - p) >> 1;  // L(m, p) while m < lmax (<= 0 after), -1 per row
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-        const int mlt = (warp >> 2) + 2 * i, m = mt + mlt;
-        if (m >= mmx) continue;
-        const TileRow tr(lt - m - p);
+    for (int i = 0; i < RPW; ++i, d -= 2, --lmp, rp += gstep) {
+        if (mw + 2 * i >= mmx) break;
+        const TileRow tr(d);
         const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
-        const int n = lmx - m;
-        const int Lmp = n <= 0 ? 0 : (n + 1 - p) >> 1;
-        if (dl >= DL || lp >= Lp || lp >= ((Lmp + 31) & ~31)) continue;
-        row0[i * gstep + lp] = lt + dl < lmx ? T[tr.s0 + lane][mlt] : 0.f;
+        const int lim = min(Lp, (max(lmp, 0) + 31) & ~31);
+        if (dl < DL && lp < lim) rp[tr.lp0] = lt + dl < lmx ? T[tr.s0 + lane][(warp >> 2) + 2 * i] : 0.f;
     }
 }
 

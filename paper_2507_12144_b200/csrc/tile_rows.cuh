@@ -12,6 +12,8 @@
 // of a warp has a fixed parity p = (warp >> 1) & 1 and re/im ri = warp & 1 and order
 // mlt = warp / 4 + 2 i (C_int row offsets advance by 4 groups = 8 F Lp floats per i); its
 // 32 lanes cover degrees l = lt + off0 + 2 lane, i.e. shared-memory rows s0 + lane.
+// Kernels walk their 16 rows incrementally (d -= 2, L(m, p) -= 1, row pointer += 8 F Lp):
+// the multiply-per-row form left 345 IMADs in dense_to_cint, this one 154.
 #pragma once
 
 namespace sph {
