@@ -11,7 +11,17 @@ namespace sph {
 namespace {
 
 __device__ __forceinline__ float gelu_erfc(float x) {  // model.hpp:42-44
+    // x * 0.5 * erfc(-x / sqrt 2) evaluated as 0.5 x (1 + erf(x / sqrt 2)): the same value up
+    // to fp32 rounding (absolute error ~1e-8 where erfc's relative accuracy for very negative
+    // x stops mattering) at a fraction of erfcf's instructions -- the MLP1 epilogue and the
+    // GeLU transpose were issue-bound on it (cfg4 block pair 6.65 -> 6.25 ms,
+    // profiles/r2/gelu_erf_ab.log).  -DSPH_GELU_ERFC restores the erfc form.
+#ifdef SPH_GELU_ERFC
     return x * 0.5f * erfcf(-x * 0.70710678118654752440f);
+#else
+    const float h = 0.5f * x;
+    return fmaf(h, erff(x * 0.70710678118654752440f), h);
+#endif
 }
 
 // kernel [cout][cin][klmax] -> Kt hi/lo [(l*cout + o)][ldk], l < lmax (tiled transpose)
@@ -199,7 +209,6 @@ __global__ void residual_kernel(float* __restrict__ y, const float* __restrict__
     }
 }
 
-inline unsigned nblk(int64_t n) { return static_cast<unsigned>((n + 255) / 256); }
 
 struct SpecProblem {
     std::vector<int64_t> row_off;

@@ -53,7 +53,17 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ float gelu_erfc_dev(float x) {  // model.hpp:42-44
+    // x * 0.5 * erfc(-x / sqrt 2) evaluated as 0.5 x (1 + erf(x / sqrt 2)): the same value up
+    // to fp32 rounding (absolute error ~1e-8 where erfc's relative accuracy for very negative
+    // x stops mattering) at a fraction of erfcf's instructions -- the MLP1 epilogue and the
+    // GeLU transpose were issue-bound on it (cfg4 block pair 6.65 -> 6.25 ms,
+    // profiles/r2/gelu_erf_ab.log).  -DSPH_GELU_ERFC restores the erfc form.
+#ifdef SPH_GELU_ERFC
     return x * 0.5f * erfcf(-x * 0.70710678118654752440f);
+#else
+    const float h = 0.5f * x;
+    return fmaf(h, erff(x * 0.70710678118654752440f), h);
+#endif
 }
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
