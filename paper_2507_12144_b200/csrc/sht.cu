@@ -132,26 +132,28 @@ void upload(DevBuf<T>& d, const std::vector<T>& h) {
 // ---------------------------------------------------------------- kernels
 // Internal coefficient layout <-> dense [F][lmax][mcols] complex (m contiguous): tiled
 // transposes through shared memory (tile_rows.cuh), both global sides in contiguous runs.
-// CTA (32 orders, 64 degrees, field f): 128 cint rows (order, parity, re/im) read as
+// CTA (32 orders, 64 degrees, FPC fields): 128 cint rows (order, parity, re/im) read as
 // 32-lane runs of lp (each run is the tile's 32 degrees of that parity class), dense rows
-// written as 32-order float2 runs (zeros above the diagonal, decided at the store).
+// written as 32-order float2 runs (zeros above the diagonal, decided at the store).  The
+// FPC fields of a CTA share every index computation (the kernels are issue-bound).
+template <int FPC>
 __global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int lmax,
                                                             int m0, int mcount, int out_mcount, int Lp,
                                                             float2* __restrict__ dense, int64_t f0) {
     constexpr int DL = 64, RPW = 128 / 8;
-    __shared__ float tre[DL][33], tim[DL][33];
+    __shared__ float tre[FPC][DL][33], tim[FPC][DL][33];
     // fields slowest: concurrently running CTAs share a field's dense rows (fields fastest,
     // for adjacent C_int rows instead, measured 2.42 vs 2.27 ms at 1024 fields)
     const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;
-    const int64_t f = f0 + blockIdx.z;
+    const int64_t f = f0 + static_cast<int64_t>(blockIdx.z) * FPC;
+    const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), F - f));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (m0 + mt <= lt + DL - 1) {  // else the whole tile is above the diagonal (m > l)
         const int p = (warp >> 1) & 1, ri = warp & 1;
-        float (*T)[33] = ri ? tim : tre;
         const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
         const int ml0 = mt + (warp >> 2);
         const float* rp = cint + ((static_cast<int64_t>(ml0) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lane;
-        float v[RPW];
+        float v[FPC][RPW];
         int sr[RPW];
         int d = lt - (m0 + ml0) - p;  // the row's first tile degree offset (TileRow), -2 per row
 #pragma unroll
@@ -159,12 +161,17 @@ __global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restr
             const TileRow tr(d);
             const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
             const bool ok = ml0 + 2 * i < mcount && dl < DL && lp < Lp && lt + dl < lmax;
-            v[i] = ok ? __ldg(rp + tr.lp0) : 0.f;
+#pragma unroll
+            for (int q = 0; q < FPC; ++q) v[q][i] = ok && q < nf ? __ldg(rp + tr.lp0 + q * 2 * Lp) : 0.f;
             sr[i] = ok ? tr.s0 + lane : -1;
         }
 #pragma unroll
-        for (int i = 0; i < RPW; ++i)
-            if (sr[i] >= 0) T[sr[i]][(warp >> 2) + 2 * i] = v[i];
+        for (int q = 0; q < FPC; ++q) {
+            float (*T)[33] = ri ? tim[q] : tre[q];
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+                if (sr[i] >= 0) T[sr[i]][(warp >> 2) + 2 * i] = v[q][i];
+        }
     }
     __syncthreads();
     const int oc = mt + lane;
@@ -172,52 +179,62 @@ __global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restr
     const bool have = mt + lane < mcount;  // orders beyond mcount are zero columns
     if (!mok) return;
     float2* dst = dense + (f * lmax + lt + warp) * out_mcount + oc;
-    const int64_t dstep = 8 * static_cast<int64_t>(out_mcount);
+    const int64_t dstep = 8 * static_cast<int64_t>(out_mcount), fstep = static_cast<int64_t>(lmax) * out_mcount;
     const int mabs = have ? m0 + mt + lane : lmax;  // stored entries: l >= mabs
     const int s0 = (warp & 1) * (DL / 2) + (warp >> 1);
 #pragma unroll
     for (int i = 0; i < DL / 8; ++i, dst += dstep) {
         const int l = lt + warp + 8 * i;
         if (l >= lmax) break;
-        *dst = mabs <= l ? make_float2(tre[s0 + 4 * i][lane], tim[s0 + 4 * i][lane]) : make_float2(0.f, 0.f);
+        const bool val = mabs <= l;
+#pragma unroll
+        for (int q = 0; q < FPC; ++q)
+            if (q < nf)
+                dst[q * fstep] = val ? make_float2(tre[q][s0 + 4 * i][lane], tim[q][s0 + 4 * i][lane])
+                                     : make_float2(0.f, 0.f);
     }
 }
 
-// CTA (32 orders, 64 degrees, field f): the dense rows of the tile loaded once as
+// CTA (32 orders, 64 degrees, FPC fields): the dense rows of the tile loaded once as
 // 32-order runs (no overlap between tiles); each (order, parity, re/im) C_int row gets
 // the 32 consecutive lp whose degrees fall in the tile, written as one 32-lane run.  The
 // degree tiles run past lmax far enough to zero every lp the inverse GEMM reads: up to
 // L(m, p) rounded to its 32-wide k-block (the padding beyond that is never touched).
+template <int FPC>
 __global__ void __launch_bounds__(256) dense_to_cint_kernel(const float2* __restrict__ dense, int64_t F, int64_t lmax,
                                                             int64_t mmax, int Lp, float* __restrict__ cint,
                                                             int64_t f0) {
     constexpr int DL = 64, RPW = 128 / 8, EPT = DL * 32 / 256;
-    __shared__ float tre[DL][33], tim[DL][33];
+    __shared__ float tre[FPC][DL][33], tim[FPC][DL][33];
     const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;  // fields slowest (3.60 vs 2.90 ms fastest)
-    const int64_t f = f0 + blockIdx.z;
+    const int64_t f = f0 + static_cast<int64_t>(blockIdx.z) * FPC;
+    const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), F - f));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int lmx = static_cast<int>(lmax), mmx = static_cast<int>(mmax);
     {  // element i: degree lt + warp + 8 i, order mt + lane; all loads before the stores
         const int m = mt + lane;
         const float2* src = dense + (f * lmax + lt + warp) * mmax + m;
-        const int64_t sstep = 8 * mmax;
+        const int64_t sstep = 8 * mmax, fstep = lmax * mmax;
         const int lmin = m < mmx ? m : lmx;  // stored entries: m <= l < lmax
-        float2 v[EPT];
+        float2 v[FPC][EPT];
 #pragma unroll
         for (int i = 0; i < EPT; ++i, src += sstep) {
             const int l = lt + warp + 8 * i;
-            v[i] = (l < lmx && lmin <= l) ? __ldg(src) : make_float2(0.f, 0.f);
+            const bool ok = l < lmx && lmin <= l;
+#pragma unroll
+            for (int q = 0; q < FPC; ++q) v[q][i] = ok && q < nf ? __ldg(src + q * fstep) : make_float2(0.f, 0.f);
         }
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
-            tre[sr][lane] = v[i].x;
-            tim[sr][lane] = v[i].y;
-        }
+        for (int q = 0; q < FPC; ++q)
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
+                tre[q][sr][lane] = v[q][i].x;
+                tim[q][sr][lane] = v[q][i].y;
+            }
     }
     __syncthreads();
     const int p = (warp >> 1) & 1, ri = warp & 1;
-    const float (*T)[33] = ri ? tim : tre;
     const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
     const int mw = mt + (warp >> 2);
     float* rp = cint + ((static_cast<int64_t>(mw) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lane;
@@ -229,8 +246,21 @@ __global__ void __launch_bounds__(256) dense_to_cint_kernel(const float2* __rest
         const TileRow tr(d);
         const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
         const int lim = min(Lp, (max(lmp, 0) + 31) & ~31);
-        if (dl < DL && lp < lim) rp[tr.lp0] = lt + dl < lmx ? T[tr.s0 + lane][(warp >> 2) + 2 * i] : 0.f;
+        if (dl < DL && lp < lim) {
+            const bool in = lt + dl < lmx;
+#pragma unroll
+            for (int q = 0; q < FPC; ++q)
+                if (q < nf) rp[tr.lp0 + q * 2 * Lp] = in ? (ri ? tim : tre)[q][tr.s0 + lane][(warp >> 2) + 2 * i] : 0.f;
+        }
     }
+}
+
+// fields per CTA of the C_int <-> dense transposes (SPH_TR_FIELDS = 1 or 2 overrides):
+// from_dense 2 (1.76 -> 1.22 ms at cfg2), to_dense 1 (2 fields: 90 registers, 2 CTAs/SM,
+// 1.40 -> 1.58 ms; profiles/r2/tr_fields_ab.log)
+int tr_fields(int dflt) {
+    static const int v = std::getenv("SPH_TR_FIELDS") ? std::atoi(std::getenv("SPH_TR_FIELDS")) : 0;
+    return v == 1 || v == 2 ? v : dflt;
 }
 
 // bins [F][nlat][mcount] complex (scaled by 2pi/nlon) -> EO_loc [mcount][2][Rp/4][2F][4]
@@ -266,12 +296,14 @@ void cint_to_dense(const ShtPlan& p, const float* cint, int64_t F, int64_t m0, i
     double pairs = 0;  // stored (l, m) entries read from cint
     for (int64_t ml = 0; ml < mcount; ++ml) pairs += static_cast<double>(std::max<int64_t>(0, p.lmax - (m0 + ml)));
     ProfScope prof("sht_to_dense", st, 8.0 * F * p.lmax * out_mcount + 8.0 * F * pairs);
-    for (int64_t f0 = 0; f0 < F; f0 += 65535) {
+    const int fpc = tr_fields(1);
+    for (int64_t f0 = 0; f0 < F; f0 += 65535LL * fpc) {
+        const int64_t nfc = std::min<int64_t>(65535LL * fpc, F - f0);
         dim3 grid(static_cast<unsigned>((out_mcount + 31) / 32), static_cast<unsigned>((p.lmax + 63) / 64),
-                  static_cast<unsigned>(std::min<int64_t>(65535, F - f0)));
-        cint_to_dense_kernel<<<grid, 256, 0, st>>>(cint, F, static_cast<int>(p.lmax), static_cast<int>(m0),
-                                                   static_cast<int>(mcount), static_cast<int>(out_mcount), p.Lp,
-                                                   reinterpret_cast<float2*>(dense), f0);
+                  static_cast<unsigned>((nfc + fpc - 1) / fpc));
+        auto k = fpc == 2 ? cint_to_dense_kernel<2> : cint_to_dense_kernel<1>;
+        k<<<grid, 256, 0, st>>>(cint, F, static_cast<int>(p.lmax), static_cast<int>(m0), static_cast<int>(mcount),
+                                static_cast<int>(out_mcount), p.Lp, reinterpret_cast<float2*>(dense), f0);
         SPH_LAUNCH_CHECK();
         count_launch();
     }
@@ -283,11 +315,13 @@ void dense_to_cint(const ShtPlan& p, const float* dense, int64_t F, float* cint,
     // degree tiles up to the last zero-padded lp: l = m + p + 2 (round_up(L(m, p), 32) - 1)
     // <= m + 2 L(m, p) + 61 <= lmax + 62
     const int64_t lend = p.lmax + 63;
-    for (int64_t f0 = 0; f0 < F; f0 += 65535) {
+    const int fpc = tr_fields(2);
+    for (int64_t f0 = 0; f0 < F; f0 += 65535LL * fpc) {
+        const int64_t nfc = std::min<int64_t>(65535LL * fpc, F - f0);
         dim3 grid(static_cast<unsigned>((p.mmax + 31) / 32), static_cast<unsigned>((lend + 63) / 64),
-                  static_cast<unsigned>(std::min<int64_t>(65535, F - f0)));
-        dense_to_cint_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(dense), F, p.lmax, p.mmax,
-                                                   p.Lp, cint, f0);
+                  static_cast<unsigned>((nfc + fpc - 1) / fpc));
+        auto k = fpc == 2 ? dense_to_cint_kernel<2> : dense_to_cint_kernel<1>;
+        k<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(dense), F, p.lmax, p.mmax, p.Lp, cint, f0);
         SPH_LAUNCH_CHECK();
         count_launch();
     }
