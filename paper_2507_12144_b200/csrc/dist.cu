@@ -237,37 +237,50 @@ __global__ void __launch_bounds__(256) cint_pack_kernel(const float* __restrict_
 // order runs, each (order, parity, re/im) C_int row's 32 lp of the tile written as one
 // run; degree tiles run to lmax + 63 so every lp the inverse GEMM reads (L(m, p) rounded
 // to its 32-wide k-block) is written, zeros beyond lmax.
+template <int FPC>
 __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restrict__ payload, int64_t F, int lmax,
                                                           int mmax, int Lp, PayloadMap pm, float* __restrict__ cint) {
     constexpr int DL = 64, RPW = 128 / 8, EPT = DL * 32 / 256;
-    __shared__ float tre[DL][33], tim[DL][33];
+    __shared__ float tre[FPC][DL][33], tim[FPC][DL][33];
     __shared__ int64_t base[DL * kMaxNw];
+    __shared__ int32_t trs[FPC > 1 ? DL * kMaxNw : 1];  // per-field payload stride (field q: + q * trs)
     const int mt = blockIdx.x * 32, lt = blockIdx.y * DL;
-    const int64_t f = blockIdx.z;
+    const int64_t f = static_cast<int64_t>(blockIdx.z) * FPC;
+    const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), F - f));
     int jlo, nj;
     stage_rowbase(base, pm, f, lt, DL, lmax, mt, mmax, jlo, nj);
+    if (FPC > 1)
+        for (int e = threadIdx.x; e < DL * nj; e += blockDim.x) {
+            const int ll = e / nj, jj = e - ll * nj;
+            if (lt + ll < lmax) trs[ll * kMaxNw + jj] = static_cast<int32_t>(__ldg(pm.tr + static_cast<int64_t>(lt + ll) * pm.nw + jlo + jj));
+        }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     {  // element i: degree lt + warp + 8 i, order mt + lane; all loads before the stores
         const int m = mt + lane;
         const int jme = m < mmax ? pm.mmap[m].x - jlo : 0;
-        float2 v[EPT];
+        float2 v[FPC][EPT];
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             const int dl = warp + 8 * i, l = lt + dl;
-            v[i] = (l < lmax && m < mmax && m <= l) ? __ldg(payload + base[dl * kMaxNw + jme] + m)
-                                                    : make_float2(0.f, 0.f);
+            const bool ok = l < lmax && m < mmax && m <= l;
+            const int64_t at = ok ? base[dl * kMaxNw + jme] + m : 0;
+            const int64_t fs = FPC > 1 && ok ? trs[dl * kMaxNw + jme] : 0;
+#pragma unroll
+            for (int q = 0; q < FPC; ++q)
+                v[q][i] = ok && q < nf ? __ldg(payload + at + q * fs) : make_float2(0.f, 0.f);
         }
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
-            tre[sr][lane] = v[i].x;
-            tim[sr][lane] = v[i].y;
-        }
+        for (int q = 0; q < FPC; ++q)
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const int sr = (warp & 1) * (DL / 2) + (warp >> 1) + 4 * i;
+                tre[q][sr][lane] = v[q][i].x;
+                tim[q][sr][lane] = v[q][i].y;
+            }
     }
     __syncthreads();
     const int p = (warp >> 1) & 1, ri = warp & 1;
-    const float (*T)[33] = ri ? tim : tre;
     const int64_t gstep = 8 * F * Lp;  // 4 groups (m += 2)
     const int mw = mt + (warp >> 2);
     float* rp = cint + ((static_cast<int64_t>(mw) * 2 + p) * 2 * F + 2 * f + ri) * Lp + lane;
@@ -279,7 +292,12 @@ __global__ void __launch_bounds__(256) cint_unpack_kernel(const float2* __restri
         const TileRow tr(d);
         const int lp = tr.lp0 + lane, dl = tr.off0 + 2 * lane;
         const int lim = min(Lp, (max(lmp, 0) + 31) & ~31);
-        if (dl < DL && lp < lim) rp[tr.lp0] = lt + dl < lmax ? T[tr.s0 + lane][(warp >> 2) + 2 * i] : 0.f;
+        if (dl < DL && lp < lim) {
+            const bool in = lt + dl < lmax;
+#pragma unroll
+            for (int q = 0; q < FPC; ++q)
+                if (q < nf) rp[tr.lp0 + q * 2 * Lp] = in ? (ri ? tim : tre)[q][tr.s0 + lane][(warp >> 2) + 2 * i] : 0.f;
+        }
     }
 }
 
@@ -759,9 +777,10 @@ struct sph_dist_sht_plan_s {
             if (cq > 0) {
                 {
                     ProfScope prof("dist_unpack_cint", st, 4.0 * ch.xia.recv_total() + 4.0 * sht->cint_elems(cq));
+                    // two fields per CTA share the index math (as sht.cu's dense_to_cint)
                     dim3 g(static_cast<unsigned>((lay.mmax + 31) / 32), static_cast<unsigned>((lay.lmax + 63 + 63) / 64),
-                           static_cast<unsigned>(cq));
-                    cint_unpack_kernel<<<g, 256, 0, st>>>(at<const float2>(w, o_pay[b]), cq,
+                           static_cast<unsigned>((cq + 1) / 2));
+                    cint_unpack_kernel<2><<<g, 256, 0, st>>>(at<const float2>(w, o_pay[b]), cq,
                                                           static_cast<int>(lay.lmax), static_cast<int>(lay.mmax),
                                                           sht->Lp, pmap(ch.b0_ia), at<float>(w, o_cint));
                     SPH_LAUNCH_CHECK();
