@@ -137,7 +137,7 @@ void upload(DevBuf<T>& d, const std::vector<T>& h) {
 // written as 32-order float2 runs (zeros above the diagonal, decided at the store).  The
 // FPC fields of a CTA share every index computation (the kernels are issue-bound).
 template <int FPC>
-__global__ void __launch_bounds__(256) cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int lmax,
+__global__ void __launch_bounds__(256, FPC == 2 ? 3 : 4) cint_to_dense_kernel(const float* __restrict__ cint, int64_t F, int lmax,
                                                             int m0, int mcount, int out_mcount, int Lp,
                                                             float2* __restrict__ dense, int64_t f0) {
     constexpr int DL = 64, RPW = 128 / 8;
@@ -256,8 +256,9 @@ __global__ void __launch_bounds__(256) dense_to_cint_kernel(const float2* __rest
 }
 
 // fields per CTA of the C_int <-> dense transposes (SPH_TR_FIELDS = 1 or 2 overrides):
-// from_dense 2 (1.76 -> 1.22 ms at cfg2), to_dense 1 (2 fields: 90 registers, 2 CTAs/SM,
-// 1.40 -> 1.58 ms; profiles/r2/tr_fields_ab.log)
+// from_dense 1.76 -> 1.22 ms at cfg2 with 2; to_dense 1.40 -> 1.31-1.36 ms with 2 once its
+// registers are capped for 3 CTAs/SM (uncapped: 90 registers, 2 CTAs/SM, 1.58 ms;
+// profiles/r2/tr_fields_ab.log, tr_fields_ab2.log)
 int tr_fields(int dflt) {
     static const int v = std::getenv("SPH_TR_FIELDS") ? std::atoi(std::getenv("SPH_TR_FIELDS")) : 0;
     return v == 1 || v == 2 ? v : dflt;
@@ -296,7 +297,7 @@ void cint_to_dense(const ShtPlan& p, const float* cint, int64_t F, int64_t m0, i
     double pairs = 0;  // stored (l, m) entries read from cint
     for (int64_t ml = 0; ml < mcount; ++ml) pairs += static_cast<double>(std::max<int64_t>(0, p.lmax - (m0 + ml)));
     ProfScope prof("sht_to_dense", st, 8.0 * F * p.lmax * out_mcount + 8.0 * F * pairs);
-    const int fpc = tr_fields(1);
+    const int fpc = tr_fields(2);
     for (int64_t f0 = 0; f0 < F; f0 += 65535LL * fpc) {
         const int64_t nfc = std::min<int64_t>(65535LL * fpc, F - f0);
         dim3 grid(static_cast<unsigned>((out_mcount + 31) / 32), static_cast<unsigned>((p.lmax + 63) / 64),

@@ -2,7 +2,7 @@
 # C_int <-> dense transposes: 2 fields per CTA sharing the index math (SPH_TR_FIELDS=2) vs 1
 cd "$(dirname "$0")/.."
 timeout -s KILL 900 python -m pytest -q -x -m gpu tests/test_sht_gpu.py tests/test_sht_shapes_gpu.py tests/test_baseline_configs_gpu.py tests/test_cpp_shim_gpu.py tests/test_consumers_gpu.py tests/test_block_gpu.py 2>&1 | tail -1
-SPH_TR_FIELDS=1 timeout -s KILL 900 python -m pytest -q -x -m gpu tests/test_sht_gpu.py tests/test_sht_shapes_gpu.py 2>&1 | tail -1
+SPH_TR_FIELDS=2 timeout -s KILL 900 python -m pytest -q -x -m gpu tests/test_sht_gpu.py tests/test_sht_shapes_gpu.py 2>&1 | tail -1
 run() {
   local lab=$1; shift
   env "$@" timeout -s KILL 300 python bench.py --workload sht --steps 10 --no-cpu --no-e2e 2>/dev/null | tail -1 | \
@@ -10,5 +10,5 @@ run() {
 }
 for rep in 1 2 3; do
   run "fields=2" SPH_TR_FIELDS=2
-  run "fields=1" SPH_TR_FIELDS=1
+  run "default " SPH_TR_FIELDS=0
 done
