@@ -111,3 +111,25 @@ def test_disco_writes_stay_in_bounds(ik, ih, iw, ok, oh, ow, cin, cout, B):
     assert u.intact() and wst.intact()
     vref = oracle.orc().disco_transpose_apply(oop, v[B - 1].cpu().numpy().astype(np.float64), mix)
     assert rel_l2(u.view[B - 1].cpu().numpy().astype(np.float64), vref) <= 1e-5
+
+
+def test_resample_and_decoder_writes_stay_in_bounds():
+    """bilinear_resample and the fused decoder group (360x720 latent -> 721x1440, odd channel
+    counts): guards intact and the guarded results equal to the plain calls (parity against
+    the reference composition is pinned in test_resample_gpu.py / test_decoder_gpu.py)."""
+    gl, go = S.build_gaussian(45, 90), S.build_equiangular(91, 180)
+    B, cin, cout = 2, 3, 5
+    lat = torch.tensor(oracle.random_field((B, cin, 45, 90), 31), dtype=torch.float32, device=DEV)
+    rp = S.ResamplePlan(gl, go)
+    r = Guarded(B * cin * 91 * 180, shape=(B, cin, 91, 180))
+    rp.apply(lat, out=r.view)
+    assert r.intact()
+    assert torch.equal(r.view, rp.apply(lat))
+    op = S.DiscoOperator(go, go, S.morlet_basis(3 * PI / 90))
+    dp = S.DecoderPlan(op, gl)
+    mix = torch.tensor(oracle.random_field((cout, cin, 9), 32), dtype=torch.float32, device=DEV)
+    y = Guarded(B * cout * 91 * 180, shape=(B, cout, 91, 180))
+    ws = Guarded(int(L.lib.sph_decoder_workspace_bytes(dp.h, B, cin, cout)), torch.uint8)
+    dp.apply(lat, mix, out=y.view, ws=ws.view)
+    assert y.intact() and ws.intact()
+    assert torch.equal(y.view, dp.apply(lat, mix))
