@@ -4,7 +4,10 @@ torch.cuda.CUDAGraph replay bit-identically to the eager calls -- the launch-bou
 configurations run as one graph launch instead of a tracing compiler."""
 import math
 
+import numpy as np
 import pytest
+
+from conftest import rel_l2
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -57,3 +60,10 @@ def test_sht_roundtrip_and_disco_capture_into_cuda_graph():
     torch.cuda.synchronize()
     assert torch.equal(y, y_eager)
     assert torch.equal(yd, yd_eager)
+    # and the replayed results against the fp64 oracle (fields / batch items at both ends)
+    xs = x.cpu().numpy().astype(np.float64)[[0, F - 1]]
+    ref = oracle.orc().sht_inverse(0, 91, 180, oracle.orc().sht_forward(0, 91, 180, 91, 90, xs))
+    assert rel_l2(y.cpu().numpy().astype(np.float64)[[0, F - 1]], ref) <= 1e-5
+    oop = oracle.orc().disco_assemble(0, 91, 180, 1, 45, 90, 3 * math.pi / 45)
+    dref = oracle.orc().disco_apply(oop, u[1].cpu().numpy().astype(np.float64), mix.cpu().numpy().astype(np.float64))
+    assert rel_l2(yd[1].cpu().numpy().astype(np.float64), dref) <= 1e-5
