@@ -76,12 +76,20 @@ __global__ void spec_gather_kernel(const float* __restrict__ cint, const int64_t
             (i < cin && lp < nlp) ? __ldg(cint + ((m * 2 + p) * twoF + 2 * (b * cin + i) + reim) * Lp + lp) : 0.f;
     }
     __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += 8) {
-        const int64_t lp = lp0 + r, l = m + p + 2 * lp;
-        const int64_t i = i0 + threadIdx.x;
-        if (lp >= Lp || l >= lmax || i >= ldx) continue;
-        const int64_t row = row_off[l] + (m * 2 + reim) * B + b;
-        Xg[row * ldx + i] = i < cin ? t[threadIdx.x][r] : 0.f;
+    // the 4 row offsets of this thread first (one dependent-load round instead of four)
+    int64_t ro[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t lp = lp0 + threadIdx.y + 8 * k, l = m + p + 2 * lp;
+        ro[k] = (lp < Lp && l < lmax) ? __ldg(row_off + l) : -1;
+    }
+    const int64_t i = i0 + threadIdx.x;
+    if (i >= ldx) return;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (ro[k] < 0) continue;
+        const int64_t row = ro[k] + (m * 2 + reim) * B + b;
+        Xg[row * ldx + i] = i < cin ? t[threadIdx.x][threadIdx.y + 8 * k] : 0.f;
     }
 }
 
@@ -99,12 +107,20 @@ __global__ void spec_scatter_kernel(const float* __restrict__ Yg, const int64_t*
     const int64_t m = z >> 1;
     const int64_t twoF = 2 * B * cout;
     const int64_t o0 = static_cast<int64_t>(blockIdx.x) * 32, lp0 = static_cast<int64_t>(blockIdx.y) * 32;
-    for (int r = threadIdx.y; r < 32; r += 8) {
-        const int64_t lp = lp0 + r, l = m + p + 2 * lp;
+    {  // row offsets, then the 4 row loads, before any shared-memory store
         const int64_t o = o0 + threadIdx.x;
-        float v = 0.f;
-        if (lp < Lp && l < lmax && o < cout) v = __ldg(Yg + (row_off[l] + (m * 2 + reim) * B + b) * ldy + o);
-        t[r][threadIdx.x] = v;
+        int64_t ro[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t lp = lp0 + threadIdx.y + 8 * k, l = m + p + 2 * lp;
+            ro[k] = (lp < Lp && l < lmax && o < cout) ? __ldg(row_off + l) : -1;
+        }
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            v[k] = ro[k] >= 0 ? __ldg(Yg + (ro[k] + (m * 2 + reim) * B + b) * ldy + o) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) t[threadIdx.y + 8 * k][threadIdx.x] = v[k];
     }
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += 8) {
